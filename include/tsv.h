@@ -1,0 +1,120 @@
+/*
+ * tsv.h - C ABI of the B200 retrieval backend (Teola vector-search / rerank primitives).
+ *
+ * This is the drop-in boundary behind Teola's primitive executor. In the reference the
+ * Searching and Reranking primitives are executed by `Simulator._execute`
+ * (reference: pkg/src/teola_sim/runtime.py:625-656), which only looks up a latency from
+ * the engine profile (pkg/src/teola_sim/engines.py:105-109). Each entry point below names
+ * the reference interface it replaces. All compute entry points are asynchronous on the
+ * caller's CUDA stream, take caller-owned device buffers as plain pointers, and return a
+ * status code (0 = OK). Handles are thread-compatible, not thread-safe; scratch space is
+ * kept per (index, stream) so concurrent streams on one index do not collide.
+ *
+ * Ordering convention of every result list: (score desc, id asc). Lists shorter than k are
+ * padded with (score = -inf, id = -1).
+ */
+#ifndef TSV_H_
+#define TSV_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSV_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define TSV_API __attribute__((visibility("default")))
+#else
+#define TSV_API
+#endif
+
+/* Status codes. Nonzero values map onto the reference's TeolaError hierarchy
+ * (pkg/src/teola_sim/errors.py:7-67) in the Python host layer:
+ *   TSV_ERR_CAPACITY -> CapacityExceeded (empty / oversize batch, errors.py:34-35)
+ *   TSV_ERR_CONFIG   -> ConfigParse      (bad dim / dtype / metric, errors.py:54-55)
+ *   TSV_ERR_DEVICE   -> DeviceError      (CUDA failure; new subclass)
+ *   TSV_ERR_ARGUMENT -> ConfigParse      (null / misaligned pointers)                     */
+enum {
+  TSV_OK = 0,
+  TSV_ERR_CAPACITY = 1,
+  TSV_ERR_CONFIG = 2,
+  TSV_ERR_DEVICE = 3,
+  TSV_ERR_ARGUMENT = 4
+};
+
+enum { TSV_BF16 = 0, TSV_F32 = 1 };               /* element types */
+enum { TSV_METRIC_IP = 0, TSV_METRIC_COSINE = 1 }; /* cosine = IP over L2-normalised rows */
+
+typedef struct tsv_index tsv_index;
+
+TSV_API int tsv_abi_version(void);
+/* Message of the last failing call on this thread ("" if none). */
+TSV_API const char* tsv_last_error(void);
+/* Kernel launches issued by this library since load (for launch accounting). */
+TSV_API int64_t tsv_launch_count(void);
+
+/* ---- corpus arena (Ingestion side; reference: optimizer.py:125-156 Ingestion node,
+ *      executed through runtime.py:653-655 from profiles/default.json:27-46 vdb-ingest0) ---- */
+
+/* Device-resident bf16 arena of up to cap_rows rows of `dim` elements (dim % 8 == 0). */
+TSV_API int tsv_index_create(int device, int dim, int metric, int64_t cap_rows, tsv_index** out);
+/* Wrap an existing device matrix [n_rows, dim] bf16 (already normalised for cosine) without
+ * copying; the caller keeps it alive. Appends are rejected on a view. */
+TSV_API int tsv_index_create_view(int device, int dim, int metric, const void* rows_dev, int64_t n_rows,
+                          tsv_index** out);
+TSV_API int tsv_index_destroy(tsv_index* idx);
+/* Append n rows (bf16 or f32, normalised when metric is cosine); *first_row receives the arena
+ * row of the first appended row. Returns TSV_ERR_CAPACITY when the arena would overflow. */
+TSV_API int tsv_index_append(tsv_index* idx, const void* rows_dev, int src_dtype, int64_t n,
+                     int64_t* first_row, void* stream);
+/* Drop rows >= n (n <= current row count). */
+TSV_API int tsv_index_truncate(tsv_index* idx, int64_t n);
+TSV_API int64_t tsv_index_rows(const tsv_index* idx);
+TSV_API int tsv_index_dim(const tsv_index* idx);
+TSV_API int tsv_index_metric(const tsv_index* idx);
+TSV_API const void* tsv_index_data(const tsv_index* idx);
+
+/* Accumulated device time of the fused scan kernel (K1) launches issued while timing is on.
+ * Reading synchronises on the recorded events. */
+TSV_API int tsv_index_set_timing(tsv_index* idx, int enable);
+TSV_API int tsv_index_scan_time(tsv_index* idx, double* total_ms, int64_t* launches);
+
+/* ---- K1: Searching primitive over one contiguous row range (global corpus / shard).
+ * Replaces the PHASE_GENERAL latency lookup of runtime.py:653-655 for engine category
+ * "search" (engines.py:21, graph.py:47-59). q_dev: [B, dim] (bf16 or f32). Emitted id =
+ * arena row + id_offset. Outputs scores/ids [B, k]. k <= 32. ---- */
+TSV_API int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int64_t row_beg,
+               int64_t row_end, int32_t id_offset, float* scores_dev, int32_t* ids_dev,
+               void* stream);
+
+/* ---- K2: segmented Searching: queries [seg_q_beg[s], seg_q_beg[s+1]) search only arena rows
+ * [seg_row_beg[s], seg_row_end[s]) (per-query indexes built by each query's own Ingestion;
+ * workloads.py:95-97). Segment arrays are host memory. local_ids != 0 emits ids relative to
+ * the segment's first row. ---- */
+TSV_API int tsv_search_segmented(tsv_index* idx, const void* q_dev, int q_dtype, int nseg,
+                         const int32_t* seg_q_beg, const int64_t* seg_row_beg,
+                         const int64_t* seg_row_end, int k, int local_ids, float* scores_dev,
+                         int32_t* ids_dev, void* stream);
+
+/* ---- K3: Reranking primitive (optimizer.py:199-218): for each of B questions score the C
+ * candidate arena rows cand_ids_dev[b, :] (id < 0 ignored), drop duplicate ids, keep k. ---- */
+TSV_API int tsv_rerank(tsv_index* idx, const void* q_dev, int q_dtype, int B, const int32_t* cand_ids_dev,
+               int C, int k, float* scores_dev, int32_t* ids_dev, void* stream);
+
+/* ---- K4: merge `lists` sorted lists per query. Input layout [lists][B][kin]; output [B][kout].
+ * This is the Aggregate join of split Searching stages (optimizer.py:620-661,
+ * runtime.py:544-549) and the cross-shard merge after the all-gather. ---- */
+TSV_API int tsv_merge_topk(const float* in_scores, const int32_t* in_ids, int lists, int B, int kin,
+                   int kout, float* out_scores, int32_t* out_ids, void* stream);
+
+/* ---- K5: L2-normalise (normalize != 0) and cast rows to bf16. ---- */
+TSV_API int tsv_normalize_rows(const void* src_dev, int src_dtype, int64_t n, int dim, int normalize,
+                       void* dst_bf16_dev, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TSV_H_ */

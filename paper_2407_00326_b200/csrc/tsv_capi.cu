@@ -1,0 +1,571 @@
+// C ABI of the retrieval backend (declared in include/tsv.h). Host-side orchestration only:
+// argument checking, arena / workspace management, TMA descriptor encoding, work-item
+// planning and kernel launches. No computation happens on the host.
+#include "../../include/tsv.h"
+#include "tsv_kernels.cuh"
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<int64_t> g_launches{0};
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(TSV_ERR_DEVICE, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define TSV_CUDA(call, what)                      \
+  do {                                            \
+    cudaError_t e__ = (call);                     \
+    if (e__ != cudaSuccess) return cuda_fail(e__, what); \
+  } while (0)
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D bf16 row-major [rows, dim] map with a [box_rows, 64] box and 128 B swizzle.
+int encode_rows_map(CUtensorMap* map, const void* base, int64_t rows, int dim, int box_rows) {
+  auto fn = get_encode_fn();
+  if (fn == nullptr) return fail(TSV_ERR_DEVICE, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t gdim[2] = {static_cast<cuuint64_t>(dim), static_cast<cuuint64_t>(std::max<int64_t>(rows, 1))};
+  cuuint64_t gstride[1] = {static_cast<cuuint64_t>(dim) * 2};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(tsv::kBlockK), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estride[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), gdim, gstride,
+                  box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(TSV_ERR_DEVICE, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return TSV_OK;
+}
+
+template <typename T>
+struct DevBuf {
+  T* ptr = nullptr;
+  size_t cap = 0;  // elements
+  int ensure(size_t n) {
+    if (n <= cap) return TSV_OK;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMalloc(&ptr, std::max<size_t>(n, 1) * sizeof(T));
+    if (e != cudaSuccess) return cuda_fail(e, "workspace cudaMalloc");
+    cap = n;
+    return TSV_OK;
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+  }
+};
+
+struct Workspace {
+  DevBuf<uint16_t> qbuf;       // bf16 staged queries
+  DevBuf<float> part_s;        // partial lists
+  DevBuf<int32_t> part_i;
+  DevBuf<tsv::ScanItem> items;
+  std::vector<tsv::ScanItem> host_items;
+  void release() {
+    qbuf.release();
+    part_s.release();
+    part_i.release();
+    items.release();
+  }
+};
+
+struct TimedLaunch {
+  cudaEvent_t a, b;
+};
+
+}  // namespace
+
+struct tsv_index {
+  int device = 0;
+  int dim = 0;
+  int metric = TSV_METRIC_IP;
+  int64_t cap_rows = 0;
+  int64_t rows = 0;
+  bool owns = true;
+  void* arena = nullptr;
+  CUtensorMap tmap_c;
+  int num_sms = 148;
+  std::map<cudaStream_t, Workspace> ws;
+  bool timing = false;
+  std::vector<TimedLaunch> timed;
+  double timed_ms = 0.0;
+  int64_t timed_launches = 0;
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+int check_dim(int dim) {
+  if (dim <= 0 || dim % 8 != 0 || dim > 16384)
+    return fail(TSV_ERR_CONFIG, "dim must be a positive multiple of 8 (<= 16384), got %d", dim);
+  return TSV_OK;
+}
+
+int check_dtype(int dt) {
+  if (dt != TSV_BF16 && dt != TSV_F32) return fail(TSV_ERR_CONFIG, "unknown dtype %d", dt);
+  return TSV_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// bf16 query matrix the scan reads: the caller's buffer when it is already bf16 and needs no
+// normalisation, otherwise a staged copy converted (and normalised for cosine) by K5.
+int stage_queries(tsv_index* idx, Workspace& w, const void* q, int q_dtype, int64_t B,
+                  cudaStream_t st, const void** out) {
+  const bool need = q_dtype != TSV_BF16 || idx->metric == TSV_METRIC_COSINE || !aligned16(q);
+  if (!need) {
+    *out = q;
+    return TSV_OK;
+  }
+  int rc = w.qbuf.ensure(static_cast<size_t>(B) * idx->dim);
+  if (rc) return rc;
+  int e = tsv::launch_normalize(q, q_dtype == TSV_F32, B, idx->dim,
+                                idx->metric == TSV_METRIC_COSINE, w.qbuf.ptr, st);
+  if (e) return cuda_fail(static_cast<cudaError_t>(e), "normalize queries");
+  g_launches++;
+  *out = w.qbuf.ptr;
+  return TSV_OK;
+}
+
+int run_scan(tsv_index* idx, int mb, int kcap, const void* qb, int64_t B, tsv::ScanParams& p,
+             int grid, cudaStream_t st) {
+  CUtensorMap tq;
+  int rc = encode_rows_map(&tq, qb, B, idx->dim, tsv::kBlockM);
+  if (rc) return rc;
+  TimedLaunch tl{};
+  if (idx->timing) {
+    TSV_CUDA(cudaEventCreate(&tl.a), "cudaEventCreate");
+    TSV_CUDA(cudaEventCreate(&tl.b), "cudaEventCreate");
+    TSV_CUDA(cudaEventRecord(tl.a, st), "cudaEventRecord");
+  }
+  int e = tsv::launch_scan_topk(mb, kcap, tq, idx->tmap_c, p, grid, st);
+  if (e) return cuda_fail(static_cast<cudaError_t>(e), "scan_topk launch");
+  g_launches++;
+  if (idx->timing) {
+    TSV_CUDA(cudaEventRecord(tl.b, st), "cudaEventRecord");
+    idx->timed.push_back(tl);
+  }
+  return TSV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tsv_abi_version(void) { return TSV_ABI_VERSION; }
+const char* tsv_last_error(void) { return g_last_error.c_str(); }
+int64_t tsv_launch_count(void) { return g_launches.load(); }
+
+static int create_common(int device, int dim, int metric, tsv_index** out) {
+  if (out == nullptr) return fail(TSV_ERR_ARGUMENT, "out is null");
+  *out = nullptr;
+  int rc = check_dim(dim);
+  if (rc) return rc;
+  if (metric != TSV_METRIC_IP && metric != TSV_METRIC_COSINE)
+    return fail(TSV_ERR_CONFIG, "unknown metric %d", metric);
+  int ndev = 0;
+  TSV_CUDA(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+  if (device < 0 || device >= ndev) return fail(TSV_ERR_CONFIG, "bad device %d", device);
+  int major = 0;
+  TSV_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device),
+           "cudaDeviceGetAttribute");
+  if (major != 10) return fail(TSV_ERR_DEVICE, "device %d is not sm_100 (major=%d)", device, major);
+  return TSV_OK;
+}
+
+int tsv_index_create(int device, int dim, int metric, int64_t cap_rows, tsv_index** out) {
+  int rc = create_common(device, dim, metric, out);
+  if (rc) return rc;
+  if (cap_rows <= 0 || cap_rows > (int64_t(1) << 31) - 1)
+    return fail(TSV_ERR_CAPACITY, "cap_rows out of range: %lld", (long long)cap_rows);
+  DeviceGuard g(device);
+  auto* idx = new tsv_index();
+  idx->device = device;
+  idx->dim = dim;
+  idx->metric = metric;
+  idx->cap_rows = cap_rows;
+  cudaDeviceGetAttribute(&idx->num_sms, cudaDevAttrMultiProcessorCount, device);
+  cudaError_t e = cudaMalloc(&idx->arena, static_cast<size_t>(cap_rows) * dim * 2);
+  if (e != cudaSuccess) {
+    delete idx;
+    return cuda_fail(e, "arena cudaMalloc");
+  }
+  rc = encode_rows_map(&idx->tmap_c, idx->arena, cap_rows, dim, tsv::kBlockN);
+  if (rc) {
+    cudaFree(idx->arena);
+    delete idx;
+    return rc;
+  }
+  *out = idx;
+  return TSV_OK;
+}
+
+int tsv_index_create_view(int device, int dim, int metric, const void* rows_dev, int64_t n_rows,
+                          tsv_index** out) {
+  int rc = create_common(device, dim, metric, out);
+  if (rc) return rc;
+  if (rows_dev == nullptr || !aligned16(rows_dev))
+    return fail(TSV_ERR_ARGUMENT, "rows_dev must be a 16-byte aligned device pointer");
+  if (n_rows <= 0 || n_rows > (int64_t(1) << 31) - 1)
+    return fail(TSV_ERR_CAPACITY, "n_rows out of range: %lld", (long long)n_rows);
+  DeviceGuard g(device);
+  auto* idx = new tsv_index();
+  idx->device = device;
+  idx->dim = dim;
+  idx->metric = metric;
+  idx->cap_rows = n_rows;
+  idx->rows = n_rows;
+  idx->owns = false;
+  idx->arena = const_cast<void*>(rows_dev);
+  cudaDeviceGetAttribute(&idx->num_sms, cudaDevAttrMultiProcessorCount, device);
+  rc = encode_rows_map(&idx->tmap_c, idx->arena, n_rows, dim, tsv::kBlockN);
+  if (rc) {
+    delete idx;
+    return rc;
+  }
+  *out = idx;
+  return TSV_OK;
+}
+
+int tsv_index_destroy(tsv_index* idx) {
+  if (idx == nullptr) return TSV_OK;
+  DeviceGuard g(idx->device);
+  for (auto& kv : idx->ws) kv.second.release();
+  for (auto& t : idx->timed) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  if (idx->owns && idx->arena) cudaFree(idx->arena);
+  delete idx;
+  return TSV_OK;
+}
+
+int tsv_index_append(tsv_index* idx, const void* rows_dev, int src_dtype, int64_t n,
+                     int64_t* first_row, void* stream) {
+  if (idx == nullptr) return fail(TSV_ERR_ARGUMENT, "index is null");
+  if (!idx->owns) return fail(TSV_ERR_CONFIG, "cannot append to a view index");
+  int rc = check_dtype(src_dtype);
+  if (rc) return rc;
+  if (n < 0) return fail(TSV_ERR_CAPACITY, "negative row count");
+  if (idx->rows + n > idx->cap_rows)
+    return fail(TSV_ERR_CAPACITY, "arena overflow: %lld + %lld > %lld", (long long)idx->rows,
+                (long long)n, (long long)idx->cap_rows);
+  if (first_row) *first_row = idx->rows;
+  if (n == 0) return TSV_OK;
+  if (rows_dev == nullptr) return fail(TSV_ERR_ARGUMENT, "rows_dev is null");
+  DeviceGuard g(idx->device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  void* dst = static_cast<uint8_t*>(idx->arena) + static_cast<size_t>(idx->rows) * idx->dim * 2;
+  if (src_dtype == TSV_BF16 && idx->metric == TSV_METRIC_IP) {
+    TSV_CUDA(cudaMemcpyAsync(dst, rows_dev, static_cast<size_t>(n) * idx->dim * 2,
+                             cudaMemcpyDeviceToDevice, st),
+             "append copy");
+  } else {
+    int e = tsv::launch_normalize(rows_dev, src_dtype == TSV_F32, n, idx->dim,
+                                  idx->metric == TSV_METRIC_COSINE, dst, st);
+    if (e) return cuda_fail(static_cast<cudaError_t>(e), "normalize rows");
+    g_launches++;
+  }
+  idx->rows += n;
+  return TSV_OK;
+}
+
+int tsv_index_truncate(tsv_index* idx, int64_t n) {
+  if (idx == nullptr) return fail(TSV_ERR_ARGUMENT, "index is null");
+  if (n < 0 || n > idx->rows) return fail(TSV_ERR_CAPACITY, "bad truncate length");
+  if (!idx->owns) return fail(TSV_ERR_CONFIG, "cannot truncate a view index");
+  idx->rows = n;
+  return TSV_OK;
+}
+
+int64_t tsv_index_rows(const tsv_index* idx) { return idx ? idx->rows : -1; }
+int tsv_index_dim(const tsv_index* idx) { return idx ? idx->dim : -1; }
+int tsv_index_metric(const tsv_index* idx) { return idx ? idx->metric : -1; }
+const void* tsv_index_data(const tsv_index* idx) { return idx ? idx->arena : nullptr; }
+
+int tsv_index_set_timing(tsv_index* idx, int enable) {
+  if (idx == nullptr) return fail(TSV_ERR_ARGUMENT, "index is null");
+  idx->timing = enable != 0;
+  return TSV_OK;
+}
+
+int tsv_index_scan_time(tsv_index* idx, double* total_ms, int64_t* launches) {
+  if (idx == nullptr) return fail(TSV_ERR_ARGUMENT, "index is null");
+  DeviceGuard g(idx->device);
+  for (auto& t : idx->timed) {
+    TSV_CUDA(cudaEventSynchronize(t.b), "cudaEventSynchronize");
+    float ms = 0.f;
+    TSV_CUDA(cudaEventElapsedTime(&ms, t.a, t.b), "cudaEventElapsedTime");
+    idx->timed_ms += ms;
+    idx->timed_launches++;
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  idx->timed.clear();
+  if (total_ms) *total_ms = idx->timed_ms;
+  if (launches) *launches = idx->timed_launches;
+  idx->timed_ms = 0.0;
+  idx->timed_launches = 0;
+  return TSV_OK;
+}
+
+int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int64_t row_beg,
+               int64_t row_end, int32_t id_offset, float* scores_dev, int32_t* ids_dev,
+               void* stream) {
+  if (idx == nullptr) return fail(TSV_ERR_ARGUMENT, "index is null");
+  int rc = check_dtype(q_dtype);
+  if (rc) return rc;
+  if (B <= 0) return fail(TSV_ERR_CAPACITY, "empty batch");
+  if (k <= 0) return fail(TSV_ERR_CONFIG, "k must be >= 1");
+  const int kcap = tsv::scan_kcap_for(k);
+  if (kcap == 0) return fail(TSV_ERR_CONFIG, "k=%d exceeds the supported maximum (32)", k);
+  if (q_dev == nullptr || scores_dev == nullptr || ids_dev == nullptr)
+    return fail(TSV_ERR_ARGUMENT, "null buffer");
+  if (row_beg < 0 || row_end > idx->rows || row_beg > row_end)
+    return fail(TSV_ERR_CAPACITY, "row range [%lld, %lld) outside arena of %lld rows",
+                (long long)row_beg, (long long)row_end, (long long)idx->rows);
+  DeviceGuard g(idx->device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  Workspace& w = idx->ws[st];
+
+  const void* qb = nullptr;
+  rc = stage_queries(idx, w, q_dev, q_dtype, B, st, &qb);
+  if (rc) return rc;
+
+  const int mb = B > tsv::kBlockM ? 2 : 1;
+  const int qg = mb * tsv::kBlockM;
+  const int nqg = (B + qg - 1) / qg;
+  const int64_t n = row_end - row_beg;
+  const int64_t tiles = std::max<int64_t>(1, (n + tsv::kBlockN - 1) / tsv::kBlockN);
+  int R = std::max(1, idx->num_sms / nqg);
+  R = static_cast<int>(std::min<int64_t>(R, tiles));
+  const int num_items = nqg * R;
+  const int grid = std::min(num_items, idx->num_sms);
+
+  tsv::ScanParams p{};
+  p.items = nullptr;
+  p.num_items = num_items;
+  p.B = B;
+  p.R = R;
+  p.id_offset = id_offset;
+  p.row_beg = row_beg;
+  p.row_end = row_end;
+  p.num_kb = (idx->dim + tsv::kBlockK - 1) / tsv::kBlockK;
+  if (R == 1) {
+    p.out_k = k;
+    p.out_scores = scores_dev;
+    p.out_ids = ids_dev;
+    return run_scan(idx, mb, kcap, qb, B, p, grid, st);
+  }
+  p.out_k = kcap;
+  rc = w.part_s.ensure(static_cast<size_t>(R) * B * kcap);
+  if (rc) return rc;
+  rc = w.part_i.ensure(static_cast<size_t>(R) * B * kcap);
+  if (rc) return rc;
+  p.out_scores = w.part_s.ptr;
+  p.out_ids = w.part_i.ptr;
+  rc = run_scan(idx, mb, kcap, qb, B, p, grid, st);
+  if (rc) return rc;
+  int e = tsv::launch_merge_topk(w.part_s.ptr, w.part_i.ptr, R, B, kcap, B, k, scores_dev, ids_dev,
+                                 st);
+  if (e) return cuda_fail(static_cast<cudaError_t>(e), "merge launch");
+  g_launches++;
+  return TSV_OK;
+}
+
+int tsv_search_segmented(tsv_index* idx, const void* q_dev, int q_dtype, int nseg,
+                         const int32_t* seg_q_beg, const int64_t* seg_row_beg,
+                         const int64_t* seg_row_end, int k, int local_ids, float* scores_dev,
+                         int32_t* ids_dev, void* stream) {
+  if (idx == nullptr) return fail(TSV_ERR_ARGUMENT, "index is null");
+  int rc = check_dtype(q_dtype);
+  if (rc) return rc;
+  if (nseg <= 0) return fail(TSV_ERR_CAPACITY, "empty batch");
+  if (seg_q_beg == nullptr || seg_row_beg == nullptr || seg_row_end == nullptr)
+    return fail(TSV_ERR_ARGUMENT, "null segment table");
+  if (k <= 0) return fail(TSV_ERR_CONFIG, "k must be >= 1");
+  const int kcap = tsv::scan_kcap_for(k);
+  if (kcap == 0) return fail(TSV_ERR_CONFIG, "k=%d exceeds the supported maximum (32)", k);
+  const int B = seg_q_beg[nseg] - seg_q_beg[0];
+  if (seg_q_beg[0] != 0 || B <= 0) return fail(TSV_ERR_CAPACITY, "bad query offsets");
+  int max_q = 0;
+  int64_t max_rows = 0;
+  for (int s = 0; s < nseg; ++s) {
+    if (seg_q_beg[s + 1] < seg_q_beg[s]) return fail(TSV_ERR_ARGUMENT, "query offsets decrease");
+    if (seg_row_beg[s] < 0 || seg_row_end[s] > idx->rows || seg_row_beg[s] > seg_row_end[s])
+      return fail(TSV_ERR_CAPACITY, "segment %d row range outside arena", s);
+    max_q = std::max(max_q, seg_q_beg[s + 1] - seg_q_beg[s]);
+    max_rows = std::max<int64_t>(max_rows, seg_row_end[s] - seg_row_beg[s]);
+  }
+  DeviceGuard g(idx->device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  Workspace& w = idx->ws[st];
+  const void* qb = nullptr;
+  rc = stage_queries(idx, w, q_dev, q_dtype, B, st, &qb);
+  if (rc) return rc;
+
+  const int mb = max_q > tsv::kBlockM ? 2 : 1;
+  const int qg = mb * tsv::kBlockM;
+  int units = 0;
+  for (int s = 0; s < nseg; ++s) units += (seg_q_beg[s + 1] - seg_q_beg[s] + qg - 1) / qg;
+  const int64_t max_tiles = std::max<int64_t>(1, (max_rows + tsv::kBlockN - 1) / tsv::kBlockN);
+  int R = std::max(1, idx->num_sms / std::max(1, units));
+  R = static_cast<int>(std::min<int64_t>(R, max_tiles));
+
+  auto& hi = w.host_items;
+  hi.clear();
+  for (int s = 0; s < nseg; ++s) {
+    const int q0 = seg_q_beg[s], q1 = seg_q_beg[s + 1];
+    const int64_t rb = seg_row_beg[s], re = seg_row_end[s];
+    const int64_t tiles = (re - rb + tsv::kBlockN - 1) / tsv::kBlockN;
+    for (int qs = q0; qs < q1; qs += qg) {
+      for (int r = 0; r < R; ++r) {
+        tsv::ScanItem it{};
+        it.q_begin = qs;
+        it.q_count = std::min(qg, q1 - qs);
+        it.row_begin = rb + (tiles * r / R) * tsv::kBlockN;
+        it.row_end = std::min(re, rb + (tiles * (r + 1) / R) * tsv::kBlockN);
+        if (it.row_end < it.row_begin) it.row_end = it.row_begin;
+        it.out_row = static_cast<int64_t>(r) * B + qs;
+        it.id_offset = local_ids ? static_cast<int32_t>(-rb) : 0;
+        hi.push_back(it);
+      }
+    }
+  }
+  rc = w.items.ensure(hi.size());
+  if (rc) return rc;
+  TSV_CUDA(cudaMemcpyAsync(w.items.ptr, hi.data(), hi.size() * sizeof(tsv::ScanItem),
+                           cudaMemcpyHostToDevice, st),
+           "items upload");
+  tsv::ScanParams p{};
+  p.items = w.items.ptr;
+  p.num_items = static_cast<int>(hi.size());
+  p.num_kb = (idx->dim + tsv::kBlockK - 1) / tsv::kBlockK;
+  const int grid = std::min(p.num_items, idx->num_sms);
+  if (R == 1) {
+    p.out_k = k;
+    p.out_scores = scores_dev;
+    p.out_ids = ids_dev;
+    return run_scan(idx, mb, kcap, qb, B, p, grid, st);
+  }
+  p.out_k = kcap;
+  rc = w.part_s.ensure(static_cast<size_t>(R) * B * kcap);
+  if (rc) return rc;
+  rc = w.part_i.ensure(static_cast<size_t>(R) * B * kcap);
+  if (rc) return rc;
+  p.out_scores = w.part_s.ptr;
+  p.out_ids = w.part_i.ptr;
+  rc = run_scan(idx, mb, kcap, qb, B, p, grid, st);
+  if (rc) return rc;
+  int e = tsv::launch_merge_topk(w.part_s.ptr, w.part_i.ptr, R, B, kcap, B, k, scores_dev, ids_dev,
+                                 st);
+  if (e) return cuda_fail(static_cast<cudaError_t>(e), "merge launch");
+  g_launches++;
+  return TSV_OK;
+}
+
+int tsv_rerank(tsv_index* idx, const void* q_dev, int q_dtype, int B, const int32_t* cand_ids_dev,
+               int C, int k, float* scores_dev, int32_t* ids_dev, void* stream) {
+  if (idx == nullptr) return fail(TSV_ERR_ARGUMENT, "index is null");
+  int rc = check_dtype(q_dtype);
+  if (rc) return rc;
+  if (B <= 0 || C <= 0) return fail(TSV_ERR_CAPACITY, "empty batch");
+  if (C > 8192) return fail(TSV_ERR_CAPACITY, "candidate_count %d exceeds 8192", C);
+  if (k <= 0) return fail(TSV_ERR_CONFIG, "k must be >= 1");
+  if (q_dev == nullptr || cand_ids_dev == nullptr || scores_dev == nullptr || ids_dev == nullptr)
+    return fail(TSV_ERR_ARGUMENT, "null buffer");
+  DeviceGuard g(idx->device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const void* q = q_dev;
+  int q_f32 = q_dtype == TSV_F32;
+  if (idx->metric == TSV_METRIC_COSINE) {
+    Workspace& w = idx->ws[st];
+    rc = stage_queries(idx, w, q_dev, q_dtype, B, st, &q);
+    if (rc) return rc;
+    q_f32 = 0;
+  }
+  int e = tsv::launch_rerank(idx->arena, idx->rows, idx->dim, q, q_f32, B, cand_ids_dev, C, k,
+                             scores_dev, ids_dev, st);
+  if (e) return cuda_fail(static_cast<cudaError_t>(e), "rerank launch");
+  g_launches++;
+  return TSV_OK;
+}
+
+int tsv_merge_topk(const float* in_scores, const int32_t* in_ids, int lists, int B, int kin,
+                   int kout, float* out_scores, int32_t* out_ids, void* stream) {
+  if (lists <= 0 || B <= 0 || kin <= 0 || kout <= 0) return fail(TSV_ERR_CAPACITY, "empty merge");
+  if (static_cast<int64_t>(lists) * kin > 8192)
+    return fail(TSV_ERR_CAPACITY, "merge of %d x %d candidates exceeds 8192", lists, kin);
+  if (!in_scores || !in_ids || !out_scores || !out_ids) return fail(TSV_ERR_ARGUMENT, "null buffer");
+  int e = tsv::launch_merge_topk(in_scores, in_ids, lists, B, kin, B, kout, out_scores, out_ids,
+                                 reinterpret_cast<cudaStream_t>(stream));
+  if (e) return cuda_fail(static_cast<cudaError_t>(e), "merge launch");
+  g_launches++;
+  return TSV_OK;
+}
+
+int tsv_normalize_rows(const void* src_dev, int src_dtype, int64_t n, int dim, int normalize,
+                       void* dst_bf16_dev, void* stream) {
+  int rc = check_dtype(src_dtype);
+  if (rc) return rc;
+  rc = check_dim(dim);
+  if (rc) return rc;
+  if (n < 0) return fail(TSV_ERR_CAPACITY, "negative row count");
+  if (n == 0) return TSV_OK;
+  if (!src_dev || !dst_bf16_dev) return fail(TSV_ERR_ARGUMENT, "null buffer");
+  int e = tsv::launch_normalize(src_dev, src_dtype == TSV_F32, n, dim, normalize, dst_bf16_dev,
+                                reinterpret_cast<cudaStream_t>(stream));
+  if (e) return cuda_fail(static_cast<cudaError_t>(e), "normalize launch");
+  g_launches++;
+  return TSV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,61 @@
+// Shared declarations for the retrieval kernels (K1 scan+top-k, K3 rerank, K4 merge, K5 normalize).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tsv {
+
+// Geometry of the fused scan (K1). Queries sit on the UMMA M side (one TMEM lane per query),
+// corpus rows on the N side; K is the embedding dimension, streamed 64 bf16 (one 128 B swizzle
+// row) per k-block.
+constexpr int kBlockM = 128;   // queries per UMMA tile
+constexpr int kBlockN = 128;   // corpus rows per tile
+constexpr int kBlockK = 64;    // bf16 elements per k-block (128 B rows, SWIZZLE_128B)
+constexpr int kNumNonEpiWarps = 4;  // warp 0 TMA, warp 1 MMA, warp 2 TMEM alloc, warp 3 idle
+
+// One unit of scan work: a block of up to MB*128 consecutive queries against a contiguous
+// corpus row range. Each query of the item produces one sorted partial list of KCAP
+// (score, id) pairs at partial row `out_row + local_query`.
+struct ScanItem {
+  int32_t q_begin;
+  int32_t q_count;
+  int64_t row_begin;
+  int64_t row_end;
+  int64_t out_row;
+  int32_t id_offset;  // emitted id = corpus row + id_offset
+  int32_t pad_;
+};
+
+struct ScanParams {
+  const ScanItem* items;  // nullptr: implicit (query-group x range) grid
+  int32_t num_items;
+  // implicit-grid description (items == nullptr)
+  int32_t B;          // number of queries
+  int32_t R;          // corpus ranges per query group
+  int32_t id_offset;  // emitted id = row + id_offset
+  int64_t row_beg;    // scanned rows [row_beg, row_end)
+  int64_t row_end;
+  int32_t num_kb;     // ceil(dim / 64)
+  int32_t out_k;      // entries written per partial row (<= KCAP)
+  float* out_scores;  // [rows][out_k]
+  int32_t* out_ids;
+};
+
+// Host-side launchers (return cudaError_t as int).
+int launch_scan_topk(int mb, int kcap, const CUtensorMap& tmap_q, const CUtensorMap& tmap_c,
+                     const ScanParams& p, int grid, cudaStream_t stream);
+int scan_kcap_for(int k);  // smallest supported list capacity >= k (0 if unsupported)
+
+int launch_merge_topk(const float* in_s, const int32_t* in_id, int lists, int B, int kin,
+                      int64_t list_stride_rows, int kout, float* out_s, int32_t* out_id,
+                      cudaStream_t stream);
+
+int launch_rerank(const void* arena, int64_t nrows, int dim, const void* q, int q_is_f32,
+                  int B, const int32_t* cand, int C, int k, float* out_s, int32_t* out_id,
+                  cudaStream_t stream);
+
+int launch_normalize(const void* src, int src_is_f32, int64_t n, int dim, int do_normalize,
+                     void* dst_bf16, cudaStream_t stream);
+
+}  // namespace tsv

@@ -1,0 +1,232 @@
+// K4 (top-k merge), K3 (gather-rerank with dedup) and K5 (row normalisation + bf16 cast).
+//
+// K4 is the device-side counterpart of the point where Teola joins pipelined search stages
+// (reference: pkg/src/teola_sim/optimizer.py:620-661 `_insert_aggregates`; executed
+// instantly on the orchestrator at pkg/src/teola_sim/runtime.py:544-549) and of the
+// cross-shard merge after the all-gather in sharded mode.
+// K3 executes a Reranking primitive (reference: optimizer.py:199-218 decomposition; executed by
+// runtime.py:653-655 from the `rerank0` table, profiles/default.json:71-94).
+//
+// Ordering everywhere: (score desc, id asc); padding entries are (-inf, -1).
+#include "tsv_kernels.cuh"
+
+#include <cuda_bf16.h>
+#include <cfloat>
+
+namespace tsv {
+namespace {
+
+// 64-bit sort key: high word = order-preserving image of the fp32 score, low word = bitwise
+// complement of the id so that smaller ids sort first among equal scores when the keys are
+// sorted descending. Padding (id == -1) maps to low word 0, i.e. last among equal scores.
+__device__ __forceinline__ uint64_t make_key(float s, int32_t id) {
+  uint32_t u = __float_as_uint(s);
+  u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+  return (static_cast<uint64_t>(u) << 32) | static_cast<uint32_t>(~static_cast<uint32_t>(id));
+}
+__device__ __forceinline__ float key_score(uint64_t k) {
+  uint32_t u = static_cast<uint32_t>(k >> 32);
+  u = (u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u;
+  return __uint_as_float(u);
+}
+__device__ __forceinline__ int32_t key_id(uint64_t k) {
+  return static_cast<int32_t>(~static_cast<uint32_t>(k & 0xFFFFFFFFu));
+}
+__device__ __forceinline__ uint64_t pad_key() { return make_key(-INFINITY, -1); }
+
+// In-place descending bitonic sort of n (power of two) keys in shared memory.
+__device__ void bitonic_sort_desc(uint64_t* keys, int n) {
+  for (int size = 2; size <= n; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      __syncthreads();
+      for (int i = threadIdx.x; i < (n >> 1); i += blockDim.x) {
+        const int lo = 2 * i - (i & (stride - 1));
+        const int hi = lo + stride;
+        const bool desc = ((lo & size) == 0);
+        const uint64_t a = keys[lo], b = keys[hi];
+        if ((a < b) == desc) {
+          keys[lo] = b;
+          keys[hi] = a;
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ int pow2_ceil(int n) {
+  int p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+
+// One block per query: gather lists * kin candidates, sort, keep kout.
+__global__ void merge_topk_kernel(const float* __restrict__ in_s, const int32_t* __restrict__ in_id,
+                                  int lists, int B, int kin, int64_t list_stride_rows, int kout,
+                                  float* __restrict__ out_s, int32_t* __restrict__ out_id) {
+  extern __shared__ uint64_t keys[];
+  const int b = blockIdx.x;
+  const int n = lists * kin;
+  const int np = pow2_ceil(n);
+  for (int i = threadIdx.x; i < np; i += blockDim.x) {
+    uint64_t key = pad_key();
+    if (i < n) {
+      const int r = i / kin;
+      const int j = i - r * kin;
+      const int64_t off = (static_cast<int64_t>(r) * list_stride_rows + b) * kin + j;
+      const int32_t id = in_id[off];
+      if (id >= 0) key = make_key(in_s[off], id);
+    }
+    keys[i] = key;
+  }
+  bitonic_sort_desc(keys, np);
+  for (int j = threadIdx.x; j < kout; j += blockDim.x) {
+    const uint64_t key = j < np ? keys[j] : pad_key();
+    const int32_t id = key_id(key);
+    out_s[static_cast<int64_t>(b) * kout + j] = id < 0 ? -INFINITY : key_score(key);
+    out_id[static_cast<int64_t>(b) * kout + j] = id;
+  }
+}
+
+// One block per question: score C candidate rows (gathered by id from the arena) against the
+// question vector, drop duplicate ids, keep the best k.
+template <int kThreads>
+__global__ void __launch_bounds__(kThreads) rerank_kernel(
+    const __nv_bfloat16* __restrict__ arena, int64_t nrows, int dim, const void* __restrict__ q,
+    int q_is_f32, const int32_t* __restrict__ cand, int C, int k, float* __restrict__ out_s,
+    int32_t* __restrict__ out_id) {
+  extern __shared__ uint8_t sm[];
+  float* qv = reinterpret_cast<float*>(sm);                       // dim floats
+  uint64_t* keys = reinterpret_cast<uint64_t*>(sm + ((dim * 4 + 15) & ~15));
+  const int b = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kWarps = kThreads / 32;
+
+  for (int d = threadIdx.x; d < dim; d += kThreads) {
+    qv[d] = q_is_f32 ? reinterpret_cast<const float*>(q)[static_cast<int64_t>(b) * dim + d]
+                     : __bfloat162float(
+                           reinterpret_cast<const __nv_bfloat16*>(q)[static_cast<int64_t>(b) * dim + d]);
+  }
+  const int np = pow2_ceil(C);
+  for (int i = threadIdx.x; i < np; i += kThreads) keys[i] = pad_key();
+  __syncthreads();
+
+  const int chunks = dim >> 3;  // 8 bf16 (16 B) per chunk; dim % 8 == 0 enforced by the host
+  for (int c = warp; c < C; c += kWarps) {
+    const int32_t id = cand[static_cast<int64_t>(b) * C + c];
+    if (id < 0 || id >= nrows) continue;  // warp-uniform
+    const uint4* row = reinterpret_cast<const uint4*>(arena + static_cast<int64_t>(id) * dim);
+    float acc = 0.f;
+    for (int ch = lane; ch < chunks; ch += 32) {
+      const uint4 raw = __ldg(row + ch);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+      const float* qq = qv + ch * 8;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const float2 f = __bfloat1622float2(h[t]);
+        acc = fmaf(f.x, qq[2 * t], acc);
+        acc = fmaf(f.y, qq[2 * t + 1], acc);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) keys[c] = make_key(acc, id);
+  }
+  bitonic_sort_desc(keys, np);
+  // Dedup: duplicates of one id carry identical scores, so they are adjacent after the sort.
+  if (threadIdx.x == 0) {
+    int w = 0;
+    int32_t last = -2;
+    for (int i = 0; i < np && w < k; ++i) {
+      const int32_t id = key_id(keys[i]);
+      if (id < 0) break;
+      if (id == last) continue;
+      last = id;
+      out_s[static_cast<int64_t>(b) * k + w] = key_score(keys[i]);
+      out_id[static_cast<int64_t>(b) * k + w] = id;
+      ++w;
+    }
+    for (; w < k; ++w) {
+      out_s[static_cast<int64_t>(b) * k + w] = -INFINITY;
+      out_id[static_cast<int64_t>(b) * k + w] = -1;
+    }
+  }
+}
+
+// One warp per row: optional L2 normalisation (fp32 math) and cast to bf16.
+__global__ void normalize_kernel(const void* __restrict__ src, int src_is_f32, int64_t n, int dim,
+                                 int do_normalize, __nv_bfloat16* __restrict__ dst) {
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  const float* sf = reinterpret_cast<const float*>(src) + row * dim;
+  const __nv_bfloat16* sb = reinterpret_cast<const __nv_bfloat16*>(src) + row * dim;
+  float ss = 0.f;
+  if (do_normalize) {
+    for (int d = lane; d < dim; d += 32) {
+      const float x = src_is_f32 ? sf[d] : __bfloat162float(sb[d]);
+      ss = fmaf(x, x, ss);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  }
+  const float scale = (do_normalize && ss > 0.f) ? rsqrtf(ss) : 1.f;
+  __nv_bfloat16* out = dst + row * dim;
+  for (int d = lane; d < dim; d += 32) {
+    const float x = src_is_f32 ? sf[d] : __bfloat162float(sb[d]);
+    out[d] = __float2bfloat16_rn(x * scale);
+  }
+}
+
+}  // namespace
+
+int launch_merge_topk(const float* in_s, const int32_t* in_id, int lists, int B, int kin,
+                      int64_t list_stride_rows, int kout, float* out_s, int32_t* out_id,
+                      cudaStream_t stream) {
+  if (B <= 0) return 0;
+  int np = 1;
+  while (np < lists * kin) np <<= 1;
+  if (np > 8192) return static_cast<int>(cudaErrorInvalidValue);
+  const size_t smem = static_cast<size_t>(np) * sizeof(uint64_t);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(merge_topk_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return static_cast<int>(e);
+  }
+  const int threads = np >= 512 ? 256 : 128;
+  merge_topk_kernel<<<B, threads, smem, stream>>>(in_s, in_id, lists, B, kin, list_stride_rows,
+                                                  kout, out_s, out_id);
+  return static_cast<int>(cudaGetLastError());
+}
+
+int launch_rerank(const void* arena, int64_t nrows, int dim, const void* q, int q_is_f32, int B,
+                  const int32_t* cand, int C, int k, float* out_s, int32_t* out_id,
+                  cudaStream_t stream) {
+  if (B <= 0) return 0;
+  int np = 1;
+  while (np < C) np <<= 1;
+  const size_t smem = ((static_cast<size_t>(dim) * 4 + 15) & ~size_t(15)) + np * sizeof(uint64_t);
+  if (smem > 200 * 1024) return static_cast<int>(cudaErrorInvalidValue);
+  constexpr int kThreads = 256;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(rerank_kernel<kThreads>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return static_cast<int>(e);
+  }
+  rerank_kernel<kThreads><<<B, kThreads, smem, stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(arena), nrows, dim, q, q_is_f32, cand, C, k, out_s,
+      out_id);
+  return static_cast<int>(cudaGetLastError());
+}
+
+int launch_normalize(const void* src, int src_is_f32, int64_t n, int dim, int do_normalize,
+                     void* dst_bf16, cudaStream_t stream) {
+  if (n <= 0) return 0;
+  constexpr int kWarps = 8;
+  const int64_t blocks = (n + kWarps - 1) / kWarps;
+  normalize_kernel<<<static_cast<unsigned>(blocks), kWarps * 32, 0, stream>>>(
+      src, src_is_f32, n, dim, do_normalize, reinterpret_cast<__nv_bfloat16*>(dst_bf16));
+  return static_cast<int>(cudaGetLastError());
+}
+
+}  // namespace tsv

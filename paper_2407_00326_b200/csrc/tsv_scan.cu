@@ -1,0 +1,324 @@
+// K1 / K2: fused inner-product scan + per-query top-k on sm_100a.
+//
+// Replaces the latency lookup that Teola's simulator performs for a Searching batch
+// (reference: pkg/src/teola_sim/runtime.py:653-655 `_execute` PHASE_GENERAL branch, whose
+// table lives in pkg/src/teola_sim/profiles/default.json:47-70 `vdb-search0`).
+//
+// Design (one persistent CTA per SM, warp-specialised):
+//   warp 0      TMA producer: per k-block, MB query tiles [128 x 64] + one corpus tile
+//               [128 x 64] bf16, SWIZZLE_128B, into a STAGES-deep smem ring.
+//   warp 1      MMA issuer: tcgen05.mma.cta_group::1.kind::f16, M=128 (queries) x N=128
+//               (corpus rows) x K=16, fp32 accumulators in TMEM, double-buffered
+//               (2 x MB x 128 columns).
+//   warps 4..   epilogue: one thread per query (= TMEM lane). tcgen05.ld 32 columns at a
+//               time, max-reduce, and only if the chunk beats the running threshold insert
+//               into a register-resident sorted list of KCAP (score, id) pairs.
+// The score matrix never leaves TMEM. Each CTA emits one sorted partial list per query per
+// work item; K4 (tsv_merge.cu) merges the partial lists of all corpus ranges.
+#include "tsv_kernels.cuh"
+#include "tsv_ptx.cuh"
+
+#include <cfloat>
+
+namespace tsv {
+namespace {
+
+template <int MB>
+struct ScanCfg {
+  static constexpr int kABytes = kBlockM * kBlockK * 2;            // 16 KB
+  static constexpr int kBBytes = kBlockN * kBlockK * 2;            // 16 KB
+  static constexpr int kStageBytes = MB * kABytes + kBBytes;
+  static constexpr int kStages = MB == 2 ? 4 : 6;
+  static constexpr int kAccCols = MB * kBlockN;                    // per accumulator buffer
+  static constexpr int kTmemCols = 2 * kAccCols;                   // double buffered
+  static constexpr int kEpiWarps = MB * 4;
+  static constexpr int kThreads = (kNumNonEpiWarps + kEpiWarps) * 32;
+  static constexpr int kBarBytes = 256;
+  static constexpr int kSmemBytes = kStages * kStageBytes + kBarBytes + 1024;  // + align slack
+};
+
+__device__ __forceinline__ void resolve_item(const ScanParams& p, int i, ScanItem& it, int qg_size) {
+  if (p.items != nullptr) {
+    it = p.items[i];
+    return;
+  }
+  const int qg = i / p.R;
+  const int r = i - qg * p.R;
+  it.q_begin = qg * qg_size;
+  it.q_count = min(qg_size, p.B - it.q_begin);
+  const int64_t n = p.row_end - p.row_beg;
+  const int64_t tiles = (n + kBlockN - 1) / kBlockN;
+  const int64_t t0 = tiles * r / p.R;
+  const int64_t t1 = tiles * (r + 1) / p.R;
+  it.row_begin = p.row_beg + t0 * kBlockN;
+  it.row_end = min(p.row_end, p.row_beg + t1 * kBlockN);
+  if (it.row_end < it.row_begin) it.row_end = it.row_begin;
+  it.out_row = static_cast<int64_t>(r) * p.B + it.q_begin;
+  it.id_offset = p.id_offset;
+}
+
+// Insert (x, xi) into a list sorted by (score desc, id asc). Precondition: x > s[K-1].
+// Elements with score >= x keep their place (they were seen earlier, so their ids are
+// smaller), the rest shift down one slot and the last one drops out.
+template <int K>
+__device__ __forceinline__ void list_insert(float (&s)[K], int32_t (&id)[K], float x, int32_t xi) {
+#pragma unroll
+  for (int i = K - 1; i > 0; --i) {
+    const bool keep = s[i] >= x;
+    const bool prev_keep = s[i - 1] >= x;
+    const float ns = keep ? s[i] : (prev_keep ? x : s[i - 1]);
+    const int32_t ni = keep ? id[i] : (prev_keep ? xi : id[i - 1]);
+    s[i] = ns;
+    id[i] = ni;
+  }
+  if (!(s[0] >= x)) {
+    s[0] = x;
+    id[0] = xi;
+  }
+}
+
+template <int K>
+__device__ __forceinline__ void scan_chunk(const uint32_t (&v)[32], float (&s)[K], int32_t (&id)[K],
+                                           int32_t id0, int valid) {
+  float m0 = fmaxf(__uint_as_float(v[0]), __uint_as_float(v[1]));
+  float m1 = fmaxf(__uint_as_float(v[2]), __uint_as_float(v[3]));
+#pragma unroll
+  for (int j = 4; j < 32; j += 4) {
+    m0 = fmaxf(m0, fmaxf(__uint_as_float(v[j]), __uint_as_float(v[j + 1])));
+    m1 = fmaxf(m1, fmaxf(__uint_as_float(v[j + 2]), __uint_as_float(v[j + 3])));
+  }
+  const float m = fmaxf(m0, m1);
+  if (m > s[K - 1]) {
+#pragma unroll 1
+    for (int j = 0; j < 32; ++j) {
+      const float x = __uint_as_float(v[j]);
+      if (x > s[K - 1] && j < valid) list_insert<K>(s, id, x, id0 + j);
+    }
+  }
+}
+
+template <int MB, int KCAP>
+__global__ void __launch_bounds__(ScanCfg<MB>::kThreads, 1)
+    scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_q,
+                     const __grid_constant__ CUtensorMap tmap_c, const ScanParams p) {
+  using Cfg = ScanCfg<MB>;
+  constexpr int kStages = Cfg::kStages;
+  constexpr int kQG = MB * kBlockM;
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * Cfg::kStageBytes);
+  uint64_t* empty_bar = full_bar + kStages;
+  uint64_t* tfull_bar = empty_bar + kStages;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&tmap_q);
+    ptx::tma_prefetch_desc(&tmap_c);
+    for (int s = 0; s < kStages; ++s) {
+      ptx::mbar_init(&full_bar[s], 1);
+      ptx::mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&tfull_bar[b], 1);
+      ptx::mbar_init(&tempty_bar[b], Cfg::kEpiWarps * 32);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) {
+    ptx::tmem_alloc(tmem_slot, Cfg::kTmemCols);
+    ptx::tmem_relinquish();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int num_items = p.num_items;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const uint64_t pol_q = ptx::policy_evict_last();
+      const uint64_t pol_c = ptx::policy_evict_normal();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int i = blockIdx.x; i < num_items; i += gridDim.x) {
+        ScanItem it;
+        resolve_item(p, i, it, kQG);
+        const int64_t ntiles = (it.row_end - it.row_begin + kBlockN - 1) / kBlockN;
+        for (int64_t t = 0; t < ntiles; ++t) {
+          const int32_t row0 = static_cast<int32_t>(it.row_begin + t * kBlockN);
+          for (int kb = 0; kb < p.num_kb; ++kb) {
+            ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+            uint8_t* st = smem + stage * Cfg::kStageBytes;
+            ptx::mbar_arrive_expect_tx(&full_bar[stage], Cfg::kStageBytes);
+#pragma unroll
+            for (int mb = 0; mb < MB; ++mb)
+              ptx::tma_load_2d(st + mb * Cfg::kABytes, &tmap_q, &full_bar[stage], kb * kBlockK,
+                               it.q_begin + mb * kBlockM, pol_q);
+            ptx::tma_load_2d(st + MB * Cfg::kABytes, &tmap_c, &full_bar[stage], kb * kBlockK, row0,
+                             pol_c);
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(kBlockM, kBlockN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int abuf = 0;
+      uint32_t aphase = 0;
+      for (int i = blockIdx.x; i < num_items; i += gridDim.x) {
+        ScanItem it;
+        resolve_item(p, i, it, kQG);
+        const int64_t ntiles = (it.row_end - it.row_begin + kBlockN - 1) / kBlockN;
+        for (int64_t t = 0; t < ntiles; ++t) {
+          ptx::mbar_wait(&tempty_bar[abuf], aphase ^ 1);
+          ptx::tc_fence_after();
+          const uint32_t d0 = tmem_base + abuf * Cfg::kAccCols;
+          for (int kb = 0; kb < p.num_kb; ++kb) {
+            ptx::mbar_wait(&full_bar[stage], phase);
+            ptx::tc_fence_after();
+            const uint32_t st = ptx::smem_u32(smem + stage * Cfg::kStageBytes);
+            const uint64_t bdesc = ptx::umma_desc_sw128(st + MB * Cfg::kABytes);
+#pragma unroll
+            for (int k = 0; k < kBlockK / 16; ++k) {
+#pragma unroll
+              for (int mb = 0; mb < MB; ++mb) {
+                const uint64_t adesc = ptx::umma_desc_sw128(st + mb * Cfg::kABytes);
+                ptx::mma_f16_ss(d0 + mb * kBlockN, adesc + 2 * k, bdesc + 2 * k, idesc,
+                                (kb | k) != 0 ? 1u : 0u);
+              }
+            }
+            ptx::mma_commit(&empty_bar[stage]);
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          ptx::mma_commit(&tfull_bar[abuf]);
+          abuf ^= 1;
+          if (abuf == 0) aphase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= kNumNonEpiWarps) {
+    // ------------------------------------------------------------ epilogue
+    const int e = warp - kNumNonEpiWarps;
+    const int quad = warp & 3;          // TMEM lane quadrant this warp may access
+    const int mb = e >> 2;              // which query tile of the group
+    const int lq = mb * kBlockM + quad * 32 + lane;  // local query index within the item
+    const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + mb * kBlockN;
+    int abuf = 0;
+    uint32_t aphase = 0;
+    for (int i = blockIdx.x; i < num_items; i += gridDim.x) {
+      ScanItem it;
+      resolve_item(p, i, it, kQG);
+      float s[KCAP];
+      int32_t id[KCAP];
+#pragma unroll
+      for (int j = 0; j < KCAP; ++j) {
+        s[j] = -FLT_MAX;
+        id[j] = -1;
+      }
+      const int64_t ntiles = (it.row_end - it.row_begin + kBlockN - 1) / kBlockN;
+      for (int64_t t = 0; t < ntiles; ++t) {
+        const int64_t row0 = it.row_begin + t * kBlockN;
+        const int valid = static_cast<int>(it.row_end - row0 < kBlockN ? it.row_end - row0 : kBlockN);
+        const int32_t id0 = static_cast<int32_t>(row0) + it.id_offset;
+        ptx::mbar_wait(&tfull_bar[abuf], aphase);
+        ptx::tc_fence_after();
+        const uint32_t taddr = lane_addr + abuf * Cfg::kAccCols;
+#pragma unroll 1
+        for (int c = 0; c < kBlockN; c += 64) {
+          uint32_t va[32], vb[32];
+          ptx::tmem_ld_32x32b_x32(taddr + c, va);
+          ptx::tmem_ld_32x32b_x32(taddr + c + 32, vb);
+          ptx::tmem_ld_wait();
+          scan_chunk<KCAP>(va, s, id, id0 + c, valid - c);
+          scan_chunk<KCAP>(vb, s, id, id0 + c + 32, valid - c - 32);
+        }
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&tempty_bar[abuf]);
+        abuf ^= 1;
+        if (abuf == 0) aphase ^= 1;
+      }
+      if (lq < it.q_count) {
+        float* os = p.out_scores + (it.out_row + lq) * p.out_k;
+        int32_t* oi = p.out_ids + (it.out_row + lq) * p.out_k;
+#pragma unroll
+        for (int j = 0; j < KCAP; ++j) {
+          if (j < p.out_k) {
+            const bool pad = id[j] < 0;
+            os[j] = pad ? -INFINITY : s[j];
+            oi[j] = pad ? -1 : id[j];
+          }
+        }
+      }
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem_base, Cfg::kTmemCols);
+  }
+}
+
+template <int MB, int KCAP>
+int launch_impl(const CUtensorMap& tq, const CUtensorMap& tc, const ScanParams& p, int grid,
+                cudaStream_t stream) {
+  using Cfg = ScanCfg<MB>;
+  auto kern = scan_topk_kernel<MB, KCAP>;
+  cudaError_t err =
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
+  if (err != cudaSuccess) return static_cast<int>(err);
+  kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, stream>>>(tq, tc, p);
+  return static_cast<int>(cudaGetLastError());
+}
+
+template <int MB>
+int dispatch_kcap(int kcap, const CUtensorMap& tq, const CUtensorMap& tc, const ScanParams& p,
+                  int grid, cudaStream_t stream) {
+  switch (kcap) {
+    case 1: return launch_impl<MB, 1>(tq, tc, p, grid, stream);
+    case 4: return launch_impl<MB, 4>(tq, tc, p, grid, stream);
+    case 8: return launch_impl<MB, 8>(tq, tc, p, grid, stream);
+    case 10: return launch_impl<MB, 10>(tq, tc, p, grid, stream);
+    case 16: return launch_impl<MB, 16>(tq, tc, p, grid, stream);
+    case 32: return launch_impl<MB, 32>(tq, tc, p, grid, stream);
+    default: return static_cast<int>(cudaErrorInvalidValue);
+  }
+}
+
+}  // namespace
+
+int scan_kcap_for(int k) {
+  static const int caps[] = {1, 4, 8, 10, 16, 32};
+  for (int c : caps)
+    if (k <= c) return c;
+  return 0;
+}
+
+int launch_scan_topk(int mb, int kcap, const CUtensorMap& tmap_q, const CUtensorMap& tmap_c,
+                     const ScanParams& p, int grid, cudaStream_t stream) {
+  if (grid <= 0) return 0;
+  if (mb == 2) return dispatch_kcap<2>(kcap, tmap_q, tmap_c, p, grid, stream);
+  if (mb == 1) return dispatch_kcap<1>(kcap, tmap_q, tmap_c, p, grid, stream);
+  return static_cast<int>(cudaErrorInvalidValue);
+}
+
+}  // namespace tsv

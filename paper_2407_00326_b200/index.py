@@ -1,0 +1,221 @@
+"""Device-resident corpus arena and the retrieval primitives over it (host side of the C ABI).
+
+PyTorch is used only for device memory and streams; every computation is a kernel of
+``lib/libtsv.so`` reached through ``_native``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Sequence
+
+import torch
+
+from . import _native as nat
+from .errors import CapacityExceeded, ConfigParse, DeviceError
+
+METRICS = {"ip": nat.TSV_METRIC_IP, "cosine": nat.TSV_METRIC_COSINE}
+_DTYPES = {torch.bfloat16: nat.TSV_BF16, torch.float32: nat.TSV_F32}
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    try:
+        return _DTYPES[t.dtype]
+    except KeyError:
+        raise ConfigParse(f"unsupported dtype {t.dtype}; expected bfloat16 or float32") from None
+
+
+def _require_cuda(t: torch.Tensor, name: str) -> None:
+    if not t.is_cuda:
+        raise DeviceError(f"{name} must be a CUDA tensor (there is no CPU path)")
+    if not t.is_contiguous():
+        raise ConfigParse(f"{name} must be contiguous")
+
+
+def _stream_handle(stream: torch.cuda.Stream | None, device: torch.device) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    return s.cuda_stream
+
+
+class _ArenaView:
+    """__cuda_array_interface__ exporter so torch can alias the arena without a copy."""
+
+    def __init__(self, ptr: int, rows: int, dim: int):
+        self.__cuda_array_interface__ = {
+            "shape": (rows, dim), "typestr": "<u2", "data": (ptr, False), "version": 3,
+            "strides": None,
+        }
+
+
+class DeviceIndex:
+    """A bf16 corpus arena on one GPU (reference role: the vector DB behind `vdb-search0`)."""
+
+    def __init__(self, dim: int, capacity: int, metric: str = "ip", device: int | None = None,
+                 _handle: int | None = None, _keepalive: torch.Tensor | None = None):
+        lib = nat.load()
+        if metric not in METRICS:
+            raise ConfigParse(f"unknown metric {metric!r}")
+        self.metric = metric
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self._keepalive = _keepalive
+        if _handle is not None:
+            self._h = ctypes.c_void_p(_handle)
+        else:
+            h = ctypes.c_void_p()
+            nat.check(lib.tsv_index_create(self.device.index, int(dim), METRICS[metric],
+                                           int(capacity), ctypes.byref(h)))
+            self._h = h
+        self.dim = int(lib.tsv_index_dim(self._h))
+
+    @classmethod
+    def view(cls, rows: torch.Tensor, metric: str = "ip") -> "DeviceIndex":
+        """Wrap an existing [n, dim] bf16 CUDA matrix without copying it."""
+        _require_cuda(rows, "rows")
+        if rows.dtype != torch.bfloat16 or rows.dim() != 2:
+            raise ConfigParse("a view index needs a 2-D bfloat16 matrix")
+        lib = nat.load()
+        h = ctypes.c_void_p()
+        nat.check(lib.tsv_index_create_view(rows.device.index, rows.shape[1], METRICS[metric],
+                                            rows.data_ptr(), rows.shape[0], ctypes.byref(h)))
+        return cls(rows.shape[1], rows.shape[0], metric, rows.device.index, _handle=h.value,
+                   _keepalive=rows)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            nat.load().tsv_index_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- arena ---------------------------------------------------------------
+    @property
+    def rows(self) -> int:
+        return int(nat.load().tsv_index_rows(self._h))
+
+    def data(self) -> torch.Tensor:
+        """Aliasing bf16 tensor [rows, dim] over the arena (what the kernels read)."""
+        ptr = nat.load().tsv_index_data(self._h)
+        t = torch.as_tensor(_ArenaView(ptr, self.rows, self.dim), device=self.device)
+        return t.view(torch.bfloat16)
+
+    def append(self, rows: torch.Tensor, stream: torch.cuda.Stream | None = None) -> int:
+        """Ingest rows (normalised for cosine); returns the arena row of the first one."""
+        _require_cuda(rows, "rows")
+        if rows.dim() != 2 or rows.shape[1] != self.dim:
+            raise ConfigParse(f"rows must be [n, {self.dim}]")
+        first = ctypes.c_int64()
+        nat.check(nat.load().tsv_index_append(self._h, rows.data_ptr(), _dtype_code(rows),
+                                              rows.shape[0], ctypes.byref(first),
+                                              _stream_handle(stream, self.device)))
+        return int(first.value)
+
+    def truncate(self, rows: int) -> None:
+        nat.check(nat.load().tsv_index_truncate(self._h, int(rows)))
+
+    def set_timing(self, enable: bool) -> None:
+        nat.check(nat.load().tsv_index_set_timing(self._h, int(bool(enable))))
+
+    def scan_time(self) -> tuple[float, int]:
+        """(total ms, launches) of fused-scan kernels since the last read (timing mode)."""
+        ms = ctypes.c_double()
+        n = ctypes.c_int64()
+        nat.check(nat.load().tsv_index_scan_time(self._h, ctypes.byref(ms), ctypes.byref(n)))
+        return float(ms.value), int(n.value)
+
+    # -- primitives ----------------------------------------------------------
+    def _check_queries(self, q: torch.Tensor) -> None:
+        _require_cuda(q, "queries")
+        if q.dim() != 2 or q.shape[1] != self.dim:
+            raise ConfigParse(f"queries must be [B, {self.dim}]")
+        if q.shape[0] == 0:
+            raise CapacityExceeded("empty batch")
+
+    def search(self, q: torch.Tensor, k: int, row_range: tuple[int, int] | None = None,
+               id_offset: int = 0, stream: torch.cuda.Stream | None = None,
+               out: tuple[torch.Tensor, torch.Tensor] | None = None):
+        """Top-k over arena rows [row_range) for each query; ids = row + id_offset."""
+        self._check_queries(q)
+        lo, hi = row_range if row_range is not None else (0, self.rows)
+        B = q.shape[0]
+        if out is None:
+            scores = torch.empty((B, k), dtype=torch.float32, device=self.device)
+            ids = torch.empty((B, k), dtype=torch.int32, device=self.device)
+        else:
+            scores, ids = out
+        nat.check(nat.load().tsv_search(self._h, q.data_ptr(), _dtype_code(q), B, int(k), int(lo),
+                                        int(hi), int(id_offset), scores.data_ptr(), ids.data_ptr(),
+                                        _stream_handle(stream, self.device)))
+        return scores, ids
+
+    def search_segmented(self, q: torch.Tensor, q_offsets: Sequence[int],
+                         row_ranges: Sequence[tuple[int, int]], k: int, local_ids: bool = True,
+                         stream: torch.cuda.Stream | None = None):
+        """Queries q[q_offsets[s]:q_offsets[s+1]] search only arena rows row_ranges[s]."""
+        self._check_queries(q)
+        nseg = len(row_ranges)
+        if nseg == 0:
+            raise CapacityExceeded("empty batch")
+        if len(q_offsets) != nseg + 1 or q_offsets[-1] != q.shape[0]:
+            raise ConfigParse("q_offsets must have nseg+1 entries ending at B")
+        qo = (ctypes.c_int32 * (nseg + 1))(*[int(x) for x in q_offsets])
+        rb = (ctypes.c_int64 * nseg)(*[int(a) for a, _ in row_ranges])
+        re = (ctypes.c_int64 * nseg)(*[int(b) for _, b in row_ranges])
+        B = q.shape[0]
+        scores = torch.empty((B, k), dtype=torch.float32, device=self.device)
+        ids = torch.empty((B, k), dtype=torch.int32, device=self.device)
+        nat.check(nat.load().tsv_search_segmented(
+            self._h, q.data_ptr(), _dtype_code(q), nseg, ctypes.cast(qo, ctypes.c_void_p),
+            ctypes.cast(rb, ctypes.c_void_p), ctypes.cast(re, ctypes.c_void_p), int(k),
+            int(bool(local_ids)), scores.data_ptr(), ids.data_ptr(),
+            _stream_handle(stream, self.device)))
+        return scores, ids
+
+    def rerank(self, q: torch.Tensor, cand_ids: torch.Tensor, k: int,
+               stream: torch.cuda.Stream | None = None):
+        """Score cand_ids[b, :] (arena rows) against q[b]; dedup ids; keep the best k."""
+        self._check_queries(q)
+        _require_cuda(cand_ids, "cand_ids")
+        if cand_ids.dtype != torch.int32 or cand_ids.dim() != 2 or cand_ids.shape[0] != q.shape[0]:
+            raise ConfigParse("cand_ids must be int32 [B, C]")
+        B, C = cand_ids.shape
+        scores = torch.empty((B, k), dtype=torch.float32, device=self.device)
+        ids = torch.empty((B, k), dtype=torch.int32, device=self.device)
+        nat.check(nat.load().tsv_rerank(self._h, q.data_ptr(), _dtype_code(q), B,
+                                        cand_ids.data_ptr(), C, int(k), scores.data_ptr(),
+                                        ids.data_ptr(), _stream_handle(stream, self.device)))
+        return scores, ids
+
+
+def merge_topk(scores: torch.Tensor, ids: torch.Tensor, k: int,
+               stream: torch.cuda.Stream | None = None):
+    """Merge [L, B, kin] sorted lists into [B, k] (Aggregate join / cross-shard merge)."""
+    _require_cuda(scores, "scores")
+    _require_cuda(ids, "ids")
+    if scores.dim() != 3 or scores.shape != ids.shape:
+        raise ConfigParse("scores/ids must be [lists, B, kin]")
+    if scores.dtype != torch.float32 or ids.dtype != torch.int32:
+        raise ConfigParse("scores must be float32 and ids int32")
+    L, B, kin = scores.shape
+    out_s = torch.empty((B, k), dtype=torch.float32, device=scores.device)
+    out_i = torch.empty((B, k), dtype=torch.int32, device=scores.device)
+    nat.check(nat.load().tsv_merge_topk(scores.data_ptr(), ids.data_ptr(), L, B, kin, int(k),
+                                        out_s.data_ptr(), out_i.data_ptr(),
+                                        _stream_handle(stream, scores.device)))
+    return out_s, out_i
+
+
+def normalize_rows(x: torch.Tensor, normalize: bool = True,
+                   stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """L2-normalise rows (fp32 math) and cast to bf16 on the device."""
+    _require_cuda(x, "x")
+    if x.dim() != 2:
+        raise ConfigParse("x must be 2-D")
+    out = torch.empty(x.shape, dtype=torch.bfloat16, device=x.device)
+    nat.check(nat.load().tsv_normalize_rows(x.data_ptr(), _dtype_code(x), x.shape[0], x.shape[1],
+                                            int(bool(normalize)), out.data_ptr(),
+                                            _stream_handle(stream, x.device)))
+    return out

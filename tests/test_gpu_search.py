@@ -1,0 +1,241 @@
+"""Parity of the fused scan + top-k (K1), merge (K4), segmented search (K2), rerank (K3) and
+normalisation (K5) against the CPU oracle, through the C ABI. Tolerance: scores within 1e-3
+relative for bf16 inputs (BASELINE.json north_star); ids bit-exact wherever the oracle's score
+gap exceeds that tolerance, otherwise inside the oracle's tie band."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+from tests._util import assert_topk, from_dev, to_dev_bf16
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-3
+
+
+def _index_from(c_np, device, metric="ip", extra=0):
+    from paper_2407_00326_b200.index import DeviceIndex
+
+    idx = DeviceIndex(c_np.shape[1], c_np.shape[0] + extra, metric=metric, device=device.index)
+    idx.append(to_dev_bf16(c_np, device))
+    return idx
+
+
+@pytest.mark.parametrize("n,dim,b,k", [
+    (1000, 64, 1, 1), (5000, 128, 16, 5), (4099, 384, 100, 10), (20000, 768, 128, 16),
+    (20000, 768, 129, 10), (30011, 1024, 256, 10), (12345, 72, 300, 32), (7, 64, 5, 10),
+    (300, 1024, 1030, 4),
+])
+def test_search_matches_oracle(cuda, n, dim, b, k):
+    c = orc.make_corpus(n, dim, seed=0)
+    q, _ = orc.make_queries(c, b, seed=1)
+    idx = _index_from(c, cuda)
+    s, i = idx.search(to_dev_bf16(q, cuda), k)
+    assert_topk(s, i, q, c, k, TOL)
+
+
+def test_planted_neighbours_rank_first(cuda):
+    c = orc.make_corpus(50000, 768, seed=0)
+    q, planted = orc.make_queries(c, 64, seed=1, planted_frac=1.0, noise=0.01)
+    idx = _index_from(c, cuda)
+    s, i = idx.search(to_dev_bf16(q, cuda), 10)
+    ids = from_dev(i)
+    assert (ids[:, 0] == planted).all()
+
+
+def test_identity_corpus_scores_are_coordinates(cuda):
+    dim = 128
+    c = np.eye(dim, dtype=np.float32)
+    rng = np.random.default_rng(5)
+    q = orc.bf16_round(rng.standard_normal((20, dim)).astype(np.float32))
+    idx = _index_from(c, cuda)
+    s, i = idx.search(to_dev_bf16(q, cuda), 8)
+    exp_s, exp_i = orc.search(q, c, 8)
+    np.testing.assert_array_equal(from_dev(i), exp_i)
+    np.testing.assert_allclose(from_dev(s), exp_s, rtol=0, atol=0)
+
+
+def test_exact_ties_break_by_ascending_id(cuda):
+    rng = np.random.default_rng(3)
+    base = orc.make_corpus(50, 256, seed=4)
+    c = np.concatenate([base] * 8, axis=0)  # each row duplicated 8x (ids r, r+50, ...)
+    perm = rng.permutation(len(c))
+    c = c[perm]
+    q = base[:12].copy()
+    idx = _index_from(c, cuda)
+    s, i = idx.search(to_dev_bf16(q, cuda), 16)
+    exp_s, exp_i = orc.search(q, c, 16)
+    np.testing.assert_array_equal(from_dev(i), exp_i)
+
+
+def test_k_exceeds_rows_pads(cuda):
+    c = orc.make_corpus(3, 64, seed=0)
+    q, _ = orc.make_queries(c, 4, seed=1)
+    idx = _index_from(c, cuda)
+    s, i = idx.search(to_dev_bf16(q, cuda), 8)
+    ids = from_dev(i)
+    assert (ids[:, 3:] == -1).all() and np.isneginf(from_dev(s)[:, 3:]).all()
+    assert_topk(s, i, q, c, 8, TOL)
+
+
+def test_row_range_and_id_offset(cuda):
+    c = orc.make_corpus(40000, 512, seed=0)
+    q, _ = orc.make_queries(c, 200, seed=1)
+    idx = _index_from(c, cuda)
+    lo, hi = 12345, 33333
+    s, i = idx.search(to_dev_bf16(q, cuda), 10, row_range=(lo, hi), id_offset=1_000_000 - lo)
+    assert_topk(s, i, q, c[lo:hi], 10, TOL, id_offset=1_000_000)
+
+
+def test_f32_queries_and_cosine(cuda):
+    import torch
+
+    rng = np.random.default_rng(9)
+    raw = rng.standard_normal((10000, 256)).astype(np.float32) * 3.0
+    from paper_2407_00326_b200.index import DeviceIndex
+
+    idx = DeviceIndex(256, 10000, metric="cosine", device=cuda.index)
+    idx.append(torch.from_numpy(raw).to(cuda))  # f32 rows, normalised on ingest
+    stored = from_dev(idx.data())
+    np.testing.assert_allclose(stored, orc.normalize_rows(raw), atol=2 ** -8)
+    qraw = rng.standard_normal((33, 256)).astype(np.float32)
+    s, i = idx.search(torch.from_numpy(qraw).to(cuda), 10)
+    assert_topk(s, i, orc.normalize_rows(qraw), stored, 10, TOL)
+
+
+def test_segmented_search_matches_oracle(cuda):
+    rng = np.random.default_rng(11)
+    sizes = [48, 32, 64, 1, 10000, 700, 129, 256]
+    nq = [1, 3, 1, 2, 16, 4, 1, 130]
+    arena = orc.make_corpus(sum(sizes), 384, seed=2)
+    q = orc.make_corpus(sum(nq), 384, seed=3)
+    row_ranges, q_off = [], [0]
+    lo = 0
+    for sz, m in zip(sizes, nq):
+        row_ranges.append((lo, lo + sz))
+        lo += sz
+        q_off.append(q_off[-1] + m)
+    idx = _index_from(arena, cuda)
+    for k, local in ((5, True), (16, False)):
+        s, i = idx.search_segmented(to_dev_bf16(q, cuda), q_off, row_ranges, k, local_ids=local)
+        gs, gi = from_dev(s), from_dev(i)
+        for sidx, (a, b) in enumerate(row_ranges):
+            qa, qb = q_off[sidx], q_off[sidx + 1]
+            off = 0 if local else a
+            probs = orc.check_topk(gs[qa:qb], gi[qa:qb], q[qa:qb], arena[a:b], k, TOL,
+                                   id_offset=off)
+            assert not probs, f"segment {sidx}: {probs[:5]}"
+
+
+def test_rerank_dedups_and_matches_oracle(cuda):
+    import torch
+
+    rng = np.random.default_rng(12)
+    arena = orc.make_corpus(5000, 768, seed=0)
+    qs = orc.make_corpus(64, 768, seed=7)
+    cand = rng.integers(0, 5000, size=(64, 200)).astype(np.int32)
+    cand[:, 100:150] = cand[:, :50]          # duplicates from a second expansion
+    cand[::7, 10] = -1                       # invalid entries are ignored
+    cand[::5, 11] = 999999
+    idx = _index_from(arena, cuda)
+    s, i = idx.rerank(to_dev_bf16(qs, cuda), torch.from_numpy(cand).to(cuda), 10)
+    exp_s, exp_i = orc.rerank(qs, arena, cand, 10)
+    gs, gi = from_dev(s), from_dev(i)
+    for r in range(64):
+        assert len(set(gi[r].tolist())) == 10
+    np.testing.assert_allclose(gs, exp_s, rtol=TOL)
+    # ids must equal the oracle wherever neighbouring scores are separated by more than tol
+    gap_ok = np.abs(np.diff(exp_s, axis=1, prepend=np.inf)) > TOL * np.abs(exp_s)
+    gap_ok &= np.abs(np.diff(exp_s, axis=1, append=-np.inf)) > TOL * np.abs(exp_s)
+    assert (gi[gap_ok] == exp_i[gap_ok]).all()
+
+
+def test_rerank_fewer_distinct_than_k_pads(cuda):
+    import torch
+
+    arena = orc.make_corpus(100, 64, seed=0)
+    q = orc.make_corpus(2, 64, seed=1)
+    cand = np.array([[5, 5, 5, 7], [1, -1, 1, 2]], dtype=np.int32)
+    idx = _index_from(arena, cuda)
+    s, i = idx.rerank(to_dev_bf16(q, cuda), torch.from_numpy(cand).to(cuda), 3)
+    gi = from_dev(i)
+    assert gi[0, 2] == -1 and set(gi[0, :2].tolist()) == {5, 7}
+    assert gi[1, 2] == -1 and set(gi[1, :2].tolist()) == {1, 2}
+
+
+def test_merge_matches_oracle(cuda):
+    import torch
+    from paper_2407_00326_b200.index import merge_topk
+
+    rng = np.random.default_rng(13)
+    L, B, kin, k = 8, 300, 16, 10
+    sc = rng.standard_normal((L, B, kin)).astype(np.float32)
+    sc = -np.sort(-sc, axis=2)
+    ids = rng.permutation(L * B * kin).reshape(L, B, kin).astype(np.int32)
+    ids[3, :, 12:] = -1
+    sc[3, :, 12:] = -np.inf
+    sc[5, :, 0] = sc[6, :, 0]  # exact cross-list ties
+    s, i = merge_topk(torch.from_numpy(sc).cuda(), torch.from_numpy(ids).cuda(), k)
+    es, ei = orc.merge(sc, ids, k)
+    np.testing.assert_array_equal(from_dev(i), ei)
+    np.testing.assert_array_equal(from_dev(s), es.astype(np.float32))
+
+
+def test_normalize_rows_matches_oracle(cuda):
+    import torch
+    from paper_2407_00326_b200.index import normalize_rows
+
+    rng = np.random.default_rng(14)
+    x = rng.standard_normal((777, 1024)).astype(np.float32) * 7
+    x[3] = 0.0
+    out = from_dev(normalize_rows(torch.from_numpy(x).cuda()))
+    np.testing.assert_allclose(out, orc.normalize_rows(x), atol=2 ** -8, rtol=2 ** -7)
+
+
+def test_errors_map_to_teola_errors(cuda):
+    import torch
+    from paper_2407_00326_b200.errors import CapacityExceeded, ConfigParse
+    from paper_2407_00326_b200.index import DeviceIndex
+
+    idx = DeviceIndex(64, 10, device=cuda.index)
+    with pytest.raises(CapacityExceeded):
+        idx.append(torch.zeros((11, 64), dtype=torch.bfloat16, device=cuda))
+    idx.append(torch.zeros((10, 64), dtype=torch.bfloat16, device=cuda))
+    with pytest.raises(CapacityExceeded):
+        idx.search(torch.zeros((0, 64), dtype=torch.bfloat16, device=cuda), 3)
+    with pytest.raises(ConfigParse):
+        idx.search(torch.zeros((2, 64), dtype=torch.bfloat16, device=cuda), 33)
+    with pytest.raises(ConfigParse):
+        DeviceIndex(60, 10, device=cuda.index)
+
+
+@pytest.mark.slow
+def test_c2_full_size_properties(cuda):
+    """C2 (1M x 768 bf16, B=256, k=10) at full size: oracle on a query subset, and
+    size-independent properties (sortedness, distinct ids, exact re-scoring) on all."""
+    import torch
+
+    n, dim, b, k = 1_000_000, 768, 256, 10
+    g = torch.Generator(device=cuda).manual_seed(0)
+    c = torch.randn((n, dim), generator=g, device=cuda)
+    from paper_2407_00326_b200.index import DeviceIndex, normalize_rows
+
+    cb = normalize_rows(c)
+    del c
+    qb = normalize_rows(torch.randn((b, dim), generator=g, device=cuda))
+    qb[:128] = cb[torch.arange(0, 128, device=cuda) * 7777]  # planted exact rows
+    idx = DeviceIndex.view(cb)
+    s, i = idx.search(qb, k)
+    gs, gi = from_dev(s), from_dev(i)
+    assert (np.diff(gs, axis=1) <= 0).all()
+    assert all(len(set(r.tolist())) == k for r in gi)
+    assert (gi[:128, 0] == np.arange(128) * 7777).all() or np.allclose(
+        gs[:128, 0], gs[:128, 1])
+    cn = from_dev(cb)
+    qn = from_dev(qb)
+    rescored = np.einsum("bd,bkd->bk", qn.astype(np.float64), cn[gi].astype(np.float64))
+    np.testing.assert_allclose(gs, rescored, rtol=TOL)
+    sub = np.r_[0:8, 128:136]
+    assert_topk(s[sub], i[sub], qn[sub], cn, k, TOL)
