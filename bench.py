@@ -1,0 +1,400 @@
+#!/usr/bin/env python
+"""Benchmark of the retrieval hot path: vector-search queries/s on a 10M x 1024 bf16 corpus.
+
+Workload (BASELINE.json metric, config C4 at k=10): B=1024 queries per step against a
+10,000,000 x 1024 bf16 corpus (cosine = inner product over L2-normalised rows), top-10 per
+query. With --gpus N the corpus is sharded N ways (strong scaling: total work fixed); each
+rank runs the fused scan + top-k (K1) and the range merge (K4) on its shard, the per-rank
+top-k lists are all-gathered over NCCL and merged again (K4). One step = one batch of B
+queries through that path.
+
+value : queries/s with queries already resident in HBM (device time, max over ranks).
+e2e   : the same through the public API with host buffers — every step copies the pinned
+        query batch host->device and the (scores, ids) result device->host.
+The corpus (20.5 GB) is far larger than L2, so no explicit L2 flush is needed.
+
+--impl reference times the reference CPU path (the C oracle port, all host threads) on the
+same config, each step a bounded sample of the corpus scaled to the full corpus.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
+
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def parse_args():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--rows", type=int, default=10_000_000)
+    ap.add_argument("--dim", type=int, default=1024)
+    ap.add_argument("--batch", type=int, default=1024)
+    ap.add_argument("--k", type=int, default=10)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="target CPU time of the bounded cpu_baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured"
+    return dict(FALLBACK_PEAKS), "fallback"
+
+
+# ---------------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples nvidia-smi clocks / throttle reasons every 200 ms while running."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows: list[list[str]] = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.index)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self) -> dict:
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+        sm = []
+        sm_max = None
+        reasons = set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                sm_max = float(r[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, r[2:]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": sm_max, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------- CPU baseline
+def cpu_sample(dim: int, batch: int, k: int, target_s: float, rows_dev=None):
+    """Time the C oracle (all host threads, fp32 accumulation) on a bounded sample of the
+    workload: `batch` queries against the first n_s corpus rows, n_s sized for ~target_s of
+    CPU work. Returns (queries/s scaled to the full corpus fraction, info dict)."""
+    import numpy as np
+
+    from oracle import c_oracle
+    from oracle import oracle as orc
+
+    lib = c_oracle.load()
+    threads = os.cpu_count() or 1
+    rng = np.random.default_rng(1)
+    q = orc.normalize_rows(rng.standard_normal((batch, dim), dtype=np.float32))
+    qb = orc.bf16_bits(q)
+    probe_rows = 4096
+    cb = (_host_rows(rows_dev, probe_rows) if rows_dev is not None
+          else orc.bf16_bits(orc.make_corpus(probe_rows, dim, seed=0)))
+    t = time.perf_counter()
+    c_oracle.search(qb, cb, k, nthreads=threads)
+    dt = max(time.perf_counter() - t, 1e-4)
+    n_s = int(min(max(probe_rows * target_s / dt, 8192), 1_000_000))
+    n_s -= n_s % 1024
+    cb = (_host_rows(rows_dev, n_s) if rows_dev is not None
+          else orc.bf16_bits(orc.make_corpus(n_s, dim, seed=0)))
+    return qb, cb, n_s, threads, lib.variant
+
+
+def _host_rows(rows_dev, n):
+    import numpy as np
+    import torch
+
+    n = min(n, rows_dev.shape[0])
+    return rows_dev[:n].view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def time_cpu(qb, cb, k, threads):
+    from oracle import c_oracle
+
+    t = time.perf_counter()
+    c_oracle.search(qb, cb, k, nthreads=threads)
+    return time.perf_counter() - t
+
+
+# ---------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    qb, cb, n_s, threads, variant = cpu_sample(args.dim, args.batch, args.k,
+                                               target_s=min(args.cpu_seconds, 4.0))
+    for _ in range(args.warmup):
+        time_cpu(qb, cb, args.k, threads)
+    total = 0.0
+    for _ in range(args.steps):
+        total += time_cpu(qb, cb, args.k, threads)
+    scale = args.rows / n_s
+    ms_per_step = total / args.steps * scale * 1000.0
+    value = args.batch / (ms_per_step / 1000.0)
+    sample = (f"{args.batch} queries x first {n_s} of the {args.rows}-row corpus per step "
+              f"(scaled x{scale:.1f}); C oracle {variant}, fp32 accumulate, OpenMP")
+    line = {
+        "impl": "reference",
+        "metric": "vector-search queries/s (10Mx1024 corpus, k=10)",
+        "value": value, "unit": "queries/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded N(0,1) rows, L2-normalised)",
+        "config": _config(args, args.rows),
+        "cpu_baseline": {"value": value, "unit": "queries/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _config(args, shard_rows):
+    return {
+        "workload": f"C4/metric: flat inner-product (cosine) search, {args.rows}x{args.dim} bf16 "
+                    f"corpus, batch {args.batch}, k={args.k}",
+        "rows": args.rows, "dim": args.dim, "batch": args.batch, "k": args.k,
+        "shard_rows": shard_rows, "parallelism": f"corpus-shard x{args.gpus}",
+        "l2": "inputs larger than L2 (corpus streamed from HBM every step)",
+    }
+
+
+# ---------------------------------------------------------------------- our arm
+def build_shard(idx_cls, rows, dim, lo, hi, device):
+    """Corpus rows [lo, hi) of the global seeded corpus; chunk c of 2^20 rows is drawn from a
+    generator seeded with c, so the corpus is identical for every sharding."""
+    import torch
+
+    chunk = 1 << 20
+    idx = idx_cls(dim, hi - lo, metric="cosine", device=device.index)
+    c0 = lo // chunk
+    while c0 * chunk < hi:
+        a, b = c0 * chunk, min(rows, (c0 + 1) * chunk)
+        g = torch.Generator(device=device).manual_seed(1000 + c0)
+        block = torch.randn((b - a, dim), generator=g, device=device)
+        s, e = max(a, lo), min(b, hi)
+        idx.append(block[s - a:e - a].contiguous())
+        del block
+        c0 += 1
+    torch.cuda.synchronize(device)
+    return idx
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2407_00326_b200 import _native
+    from paper_2407_00326_b200.index import DeviceIndex, merge_topk, normalize_rows
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    _native.load()
+
+    B, D, k, N = args.batch, args.dim, args.k, args.rows
+    lo, hi = N * rank // world, N * (rank + 1) // world
+    idx = build_shard(DeviceIndex, N, D, lo, hi, dev)
+
+    g = torch.Generator(device=dev).manual_seed(1)
+    q_dev = normalize_rows(torch.randn((B, D), generator=g, device=dev))
+    q_host = torch.empty((B, D), dtype=torch.bfloat16, pin_memory=True)
+    q_host.copy_(q_dev)
+    s_loc = torch.empty((B, k), dtype=torch.float32, device=dev)
+    i_loc = torch.empty((B, k), dtype=torch.int32, device=dev)
+    s_all = torch.empty((world, B, k), dtype=torch.float32, device=dev)
+    i_all = torch.empty((world, B, k), dtype=torch.int32, device=dev)
+    s_host = torch.empty((B, k), dtype=torch.float32, pin_memory=True)
+    i_host = torch.empty((B, k), dtype=torch.int32, pin_memory=True)
+
+    def step(q):
+        idx.search(q, k, id_offset=lo, out=(s_loc, i_loc))
+        if world == 1:
+            return s_loc, i_loc
+        dist.all_gather_into_tensor(s_all, s_loc)
+        dist.all_gather_into_tensor(i_all, i_loc)
+        return merge_topk(s_all, i_all, k)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step(q_dev)
+    barrier()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    # ---- device-resident timed region
+    idx.set_timing(True)
+    idx.scan_time()
+    n0 = _native.launch_count()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        step(q_dev)
+    ev1.record()
+    barrier()
+    launches = _native.launch_count() - n0
+    dev_ms = max_over_ranks(ev0.elapsed_time(ev1))
+    scan_ms, scan_launches = idx.scan_time()
+    idx.set_timing(False)
+
+    # ---- end-to-end timed region (host buffers, copies inside)
+    barrier()
+    ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev2.record()
+    for _ in range(args.steps):
+        q_dev.copy_(q_host, non_blocking=True)
+        s, i = step(q_dev)
+        s_host.copy_(s, non_blocking=True)
+        i_host.copy_(i, non_blocking=True)
+    ev3.record()
+    barrier()
+    e2e_ms = max_over_ranks(ev2.elapsed_time(ev3))
+    clk = clocks.stop()
+
+    peaks, peak_src = load_peaks()
+    avg_scan_ms = scan_ms / max(scan_launches, 1)
+    n_local = hi - lo
+    flops = 2.0 * B * n_local * D
+    bytes_alg = n_local * D * 2 + B * D * 2 + B * k * 8
+    achieved_tf = flops / (avg_scan_ms / 1000.0) / 1e12
+    achieved_gbs = bytes_alg / (avg_scan_ms / 1000.0) / 1e9
+    peak_tf = float(peaks.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"]))
+    peak_tf_sus = float(peaks.get("bf16_tflops_sustained", FALLBACK_PEAKS["bf16_tflops_sustained"]))
+    peak_bw = float(peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"]))
+    t_tc = flops / (peak_tf * 1e12)
+    t_bw = bytes_alg / (peak_bw * 1e9)
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        try:
+            tj = json.loads(tf.read_text())
+            key = f"{n_local}x{D}xB{B}k{k}"
+            traffic = tj.get(key)
+        except (ValueError, OSError):
+            traffic = None
+    if t_tc >= t_bw:
+        roof = {"bound": "tensor", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
+                "frac": achieved_tf / peak_tf, "traffic": traffic,
+                "frac_of_sustained": achieved_tf / peak_tf_sus}
+    else:
+        roof = {"bound": "hbm", "achieved": achieved_gbs, "peak": peak_bw, "unit": "GB/s",
+                "frac": achieved_gbs / peak_bw, "traffic": traffic}
+    roof.update({"kernel": "scan_topk_kernel (K1, tcgen05 fused IP + top-k)",
+                 "avg_launch_ms": avg_scan_ms, "launches_timed": scan_launches,
+                 "algorithmic_flops_per_launch": flops,
+                 "algorithmic_bytes_per_launch": bytes_alg,
+                 "peak_source": f"{peak_src} (MEASURED_PEAKS.json burst bf16 / copy GB/s)"
+                 if peak_src == "measured" else "fallback (B200_PROFILING.md)"})
+
+    value = B * args.steps / (dev_ms / 1000.0)
+    e2e_value = B * args.steps / (e2e_ms / 1000.0)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        qb, cb, n_s, threads, variant = cpu_sample(D, B, k, args.cpu_seconds, rows_dev=idx.data())
+        dt = time_cpu(qb, cb, k, threads)
+        cpu_qps = B / (dt * N / n_s)
+        cpu = {"value": cpu_qps, "unit": "queries/s", "cores": threads, "kind": "port",
+               "sample": f"{B} queries x first {n_s} corpus rows (of {N}); time scaled by "
+                         f"{N / n_s:.1f}; C oracle ({variant}), fp32 accumulate, OpenMP, "
+                         f"{dt:.2f} s measured"}
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        line = {
+            "metric": "vector-search queries/s (10Mx1024 corpus, k=10)",
+            "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded N(0,1) rows and queries, L2-normalised on device)",
+            "config": _config(args, n_local),
+            "e2e": {"value": e2e_value, "unit": "queries/s",
+                    "h2d_bytes_per_step": B * D * 2, "d2h_bytes_per_step": B * k * 8,
+                    "ms_per_step": e2e_ms / args.steps,
+                    "path": "DeviceIndex.search (C ABI tsv_search) + NCCL all-gather + "
+                            "tsv_merge_topk, pinned host buffers"},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "gpu_launches": launches,
+            "gpu_launches_per_step": launches / args.steps,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())
