@@ -134,7 +134,7 @@ def cpu_sample(dim: int, batch: int, k: int, target_s: float, rows_dev=None):
     rng = np.random.default_rng(1)
     q = orc.normalize_rows(rng.standard_normal((batch, dim), dtype=np.float32))
     qb = orc.bf16_bits(q)
-    probe_rows = 4096
+    probe_rows = 16384
     cb = (_host_rows(rows_dev, probe_rows) if rows_dev is not None
           else orc.bf16_bits(orc.make_corpus(probe_rows, dim, seed=0)))
     t = time.perf_counter()

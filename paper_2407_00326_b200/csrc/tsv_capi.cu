@@ -154,6 +154,11 @@ int check_dtype(int dt) {
   return TSV_OK;
 }
 
+bool env_flag(const char* name) {
+  const char* v = getenv(name);
+  return v != nullptr && v[0] != '\0' && v[0] != '0';
+}
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 // bf16 query matrix the scan reads: the caller's buffer when it is already bf16 and needs no
@@ -380,15 +385,24 @@ int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int
   rc = stage_queries(idx, w, q_dev, q_dtype, B, st, &qb);
   if (rc) return rc;
 
-  const int mb = B > tsv::kBlockM ? 2 : 1;
-  const int qg = mb * tsv::kBlockM;
+  // B > 128: CTA-pair kernel (256 queries x 256 rows per pair tile); otherwise one CTA per
+  // 128-query group with 128-row tiles.
+  const bool pair = B > tsv::kBlockM && !env_flag("TSV_NO_PAIR");
+  const int mb = pair ? tsv::kPairMode : 1;
+  const int qg = pair ? tsv::kPairQG : tsv::kBlockM;
+  const int tile_rows = pair ? tsv::kPairTileRows : tsv::kBlockN;
+  const int units = pair ? idx->num_sms / 2 : idx->num_sms;  // concurrent workers
   const int nqg = (B + qg - 1) / qg;
   const int64_t n = row_end - row_beg;
-  const int64_t tiles = std::max<int64_t>(1, (n + tsv::kBlockN - 1) / tsv::kBlockN);
-  int R = std::max(1, idx->num_sms / nqg);
+  const int64_t tiles = std::max<int64_t>(1, (n + tile_rows - 1) / tile_rows);
+  // Ranges per query group: one round over all workers when that idles at most ~3% of them,
+  // otherwise two full rounds (every worker busy; the corpus is then streamed twice).
+  int R = std::max(1, units / nqg);
+  if (nqg * R < units * 97 / 100 && (2 * units) % nqg == 0) R = 2 * units / nqg;
+  if (const char* e = getenv("TSV_SCAN_RANGES")) R = std::max(1, atoi(e));
   R = static_cast<int>(std::min<int64_t>(R, tiles));
   const int num_items = nqg * R;
-  const int grid = std::min(num_items, idx->num_sms);
+  const int grid = pair ? 2 * std::min(num_items, units) : std::min(num_items, units);
 
   tsv::ScanParams p{};
   p.items = nullptr;

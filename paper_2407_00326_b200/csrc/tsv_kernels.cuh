@@ -42,6 +42,13 @@ struct ScanParams {
   int32_t* out_ids;
 };
 
+// `mb` argument of launch_scan_topk selecting the CTA-pair kernel: 256 queries x 256 corpus
+// rows per pair tile (tcgen05 cta_group::2); the tensor map for queries then uses 128-row
+// boxes and the corpus map 128-row boxes (each CTA loads its half).
+constexpr int kPairMode = 4;
+constexpr int kPairQG = 256;
+constexpr int kPairTileRows = 256;
+
 // Host-side launchers (return cudaError_t as int).
 int launch_scan_topk(int mb, int kcap, const CUtensorMap& tmap_q, const CUtensorMap& tmap_c,
                      const ScanParams& p, int grid, cudaStream_t stream);

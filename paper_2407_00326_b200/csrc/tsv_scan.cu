@@ -37,7 +37,8 @@ struct ScanCfg {
   static constexpr int kSmemBytes = kStages * kStageBytes + kBarBytes + 1024;  // + align slack
 };
 
-__device__ __forceinline__ void resolve_item(const ScanParams& p, int i, ScanItem& it, int qg_size) {
+__device__ __forceinline__ void resolve_item(const ScanParams& p, int i, ScanItem& it, int qg_size,
+                                             int tile_rows = kBlockN) {
   if (p.items != nullptr) {
     it = p.items[i];
     return;
@@ -47,11 +48,11 @@ __device__ __forceinline__ void resolve_item(const ScanParams& p, int i, ScanIte
   it.q_begin = qg * qg_size;
   it.q_count = min(qg_size, p.B - it.q_begin);
   const int64_t n = p.row_end - p.row_beg;
-  const int64_t tiles = (n + kBlockN - 1) / kBlockN;
+  const int64_t tiles = (n + tile_rows - 1) / tile_rows;
   const int64_t t0 = tiles * r / p.R;
   const int64_t t1 = tiles * (r + 1) / p.R;
-  it.row_begin = p.row_beg + t0 * kBlockN;
-  it.row_end = min(p.row_end, p.row_beg + t1 * kBlockN);
+  it.row_begin = p.row_beg + t0 * tile_rows;
+  it.row_end = min(p.row_end, p.row_beg + t1 * tile_rows);
   if (it.row_end < it.row_begin) it.row_end = it.row_begin;
   it.out_row = static_cast<int64_t>(r) * p.B + it.q_begin;
   it.id_offset = p.id_offset;
@@ -114,7 +115,9 @@ __global__ void __launch_bounds__(ScanCfg<MB>::kThreads, 1)
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
 
-  const int warp = threadIdx.x >> 5;
+  // shfl makes the warp index provably warp-uniform, so role branches are not divergent and
+  // the producer / MMA loops keep their operands in uniform registers.
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
@@ -143,75 +146,74 @@ __global__ void __launch_bounds__(ScanCfg<MB>::kThreads, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      const uint64_t pol_q = ptx::policy_evict_last();
-      const uint64_t pol_c = ptx::policy_evict_normal();
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int i = blockIdx.x; i < num_items; i += gridDim.x) {
-        ScanItem it;
-        resolve_item(p, i, it, kQG);
-        const int64_t ntiles = (it.row_end - it.row_begin + kBlockN - 1) / kBlockN;
-        for (int64_t t = 0; t < ntiles; ++t) {
-          const int32_t row0 = static_cast<int32_t>(it.row_begin + t * kBlockN);
-          for (int kb = 0; kb < p.num_kb; ++kb) {
-            ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
-            uint8_t* st = smem + stage * Cfg::kStageBytes;
-            ptx::mbar_arrive_expect_tx(&full_bar[stage], Cfg::kStageBytes);
+    // The whole warp walks the loop (warp-uniform operands); one elected lane issues.
+    const uint64_t pol_q = ptx::policy_evict_last();
+    const uint64_t pol_c = ptx::policy_evict_normal();
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int i = blockIdx.x; i < num_items; i += gridDim.x) {
+      ScanItem it;
+      resolve_item(p, i, it, kQG);
+      const int64_t ntiles = (it.row_end - it.row_begin + kBlockN - 1) / kBlockN;
+      for (int64_t t = 0; t < ntiles; ++t) {
+        const int32_t row0 = static_cast<int32_t>(it.row_begin + t * kBlockN);
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* st = smem + stage * Cfg::kStageBytes;
+          ptx::mbar_arrive_expect_tx_warp(&full_bar[stage], Cfg::kStageBytes);
 #pragma unroll
-            for (int mb = 0; mb < MB; ++mb)
-              ptx::tma_load_2d(st + mb * Cfg::kABytes, &tmap_q, &full_bar[stage], kb * kBlockK,
-                               it.q_begin + mb * kBlockM, pol_q);
-            ptx::tma_load_2d(st + MB * Cfg::kABytes, &tmap_c, &full_bar[stage], kb * kBlockK, row0,
-                             pol_c);
-            if (++stage == kStages) {
-              stage = 0;
-              phase ^= 1;
-            }
+          for (int mb = 0; mb < MB; ++mb)
+            ptx::tma_load_2d_warp(st + mb * Cfg::kABytes, &tmap_q, &full_bar[stage], kb * kBlockK,
+                                  it.q_begin + mb * kBlockM, pol_q);
+          ptx::tma_load_2d_warp(st + MB * Cfg::kABytes, &tmap_c, &full_bar[stage], kb * kBlockK,
+                                row0, pol_c);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
           }
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = ptx::idesc_bf16_f32(kBlockM, kBlockN);
-      int stage = 0;
-      uint32_t phase = 0;
-      int abuf = 0;
-      uint32_t aphase = 0;
-      for (int i = blockIdx.x; i < num_items; i += gridDim.x) {
-        ScanItem it;
-        resolve_item(p, i, it, kQG);
-        const int64_t ntiles = (it.row_end - it.row_begin + kBlockN - 1) / kBlockN;
-        for (int64_t t = 0; t < ntiles; ++t) {
-          ptx::mbar_wait(&tempty_bar[abuf], aphase ^ 1);
+    // Warp-uniform loop; descriptors are built from the smem base plus compile-time offsets.
+    constexpr uint32_t idesc = ptx::idesc_bf16_f32(kBlockM, kBlockN);
+    const uint64_t desc0 = ptx::umma_desc_sw128(ptx::smem_u32(smem));
+    int stage = 0;
+    uint32_t phase = 0;
+    int abuf = 0;
+    uint32_t aphase = 0;
+    for (int i = blockIdx.x; i < num_items; i += gridDim.x) {
+      ScanItem it;
+      resolve_item(p, i, it, kQG);
+      const int64_t ntiles = (it.row_end - it.row_begin + kBlockN - 1) / kBlockN;
+      for (int64_t t = 0; t < ntiles; ++t) {
+        ptx::mbar_wait(&tempty_bar[abuf], aphase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d0 = tmem_base + abuf * Cfg::kAccCols;
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          ptx::mbar_wait(&full_bar[stage], phase);
           ptx::tc_fence_after();
-          const uint32_t d0 = tmem_base + abuf * Cfg::kAccCols;
-          for (int kb = 0; kb < p.num_kb; ++kb) {
-            ptx::mbar_wait(&full_bar[stage], phase);
-            ptx::tc_fence_after();
-            const uint32_t st = ptx::smem_u32(smem + stage * Cfg::kStageBytes);
-            const uint64_t bdesc = ptx::umma_desc_sw128(st + MB * Cfg::kABytes);
+          const uint64_t sdesc = desc0 + static_cast<uint64_t>((stage * Cfg::kStageBytes) >> 4);
 #pragma unroll
-            for (int k = 0; k < kBlockK / 16; ++k) {
+          for (int k = 0; k < kBlockK / 16; ++k) {
 #pragma unroll
-              for (int mb = 0; mb < MB; ++mb) {
-                const uint64_t adesc = ptx::umma_desc_sw128(st + mb * Cfg::kABytes);
-                ptx::mma_f16_ss(d0 + mb * kBlockN, adesc + 2 * k, bdesc + 2 * k, idesc,
-                                (kb | k) != 0 ? 1u : 0u);
-              }
-            }
-            ptx::mma_commit(&empty_bar[stage]);
-            if (++stage == kStages) {
-              stage = 0;
-              phase ^= 1;
+            for (int mb = 0; mb < MB; ++mb) {
+              ptx::mma_f16_ss_warp(d0 + mb * kBlockN,
+                                   sdesc + static_cast<uint64_t>((mb * Cfg::kABytes) >> 4) + 2 * k,
+                                   sdesc + static_cast<uint64_t>((MB * Cfg::kABytes) >> 4) + 2 * k,
+                                   idesc, (kb | k) != 0 ? 1u : 0u);
             }
           }
-          ptx::mma_commit(&tfull_bar[abuf]);
-          abuf ^= 1;
-          if (abuf == 0) aphase ^= 1;
+          ptx::mma_commit_warp(&empty_bar[stage]);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
+        ptx::mma_commit_warp(&tfull_bar[abuf]);
+        abuf ^= 1;
+        if (abuf == 0) aphase ^= 1;
       }
     }
   } else if (warp >= kNumNonEpiWarps) {
@@ -278,6 +280,209 @@ __global__ void __launch_bounds__(ScanCfg<MB>::kThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2). A pair of SMs computes M=256 queries x N=256 corpus rows per
+// MMA: each CTA stages its 128 query rows and 128 corpus rows of every k-block, the leader CTA
+// issues tcgen05.mma.cta_group::2 and each CTA's TMEM receives its own 128 query rows x 256
+// columns. Per SM this halves the shared-memory operand bytes per MAC compared with the
+// single-CTA 128x128 tile, which is what keeps the tensor pipe fed.
+struct Pair {
+  static constexpr int kTileRows = 256;                 // corpus rows per pair tile (N)
+  static constexpr int kQG = 256;                       // queries per pair (M)
+  static constexpr int kHalfBytes = 128 * kBlockK * 2;  // 16 KB: one CTA's half of A or B
+  static constexpr int kStageBytes = 2 * kHalfBytes;    // A half + B half per CTA
+  static constexpr int kStages = 6;
+  static constexpr int kAccCols = 256;
+  static constexpr int kTmemCols = 512;                 // 2 accumulator buffers
+  static constexpr int kEpiWarps = 4;
+  static constexpr int kThreads = (kNumNonEpiWarps + kEpiWarps) * 32;
+  static constexpr int kSmemBytes = kStages * kStageBytes + 256 + 1024;
+};
+
+template <int KCAP>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
+    scan_topk_pair_kernel(const __grid_constant__ CUtensorMap tmap_q,
+                          const __grid_constant__ CUtensorMap tmap_c, const ScanParams p) {
+  constexpr int kStages = Pair::kStages;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * Pair::kStageBytes);
+  uint64_t* empty_bar = full_bar + kStages;
+  uint64_t* tfull_bar = empty_bar + kStages;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1;
+  const int npairs = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&tmap_q);
+    ptx::tma_prefetch_desc(&tmap_c);
+    for (int s = 0; s < kStages; ++s) {
+      ptx::mbar_init(&full_bar[s], 1);
+      ptx::mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&tfull_bar[b], 1);
+      ptx::mbar_init(&tempty_bar[b], 2 * Pair::kEpiWarps);  // one arrival per epilogue warp
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) {
+    ptx::tmem_alloc2(tmem_slot, Pair::kTmemCols);
+    ptx::tmem_relinquish2();
+  }
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int num_items = p.num_items;
+
+  if (warp == 0) {
+    // ---- TMA producer (both CTAs): own halves of A and B, completion on the leader's barrier
+    const uint64_t pol_q = ptx::policy_evict_last();
+    const uint64_t pol_c = ptx::policy_evict_normal();
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int i = pair; i < num_items; i += npairs) {
+      ScanItem it;
+      resolve_item(p, i, it, Pair::kQG, Pair::kTileRows);
+      const int64_t ntiles = (it.row_end - it.row_begin + Pair::kTileRows - 1) / Pair::kTileRows;
+      for (int64_t t = 0; t < ntiles; ++t) {
+        const int32_t row0 = static_cast<int32_t>(it.row_begin + t * Pair::kTileRows) + rank * 128;
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* st = smem + stage * Pair::kStageBytes;
+          const uint32_t fb = ptx::mapa(ptx::smem_u32(&full_bar[stage]), 0);
+          if (leader) ptx::mbar_arrive_expect_tx_warp(&full_bar[stage], 2 * Pair::kStageBytes);
+          ptx::tma_load_2d_pair_warp(st, &tmap_q, fb, kb * kBlockK, it.q_begin + rank * 128, pol_q);
+          ptx::tma_load_2d_pair_warp(st + Pair::kHalfBytes, &tmap_c, fb, kb * kBlockK, row0, pol_c);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---- MMA issuer (leader CTA only)
+    if (leader) {
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(256, 256);
+      const uint64_t desc0 = ptx::umma_desc_sw128(ptx::smem_u32(smem));
+      int stage = 0;
+      uint32_t phase = 0;
+      int abuf = 0;
+      uint32_t aphase = 0;
+      for (int i = pair; i < num_items; i += npairs) {
+        ScanItem it;
+        resolve_item(p, i, it, Pair::kQG, Pair::kTileRows);
+        const int64_t ntiles = (it.row_end - it.row_begin + Pair::kTileRows - 1) / Pair::kTileRows;
+        for (int64_t t = 0; t < ntiles; ++t) {
+          ptx::mbar_wait(&tempty_bar[abuf], aphase ^ 1);
+          ptx::tc_fence_after();
+          const uint32_t d0 = tmem_base + abuf * Pair::kAccCols;
+          for (int kb = 0; kb < p.num_kb; ++kb) {
+            ptx::mbar_wait(&full_bar[stage], phase);
+            ptx::tc_fence_after();
+            const uint64_t sdesc = desc0 + static_cast<uint64_t>((stage * Pair::kStageBytes) >> 4);
+#pragma unroll
+            for (int k = 0; k < kBlockK / 16; ++k)
+              ptx::mma2_f16_ss_warp(d0, sdesc + 2 * k,
+                                    sdesc + static_cast<uint64_t>(Pair::kHalfBytes >> 4) + 2 * k,
+                                    idesc, (kb | k) != 0 ? 1u : 0u);
+            ptx::mma2_commit_mc_warp(&empty_bar[stage], 0x3);
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          ptx::mma2_commit_mc_warp(&tfull_bar[abuf], 0x3);
+          abuf ^= 1;
+          if (abuf == 0) aphase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= kNumNonEpiWarps) {
+    // ---- epilogue (both CTAs): thread = one query row of this CTA's 128, 256 columns per tile
+    const int quad = warp & 3;
+    const int lq = static_cast<int>(rank) * 128 + quad * 32 + lane;
+    const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
+    const uint32_t tempty_leader0 = ptx::mapa(ptx::smem_u32(&tempty_bar[0]), 0);
+    int abuf = 0;
+    uint32_t aphase = 0;
+    for (int i = pair; i < num_items; i += npairs) {
+      ScanItem it;
+      resolve_item(p, i, it, Pair::kQG, Pair::kTileRows);
+      float s[KCAP];
+      int32_t id[KCAP];
+#pragma unroll
+      for (int j = 0; j < KCAP; ++j) {
+        s[j] = -FLT_MAX;
+        id[j] = -1;
+      }
+      const int64_t ntiles = (it.row_end - it.row_begin + Pair::kTileRows - 1) / Pair::kTileRows;
+      for (int64_t t = 0; t < ntiles; ++t) {
+        const int64_t row0 = it.row_begin + t * Pair::kTileRows;
+        const int valid = static_cast<int>(
+            it.row_end - row0 < Pair::kTileRows ? it.row_end - row0 : Pair::kTileRows);
+        const int32_t id0 = static_cast<int32_t>(row0) + it.id_offset;
+        ptx::mbar_wait(&tfull_bar[abuf], aphase);
+        ptx::tc_fence_after();
+        const uint32_t taddr = lane_addr + abuf * Pair::kAccCols;
+#pragma unroll 1
+        for (int c = 0; c < Pair::kTileRows; c += 64) {
+          uint32_t va[32], vb[32];
+          ptx::tmem_ld_32x32b_x32(taddr + c, va);
+          ptx::tmem_ld_32x32b_x32(taddr + c + 32, vb);
+          ptx::tmem_ld_wait();
+          scan_chunk<KCAP>(va, s, id, id0 + c, valid - c);
+          scan_chunk<KCAP>(vb, s, id, id0 + c + 32, valid - c - 32);
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader0 + abuf * 8);
+        abuf ^= 1;
+        if (abuf == 0) aphase ^= 1;
+      }
+      if (lq < it.q_count) {
+        float* os = p.out_scores + (it.out_row + lq) * p.out_k;
+        int32_t* oi = p.out_ids + (it.out_row + lq) * p.out_k;
+#pragma unroll
+        for (int j = 0; j < KCAP; ++j) {
+          if (j < p.out_k) {
+            const bool pad = id[j] < 0;
+            os[j] = pad ? -INFINITY : s[j];
+            oi[j] = pad ? -1 : id[j];
+          }
+        }
+      }
+    }
+  }
+
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc2(tmem_base, Pair::kTmemCols);
+  }
+}
+
+template <int KCAP>
+int launch_pair_impl(const CUtensorMap& tq, const CUtensorMap& tc, const ScanParams& p, int grid,
+                     cudaStream_t stream) {
+  auto kern = scan_topk_pair_kernel<KCAP>;
+  cudaError_t err =
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Pair::kSmemBytes);
+  if (err != cudaSuccess) return static_cast<int>(err);
+  kern<<<grid, Pair::kThreads, Pair::kSmemBytes, stream>>>(tq, tc, p);
+  return static_cast<int>(cudaGetLastError());
+}
+
 template <int MB, int KCAP>
 int launch_impl(const CUtensorMap& tq, const CUtensorMap& tc, const ScanParams& p, int grid,
                 cudaStream_t stream) {
@@ -304,6 +509,19 @@ int dispatch_kcap(int kcap, const CUtensorMap& tq, const CUtensorMap& tc, const 
   }
 }
 
+int dispatch_pair(int kcap, const CUtensorMap& tq, const CUtensorMap& tc, const ScanParams& p,
+                  int grid, cudaStream_t stream) {
+  switch (kcap) {
+    case 1: return launch_pair_impl<1>(tq, tc, p, grid, stream);
+    case 4: return launch_pair_impl<4>(tq, tc, p, grid, stream);
+    case 8: return launch_pair_impl<8>(tq, tc, p, grid, stream);
+    case 10: return launch_pair_impl<10>(tq, tc, p, grid, stream);
+    case 16: return launch_pair_impl<16>(tq, tc, p, grid, stream);
+    case 32: return launch_pair_impl<32>(tq, tc, p, grid, stream);
+    default: return static_cast<int>(cudaErrorInvalidValue);
+  }
+}
+
 }  // namespace
 
 int scan_kcap_for(int k) {
@@ -318,6 +536,7 @@ int launch_scan_topk(int mb, int kcap, const CUtensorMap& tmap_q, const CUtensor
   if (grid <= 0) return 0;
   if (mb == 2) return dispatch_kcap<2>(kcap, tmap_q, tmap_c, p, grid, stream);
   if (mb == 1) return dispatch_kcap<1>(kcap, tmap_q, tmap_c, p, grid, stream);
+  if (mb == kPairMode) return dispatch_pair(kcap, tmap_q, tmap_c, p, grid, stream);
   return static_cast<int>(cudaErrorInvalidValue);
 }
 
