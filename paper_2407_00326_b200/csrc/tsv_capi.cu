@@ -65,9 +65,17 @@ int encode_rows_map(CUtensorMap* map, const void* base, int64_t rows, int dim, i
   cuuint64_t gstride[1] = {static_cast<cuuint64_t>(dim) * 2};
   cuuint32_t box[2] = {static_cast<cuuint32_t>(tsv::kBlockK), static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estride[2] = {1, 1};
+  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_NONE;
+  if (const char* e = getenv("TSV_L2_PROMO")) {
+    const int v = atoi(e);
+    promo = v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                   : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                             : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                        : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), gdim, gstride,
-                  box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promo,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(TSV_ERR_DEVICE, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return TSV_OK;
 }

@@ -90,7 +90,10 @@ __device__ __forceinline__ void scan_chunk(const uint32_t (&v)[32], float (&s)[K
   }
   const float m = fmaxf(m0, m1);
   if (m > s[K - 1]) {
-#pragma unroll 1
+    // Rare path, fully unrolled so the chunk stays in registers (a rolled loop would index
+    // v[] dynamically and spill it to local memory, whose L1 traffic competes with the
+    // tensor core's shared-memory operand reads).
+#pragma unroll
     for (int j = 0; j < 32; ++j) {
       const float x = __uint_as_float(v[j]);
       if (x > s[K - 1] && j < valid) list_insert<K>(s, id, x, id0 + j);
