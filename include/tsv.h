@@ -84,7 +84,8 @@ TSV_API int tsv_index_scan_time(tsv_index* idx, double* total_ms, int64_t* launc
 /* ---- K1: Searching primitive over one contiguous row range (global corpus / shard).
  * Replaces the PHASE_GENERAL latency lookup of runtime.py:653-655 for engine category
  * "search" (engines.py:21, graph.py:47-59). q_dev: [B, dim] (bf16 or f32). Emitted id =
- * arena row + id_offset. Outputs scores/ids [B, k]. k <= 32. ---- */
+ * arena row + id_offset. Outputs scores/ids [B, k]. k <= 128 (k <= 32 keeps the top-k lists in registers and
+ * uses the CTA-pair kernel for B > 128; larger k keeps them in shared memory). ---- */
 TSV_API int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int64_t row_beg,
                int64_t row_end, int32_t id_offset, float* scores_dev, int32_t* ids_dev,
                void* stream);
@@ -105,9 +106,10 @@ TSV_API int tsv_rerank(tsv_index* idx, const void* q_dev, int q_dtype, int B, co
 
 /* ---- K4: merge `lists` sorted lists per query. Input layout [lists][B][kin]; output [B][kout].
  * This is the Aggregate join of split Searching stages (optimizer.py:620-661,
- * runtime.py:544-549) and the cross-shard merge after the all-gather. ---- */
+ * runtime.py:544-549) and the cross-shard merge after the all-gather. dedup != 0 keeps one
+ * entry per id (partial rerank lists of one question over overlapping candidates). ---- */
 TSV_API int tsv_merge_topk(const float* in_scores, const int32_t* in_ids, int lists, int B, int kin,
-                   int kout, float* out_scores, int32_t* out_ids, void* stream);
+                   int kout, int dedup, float* out_scores, int32_t* out_ids, void* stream);
 
 /* ---- K5: L2-normalise (normalize != 0) and cast rows to bf16. ---- */
 TSV_API int tsv_normalize_rows(const void* src_dev, int src_dtype, int64_t n, int dim, int normalize,

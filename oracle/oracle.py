@@ -66,7 +66,7 @@ def normalize_rows(x: np.ndarray) -> np.ndarray:
     """K5 restated: L2-normalise in fp32 (sum of squares, then x * rsqrt) and round to bf16."""
     f = np.asarray(x, dtype=np.float32)
     ss = np.einsum("ij,ij->i", f.astype(np.float64), f.astype(np.float64)).astype(np.float32)
-    scale = np.where(ss > 0, 1.0 / np.sqrt(ss), 1.0).astype(np.float32)
+    scale = (1.0 / np.sqrt(np.where(ss > 0, ss, 1.0))).astype(np.float32)
     return bf16_round(f * scale[:, None])
 
 

@@ -48,7 +48,7 @@ SIGNATURES = {
     "tsv_search_segmented": (c_int, [c_vp, c_vp, c_int, c_int, c_vp, c_vp, c_vp, c_int, c_int,
                                      c_vp, c_vp, c_vp]),
     "tsv_rerank": (c_int, [c_vp, c_vp, c_int, c_int, c_vp, c_int, c_int, c_vp, c_vp, c_vp]),
-    "tsv_merge_topk": (c_int, [c_vp, c_vp, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp]),
+    "tsv_merge_topk": (c_int, [c_vp, c_vp, c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp]),
     "tsv_normalize_rows": (c_int, [c_vp, c_int, c_i64, c_int, c_int, c_vp, c_vp]),
 }
 

@@ -1,0 +1,433 @@
+"""RetrievalBackend: executes Searching / Reranking batch plans on B200 GPUs.
+
+This is what `Simulator._execute` hands a plan to for the engines it is bound to (in the
+reference the same call returns `latency(profile, load)`; pkg/src/teola_sim/runtime.py:653-655).
+Engine replicas map to GPUs (`EngineProfile.instances`, chosen by `select_instance`,
+engines.py:156-164). Data flows through the object store exactly along the graph's edges:
+
+  Embedding (modeled)   -> query vectors [items, D] for the node's slice (seeded synthetic)
+  Ingestion (modeled)   -> chunk vectors appended to the replica's device arena; the query's
+                           index is a contiguous arena segment (all ingest stages of a query
+                           write into one reserved segment at their slice offsets)
+  Searching (GPU, K1/K2)-> per query top-k (scores, chunk ids), query-major, for the stage's
+                           slice; a whole topology-aware batch is ONE segmented launch, each
+                           entry searching its own query's index segment (or the resident
+                           global corpus when the node has no index input)
+  Aggregate (K4 / cat)  -> stage results concatenated in slice order (optimizer.py:620-661)
+  Reranking (GPU, K3)   -> candidate chunks scored against the question vector, deduplicated,
+                           top_k kept; requests (candidates) split across batches are merged
+                           with K4 when the node completes
+
+Timing: "profile" keeps the profile latency as the batch duration (reference-identical
+traces); "measured" returns the device time of the batch's launches (CUDA events on the
+replica's stream). Either way the kernels run and the results are real.
+"""
+
+from __future__ import annotations
+
+import hashlib
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _native
+from .engines import EngineProfile, latency
+from .errors import CapacityExceeded, ConfigParse
+from .graph import PrimitiveKind, PrimitiveNode
+from .index import DeviceIndex, merge_topk, normalize_rows
+
+TIMING_PROFILE = "profile"
+TIMING_MEASURED = "measured"
+
+
+def _seed(*parts) -> int:
+    h = hashlib.sha256("|".join(str(p) for p in parts).encode()).digest()
+    return int.from_bytes(h[:8], "little") & ((1 << 63) - 1)
+
+
+class SyntheticData:
+    """Deterministic stand-ins for the outputs of the modeled (non-GPU) primitives.
+
+    Chunk vectors of a query's documents and its expanded-query vectors are seeded from
+    (query id, key, item), so every stage split produces exactly the rows the unsplit node
+    would. A `planted` fraction of query vectors are near-copies of one of the query's own
+    chunks (the retrieval target), mirroring the bench's planted-neighbour queries."""
+
+    def __init__(self, dim: int, seed: int = 0, planted: float = 0.5, noise: float = 0.05):
+        self.dim = dim
+        self.seed = seed
+        self.planted = planted
+        self.noise = noise
+
+    def _rows(self, device, tag: tuple, n: int) -> torch.Tensor:
+        g = torch.Generator(device=device).manual_seed(_seed(self.seed, *tag))
+        return torch.randn((n, self.dim), generator=g, device=device)
+
+    def chunks(self, device, query_id: str, key: str, lo: int, hi: int, total: int) -> torch.Tensor:
+        return normalize_rows(self._rows(device, ("chunks", query_id, key, total), total)[lo:hi])
+
+    def queries(self, device, query_id: str, key: str, lo: int, hi: int, total: int,
+                n_chunks: int | None = None, chunk_key: str | None = None) -> torch.Tensor:
+        q = self._rows(device, ("queries", query_id, key, total), total)
+        if n_chunks and chunk_key is not None and self.planted > 0:
+            m = int(round(total * self.planted))
+            g = torch.Generator(device="cpu").manual_seed(_seed(self.seed, "plant", query_id))
+            rows = torch.randint(0, n_chunks, (m,), generator=g)
+            base = self._rows(device, ("chunks", query_id, chunk_key, n_chunks), n_chunks)
+            q[:m] = base[rows.to(device)] + self.noise * q[:m]
+        return normalize_rows(q[lo:hi].contiguous())
+
+    def question(self, device, query_id: str) -> torch.Tensor:
+        return normalize_rows(self._rows(device, ("question", query_id), 1))
+
+
+@dataclass
+class IndexSegment:
+    """A query's per-query index: rows [row_beg, row_end) of one replica's arena."""
+
+    replica: int
+    row_beg: int
+    row_end: int
+    filled: int = 0
+
+
+@dataclass
+class SearchResult:
+    """Searching output for queries [q_lo, q_hi) of the node: (scores, ids) [n, k] on device;
+    ids are chunk ids within the query's index (or global corpus ids). `ready` is recorded on
+    the producing replica stream; consumers on other streams wait on it."""
+
+    scores: torch.Tensor
+    ids: torch.Tensor
+    q_lo: int
+    q_hi: int
+    slice_of: tuple[int, int, int] | None = None
+    ready: torch.cuda.Event | None = None
+    replica: int = 0
+
+
+@dataclass
+class Replica:
+    device: torch.device
+    stream: torch.cuda.Stream
+    arena: DeviceIndex
+
+
+class RetrievalBackend:
+    """Executes batches of the bound retrieval engines on GPU replicas.
+
+    engines: engine ids to serve (default: every engine of category search/rerank that the
+    workflow uses for vector search — `vdb-search0`, `rerank0`). `web0` / `tool0` searches
+    stay latency-modeled."""
+
+    def __init__(self, dim: int, devices: list[int] | None = None, arena_rows: int = 1 << 20,
+                 engines=("vdb-search0", "rerank0"), timing: str = TIMING_PROFILE,
+                 data: SyntheticData | None = None, metric: str = "cosine",
+                 global_index: DeviceIndex | None = None):
+        if timing not in (TIMING_PROFILE, TIMING_MEASURED):
+            raise ConfigParse(f"unknown timing mode {timing!r}")
+        _native.load()
+        self.dim = dim
+        self.timing = timing
+        self.engines = set(engines)
+        self.data = data or SyntheticData(dim)
+        self.global_index = global_index
+        devs = devices if devices is not None else [torch.cuda.current_device()]
+        self.replicas = []
+        for d in devs:
+            dev = torch.device("cuda", d)
+            with torch.cuda.device(dev):
+                self.replicas.append(Replica(dev, torch.cuda.Stream(dev),
+                                             DeviceIndex(dim, arena_rows, metric=metric, device=d)))
+        self.segments: dict[tuple[str, str, int], IndexSegment] = {}  # (query, key, replica)
+        # (query id, node id) -> [(first request, scores, ids)] of batches run so far
+        self.acc: dict[tuple[str, str], list] = {}
+        self.launches = 0
+        self.device_ms_total = 0.0
+
+    # -- binding ---------------------------------------------------------------------
+    def serves(self, profile: EngineProfile) -> bool:
+        return profile.engine_id in self.engines and profile.category in ("search", "rerank")
+
+    def replica_for(self, instance) -> Replica:
+        iid = 0 if instance is None else instance.instance_id
+        return self.replicas[iid % len(self.replicas)]
+
+    def home(self, query_id: str) -> int:
+        return _seed("home", query_id) % len(self.replicas)
+
+    # -- graph-tier hooks --------------------------------------------------------------
+    def on_submit(self, ctx) -> None:
+        pass
+
+    def on_complete(self, ctx, node: PrimitiveNode) -> None:
+        """Materialise the device data a completed node produces."""
+        kind = node.kind
+        if kind is PrimitiveKind.INGESTION:
+            for key, p in node.meta.outputs.items():
+                self._ingest(ctx, node, key, p.items)
+        elif kind is PrimitiveKind.EMBEDDING:
+            for key, p in node.meta.outputs.items():
+                lo, hi, total = node.meta.slice_of.get(key, (0, p.items, p.items))
+                ctx.data[(node.node_id, key)] = ("queries", key, lo, hi, total)
+        elif kind is PrimitiveKind.AGGREGATE:
+            key = node.meta.inputs[0]
+            parts = [(ctx.data.get((e.src, key)), e.src) for e in ctx.graph.edges
+                     if e.dst == node.node_id and e.key == key]
+            parts = [p for p, _ in parts if isinstance(p, SearchResult)]
+            if parts:
+                # Aggregate = concatenation of the stage results in slice order, ordered after
+                # every stage's launch (stream waits, no host sync).
+                parts.sort(key=lambda r: (r.slice_of or (0,))[0])
+                rep = self.replicas[parts[0].replica]
+                with self._on(rep):
+                    for p_ in parts:
+                        if p_.ready is not None:
+                            rep.stream.wait_event(p_.ready)
+                    res = SearchResult(torch.cat([p_.scores for p_ in parts]),
+                                       torch.cat([p_.ids for p_ in parts]),
+                                       min(p_.q_lo for p_ in parts), max(p_.q_hi for p_ in parts),
+                                       replica=parts[0].replica)
+                    res.ready = self._record(rep)
+                ctx.data[(node.node_id, key)] = res
+        elif kind in (PrimitiveKind.SEARCHING, PrimitiveKind.RERANKING):
+            self._finalize(ctx, node)
+
+    def _on(self, rep: Replica):
+        """Context: make `rep`'s device and stream current for torch ops and our launches."""
+        return _StreamCtx(rep)
+
+    @staticmethod
+    def _record(rep: Replica) -> torch.cuda.Event:
+        ev = torch.cuda.Event()
+        ev.record(rep.stream)
+        return ev
+
+    def _ingest(self, ctx, node, key, items):
+        lo, hi, total = node.meta.slice_of.get(key, (0, items, items))
+        r = self.home(ctx.query_id)
+        seg = self._segment(ctx.query_id, key, r, total)
+        rep = self.replicas[r]
+        with self._on(rep):
+            rows = self.data.chunks(rep.device, ctx.query_id, key, lo, hi, total)
+            dst = rep.arena.data()[seg.row_beg + lo: seg.row_beg + hi]
+            dst.copy_(rows.to(torch.bfloat16))
+        seg.filled += hi - lo
+        ctx.data[(node.node_id, key)] = ("index", key, total)
+
+    def _segment(self, query_id, key, replica, total) -> IndexSegment:
+        seg = self.segments.get((query_id, key, replica))
+        if seg is None:
+            rep = self.replicas[replica]
+            with self._on(rep):
+                first = rep.arena.append(torch.zeros((total, self.dim), dtype=torch.bfloat16,
+                                                     device=rep.device), stream=rep.stream)
+            seg = IndexSegment(replica, first, first + total)
+            self.segments[(query_id, key, replica)] = seg
+        return seg
+
+    def _local_segment(self, query_id, key, replica) -> IndexSegment:
+        """The query's index on `replica`; copied from its home GPU over NVLink on first use."""
+        seg = self.segments.get((query_id, key, replica))
+        if seg is not None:
+            return seg
+        home = self.segments.get((query_id, key, self.home(query_id)))
+        if home is None:
+            raise CapacityExceeded(f"index {key!r} of {query_id} was never ingested")
+        n = home.row_end - home.row_beg
+        src = self.replicas[home.replica]
+        dst_rep = self.replicas[replica]
+        src.stream.synchronize()
+        with self._on(dst_rep):  # peer copy over NVLink, then append on the local stream
+            rows = src.arena.data()[home.row_beg:home.row_end].to(dst_rep.device)
+            first = dst_rep.arena.append(rows, stream=dst_rep.stream)
+        seg = IndexSegment(replica, first, first + n, n)
+        self.segments[(query_id, key, replica)] = seg
+        return seg
+
+    # -- execution ------------------------------------------------------------------------
+    def execute(self, profile: EngineProfile, plan, t: float, instance) -> tuple[float, float | None]:
+        if not plan.entries:
+            raise CapacityExceeded("empty batch")
+        rep = self.replica_for(instance)
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        with self._on(rep):
+            start.record(rep.stream)
+            if profile.category == "search":
+                self._search_batch(rep, plan)
+            else:
+                self._rerank_batch(rep, plan)
+            end.record(rep.stream)
+        self.launches += 1
+        if self.timing == TIMING_MEASURED:
+            end.synchronize()
+            ms = start.elapsed_time(end)
+            self.device_ms_total += ms
+            return ms, ms
+        return latency(profile, plan.load), None
+
+    def _inputs(self, ctx, node, want: str):
+        """Data arriving on the node's input edges whose producer tag is `want`."""
+        out = []
+        for e in ctx.graph.edges:
+            if e.dst == node.node_id and e.key is not None:
+                d = ctx.data.get((e.src, e.key))
+                if isinstance(d, tuple) and d[0] == want:
+                    out.append((e.src, d))
+                elif want == "result" and isinstance(d, SearchResult):
+                    out.append((e.src, d))
+        return out
+
+    def _query_rows(self, rep, task, lo: int, hi: int) -> torch.Tensor:
+        """Query vectors for requests [lo, hi) of a Searching task (node-relative)."""
+        ctx, node = task.ctx, task.node
+        key_out = next(iter(node.meta.outputs))
+        q_lo_node, _ = _stage_queries(node, key_out)
+        srcs = self._inputs(ctx, node, "queries")
+        idx = self._inputs(ctx, node, "index")
+        n_chunks = idx[0][1][2] if idx else None
+        chunk_key = idx[0][1][1] if idx else None
+        if not srcs:
+            raise CapacityExceeded(f"{node.node_id}: no query vectors on its inputs")
+        # the embedding producers cover the node's query slice (aligned or replicated)
+        total = srcs[0][1][4]
+        key = srcs[0][1][1]
+        return self.data.queries(rep.device, ctx.query_id, key, q_lo_node + lo, q_lo_node + hi,
+                                 total, n_chunks, chunk_key)
+
+    def _search_batch(self, rep: Replica, plan) -> None:
+        qs, q_off, ranges, metas = [], [0], [], []
+        kmax = 1
+        use_global = False
+        for task, n in plan.entries:
+            node = task.node
+            key_out = next(iter(node.meta.outputs))
+            k = node.meta.outputs[key_out].items // max(1, node.meta.batch_items)
+            kmax = max(kmax, k)
+            lo = task.next_request
+            qs.append(self._query_rows(rep, task, lo, lo + n))
+            q_off.append(q_off[-1] + n)
+            idx = self._inputs(task.ctx, node, "index")
+            if idx:
+                seg = self._local_segment(task.ctx.query_id, idx[0][1][1],
+                                          self.replicas.index(rep))
+                ranges.append((seg.row_beg, seg.row_end))
+            else:
+                if self.global_index is None:
+                    raise CapacityExceeded(f"{node.node_id}: no index input and no global corpus")
+                use_global = True
+                ranges.append((0, self.global_index.rows))
+            metas.append((task, lo, n, k))
+        q = torch.cat(qs)
+        if kmax > 128:
+            raise ConfigParse(f"per_query_top_k={kmax} exceeds the fused kernel's limit (128)")
+        if use_global:
+            scores, ids = self.global_index.search(q, kmax, stream=rep.stream)
+        else:
+            scores, ids = rep.arena.search_segmented(q, q_off, ranges, kmax, local_ids=True,
+                                                     stream=rep.stream)
+        ready = self._record(rep)
+        r = self.replicas.index(rep)
+        for (task, lo, n, k), a in zip(metas, q_off[:-1]):
+            self.acc.setdefault((task.ctx.query_id, task.node_id), []).append(
+                (lo, scores[a:a + n, :k], ids[a:a + n, :k], ready, r))
+
+    def _rerank_batch(self, rep: Replica, plan) -> None:
+        for task, n in plan.entries:
+            node, ctx = task.node, task.ctx
+            key_out = next(iter(node.meta.outputs))
+            top_k = node.meta.outputs[key_out].items
+            cands = self._inputs(ctx, node, "result")
+            if not cands:
+                raise CapacityExceeded(f"{node.node_id}: no candidate input")
+            res = cands[0][1]
+            if res.ready is not None:
+                rep.stream.wait_event(res.ready)
+            flat = res.ids.reshape(-1)
+            lo = task.next_request
+            part = flat[lo:lo + n]
+            idx = self._inputs(ctx, node, "index") or self._index_of_search(ctx, cands[0][0])
+            seg = self._local_segment(ctx.query_id, idx[0][1][1], self.replicas.index(rep))
+            rows = torch.where(part >= 0, part + seg.row_beg, part).to(torch.int32)
+            qv = self.data.question(rep.device, ctx.query_id)
+            s, i = rep.arena.rerank(qv, rows.reshape(1, -1).contiguous(), top_k, stream=rep.stream)
+            i = torch.where(i >= 0, i - seg.row_beg, i).to(torch.int32)
+            self.acc.setdefault((ctx.query_id, task.node_id), []).append(
+                (lo, s, i, self._record(rep), self.replicas.index(rep)))
+
+    def _index_of_search(self, ctx, producer: str):
+        """Walk back from an Aggregate / Searching producer to the Searching node's index input."""
+        seen = {producer}
+        frontier = [producer]
+        while frontier:
+            nid = frontier.pop()
+            node = ctx.graph.nodes[nid]
+            if node.kind is PrimitiveKind.SEARCHING:
+                got = self._inputs(ctx, node, "index")
+                if got:
+                    return got
+            for e in ctx.graph.edges:
+                if e.dst == nid and e.src not in seen:
+                    seen.add(e.src)
+                    frontier.append(e.src)
+        raise CapacityExceeded("rerank candidates do not trace back to an indexed search")
+
+    def _finalize(self, ctx, node) -> None:
+        """All requests of a retrieval node are done: assemble its output from the per-batch
+        partial results (batches may have split the node's requests)."""
+        parts = self.acc.pop((ctx.query_id, node.node_id), [])
+        if not parts:
+            return
+        parts.sort(key=lambda p: p[0])
+        key = next(iter(node.meta.outputs))
+        rep = self.replicas[parts[0][4]]
+        with self._on(rep):
+            for p_ in parts:
+                rep.stream.wait_event(p_[3])
+            if node.kind is PrimitiveKind.SEARCHING:
+                q_lo, q_hi = _stage_queries(node, key)
+                res = SearchResult(torch.cat([p_[1] for p_ in parts]),
+                                   torch.cat([p_[2] for p_ in parts]), q_lo, q_hi,
+                                   node.meta.slice_of.get(key), replica=parts[0][4])
+            else:
+                top_k = node.meta.outputs[key].items
+                if len(parts) == 1:
+                    s_, i_ = parts[0][1], parts[0][2]
+                else:  # candidates split across batches: merge the partial top-k lists (K4)
+                    s_, i_ = merge_topk(torch.stack([p_[1] for p_ in parts]),
+                                        torch.stack([p_[2] for p_ in parts]), top_k,
+                                        stream=rep.stream, dedup=True)
+                res = SearchResult(s_, i_, 0, 1, None, replica=parts[0][4])
+            res.ready = self._record(rep)
+        ctx.data[(node.node_id, key)] = res
+
+    def finish(self) -> None:
+        for rep in self.replicas:
+            rep.stream.synchronize()
+
+
+class _StreamCtx:
+    def __init__(self, rep: Replica):
+        self.rep = rep
+        self._dev = torch.cuda.device(rep.device)
+        self._st = torch.cuda.stream(rep.stream)
+
+    def __enter__(self):
+        self._dev.__enter__()
+        self._st.__enter__()
+        return self.rep
+
+    def __exit__(self, *exc):
+        self._st.__exit__(*exc)
+        self._dev.__exit__(*exc)
+        return False
+
+
+def _stage_queries(node: PrimitiveNode, key: str) -> tuple[int, int]:
+    out = node.meta.outputs[key]
+    s = node.meta.slice_of.get(key)
+    if s is None:
+        return 0, node.meta.batch_items
+    k = out.items // max(1, node.meta.batch_items)
+    return s[0] // k, s[1] // k

@@ -162,6 +162,8 @@ int check_dtype(int dt) {
   return TSV_OK;
 }
 
+constexpr int kMergeCap = 8192;  // candidates per query the merge kernel sorts in smem
+
 bool env_flag(const char* name) {
   const char* v = getenv(name);
   return v != nullptr && v[0] != '\0' && v[0] != '0';
@@ -379,7 +381,7 @@ int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int
   if (B <= 0) return fail(TSV_ERR_CAPACITY, "empty batch");
   if (k <= 0) return fail(TSV_ERR_CONFIG, "k must be >= 1");
   const int kcap = tsv::scan_kcap_for(k);
-  if (kcap == 0) return fail(TSV_ERR_CONFIG, "k=%d exceeds the supported maximum (32)", k);
+  if (kcap == 0) return fail(TSV_ERR_CONFIG, "k=%d exceeds the supported maximum (128)", k);
   if (q_dev == nullptr || scores_dev == nullptr || ids_dev == nullptr)
     return fail(TSV_ERR_ARGUMENT, "null buffer");
   if (row_beg < 0 || row_end > idx->rows || row_beg > row_end)
@@ -395,7 +397,7 @@ int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int
 
   // B > 128: CTA-pair kernel (256 queries x 256 rows per pair tile); otherwise one CTA per
   // 128-query group with 128-row tiles.
-  const bool pair = B > tsv::kBlockM && !env_flag("TSV_NO_PAIR");
+  const bool pair = B > tsv::kBlockM && kcap <= tsv::kMaxRegK && !env_flag("TSV_NO_PAIR");
   const int mb = pair ? tsv::kPairMode : 1;
   const int qg = pair ? tsv::kPairQG : tsv::kBlockM;
   const int tile_rows = pair ? tsv::kPairTileRows : tsv::kBlockN;
@@ -409,6 +411,7 @@ int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int
   if (nqg * R < units * 97 / 100 && (2 * units) % nqg == 0) R = 2 * units / nqg;
   if (const char* e = getenv("TSV_SCAN_RANGES")) R = std::max(1, atoi(e));
   R = static_cast<int>(std::min<int64_t>(R, tiles));
+  R = std::min(R, kMergeCap / kcap);  // the range merge holds R * kcap candidates per query
   const int num_items = nqg * R;
   const int grid = pair ? 2 * std::min(num_items, units) : std::min(num_items, units);
 
@@ -455,7 +458,7 @@ int tsv_search_segmented(tsv_index* idx, const void* q_dev, int q_dtype, int nse
     return fail(TSV_ERR_ARGUMENT, "null segment table");
   if (k <= 0) return fail(TSV_ERR_CONFIG, "k must be >= 1");
   const int kcap = tsv::scan_kcap_for(k);
-  if (kcap == 0) return fail(TSV_ERR_CONFIG, "k=%d exceeds the supported maximum (32)", k);
+  if (kcap == 0) return fail(TSV_ERR_CONFIG, "k=%d exceeds the supported maximum (128)", k);
   const int B = seg_q_beg[nseg] - seg_q_beg[0];
   if (seg_q_beg[0] != 0 || B <= 0) return fail(TSV_ERR_CAPACITY, "bad query offsets");
   int max_q = 0;
@@ -474,13 +477,14 @@ int tsv_search_segmented(tsv_index* idx, const void* q_dev, int q_dtype, int nse
   rc = stage_queries(idx, w, q_dev, q_dtype, B, st, &qb);
   if (rc) return rc;
 
-  const int mb = max_q > tsv::kBlockM ? 2 : 1;
+  const int mb = (max_q > tsv::kBlockM && kcap <= tsv::kMaxRegK) ? 2 : 1;
   const int qg = mb * tsv::kBlockM;
   int units = 0;
   for (int s = 0; s < nseg; ++s) units += (seg_q_beg[s + 1] - seg_q_beg[s] + qg - 1) / qg;
   const int64_t max_tiles = std::max<int64_t>(1, (max_rows + tsv::kBlockN - 1) / tsv::kBlockN);
   int R = std::max(1, idx->num_sms / std::max(1, units));
   R = static_cast<int>(std::min<int64_t>(R, max_tiles));
+  R = std::min(R, kMergeCap / kcap);
 
   auto& hi = w.host_items;
   hi.clear();
@@ -562,13 +566,13 @@ int tsv_rerank(tsv_index* idx, const void* q_dev, int q_dtype, int B, const int3
 }
 
 int tsv_merge_topk(const float* in_scores, const int32_t* in_ids, int lists, int B, int kin,
-                   int kout, float* out_scores, int32_t* out_ids, void* stream) {
+                   int kout, int dedup, float* out_scores, int32_t* out_ids, void* stream) {
   if (lists <= 0 || B <= 0 || kin <= 0 || kout <= 0) return fail(TSV_ERR_CAPACITY, "empty merge");
   if (static_cast<int64_t>(lists) * kin > 8192)
     return fail(TSV_ERR_CAPACITY, "merge of %d x %d candidates exceeds 8192", lists, kin);
   if (!in_scores || !in_ids || !out_scores || !out_ids) return fail(TSV_ERR_ARGUMENT, "null buffer");
   int e = tsv::launch_merge_topk(in_scores, in_ids, lists, B, kin, B, kout, out_scores, out_ids,
-                                 reinterpret_cast<cudaStream_t>(stream));
+                                 reinterpret_cast<cudaStream_t>(stream), dedup);
   if (e) return cuda_fail(static_cast<cudaError_t>(e), "merge launch");
   g_launches++;
   return TSV_OK;

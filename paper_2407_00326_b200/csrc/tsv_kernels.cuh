@@ -53,10 +53,12 @@ constexpr int kPairTileRows = 256;
 int launch_scan_topk(int mb, int kcap, const CUtensorMap& tmap_q, const CUtensorMap& tmap_c,
                      const ScanParams& p, int grid, cudaStream_t stream);
 int scan_kcap_for(int k);  // smallest supported list capacity >= k (0 if unsupported)
+constexpr int kMaxRegK = 32;   // larger k uses shared-memory lists (single-CTA, 128 queries)
+constexpr int kMaxK = 128;
 
 int launch_merge_topk(const float* in_s, const int32_t* in_id, int lists, int B, int kin,
                       int64_t list_stride_rows, int kout, float* out_s, int32_t* out_id,
-                      cudaStream_t stream);
+                      cudaStream_t stream, int dedup = 0);
 
 int launch_rerank(const void* arena, int64_t nrows, int dim, const void* q, int q_is_f32,
                   int B, const int32_t* cand, int C, int k, float* out_s, int32_t* out_id,

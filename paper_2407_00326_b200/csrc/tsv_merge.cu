@@ -63,7 +63,8 @@ __device__ __forceinline__ int pow2_ceil(int n) {
 // One block per query: gather lists * kin candidates, sort, keep kout.
 __global__ void merge_topk_kernel(const float* __restrict__ in_s, const int32_t* __restrict__ in_id,
                                   int lists, int B, int kin, int64_t list_stride_rows, int kout,
-                                  float* __restrict__ out_s, int32_t* __restrict__ out_id) {
+                                  float* __restrict__ out_s, int32_t* __restrict__ out_id,
+                                  int dedup) {
   extern __shared__ uint64_t keys[];
   const int b = blockIdx.x;
   const int n = lists * kin;
@@ -80,6 +81,27 @@ __global__ void merge_topk_kernel(const float* __restrict__ in_s, const int32_t*
     keys[i] = key;
   }
   bitonic_sort_desc(keys, np);
+  if (dedup) {
+    // Copies of one id carry identical scores, so they are adjacent after the sort.
+    if (threadIdx.x == 0) {
+      int w = 0;
+      int32_t last = -2;
+      for (int i = 0; i < np && w < kout; ++i) {
+        const int32_t id = key_id(keys[i]);
+        if (id < 0) break;
+        if (id == last) continue;
+        last = id;
+        out_s[static_cast<int64_t>(b) * kout + w] = key_score(keys[i]);
+        out_id[static_cast<int64_t>(b) * kout + w] = id;
+        ++w;
+      }
+      for (; w < kout; ++w) {
+        out_s[static_cast<int64_t>(b) * kout + w] = -INFINITY;
+        out_id[static_cast<int64_t>(b) * kout + w] = -1;
+      }
+    }
+    return;
+  }
   for (int j = threadIdx.x; j < kout; j += blockDim.x) {
     const uint64_t key = j < np ? keys[j] : pad_key();
     const int32_t id = key_id(key);
@@ -182,7 +204,7 @@ __global__ void normalize_kernel(const void* __restrict__ src, int src_is_f32, i
 
 int launch_merge_topk(const float* in_s, const int32_t* in_id, int lists, int B, int kin,
                       int64_t list_stride_rows, int kout, float* out_s, int32_t* out_id,
-                      cudaStream_t stream) {
+                      cudaStream_t stream, int dedup) {
   if (B <= 0) return 0;
   int np = 1;
   while (np < lists * kin) np <<= 1;
@@ -195,7 +217,7 @@ int launch_merge_topk(const float* in_s, const int32_t* in_id, int lists, int B,
   }
   const int threads = np >= 512 ? 256 : 128;
   merge_topk_kernel<<<B, threads, smem, stream>>>(in_s, in_id, lists, B, kin, list_stride_rows,
-                                                  kout, out_s, out_id);
+                                                  kout, out_s, out_id, dedup);
   return static_cast<int>(cudaGetLastError());
 }
 

@@ -23,18 +23,27 @@
 namespace tsv {
 namespace {
 
-template <int MB>
+// Lists of more than kRegListMax entries live in shared memory (one column per query thread,
+// entry j of thread t at [j * 128 + t], so lock-step accesses are bank-conflict free).
+constexpr int kRegListMax = 32;
+
+template <int MB, int KCAP = 1>
 struct ScanCfg {
+  static constexpr bool kSmemList = KCAP > kRegListMax;
   static constexpr int kABytes = kBlockM * kBlockK * 2;            // 16 KB
   static constexpr int kBBytes = kBlockN * kBlockK * 2;            // 16 KB
   static constexpr int kStageBytes = MB * kABytes + kBBytes;
-  static constexpr int kStages = MB == 2 ? 4 : 6;
+  static constexpr int kListBytes = kSmemList ? kBlockM * KCAP * 8 : 0;
+  static constexpr int kStages =
+      kSmemList ? (227 * 1024 - 2048 - kListBytes) / kStageBytes : (MB == 2 ? 4 : 6);
   static constexpr int kAccCols = MB * kBlockN;                    // per accumulator buffer
   static constexpr int kTmemCols = 2 * kAccCols;                   // double buffered
   static constexpr int kEpiWarps = MB * 4;
   static constexpr int kThreads = (kNumNonEpiWarps + kEpiWarps) * 32;
   static constexpr int kBarBytes = 256;
-  static constexpr int kSmemBytes = kStages * kStageBytes + kBarBytes + 1024;  // + align slack
+  static constexpr int kSmemBytes = kStages * kStageBytes + kListBytes + kBarBytes + 1024;
+  static_assert(!kSmemList || MB == 1, "shared-memory lists need one query tile per CTA");
+  static_assert(kStages >= 2, "not enough shared memory for the pipeline");
 };
 
 __device__ __forceinline__ void resolve_item(const ScanParams& p, int i, ScanItem& it, int qg_size,
@@ -101,18 +110,58 @@ __device__ __forceinline__ void scan_chunk(const uint32_t (&v)[32], float (&s)[K
   }
 }
 
+// Shared-memory list variant (KCAP > 32): the list of thread t is the column t of
+// ls/li[KCAP][128]; `tau` caches the last entry (the admission threshold).
+template <int K>
+__device__ __forceinline__ void smem_list_insert(float* ls, int32_t* li, int t, float x, int32_t xi,
+                                                 float& tau) {
+  int p = K - 1;
+  while (p > 0 && ls[(p - 1) * kBlockM + t] < x) {
+    ls[p * kBlockM + t] = ls[(p - 1) * kBlockM + t];
+    li[p * kBlockM + t] = li[(p - 1) * kBlockM + t];
+    --p;
+  }
+  ls[p * kBlockM + t] = x;
+  li[p * kBlockM + t] = xi;
+  tau = ls[(K - 1) * kBlockM + t];
+}
+
+template <int K>
+__device__ __forceinline__ void scan_chunk_smem(const uint32_t (&v)[32], float* ls, int32_t* li,
+                                                int t, float& tau, int32_t id0, int valid) {
+  float m0 = fmaxf(__uint_as_float(v[0]), __uint_as_float(v[1]));
+  float m1 = fmaxf(__uint_as_float(v[2]), __uint_as_float(v[3]));
+#pragma unroll
+  for (int j = 4; j < 32; j += 4) {
+    m0 = fmaxf(m0, fmaxf(__uint_as_float(v[j]), __uint_as_float(v[j + 1])));
+    m1 = fmaxf(m1, fmaxf(__uint_as_float(v[j + 2]), __uint_as_float(v[j + 3])));
+  }
+  if (fmaxf(m0, m1) > tau) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const float x = __uint_as_float(v[j]);
+      if (x > tau && j < valid) smem_list_insert<K>(ls, li, t, x, id0 + j, tau);
+    }
+  }
+}
+
 template <int MB, int KCAP>
-__global__ void __launch_bounds__(ScanCfg<MB>::kThreads, 1)
+__global__ void __launch_bounds__(ScanCfg<MB, KCAP>::kThreads, 1)
     scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_q,
                      const __grid_constant__ CUtensorMap tmap_c, const ScanParams p) {
-  using Cfg = ScanCfg<MB>;
+  using Cfg = ScanCfg<MB, KCAP>;
   constexpr int kStages = Cfg::kStages;
   constexpr int kQG = MB * kBlockM;
+  constexpr bool kSmemList = Cfg::kSmemList;
+  constexpr int kRegK = kSmemList ? 1 : KCAP;
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * Cfg::kStageBytes);
+  float* list_s = reinterpret_cast<float*>(smem + kStages * Cfg::kStageBytes);
+  int32_t* list_i = reinterpret_cast<int32_t*>(list_s + (kSmemList ? KCAP * kBlockM : 0));
+  uint64_t* full_bar =
+      reinterpret_cast<uint64_t*>(smem + kStages * Cfg::kStageBytes + Cfg::kListBytes);
   uint64_t* empty_bar = full_bar + kStages;
   uint64_t* tfull_bar = empty_bar + kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
@@ -231,12 +280,20 @@ __global__ void __launch_bounds__(ScanCfg<MB>::kThreads, 1)
     for (int i = blockIdx.x; i < num_items; i += gridDim.x) {
       ScanItem it;
       resolve_item(p, i, it, kQG);
-      float s[KCAP];
-      int32_t id[KCAP];
+      float s[kRegK];
+      int32_t id[kRegK];
+      float tau = -FLT_MAX;
+      const int t_epi = quad * 32 + lane;  // column of this thread's shared-memory list
 #pragma unroll
-      for (int j = 0; j < KCAP; ++j) {
+      for (int j = 0; j < kRegK; ++j) {
         s[j] = -FLT_MAX;
         id[j] = -1;
+      }
+      if constexpr (kSmemList) {
+        for (int j = 0; j < KCAP; ++j) {
+          list_s[j * kBlockM + t_epi] = -FLT_MAX;
+          list_i[j * kBlockM + t_epi] = -1;
+        }
       }
       const int64_t ntiles = (it.row_end - it.row_begin + kBlockN - 1) / kBlockN;
       for (int64_t t = 0; t < ntiles; ++t) {
@@ -252,8 +309,13 @@ __global__ void __launch_bounds__(ScanCfg<MB>::kThreads, 1)
           ptx::tmem_ld_32x32b_x32(taddr + c, va);
           ptx::tmem_ld_32x32b_x32(taddr + c + 32, vb);
           ptx::tmem_ld_wait();
-          scan_chunk<KCAP>(va, s, id, id0 + c, valid - c);
-          scan_chunk<KCAP>(vb, s, id, id0 + c + 32, valid - c - 32);
+          if constexpr (kSmemList) {
+            scan_chunk_smem<KCAP>(va, list_s, list_i, t_epi, tau, id0 + c, valid - c);
+            scan_chunk_smem<KCAP>(vb, list_s, list_i, t_epi, tau, id0 + c + 32, valid - c - 32);
+          } else {
+            scan_chunk<kRegK>(va, s, id, id0 + c, valid - c);
+            scan_chunk<kRegK>(vb, s, id, id0 + c + 32, valid - c - 32);
+          }
         }
         ptx::tc_fence_before();
         ptx::mbar_arrive(&tempty_bar[abuf]);
@@ -263,12 +325,20 @@ __global__ void __launch_bounds__(ScanCfg<MB>::kThreads, 1)
       if (lq < it.q_count) {
         float* os = p.out_scores + (it.out_row + lq) * p.out_k;
         int32_t* oi = p.out_ids + (it.out_row + lq) * p.out_k;
+        if constexpr (kSmemList) {
+          for (int j = 0; j < p.out_k; ++j) {
+            const int32_t v = list_i[j * kBlockM + t_epi];
+            os[j] = v < 0 ? -INFINITY : list_s[j * kBlockM + t_epi];
+            oi[j] = v < 0 ? -1 : v;
+          }
+        } else {
 #pragma unroll
-        for (int j = 0; j < KCAP; ++j) {
-          if (j < p.out_k) {
-            const bool pad = id[j] < 0;
-            os[j] = pad ? -INFINITY : s[j];
-            oi[j] = pad ? -1 : id[j];
+          for (int j = 0; j < kRegK; ++j) {
+            if (j < p.out_k) {
+              const bool pad = id[j] < 0;
+              os[j] = pad ? -INFINITY : s[j];
+              oi[j] = pad ? -1 : id[j];
+            }
           }
         }
       }
@@ -489,7 +559,7 @@ int launch_pair_impl(const CUtensorMap& tq, const CUtensorMap& tc, const ScanPar
 template <int MB, int KCAP>
 int launch_impl(const CUtensorMap& tq, const CUtensorMap& tc, const ScanParams& p, int grid,
                 cudaStream_t stream) {
-  using Cfg = ScanCfg<MB>;
+  using Cfg = ScanCfg<MB, KCAP>;
   auto kern = scan_topk_kernel<MB, KCAP>;
   cudaError_t err =
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
@@ -508,6 +578,12 @@ int dispatch_kcap(int kcap, const CUtensorMap& tq, const CUtensorMap& tc, const 
     case 10: return launch_impl<MB, 10>(tq, tc, p, grid, stream);
     case 16: return launch_impl<MB, 16>(tq, tc, p, grid, stream);
     case 32: return launch_impl<MB, 32>(tq, tc, p, grid, stream);
+    case 64:
+      if constexpr (MB == 1) return launch_impl<1, 64>(tq, tc, p, grid, stream);
+      return static_cast<int>(cudaErrorInvalidValue);
+    case 128:
+      if constexpr (MB == 1) return launch_impl<1, 128>(tq, tc, p, grid, stream);
+      return static_cast<int>(cudaErrorInvalidValue);
     default: return static_cast<int>(cudaErrorInvalidValue);
   }
 }
@@ -528,7 +604,7 @@ int dispatch_pair(int kcap, const CUtensorMap& tq, const CUtensorMap& tc, const 
 }  // namespace
 
 int scan_kcap_for(int k) {
-  static const int caps[] = {1, 4, 8, 10, 16, 32};
+  static const int caps[] = {1, 4, 8, 10, 16, 32, 64, 128};
   for (int c : caps)
     if (k <= c) return c;
   return 0;

@@ -191,8 +191,9 @@ class DeviceIndex:
 
 
 def merge_topk(scores: torch.Tensor, ids: torch.Tensor, k: int,
-               stream: torch.cuda.Stream | None = None):
-    """Merge [L, B, kin] sorted lists into [B, k] (Aggregate join / cross-shard merge)."""
+               stream: torch.cuda.Stream | None = None, dedup: bool = False):
+    """Merge [L, B, kin] sorted lists into [B, k] (Aggregate join / cross-shard merge);
+    dedup keeps one entry per id."""
     _require_cuda(scores, "scores")
     _require_cuda(ids, "ids")
     if scores.dim() != 3 or scores.shape != ids.shape:
@@ -203,7 +204,7 @@ def merge_topk(scores: torch.Tensor, ids: torch.Tensor, k: int,
     out_s = torch.empty((B, k), dtype=torch.float32, device=scores.device)
     out_i = torch.empty((B, k), dtype=torch.int32, device=scores.device)
     nat.check(nat.load().tsv_merge_topk(scores.data_ptr(), ids.data_ptr(), L, B, kin, int(k),
-                                        out_s.data_ptr(), out_i.data_ptr(),
+                                        int(bool(dedup)), out_s.data_ptr(), out_i.data_ptr(),
                                         _stream_handle(stream, scores.device)))
     return out_s, out_i
 

@@ -26,7 +26,8 @@ def _index_from(c_np, device, metric="ip", extra=0):
 @pytest.mark.parametrize("n,dim,b,k", [
     (1000, 64, 1, 1), (5000, 128, 16, 5), (4099, 384, 100, 10), (20000, 768, 128, 16),
     (20000, 768, 129, 10), (30011, 1024, 256, 10), (12345, 72, 300, 32), (7, 64, 5, 10),
-    (300, 1024, 1030, 4),
+    (300, 1024, 1030, 4), (20000, 768, 300, 50), (5000, 256, 64, 100), (3000, 128, 20, 128),
+    (100, 64, 3, 64),
 ])
 def test_search_matches_oracle(cuda, n, dim, b, k):
     c = orc.make_corpus(n, dim, seed=0)
@@ -118,7 +119,7 @@ def test_segmented_search_matches_oracle(cuda):
         lo += sz
         q_off.append(q_off[-1] + m)
     idx = _index_from(arena, cuda)
-    for k, local in ((5, True), (16, False)):
+    for k, local in ((5, True), (16, False), (50, True)):
         s, i = idx.search_segmented(to_dev_bf16(q, cuda), q_off, row_ranges, k, local_ids=local)
         gs, gi = from_dev(s), from_dev(i)
         for sidx, (a, b) in enumerate(row_ranges):
@@ -206,7 +207,7 @@ def test_errors_map_to_teola_errors(cuda):
     with pytest.raises(CapacityExceeded):
         idx.search(torch.zeros((0, 64), dtype=torch.bfloat16, device=cuda), 3)
     with pytest.raises(ConfigParse):
-        idx.search(torch.zeros((2, 64), dtype=torch.bfloat16, device=cuda), 33)
+        idx.search(torch.zeros((2, 64), dtype=torch.bfloat16, device=cuda), 129)
     with pytest.raises(ConfigParse):
         DeviceIndex(60, 10, device=cuda.index)
 
