@@ -233,7 +233,8 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_2407_00326_b200 import _native
-    from paper_2407_00326_b200.index import DeviceIndex, merge_topk, normalize_rows
+    from paper_2407_00326_b200.index import DeviceIndex, normalize_rows
+    from paper_2407_00326_b200.sharded import ShardedSearch, shard_range
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -245,27 +246,19 @@ def run_ours(args):
     _native.load()
 
     B, D, k, N = args.batch, args.dim, args.k, args.rows
-    lo, hi = N * rank // world, N * (rank + 1) // world
+    lo, hi = shard_range(N, rank, world)
     idx = build_shard(DeviceIndex, N, D, lo, hi, dev)
 
     g = torch.Generator(device=dev).manual_seed(1)
     q_dev = normalize_rows(torch.randn((B, D), generator=g, device=dev))
     q_host = torch.empty((B, D), dtype=torch.bfloat16, pin_memory=True)
     q_host.copy_(q_dev)
-    s_loc = torch.empty((B, k), dtype=torch.float32, device=dev)
-    i_loc = torch.empty((B, k), dtype=torch.int32, device=dev)
-    s_all = torch.empty((world, B, k), dtype=torch.float32, device=dev)
-    i_all = torch.empty((world, B, k), dtype=torch.int32, device=dev)
     s_host = torch.empty((B, k), dtype=torch.float32, pin_memory=True)
     i_host = torch.empty((B, k), dtype=torch.int32, pin_memory=True)
+    sharded = ShardedSearch(idx, N, rank=rank, world=world)
 
     def step(q):
-        idx.search(q, k, id_offset=lo, out=(s_loc, i_loc))
-        if world == 1:
-            return s_loc, i_loc
-        dist.all_gather_into_tensor(s_all, s_loc)
-        dist.all_gather_into_tensor(i_all, i_loc)
-        return merge_topk(s_all, i_all, k)
+        return sharded.search(q, k)
 
     def barrier():
         if world > 1:
@@ -375,8 +368,9 @@ def run_ours(args):
             "e2e": {"value": e2e_value, "unit": "queries/s",
                     "h2d_bytes_per_step": B * D * 2, "d2h_bytes_per_step": B * k * 8,
                     "ms_per_step": e2e_ms / args.steps,
-                    "path": "DeviceIndex.search (C ABI tsv_search) + NCCL all-gather + "
-                            "tsv_merge_topk, pinned host buffers"},
+                    "path": "ShardedSearch.search -> DeviceIndex.search (C ABI tsv_search) "
+                            "[+ NCCL all-gather + tsv_merge_topk when sharded], pinned host "
+                            "buffers"},
             "roofline": roof,
             "cpu_baseline": cpu,
             "gpu_launches": launches,

@@ -1,0 +1,111 @@
+"""The CPU oracle is pinned to known-answer vectors and the C restatement agrees with the
+numpy one (these run without a GPU)."""
+
+from __future__ import annotations
+
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+
+KATS = json.loads((Path(__file__).resolve().parent / "golden" / "retrieval_kats.json").read_text())
+
+
+def _exp(kat):
+    ids = np.array(kat["ids"], dtype=np.int64)
+    scores = np.array([[(-np.inf if v is None else v) for v in row] for row in kat["scores"]])
+    return scores, ids
+
+
+@pytest.mark.parametrize("name", ["planted", "identity", "ties", "k_ge_n"])
+def test_search_known_answers(name):
+    kat = KATS[name]
+    c = np.array(kat["corpus"], np.float32)
+    q = np.array(kat["queries"], np.float32)
+    s, i = orc.search(q, c, kat["k"])
+    es, ei = _exp(kat)
+    np.testing.assert_array_equal(i, ei)
+    np.testing.assert_array_equal(s, es)
+
+
+def test_rerank_known_answer_dedups():
+    kat = KATS["dup_rerank"]
+    c = np.array(kat["corpus"], np.float32)
+    q = np.array(kat["queries"], np.float32)
+    s, i = orc.rerank(q, c, np.array(kat["candidates"]), kat["k"])
+    es, ei = _exp(kat)
+    np.testing.assert_array_equal(i, ei)
+    np.testing.assert_array_equal(s, es)
+
+
+def test_shard_merge_known_answer():
+    kat = KATS["shards"]
+    c = np.array(kat["corpus"], np.float32)
+    q = np.array(kat["queries"], np.float32)
+    world, k = kat["world"], kat["k"]
+    n = len(c)
+    lists_s, lists_i = [], []
+    for r in range(world):
+        lo, hi = n * r // world, n * (r + 1) // world
+        s, i = orc.search(q, c[lo:hi], k, id_offset=lo)
+        lists_s.append(s)
+        lists_i.append(i)
+    s, i = orc.merge(np.stack(lists_s), np.stack(lists_i), k)
+    es, ei = _exp(kat)
+    np.testing.assert_array_equal(i, ei)
+    np.testing.assert_array_equal(s, es)
+
+
+def test_aggregate_is_slice_order_concatenation():
+    """Aggregate joins stage outputs in slice order (optimizer.py:620-661): searching the
+    query stages separately and concatenating equals searching them together."""
+    c = orc.make_corpus(500, 64, seed=3)
+    q, _ = orc.make_queries(c, 9, seed=4)
+    whole = orc.search(q, c, 6)
+    parts = [orc.search(q[a:b], c, 6) for a, b in ((0, 3), (3, 6), (6, 9))]
+    np.testing.assert_array_equal(np.concatenate([p[1] for p in parts]), whole[1])
+
+
+def test_comparator_detects_wrong_ids_and_accepts_tie_swaps():
+    c = orc.make_corpus(2000, 64, seed=0)
+    q, _ = orc.make_queries(c, 4, seed=1)
+    s, i = orc.search(q, c, 5)
+    assert orc.check_topk(s, i, q, c, 5, 1e-3) == []
+    bad = i.copy()
+    bad[0, 0] = (bad[0, 0] + 1) % 2000
+    assert orc.check_topk(s, bad, q, c, 5, 1e-3)
+    # exact duplicate rows: swapping the two tied ids is inside the tie band
+    c2 = np.concatenate([c, c[:1]])
+    q2 = c[:1].copy()
+    s2, i2 = orc.search(q2, c2, 2)
+    assert set(i2[0].tolist()) == {0, 2000}
+    assert orc.check_topk(s2, i2[:, ::-1].copy(), q2, c2, 2, 1e-3) == []
+
+
+def test_bf16_rounding_is_round_to_nearest_even():
+    x = np.array([1.0 + 2 ** -8, 1.0 + 3 * 2 ** -8, -2.5, 0.0], np.float32)
+    r = orc.bf16_round(x)
+    np.testing.assert_array_equal(r, np.array([1.0, 1.0 + 2 ** -6, -2.5, 0.0], np.float32))
+
+
+def test_c_oracle_matches_numpy_oracle():
+    from oracle import c_oracle
+
+    c = orc.make_corpus(3000, 128, seed=5)
+    q, _ = orc.make_queries(c, 37, seed=6)
+    for use_double in (False, True):
+        s, i = c_oracle.search(orc.bf16_bits(q), orc.bf16_bits(c), 10, use_double=use_double,
+                               nthreads=4, id_offset=100)
+        assert orc.check_topk(s, i, q, c, 10, 1e-5, id_offset=100) == []
+    for name in ("planted", "ties", "k_ge_n", "identity"):
+        kat = KATS[name]
+        cc = np.array(kat["corpus"], np.float32)
+        qq = np.array(kat["queries"], np.float32)
+        s, i = c_oracle.search(orc.bf16_bits(qq), orc.bf16_bits(cc), kat["k"], use_double=True,
+                               nthreads=3)
+        es, ei = _exp(kat)
+        np.testing.assert_array_equal(i, ei)
+        np.testing.assert_array_equal(s, es.astype(np.float32))
