@@ -102,12 +102,14 @@ struct DevBuf {
 };
 
 struct Workspace {
+  DevBuf<int32_t> counter;     // dynamic-unit scheduler counter
   DevBuf<uint16_t> qbuf;       // bf16 staged queries
   DevBuf<float> part_s;        // partial lists
   DevBuf<int32_t> part_i;
   DevBuf<tsv::ScanItem> items;
   std::vector<tsv::ScanItem> host_items;
   void release() {
+    counter.release();
     qbuf.release();
     part_s.release();
     part_i.release();
@@ -424,6 +426,33 @@ int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int
   p.row_beg = row_beg;
   p.row_end = row_end;
   p.num_kb = (idx->dim + tsv::kBlockK - 1) / tsv::kBlockK;
+
+  if (pair && nqg <= 64 && !env_flag("TSV_STATIC_PAIR")) {
+    // Dynamic-unit pair kernel: every pair keeps one list per query; K4 merges the pairs.
+    const int npairs = idx->num_sms / 2;
+    const int stride = (kcap + 3) & ~3;
+    rc = w.counter.ensure(1);
+    if (rc) return rc;
+    rc = w.part_s.ensure(static_cast<size_t>(npairs) * B * stride);
+    if (rc) return rc;
+    rc = w.part_i.ensure(static_cast<size_t>(npairs) * B * stride);
+    if (rc) return rc;
+    TSV_CUDA(cudaMemsetAsync(w.counter.ptr, 0, sizeof(int32_t), st), "counter reset");
+    p.counter = w.counter.ptr;
+    p.flags = env_flag("TSV_DYN_CTA_WAITS") ? 1 : 0;
+    p.chunk = 1;
+    if (const char* e = getenv("TSV_DYN_CHUNK")) p.chunk = std::max(1, atoi(e));
+    p.out_k = stride;
+    p.out_scores = w.part_s.ptr;
+    p.out_ids = w.part_i.ptr;
+    rc = run_scan(idx, tsv::kPairDynMode, kcap, qb, B, p, 2 * npairs, st);
+    if (rc) return rc;
+    int e = tsv::launch_merge_topk(w.part_s.ptr, w.part_i.ptr, npairs, B, stride, B, k,
+                                   scores_dev, ids_dev, st);
+    if (e) return cuda_fail(static_cast<cudaError_t>(e), "merge launch");
+    g_launches++;
+    return TSV_OK;
+  }
   if (R == 1) {
     p.out_k = k;
     p.out_scores = scores_dev;

@@ -40,7 +40,15 @@ struct ScanParams {
   int32_t out_k;      // entries written per partial row (<= KCAP)
   float* out_scores;  // [rows][out_k]
   int32_t* out_ids;
+  // dynamic-unit pair kernel: work counter (zeroed before the launch); partial / state lists
+  // are rows pair * B + query with out_k (a multiple of 4) entries each
+  int32_t* counter;
+  int32_t flags;  // bit 0: CTA-scope (not cluster-scope) unit/accumulator barrier waits
+  int32_t chunk;  // corpus tiles per dynamic unit
 };
+
+// `mb` argument selecting the dynamic-unit CTA-pair kernel (see tsv_scan.cu).
+constexpr int kPairDynMode = 5;
 
 // `mb` argument of launch_scan_topk selecting the CTA-pair kernel: 256 queries x 256 corpus
 // rows per pair tile (tcgen05 cta_group::2); the tensor map for queries then uses 128-row
