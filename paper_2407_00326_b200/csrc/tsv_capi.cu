@@ -427,8 +427,10 @@ int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int
   p.row_end = row_end;
   p.num_kb = (idx->dim + tsv::kBlockK - 1) / tsv::kBlockK;
 
-  if (pair && nqg <= 64 && !env_flag("TSV_STATIC_PAIR")) {
-    // Dynamic-unit pair kernel: every pair keeps one list per query; K4 merges the pairs.
+  if (pair && nqg <= 64 && env_flag("TSV_DYN")) {
+    // Dynamic-unit pair kernel (experimental, opt-in): every pair keeps one list per query;
+    // K4 merges the pairs. Streams the corpus from HBM once for any B, but is slower than the
+    // static range kernel today ("dynamic units").
     const int npairs = idx->num_sms / 2;
     const int stride = (kcap + 3) & ~3;
     rc = w.counter.ensure(1);
