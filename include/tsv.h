@@ -60,6 +60,11 @@ TSV_API int64_t tsv_launch_count(void);
 
 /* Device-resident bf16 arena of up to cap_rows rows of `dim` elements (dim % 8 == 0). */
 TSV_API int tsv_index_create(int device, int dim, int metric, int64_t cap_rows, tsv_index** out);
+/* storage = TSV_BF16 (default arena, 2 B/element) or TSV_F32 (fp32 mode: each row is kept as a
+ * tf32 "hi" plane plus an fp32 residual "lo" plane, 8 B/element; search runs 3xTF32 on the
+ * tensor cores, scores within 1e-5 relative; k <= 64). */
+TSV_API int tsv_index_create2(int device, int dim, int metric, int storage, int64_t cap_rows,
+                              tsv_index** out);
 /* Wrap an existing device matrix [n_rows, dim] bf16 (already normalised for cosine) without
  * copying; the caller keeps it alive. Appends are rejected on a view. */
 TSV_API int tsv_index_create_view(int device, int dim, int metric, const void* rows_dev, int64_t n_rows,
@@ -74,7 +79,9 @@ TSV_API int tsv_index_truncate(tsv_index* idx, int64_t n);
 TSV_API int64_t tsv_index_rows(const tsv_index* idx);
 TSV_API int tsv_index_dim(const tsv_index* idx);
 TSV_API int tsv_index_metric(const tsv_index* idx);
-TSV_API const void* tsv_index_data(const tsv_index* idx);
+TSV_API const void* tsv_index_data(const tsv_index* idx);     /* bf16 rows, or the fp32 hi plane */
+TSV_API const void* tsv_index_data_lo(const tsv_index* idx);  /* fp32 residual plane (TSV_F32) */
+TSV_API int tsv_index_storage(const tsv_index* idx);
 
 /* Accumulated device time of the fused scan kernel (K1) launches issued while timing is on.
  * Reading synchronises on the recorded events. */

@@ -33,6 +33,7 @@ SIGNATURES = {
     "tsv_last_error": (ctypes.c_char_p, []),
     "tsv_launch_count": (c_i64, []),
     "tsv_index_create": (c_int, [c_int, c_int, c_int, c_i64, ctypes.POINTER(c_vp)]),
+    "tsv_index_create2": (c_int, [c_int, c_int, c_int, c_int, c_i64, ctypes.POINTER(c_vp)]),
     "tsv_index_create_view": (c_int, [c_int, c_int, c_int, c_vp, c_i64, ctypes.POINTER(c_vp)]),
     "tsv_index_destroy": (c_int, [c_vp]),
     "tsv_index_append": (c_int, [c_vp, c_vp, c_int, c_i64, ctypes.POINTER(c_i64), c_vp]),
@@ -41,6 +42,8 @@ SIGNATURES = {
     "tsv_index_dim": (c_int, [c_vp]),
     "tsv_index_metric": (c_int, [c_vp]),
     "tsv_index_data": (c_vp, [c_vp]),
+    "tsv_index_data_lo": (c_vp, [c_vp]),
+    "tsv_index_storage": (c_int, [c_vp]),
     "tsv_index_set_timing": (c_int, [c_vp, c_int]),
     "tsv_index_scan_time": (c_int, [c_vp, ctypes.POINTER(c_dbl), ctypes.POINTER(c_i64)]),
     "tsv_search": (c_int, [c_vp, c_vp, c_int, c_int, c_int, c_i64, c_i64, c_i32, c_vp, c_vp,

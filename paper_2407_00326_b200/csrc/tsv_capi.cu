@@ -58,12 +58,15 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
 }
 
 // 2-D bf16 row-major [rows, dim] map with a [box_rows, 64] box and 128 B swizzle.
-int encode_rows_map(CUtensorMap* map, const void* base, int64_t rows, int dim, int box_rows) {
+int encode_rows_map(CUtensorMap* map, const void* base, int64_t rows, int dim, int box_rows,
+                    bool f32 = false) {
   auto fn = get_encode_fn();
   if (fn == nullptr) return fail(TSV_ERR_DEVICE, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t esize = f32 ? 4 : 2;
   cuuint64_t gdim[2] = {static_cast<cuuint64_t>(dim), static_cast<cuuint64_t>(std::max<int64_t>(rows, 1))};
-  cuuint64_t gstride[1] = {static_cast<cuuint64_t>(dim) * 2};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(tsv::kBlockK), static_cast<cuuint32_t>(box_rows)};
+  cuuint64_t gstride[1] = {static_cast<cuuint64_t>(dim) * esize};
+  // one 128-byte swizzle row per box row: 64 bf16 or 32 fp32 elements
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / esize), static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estride[2] = {1, 1};
   CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_NONE;
   if (const char* e = getenv("TSV_L2_PROMO")) {
@@ -73,7 +76,8 @@ int encode_rows_map(CUtensorMap* map, const void* base, int64_t rows, int dim, i
                              : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
                                         : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   }
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), gdim, gstride,
+  CUresult r = fn(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                  const_cast<void*>(base), gdim, gstride,
                   box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promo,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(TSV_ERR_DEVICE, "cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -104,6 +108,7 @@ struct DevBuf {
 struct Workspace {
   DevBuf<int32_t> counter;     // dynamic-unit scheduler counter
   DevBuf<uint16_t> qbuf;       // bf16 staged queries
+  DevBuf<float> qhi, qlo;      // fp32-mode query planes
   DevBuf<float> part_s;        // partial lists
   DevBuf<int32_t> part_i;
   DevBuf<tsv::ScanItem> items;
@@ -111,6 +116,8 @@ struct Workspace {
   void release() {
     counter.release();
     qbuf.release();
+    qhi.release();
+    qlo.release();
     part_s.release();
     part_i.release();
     items.release();
@@ -132,6 +139,9 @@ struct tsv_index {
   bool owns = true;
   void* arena = nullptr;
   CUtensorMap tmap_c;
+  int storage = TSV_BF16;       // TSV_F32: arena = tf32 "hi" plane, arena_lo = residual plane
+  float* arena_lo = nullptr;
+  CUtensorMap tmap_c_lo;
   int num_sms = 148;
   std::map<cudaStream_t, Workspace> ws;
   bool timing = false;
@@ -213,6 +223,43 @@ int run_scan(tsv_index* idx, int mb, int kcap, const void* qb, int64_t B, tsv::S
   return TSV_OK;
 }
 
+// fp32 mode: split queries into (hi, lo) planes (normalised for cosine).
+int stage_queries_f32(tsv_index* idx, Workspace& w, const void* q, int q_dtype, int64_t B,
+                      cudaStream_t st) {
+  int rc = w.qhi.ensure(static_cast<size_t>(B) * idx->dim);
+  if (rc) return rc;
+  rc = w.qlo.ensure(static_cast<size_t>(B) * idx->dim);
+  if (rc) return rc;
+  int e = tsv::launch_split_f32(q, q_dtype == TSV_F32, B, idx->dim,
+                                idx->metric == TSV_METRIC_COSINE, w.qhi.ptr, w.qlo.ptr, st);
+  if (e) return cuda_fail(static_cast<cudaError_t>(e), "split queries");
+  g_launches++;
+  return TSV_OK;
+}
+
+int run_scan_f32(tsv_index* idx, int kcap, Workspace& w, int64_t B, tsv::ScanParams& p, int grid,
+                 cudaStream_t st) {
+  CUtensorMap tq, tq_lo;
+  int rc = encode_rows_map(&tq, w.qhi.ptr, B, idx->dim, tsv::kBlockM, true);
+  if (rc) return rc;
+  rc = encode_rows_map(&tq_lo, w.qlo.ptr, B, idx->dim, tsv::kBlockM, true);
+  if (rc) return rc;
+  TimedLaunch tl{};
+  if (idx->timing) {
+    TSV_CUDA(cudaEventCreate(&tl.a), "cudaEventCreate");
+    TSV_CUDA(cudaEventCreate(&tl.b), "cudaEventCreate");
+    TSV_CUDA(cudaEventRecord(tl.a, st), "cudaEventRecord");
+  }
+  int e = tsv::launch_scan_topk_tf32(kcap, tq, idx->tmap_c, tq_lo, idx->tmap_c_lo, p, grid, st);
+  if (e) return cuda_fail(static_cast<cudaError_t>(e), "scan_topk (fp32) launch");
+  g_launches++;
+  if (idx->timing) {
+    TSV_CUDA(cudaEventRecord(tl.b, st), "cudaEventRecord");
+    idx->timed.push_back(tl);
+  }
+  return TSV_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -238,8 +285,11 @@ static int create_common(int device, int dim, int metric, tsv_index** out) {
   return TSV_OK;
 }
 
-int tsv_index_create(int device, int dim, int metric, int64_t cap_rows, tsv_index** out) {
+int tsv_index_create2(int device, int dim, int metric, int storage, int64_t cap_rows,
+                      tsv_index** out) {
   int rc = create_common(device, dim, metric, out);
+  if (rc) return rc;
+  rc = check_dtype(storage);
   if (rc) return rc;
   if (cap_rows <= 0 || cap_rows > (int64_t(1) << 31) - 1)
     return fail(TSV_ERR_CAPACITY, "cap_rows out of range: %lld", (long long)cap_rows);
@@ -248,21 +298,32 @@ int tsv_index_create(int device, int dim, int metric, int64_t cap_rows, tsv_inde
   idx->device = device;
   idx->dim = dim;
   idx->metric = metric;
+  idx->storage = storage;
   idx->cap_rows = cap_rows;
   cudaDeviceGetAttribute(&idx->num_sms, cudaDevAttrMultiProcessorCount, device);
-  cudaError_t e = cudaMalloc(&idx->arena, static_cast<size_t>(cap_rows) * dim * 2);
+  const bool f32 = storage == TSV_F32;
+  const size_t bytes = static_cast<size_t>(cap_rows) * dim * (f32 ? 4 : 2);
+  cudaError_t e = cudaMalloc(&idx->arena, bytes);
+  if (e == cudaSuccess && f32) e = cudaMalloc(&idx->arena_lo, bytes);
   if (e != cudaSuccess) {
+    if (idx->arena) cudaFree(idx->arena);
     delete idx;
     return cuda_fail(e, "arena cudaMalloc");
   }
-  rc = encode_rows_map(&idx->tmap_c, idx->arena, cap_rows, dim, tsv::kBlockN);
+  rc = encode_rows_map(&idx->tmap_c, idx->arena, cap_rows, dim, tsv::kBlockN, f32);
+  if (!rc && f32) rc = encode_rows_map(&idx->tmap_c_lo, idx->arena_lo, cap_rows, dim, tsv::kBlockN, true);
   if (rc) {
     cudaFree(idx->arena);
+    if (idx->arena_lo) cudaFree(idx->arena_lo);
     delete idx;
     return rc;
   }
   *out = idx;
   return TSV_OK;
+}
+
+int tsv_index_create(int device, int dim, int metric, int64_t cap_rows, tsv_index** out) {
+  return tsv_index_create2(device, dim, metric, TSV_BF16, cap_rows, out);
 }
 
 int tsv_index_create_view(int device, int dim, int metric, const void* rows_dev, int64_t n_rows,
@@ -301,6 +362,7 @@ int tsv_index_destroy(tsv_index* idx) {
     cudaEventDestroy(t.b);
   }
   if (idx->owns && idx->arena) cudaFree(idx->arena);
+  if (idx->arena_lo) cudaFree(idx->arena_lo);
   delete idx;
   return TSV_OK;
 }
@@ -320,6 +382,16 @@ int tsv_index_append(tsv_index* idx, const void* rows_dev, int src_dtype, int64_
   if (rows_dev == nullptr) return fail(TSV_ERR_ARGUMENT, "rows_dev is null");
   DeviceGuard g(idx->device);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (idx->storage == TSV_F32) {
+    const size_t off = static_cast<size_t>(idx->rows) * idx->dim;
+    int e = tsv::launch_split_f32(rows_dev, src_dtype == TSV_F32, n, idx->dim,
+                                  idx->metric == TSV_METRIC_COSINE,
+                                  static_cast<float*>(idx->arena) + off, idx->arena_lo + off, st);
+    if (e) return cuda_fail(static_cast<cudaError_t>(e), "split rows");
+    g_launches++;
+    idx->rows += n;
+    return TSV_OK;
+  }
   void* dst = static_cast<uint8_t*>(idx->arena) + static_cast<size_t>(idx->rows) * idx->dim * 2;
   if (src_dtype == TSV_BF16 && idx->metric == TSV_METRIC_IP) {
     TSV_CUDA(cudaMemcpyAsync(dst, rows_dev, static_cast<size_t>(n) * idx->dim * 2,
@@ -347,6 +419,8 @@ int64_t tsv_index_rows(const tsv_index* idx) { return idx ? idx->rows : -1; }
 int tsv_index_dim(const tsv_index* idx) { return idx ? idx->dim : -1; }
 int tsv_index_metric(const tsv_index* idx) { return idx ? idx->metric : -1; }
 const void* tsv_index_data(const tsv_index* idx) { return idx ? idx->arena : nullptr; }
+const void* tsv_index_data_lo(const tsv_index* idx) { return idx ? idx->arena_lo : nullptr; }
+int tsv_index_storage(const tsv_index* idx) { return idx ? idx->storage : -1; }
 
 int tsv_index_set_timing(tsv_index* idx, int enable) {
   if (idx == nullptr) return fail(TSV_ERR_ARGUMENT, "index is null");
@@ -392,14 +466,18 @@ int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int
   DeviceGuard g(idx->device);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   Workspace& w = idx->ws[st];
+  const bool f32 = idx->storage == TSV_F32;
+  if (f32 && kcap > tsv::kMaxKF32)
+    return fail(TSV_ERR_CONFIG, "k=%d exceeds the fp32-mode maximum (%d)", k, tsv::kMaxKF32);
 
   const void* qb = nullptr;
-  rc = stage_queries(idx, w, q_dev, q_dtype, B, st, &qb);
+  rc = f32 ? stage_queries_f32(idx, w, q_dev, q_dtype, B, st)
+           : stage_queries(idx, w, q_dev, q_dtype, B, st, &qb);
   if (rc) return rc;
 
   // B > 128: CTA-pair kernel (256 queries x 256 rows per pair tile); otherwise one CTA per
   // 128-query group with 128-row tiles.
-  const bool pair = B > tsv::kBlockM && kcap <= tsv::kMaxRegK && !env_flag("TSV_NO_PAIR");
+  const bool pair = !f32 && B > tsv::kBlockM && kcap <= tsv::kMaxRegK && !env_flag("TSV_NO_PAIR");
   const int mb = pair ? tsv::kPairMode : 1;
   const int qg = pair ? tsv::kPairQG : tsv::kBlockM;
   const int tile_rows = pair ? tsv::kPairTileRows : tsv::kBlockN;
@@ -425,7 +503,8 @@ int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int
   p.id_offset = id_offset;
   p.row_beg = row_beg;
   p.row_end = row_end;
-  p.num_kb = (idx->dim + tsv::kBlockK - 1) / tsv::kBlockK;
+  const int kb_elems = f32 ? 32 : tsv::kBlockK;  // elements per 128-byte k-block row
+  p.num_kb = (idx->dim + kb_elems - 1) / kb_elems;
 
   if (pair && nqg <= 64 && env_flag("TSV_DYN")) {
     // Dynamic-unit pair kernel (experimental, opt-in): every pair keeps one list per query;
@@ -459,7 +538,8 @@ int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int
     p.out_k = k;
     p.out_scores = scores_dev;
     p.out_ids = ids_dev;
-    return run_scan(idx, mb, kcap, qb, B, p, grid, st);
+    return f32 ? run_scan_f32(idx, kcap, w, B, p, grid, st)
+               : run_scan(idx, mb, kcap, qb, B, p, grid, st);
   }
   p.out_k = kcap;
   rc = w.part_s.ensure(static_cast<size_t>(R) * B * kcap);
@@ -468,7 +548,8 @@ int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int
   if (rc) return rc;
   p.out_scores = w.part_s.ptr;
   p.out_ids = w.part_i.ptr;
-  rc = run_scan(idx, mb, kcap, qb, B, p, grid, st);
+  rc = f32 ? run_scan_f32(idx, kcap, w, B, p, grid, st)
+           : run_scan(idx, mb, kcap, qb, B, p, grid, st);
   if (rc) return rc;
   int e = tsv::launch_merge_topk(w.part_s.ptr, w.part_i.ptr, R, B, kcap, B, k, scores_dev, ids_dev,
                                  st);
@@ -504,11 +585,15 @@ int tsv_search_segmented(tsv_index* idx, const void* q_dev, int q_dtype, int nse
   DeviceGuard g(idx->device);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   Workspace& w = idx->ws[st];
+  const bool f32 = idx->storage == TSV_F32;
+  if (f32 && kcap > tsv::kMaxKF32)
+    return fail(TSV_ERR_CONFIG, "k=%d exceeds the fp32-mode maximum (%d)", k, tsv::kMaxKF32);
   const void* qb = nullptr;
-  rc = stage_queries(idx, w, q_dev, q_dtype, B, st, &qb);
+  rc = f32 ? stage_queries_f32(idx, w, q_dev, q_dtype, B, st)
+           : stage_queries(idx, w, q_dev, q_dtype, B, st, &qb);
   if (rc) return rc;
 
-  const int mb = (max_q > tsv::kBlockM && kcap <= tsv::kMaxRegK) ? 2 : 1;
+  const int mb = (!f32 && max_q > tsv::kBlockM && kcap <= tsv::kMaxRegK) ? 2 : 1;
   const int qg = mb * tsv::kBlockM;
   int units = 0;
   for (int s = 0; s < nseg; ++s) units += (seg_q_beg[s + 1] - seg_q_beg[s] + qg - 1) / qg;
@@ -545,13 +630,15 @@ int tsv_search_segmented(tsv_index* idx, const void* q_dev, int q_dtype, int nse
   tsv::ScanParams p{};
   p.items = w.items.ptr;
   p.num_items = static_cast<int>(hi.size());
-  p.num_kb = (idx->dim + tsv::kBlockK - 1) / tsv::kBlockK;
+  const int kb_elems = f32 ? 32 : tsv::kBlockK;
+  p.num_kb = (idx->dim + kb_elems - 1) / kb_elems;
   const int grid = std::min(p.num_items, idx->num_sms);
   if (R == 1) {
     p.out_k = k;
     p.out_scores = scores_dev;
     p.out_ids = ids_dev;
-    return run_scan(idx, mb, kcap, qb, B, p, grid, st);
+    return f32 ? run_scan_f32(idx, kcap, w, B, p, grid, st)
+               : run_scan(idx, mb, kcap, qb, B, p, grid, st);
   }
   p.out_k = kcap;
   rc = w.part_s.ensure(static_cast<size_t>(R) * B * kcap);
@@ -560,7 +647,8 @@ int tsv_search_segmented(tsv_index* idx, const void* q_dev, int q_dtype, int nse
   if (rc) return rc;
   p.out_scores = w.part_s.ptr;
   p.out_ids = w.part_i.ptr;
-  rc = run_scan(idx, mb, kcap, qb, B, p, grid, st);
+  rc = f32 ? run_scan_f32(idx, kcap, w, B, p, grid, st)
+           : run_scan(idx, mb, kcap, qb, B, p, grid, st);
   if (rc) return rc;
   int e = tsv::launch_merge_topk(w.part_s.ptr, w.part_i.ptr, R, B, kcap, B, k, scores_dev, ids_dev,
                                  st);
@@ -582,15 +670,26 @@ int tsv_rerank(tsv_index* idx, const void* q_dev, int q_dtype, int B, const int3
   DeviceGuard g(idx->device);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const void* q = q_dev;
+  const float* q_lo = nullptr;
   int q_f32 = q_dtype == TSV_F32;
-  if (idx->metric == TSV_METRIC_COSINE) {
+  const bool f32 = idx->storage == TSV_F32;
+  if (f32) {  // exact fp32 question (hi + lo) against the hi + lo rows
+    Workspace& w = idx->ws[st];
+    rc = stage_queries_f32(idx, w, q_dev, q_dtype, B, st);
+    if (rc) return rc;
+    q = w.qhi.ptr;
+    q_lo = w.qlo.ptr;
+    q_f32 = 1;
+  } else if (idx->metric == TSV_METRIC_COSINE) {
     Workspace& w = idx->ws[st];
     rc = stage_queries(idx, w, q_dev, q_dtype, B, st, &q);
     if (rc) return rc;
     q_f32 = 0;
   }
-  int e = tsv::launch_rerank(idx->arena, idx->rows, idx->dim, q, q_f32, B, cand_ids_dev, C, k,
-                             scores_dev, ids_dev, st);
+  int e = tsv::launch_rerank(f32 ? nullptr : idx->arena,
+                             f32 ? static_cast<const float*>(idx->arena) : nullptr,
+                             f32 ? idx->arena_lo : nullptr, idx->rows, idx->dim, q, q_lo, q_f32,
+                             B, cand_ids_dev, C, k, scores_dev, ids_dev, st);
   if (e) return cuda_fail(static_cast<cudaError_t>(e), "rerank launch");
   g_launches++;
   return TSV_OK;

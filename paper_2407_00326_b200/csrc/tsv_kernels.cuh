@@ -61,6 +61,14 @@ constexpr int kPairTileRows = 256;
 int launch_scan_topk(int mb, int kcap, const CUtensorMap& tmap_q, const CUtensorMap& tmap_c,
                      const ScanParams& p, int grid, cudaStream_t stream);
 int scan_kcap_for(int k);  // smallest supported list capacity >= k (0 if unsupported)
+// fp32 mode (3xTF32): hi / lo planes of queries and corpus, single-CTA kernel, k <= 64
+int launch_scan_topk_tf32(int kcap, const CUtensorMap& tmap_q, const CUtensorMap& tmap_c,
+                          const CUtensorMap& tmap_q_lo, const CUtensorMap& tmap_c_lo,
+                          const ScanParams& p, int grid, cudaStream_t stream);
+constexpr int kMaxKF32 = 64;
+// Split rows into tf32 hi / residual lo planes (fp32 storage), optionally L2-normalised.
+int launch_split_f32(const void* src, int src_is_f32, int64_t n, int dim, int do_normalize,
+                     float* hi, float* lo, cudaStream_t stream);
 constexpr int kMaxRegK = 32;   // larger k uses shared-memory lists (single-CTA, 128 queries)
 constexpr int kMaxK = 128;
 
@@ -68,8 +76,9 @@ int launch_merge_topk(const float* in_s, const int32_t* in_id, int lists, int B,
                       int64_t list_stride_rows, int kout, float* out_s, int32_t* out_id,
                       cudaStream_t stream, int dedup = 0);
 
-int launch_rerank(const void* arena, int64_t nrows, int dim, const void* q, int q_is_f32,
-                  int B, const int32_t* cand, int C, int k, float* out_s, int32_t* out_id,
+int launch_rerank(const void* arena, const float* arena_hi, const float* arena_lo, int64_t nrows,
+                  int dim, const void* q, const float* q_lo, int q_is_f32, int B,
+                  const int32_t* cand, int C, int k, float* out_s, int32_t* out_id,
                   cudaStream_t stream);
 
 int launch_normalize(const void* src, int src_is_f32, int64_t n, int dim, int do_normalize,

@@ -114,9 +114,10 @@ __global__ void merge_topk_kernel(const float* __restrict__ in_s, const int32_t*
 // question vector, drop duplicate ids, keep the best k.
 template <int kThreads>
 __global__ void __launch_bounds__(kThreads) rerank_kernel(
-    const __nv_bfloat16* __restrict__ arena, int64_t nrows, int dim, const void* __restrict__ q,
-    int q_is_f32, const int32_t* __restrict__ cand, int C, int k, float* __restrict__ out_s,
-    int32_t* __restrict__ out_id) {
+    const __nv_bfloat16* __restrict__ arena, const float* __restrict__ arena_hi,
+    const float* __restrict__ arena_lo, int64_t nrows, int dim, const void* __restrict__ q,
+    const float* __restrict__ q_lo, int q_is_f32, const int32_t* __restrict__ cand, int C, int k,
+    float* __restrict__ out_s, int32_t* __restrict__ out_id) {
   extern __shared__ uint8_t sm[];
   float* qv = reinterpret_cast<float*>(sm);                       // dim floats
   uint64_t* keys = reinterpret_cast<uint64_t*>(sm + ((dim * 4 + 15) & ~15));
@@ -125,9 +126,9 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(
   constexpr int kWarps = kThreads / 32;
 
   for (int d = threadIdx.x; d < dim; d += kThreads) {
-    qv[d] = q_is_f32 ? reinterpret_cast<const float*>(q)[static_cast<int64_t>(b) * dim + d]
-                     : __bfloat162float(
-                           reinterpret_cast<const __nv_bfloat16*>(q)[static_cast<int64_t>(b) * dim + d]);
+    const int64_t o = static_cast<int64_t>(b) * dim + d;
+    qv[d] = q_is_f32 ? reinterpret_cast<const float*>(q)[o] + (q_lo ? q_lo[o] : 0.f)
+                     : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(q)[o]);
   }
   const int np = pow2_ceil(C);
   for (int i = threadIdx.x; i < np; i += kThreads) keys[i] = pad_key();
@@ -137,9 +138,21 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(
   for (int c = warp; c < C; c += kWarps) {
     const int32_t id = cand[static_cast<int64_t>(b) * C + c];
     if (id < 0 || id >= nrows) continue;  // warp-uniform
-    const uint4* row = reinterpret_cast<const uint4*>(arena + static_cast<int64_t>(id) * dim);
     float acc = 0.f;
-    for (int ch = lane; ch < chunks; ch += 32) {
+    if (arena_hi != nullptr) {  // fp32 storage: row = hi + lo, fp32 FMA
+      const float4* hi = reinterpret_cast<const float4*>(arena_hi + static_cast<int64_t>(id) * dim);
+      const float4* lo = reinterpret_cast<const float4*>(arena_lo + static_cast<int64_t>(id) * dim);
+      for (int ch = lane; ch < (dim >> 2); ch += 32) {
+        const float4 h = __ldg(hi + ch), l = __ldg(lo + ch);
+        const float* qq = qv + ch * 4;
+        acc = fmaf(h.x + l.x, qq[0], acc);
+        acc = fmaf(h.y + l.y, qq[1], acc);
+        acc = fmaf(h.z + l.z, qq[2], acc);
+        acc = fmaf(h.w + l.w, qq[3], acc);
+      }
+    }
+    const uint4* row = reinterpret_cast<const uint4*>(arena + static_cast<int64_t>(id) * dim);
+    for (int ch = lane; arena_hi == nullptr && ch < chunks; ch += 32) {
       const uint4 raw = __ldg(row + ch);
       const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
       const float* qq = qv + ch * 8;
@@ -200,7 +213,45 @@ __global__ void normalize_kernel(const void* __restrict__ src, int src_is_f32, i
   }
 }
 
+// One warp per row: optional L2 normalisation (fp32) and split into a tf32 "hi" plane (low 13
+// mantissa bits cleared) and the fp32 residual "lo" = x - hi, so hi*hi + hi*lo + lo*hi on the
+// tf32 tensor cores reproduces fp32 products to ~2^-21 relative (fp32 mode, K1f).
+__global__ void split_f32_kernel(const void* __restrict__ src, int src_is_f32, int64_t n, int dim,
+                                 int do_normalize, float* __restrict__ hi, float* __restrict__ lo) {
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  const float* sf = reinterpret_cast<const float*>(src) + row * dim;
+  const __nv_bfloat16* sb = reinterpret_cast<const __nv_bfloat16*>(src) + row * dim;
+  float ss = 0.f;
+  if (do_normalize) {
+    for (int d = lane; d < dim; d += 32) {
+      const float x = src_is_f32 ? sf[d] : __bfloat162float(sb[d]);
+      ss = fmaf(x, x, ss);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  }
+  const float scale = (do_normalize && ss > 0.f) ? 1.0f / sqrtf(ss) : 1.f;
+  for (int d = lane; d < dim; d += 32) {
+    const float x = (src_is_f32 ? sf[d] : __bfloat162float(sb[d])) * scale;
+    const float h = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+    hi[row * dim + d] = h;
+    lo[row * dim + d] = x - h;
+  }
+}
+
 }  // namespace
+
+int launch_split_f32(const void* src, int src_is_f32, int64_t n, int dim, int do_normalize,
+                     float* hi, float* lo, cudaStream_t stream) {
+  if (n <= 0) return 0;
+  constexpr int kWarps = 8;
+  const int64_t blocks = (n + kWarps - 1) / kWarps;
+  split_f32_kernel<<<static_cast<unsigned>(blocks), kWarps * 32, 0, stream>>>(
+      src, src_is_f32, n, dim, do_normalize, hi, lo);
+  return static_cast<int>(cudaGetLastError());
+}
 
 int launch_merge_topk(const float* in_s, const int32_t* in_id, int lists, int B, int kin,
                       int64_t list_stride_rows, int kout, float* out_s, int32_t* out_id,
@@ -221,7 +272,8 @@ int launch_merge_topk(const float* in_s, const int32_t* in_id, int lists, int B,
   return static_cast<int>(cudaGetLastError());
 }
 
-int launch_rerank(const void* arena, int64_t nrows, int dim, const void* q, int q_is_f32, int B,
+int launch_rerank(const void* arena, const float* arena_hi, const float* arena_lo, int64_t nrows,
+                  int dim, const void* q, const float* q_lo, int q_is_f32, int B,
                   const int32_t* cand, int C, int k, float* out_s, int32_t* out_id,
                   cudaStream_t stream) {
   if (B <= 0) return 0;
@@ -236,8 +288,8 @@ int launch_rerank(const void* arena, int64_t nrows, int dim, const void* q, int 
     if (e != cudaSuccess) return static_cast<int>(e);
   }
   rerank_kernel<kThreads><<<B, kThreads, smem, stream>>>(
-      reinterpret_cast<const __nv_bfloat16*>(arena), nrows, dim, q, q_is_f32, cand, C, k, out_s,
-      out_id);
+      reinterpret_cast<const __nv_bfloat16*>(arena), arena_hi, arena_lo, nrows, dim, q, q_lo,
+      q_is_f32, cand, C, k, out_s, out_id);
   return static_cast<int>(cudaGetLastError());
 }
 

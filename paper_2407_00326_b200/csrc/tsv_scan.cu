@@ -27,22 +27,31 @@ namespace {
 // entry j of thread t at [j * 128 + t], so lock-step accesses are bank-conflict free).
 constexpr int kRegListMax = 32;
 
-template <int MB, int KCAP = 1>
+// TF32 = fp32 mode (K1f): operands are fp32 (hi, lo) splits, 32 elements per 128-byte k-block
+// row, three kind::tf32 MMAs per k-step (hi*hi + hi*lo + lo*hi).
+template <int MB, int KCAP = 1, bool TF32 = false>
 struct ScanCfg {
   static constexpr bool kSmemList = KCAP > kRegListMax;
-  static constexpr int kABytes = kBlockM * kBlockK * 2;            // 16 KB
-  static constexpr int kBBytes = kBlockN * kBlockK * 2;            // 16 KB
-  static constexpr int kStageBytes = MB * kABytes + kBBytes;
+  static constexpr int kParts = TF32 ? 2 : 1;                      // hi (+ lo) planes
+  static constexpr int kABytes = kBlockM * 128;                    // 16 KB per plane tile
+  static constexpr int kBBytes = kBlockN * 128;                    // 16 KB per plane tile
+  static constexpr int kStageBytes = kParts * (MB * kABytes + kBBytes);
   static constexpr int kListBytes = kSmemList ? kBlockM * KCAP * 8 : 0;
   static constexpr int kStages =
-      kSmemList ? (227 * 1024 - 2048 - kListBytes) / kStageBytes : (MB == 2 ? 4 : 6);
-  static constexpr int kAccCols = MB * kBlockN;                    // per accumulator buffer
-  static constexpr int kTmemCols = 2 * kAccCols;                   // double buffered
+      (kSmemList || TF32) ? (227 * 1024 - 2048 - kListBytes) / kStageBytes : (MB == 2 ? 4 : 6);
+  // fp32 mode keeps three accumulators per tile (hi*hi of even k-blocks, of odd k-blocks, and
+  // the small hi*lo + lo*hi terms): the tensor core accumulates with truncation, so fewer
+  // additions per accumulator keep the sum within 1e-5; they are added (round-to-nearest) in
+  // the epilogue. That needs 384 columns, so fp32 mode runs single-buffered.
+  static constexpr int kAccBufs = TF32 ? 1 : 2;
+  static constexpr int kAccCols = TF32 ? 3 * kBlockN : MB * kBlockN;  // per accumulator buffer
+  static constexpr int kTmemCols = TF32 ? 512 : 2 * kAccCols;
   static constexpr int kEpiWarps = MB * 4;
   static constexpr int kThreads = (kNumNonEpiWarps + kEpiWarps) * 32;
   static constexpr int kBarBytes = 256;
   static constexpr int kSmemBytes = kStages * kStageBytes + kListBytes + kBarBytes + 1024;
   static_assert(!kSmemList || MB == 1, "shared-memory lists need one query tile per CTA");
+  static_assert(!TF32 || MB == 1, "fp32 mode uses one query tile per CTA");
   static_assert(kStages >= 2, "not enough shared memory for the pipeline");
 };
 
@@ -145,11 +154,14 @@ __device__ __forceinline__ void scan_chunk_smem(const uint32_t (&v)[32], float* 
   }
 }
 
-template <int MB, int KCAP>
-__global__ void __launch_bounds__(ScanCfg<MB, KCAP>::kThreads, 1)
+template <int MB, int KCAP, bool TF32>
+__global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
     scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_q,
-                     const __grid_constant__ CUtensorMap tmap_c, const ScanParams p) {
-  using Cfg = ScanCfg<MB, KCAP>;
+                     const __grid_constant__ CUtensorMap tmap_c,
+                     const __grid_constant__ CUtensorMap tmap_q_lo,
+                     const __grid_constant__ CUtensorMap tmap_c_lo, const ScanParams p) {
+  using Cfg = ScanCfg<MB, KCAP, TF32>;
+  constexpr int kElemsPerKb = TF32 ? 32 : kBlockK;  // elements per 128-byte k-block row
   constexpr int kStages = Cfg::kStages;
   constexpr int kQG = MB * kBlockM;
   constexpr bool kSmemList = Cfg::kSmemList;
@@ -215,10 +227,17 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP>::kThreads, 1)
           ptx::mbar_arrive_expect_tx_warp(&full_bar[stage], Cfg::kStageBytes);
 #pragma unroll
           for (int mb = 0; mb < MB; ++mb)
-            ptx::tma_load_2d_warp(st + mb * Cfg::kABytes, &tmap_q, &full_bar[stage], kb * kBlockK,
-                                  it.q_begin + mb * kBlockM, pol_q);
-          ptx::tma_load_2d_warp(st + MB * Cfg::kABytes, &tmap_c, &full_bar[stage], kb * kBlockK,
-                                row0, pol_c);
+            ptx::tma_load_2d_warp(st + mb * Cfg::kABytes, &tmap_q, &full_bar[stage],
+                                  kb * kElemsPerKb, it.q_begin + mb * kBlockM, pol_q);
+          ptx::tma_load_2d_warp(st + MB * Cfg::kABytes, &tmap_c, &full_bar[stage],
+                                kb * kElemsPerKb, row0, pol_c);
+          if constexpr (TF32) {  // lo planes follow the hi planes in the stage
+            uint8_t* lo = st + MB * Cfg::kABytes + Cfg::kBBytes;
+            ptx::tma_load_2d_warp(lo, &tmap_q_lo, &full_bar[stage], kb * kElemsPerKb,
+                                  it.q_begin, pol_q);
+            ptx::tma_load_2d_warp(lo + Cfg::kABytes, &tmap_c_lo, &full_bar[stage],
+                                  kb * kElemsPerKb, row0, pol_c);
+          }
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
@@ -230,6 +249,7 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP>::kThreads, 1)
     // ------------------------------------------------------------ MMA issuer
     // Warp-uniform loop; descriptors are built from the smem base plus compile-time offsets.
     constexpr uint32_t idesc = ptx::idesc_bf16_f32(kBlockM, kBlockN);
+    constexpr uint32_t idesc_tf32 = ptx::idesc_tf32_f32(kBlockM, kBlockN);
     const uint64_t desc0 = ptx::umma_desc_sw128(ptx::smem_u32(smem));
     int stage = 0;
     uint32_t phase = 0;
@@ -247,6 +267,23 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP>::kThreads, 1)
           ptx::mbar_wait(&full_bar[stage], phase);
           ptx::tc_fence_after();
           const uint64_t sdesc = desc0 + static_cast<uint64_t>((stage * Cfg::kStageBytes) >> 4);
+          if constexpr (TF32) {
+            // 3xTF32: hi*hi + hi*lo + lo*hi, each K=8 fp32 (32 bytes) per instruction
+            const uint64_t a_hi = sdesc;
+            const uint64_t b_hi = sdesc + static_cast<uint64_t>(Cfg::kABytes >> 4);
+            const uint64_t a_lo = sdesc + static_cast<uint64_t>((Cfg::kABytes + Cfg::kBBytes) >> 4);
+            const uint64_t b_lo = a_lo + static_cast<uint64_t>(Cfg::kABytes >> 4);
+            const uint32_t d_main = d0 + (kb & 1) * kBlockN;
+            const uint32_t d_small = d0 + 2 * kBlockN;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              ptx::mma_tf32_ss_warp(d_main, a_hi + 2 * k, b_hi + 2 * k, idesc_tf32,
+                                    ((kb >> 1) | k) != 0 ? 1u : 0u);
+              ptx::mma_tf32_ss_warp(d_small, a_hi + 2 * k, b_lo + 2 * k, idesc_tf32,
+                                    (kb | k) != 0 ? 1u : 0u);
+              ptx::mma_tf32_ss_warp(d_small, a_lo + 2 * k, b_hi + 2 * k, idesc_tf32, 1u);
+            }
+          } else {
 #pragma unroll
           for (int k = 0; k < kBlockK / 16; ++k) {
 #pragma unroll
@@ -257,6 +294,7 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP>::kThreads, 1)
                                    idesc, (kb | k) != 0 ? 1u : 0u);
             }
           }
+          }
           ptx::mma_commit_warp(&empty_bar[stage]);
           if (++stage == kStages) {
             stage = 0;
@@ -264,8 +302,10 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP>::kThreads, 1)
           }
         }
         ptx::mma_commit_warp(&tfull_bar[abuf]);
-        abuf ^= 1;
-        if (abuf == 0) aphase ^= 1;
+        if (++abuf == Cfg::kAccBufs) {
+          abuf = 0;
+          aphase ^= 1;
+        }
       }
     }
   } else if (warp >= kNumNonEpiWarps) {
@@ -303,6 +343,26 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP>::kThreads, 1)
         ptx::mbar_wait(&tfull_bar[abuf], aphase);
         ptx::tc_fence_after();
         const uint32_t taddr = lane_addr + abuf * Cfg::kAccCols;
+        if constexpr (TF32) {
+          // score = even-k hi*hi + odd-k hi*hi + (hi*lo + lo*hi), added round-to-nearest
+#pragma unroll 1
+          for (int c = 0; c < kBlockN; c += 32) {
+            uint32_t va[32], vb[32], vc[32];
+            ptx::tmem_ld_32x32b_x32(taddr + c, va);
+            ptx::tmem_ld_32x32b_x32(taddr + kBlockN + c, vb);
+            ptx::tmem_ld_32x32b_x32(taddr + 2 * kBlockN + c, vc);
+            ptx::tmem_ld_wait();
+            const float odd = p.num_kb > 1 ? 1.f : 0.f;  // odd-k accumulator unused if 1 k-block
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              va[j] = __float_as_uint(__uint_as_float(va[j]) + odd * __uint_as_float(vb[j]) +
+                                      __uint_as_float(vc[j]));
+            if constexpr (kSmemList)
+              scan_chunk_smem<KCAP>(va, list_s, list_i, t_epi, tau, id0 + c, valid - c);
+            else
+              scan_chunk<kRegK>(va, s, id, id0 + c, valid - c);
+          }
+        } else {
 #pragma unroll 1
         for (int c = 0; c < kBlockN; c += 64) {
           uint32_t va[32], vb[32];
@@ -317,10 +377,13 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP>::kThreads, 1)
             scan_chunk<kRegK>(vb, s, id, id0 + c + 32, valid - c - 32);
           }
         }
+        }
         ptx::tc_fence_before();
         ptx::mbar_arrive(&tempty_bar[abuf]);
-        abuf ^= 1;
-        if (abuf == 0) aphase ^= 1;
+        if (++abuf == Cfg::kAccBufs) {
+          abuf = 0;
+          aphase ^= 1;
+        }
       }
       if (lq < it.q_count) {
         float* os = p.out_scores + (it.out_row + lq) * p.out_k;
@@ -876,15 +939,17 @@ int launch_pair_impl(const CUtensorMap& tq, const CUtensorMap& tc, const ScanPar
   return static_cast<int>(cudaGetLastError());
 }
 
-template <int MB, int KCAP>
+template <int MB, int KCAP, bool TF32 = false>
 int launch_impl(const CUtensorMap& tq, const CUtensorMap& tc, const ScanParams& p, int grid,
-                cudaStream_t stream) {
-  using Cfg = ScanCfg<MB, KCAP>;
-  auto kern = scan_topk_kernel<MB, KCAP>;
+                cudaStream_t stream, const CUtensorMap* tq_lo = nullptr,
+                const CUtensorMap* tc_lo = nullptr) {
+  using Cfg = ScanCfg<MB, KCAP, TF32>;
+  auto kern = scan_topk_kernel<MB, KCAP, TF32>;
   cudaError_t err =
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
   if (err != cudaSuccess) return static_cast<int>(err);
-  kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, stream>>>(tq, tc, p);
+  kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, stream>>>(tq, tc, tq_lo ? *tq_lo : tq,
+                                                          tc_lo ? *tc_lo : tc, p);
   return static_cast<int>(cudaGetLastError());
 }
 
@@ -923,11 +988,32 @@ int dispatch_pair(int kcap, const CUtensorMap& tq, const CUtensorMap& tc, const 
 
 }  // namespace
 
+int dispatch_tf32(int kcap, const CUtensorMap& tq, const CUtensorMap& tc, const CUtensorMap& tq_lo,
+                  const CUtensorMap& tc_lo, const ScanParams& p, int grid, cudaStream_t stream) {
+  switch (kcap) {
+    case 1: return launch_impl<1, 1, true>(tq, tc, p, grid, stream, &tq_lo, &tc_lo);
+    case 4: return launch_impl<1, 4, true>(tq, tc, p, grid, stream, &tq_lo, &tc_lo);
+    case 8: return launch_impl<1, 8, true>(tq, tc, p, grid, stream, &tq_lo, &tc_lo);
+    case 10: return launch_impl<1, 10, true>(tq, tc, p, grid, stream, &tq_lo, &tc_lo);
+    case 16: return launch_impl<1, 16, true>(tq, tc, p, grid, stream, &tq_lo, &tc_lo);
+    case 32: return launch_impl<1, 32, true>(tq, tc, p, grid, stream, &tq_lo, &tc_lo);
+    case 64: return launch_impl<1, 64, true>(tq, tc, p, grid, stream, &tq_lo, &tc_lo);
+    default: return static_cast<int>(cudaErrorInvalidValue);
+  }
+}
+
 int scan_kcap_for(int k) {
   static const int caps[] = {1, 4, 8, 10, 16, 32, 64, 128};
   for (int c : caps)
     if (k <= c) return c;
   return 0;
+}
+
+int launch_scan_topk_tf32(int kcap, const CUtensorMap& tmap_q, const CUtensorMap& tmap_c,
+                          const CUtensorMap& tmap_q_lo, const CUtensorMap& tmap_c_lo,
+                          const ScanParams& p, int grid, cudaStream_t stream) {
+  if (grid <= 0) return 0;
+  return dispatch_tf32(kcap, tmap_q, tmap_c, tmap_q_lo, tmap_c_lo, p, grid, stream);
 }
 
 int launch_scan_topk(int mb, int kcap, const CUtensorMap& tmap_q, const CUtensorMap& tmap_c,

@@ -40,21 +40,29 @@ def _stream_handle(stream: torch.cuda.Stream | None, device: torch.device) -> in
 class _ArenaView:
     """__cuda_array_interface__ exporter so torch can alias the arena without a copy."""
 
-    def __init__(self, ptr: int, rows: int, dim: int):
+    def __init__(self, ptr: int, rows: int, dim: int, typestr: str = "<u2"):
         self.__cuda_array_interface__ = {
-            "shape": (rows, dim), "typestr": "<u2", "data": (ptr, False), "version": 3,
+            "shape": (rows, dim), "typestr": typestr, "data": (ptr, False), "version": 3,
             "strides": None,
         }
+
+
+STORAGE = {"bf16": nat.TSV_BF16, "f32": nat.TSV_F32}
 
 
 class DeviceIndex:
     """A bf16 corpus arena on one GPU (reference role: the vector DB behind `vdb-search0`)."""
 
     def __init__(self, dim: int, capacity: int, metric: str = "ip", device: int | None = None,
-                 _handle: int | None = None, _keepalive: torch.Tensor | None = None):
+                 storage: str = "bf16", _handle: int | None = None,
+                 _keepalive: torch.Tensor | None = None):
+        """storage="f32" is the fp32 mode: rows kept as tf32 hi + fp32 residual planes, search
+        by 3xTF32 tensor-core products (scores within 1e-5 relative, k <= 64)."""
         lib = nat.load()
         if metric not in METRICS:
             raise ConfigParse(f"unknown metric {metric!r}")
+        if storage not in STORAGE:
+            raise ConfigParse(f"unknown storage {storage!r}")
         self.metric = metric
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
         self._keepalive = _keepalive
@@ -62,10 +70,11 @@ class DeviceIndex:
             self._h = ctypes.c_void_p(_handle)
         else:
             h = ctypes.c_void_p()
-            nat.check(lib.tsv_index_create(self.device.index, int(dim), METRICS[metric],
-                                           int(capacity), ctypes.byref(h)))
+            nat.check(lib.tsv_index_create2(self.device.index, int(dim), METRICS[metric],
+                                            STORAGE[storage], int(capacity), ctypes.byref(h)))
             self._h = h
         self.dim = int(lib.tsv_index_dim(self._h))
+        self.storage = "f32" if lib.tsv_index_storage(self._h) == nat.TSV_F32 else "bf16"
 
     @classmethod
     def view(cls, rows: torch.Tensor, metric: str = "ip") -> "DeviceIndex":
@@ -97,10 +106,23 @@ class DeviceIndex:
         return int(nat.load().tsv_index_rows(self._h))
 
     def data(self) -> torch.Tensor:
-        """Aliasing bf16 tensor [rows, dim] over the arena (what the kernels read)."""
+        """bf16 storage: aliasing tensor [rows, dim] over the arena (what the kernels read).
+        f32 storage: the fp32 rows the kernels represent (hi + lo planes, a new tensor)."""
+        if self.storage == "f32":
+            hi, lo = self.planes()
+            return hi + lo
         ptr = nat.load().tsv_index_data(self._h)
         t = torch.as_tensor(_ArenaView(ptr, self.rows, self.dim), device=self.device)
         return t.view(torch.bfloat16)
+
+    def planes(self) -> tuple[torch.Tensor, torch.Tensor]:
+        """fp32 mode: aliasing (hi, lo) float32 tensors [rows, dim]."""
+        if self.storage != "f32":
+            raise ConfigParse("planes() needs an f32-storage index")
+        lib = nat.load()
+        mk = lambda ptr: torch.as_tensor(_ArenaView(ptr, self.rows, self.dim, "<f4"),
+                                         device=self.device)
+        return mk(lib.tsv_index_data(self._h)), mk(lib.tsv_index_data_lo(self._h))
 
     def append(self, rows: torch.Tensor, stream: torch.cuda.Stream | None = None) -> int:
         """Ingest rows (normalised for cosine); returns the arena row of the first one."""

@@ -240,3 +240,42 @@ def test_c2_full_size_properties(cuda):
     np.testing.assert_allclose(gs, rescored, rtol=TOL)
     sub = np.r_[0:8, 128:136]
     assert_topk(s[sub], i[sub], qn[sub], cn, k, TOL)
+
+
+@pytest.mark.parametrize("n,dim,b,k", [(20000, 256, 64, 10), (5000, 1024, 300, 32),
+                                       (3333, 96, 5, 64), (50, 64, 3, 10)])
+def test_fp32_mode_matches_oracle_at_1e5(cuda, n, dim, b, k):
+    """fp32 mode (K1f, 3xTF32): scores within 1e-5 relative of the exact fp32 products."""
+    import torch
+    from paper_2407_00326_b200.index import DeviceIndex
+
+    rng = np.random.default_rng(21)
+    raw = rng.standard_normal((n, dim)).astype(np.float32)
+    idx = DeviceIndex(dim, n, metric="cosine", device=cuda.index, storage="f32")
+    idx.append(torch.from_numpy(raw).to(cuda))
+    hi, lo = idx.planes()
+    stored = (hi.double() + lo.double()).cpu().numpy()
+    ref = raw / np.linalg.norm(raw, axis=1, keepdims=True)
+    np.testing.assert_allclose(stored, ref, atol=1e-6)
+    qraw = rng.standard_normal((b, dim)).astype(np.float32)
+    qraw[: b // 2] = raw[rng.integers(0, n, b // 2)] + 0.01 * qraw[: b // 2]
+    s, i = idx.search(torch.from_numpy(qraw).to(cuda), k)
+    qn = (qraw / np.linalg.norm(qraw, axis=1, keepdims=True)).astype(np.float64)
+    # the device normalises in fp32; compare against the exact products of those vectors
+    probs = orc.check_topk(from_dev(s), from_dev(i), qn, stored, k, 1e-5)
+    assert not probs, probs[:5]
+
+
+def test_fp32_mode_rerank(cuda):
+    import torch
+    from paper_2407_00326_b200.index import DeviceIndex
+
+    rng = np.random.default_rng(22)
+    raw = rng.standard_normal((4000, 128)).astype(np.float32)
+    idx = DeviceIndex(128, 4000, metric="ip", device=cuda.index, storage="f32")
+    idx.append(torch.from_numpy(raw).to(cuda))
+    q = rng.standard_normal((8, 128)).astype(np.float32)
+    cand = rng.integers(0, 4000, size=(8, 100)).astype(np.int32)
+    s, i = idx.rerank(torch.from_numpy(q).to(cuda), torch.from_numpy(cand).to(cuda), 5)
+    es, ei = orc.rerank(q.astype(np.float64), raw.astype(np.float64), cand, 5)
+    np.testing.assert_allclose(from_dev(s), es, rtol=1e-5)
