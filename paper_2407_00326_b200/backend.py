@@ -246,7 +246,9 @@ class RetrievalBackend:
         return seg
 
     # -- execution ------------------------------------------------------------------------
-    def execute(self, profile: EngineProfile, plan, t: float, instance) -> tuple[float, float | None]:
+    def launch(self, profile: EngineProfile, plan, instance):
+        """Enqueue the batch's kernels on the replica stream without waiting; returns the
+        (start, end) CUDA events bracketing them."""
         if not plan.entries:
             raise CapacityExceeded("empty batch")
         rep = self.replica_for(instance)
@@ -260,6 +262,12 @@ class RetrievalBackend:
                 self._rerank_batch(rep, plan)
             end.record(rep.stream)
         self.launches += 1
+        return start, end
+
+    def execute(self, profile: EngineProfile, plan, t: float, instance) -> tuple[float, float | None]:
+        """Simulator hook: run the batch; duration = profile latency ("profile") or the device
+        time of the launches ("measured", synchronises on the batch's end event)."""
+        start, end = self.launch(profile, plan, instance)
         if self.timing == TIMING_MEASURED:
             end.synchronize()
             ms = start.elapsed_time(end)

@@ -1,0 +1,158 @@
+"""Real-time stream/event execution of e-graphs, and CUDA-graph capture of a search.
+
+Replaces the reference's threaded execution mode (pkg/src/teola_sim/threaded.py:130-182:
+one Python thread per engine forming batches under a lock and sleeping `latency / speed`).
+Here one host thread runs the same two-tier scheduler as the simulator (the mirror in
+runtime.py: per-query graph tier, form_batch_topo / form_batch_blind, select_instance), but:
+
+  * GPU engines (`vdb-search0`, `rerank0`) launch their batch on the chosen replica's CUDA
+    stream and return immediately; the batch completes when its end event completes
+    (polled, no host blocking), so batches on different replicas run concurrently and stage
+    pipelines of different queries overlap;
+  * Aggregate joins are stream-ordered (cudaStreamWaitEvent + concat/K4 in the backend), so
+    no host synchronisation sits between search stages and the rerank that consumes them;
+  * modelled engines (LLM, embedding, ingest, web) complete after their profile latency in
+    wall time divided by `speed` (the threaded mode's semantics).
+
+Timestamps in the trace are wall-clock milliseconds x speed since start (threaded.py:58-59).
+
+`CapturedSearch` captures a fixed-shape search (query staging + fused scan + merge) into a
+CUDA graph and replays it: one graph launch per batch instead of three kernel launches, for
+the launch-bound small-batch retrieval of per-query workflows.
+"""
+
+from __future__ import annotations
+
+import heapq
+import math
+import time
+
+import torch
+
+from .engines import EngineSet
+from .runtime import BatchRecord, RuntimeOptions, Simulator
+
+
+class StreamRuntime(Simulator):
+    """Wall-clock execution of submitted e-graphs; retrieval batches complete on CUDA events."""
+
+    def __init__(self, engines: EngineSet, backend, options: RuntimeOptions | None = None,
+                 speed: float = 1.0, poll_us: float = 20.0, timeout_s: float = 60.0):
+        super().__init__(engines, options, backend=backend)
+        self.speed = speed
+        self.poll_s = poll_us * 1e-6
+        self.timeout_s = timeout_s
+        self._t0 = None
+        self._inflight: list[tuple] = []  # (end_event, start_event, state, instance, plan, t)
+
+    def _wall(self) -> float:
+        return (time.perf_counter() - self._t0) * 1000.0 * self.speed
+
+    # GPU batches: launch and return; completion is discovered by polling the end event.
+    def _dispatch(self, state, plan, t):
+        profile = state.profile
+        if not (self.backend is not None and self.backend.serves(profile)
+                and plan.phase == "general"):
+            return super()._dispatch(state, plan, t)
+        from .engines import select_instance
+
+        instance = select_instance(state.instances, profile.category, t)
+        assert instance is not None
+        start, end = self.backend.launch(profile, plan, instance)
+        instance.busy_until = math.inf  # busy until the end event fires
+        instance.executed_requests += sum(n for _, n in plan.entries)
+        for task, n in plan.entries:
+            task.next_request += n
+            self._emit(t, task.ctx, task.node, "batch")
+            if task.ctx.stats[task.node_id].first_start_ms is None:
+                task.ctx.stats[task.node_id].first_start_ms = t
+                self._emit(t, task.ctx, task.node, "start")
+        state.queue = [task for task in state.queue if task.pending() > 0]
+        self._inflight.append((end, start, state, instance, plan, t))
+
+    def _poll(self, t: float) -> bool:
+        done, still = [], []
+        for x in self._inflight:
+            (done if x[0].query() else still).append(x)
+        if not done:
+            return False
+        self._inflight = still
+        for end, start, state, instance, plan, t0 in done:
+            instance.busy_until = t
+            device_ms = start.elapsed_time(end)
+            for task, n in plan.entries:
+                self._push(t, self._REQ_DONE, (task, n))
+            self._push(t, self._BATCH_DONE, (state.profile.engine_id, instance.instance_id, 0.0))
+            self.trace.batches.append(BatchRecord(state.profile.engine_id, instance.instance_id,
+                                                  t0, t, plan.load, self._cap(state), plan.phase,
+                                                  plan.node_ids(), device_ms))
+        return True
+
+    def run(self, until: float | None = None):
+        self._t0 = time.perf_counter()
+        deadline = time.perf_counter() + self.timeout_s
+        while self._events or self._inflight:
+            if time.perf_counter() > deadline:
+                raise TimeoutError("stream runtime did not quiesce")
+            t = self._wall()
+            progressed = self._poll(t)
+            while self._events and self._events[0][0] <= t:
+                ts, _, tag, payload = heapq.heappop(self._events)
+                self.now = ts
+                self._handle(tag, payload, ts)
+                progressed = True
+            for eid in sorted(self._dirty):
+                self._try_form(eid, t)
+            self._dirty.clear()
+            if not progressed:
+                nxt = self._events[0][0] if self._events else math.inf
+                wait_s = min(self.poll_s, max(0.0, (nxt - t) / 1000.0 / self.speed))
+                if wait_s > 0:
+                    time.sleep(wait_s)
+        if self.backend is not None:
+            self.backend.finish()
+        return self.trace
+
+
+def run_streamed(engines: EngineSet, graphs_with_arrivals, backend,
+                 options: RuntimeOptions | None = None, speed: float = 1.0):
+    """Submit (graph, arrival_ms) pairs and execute them in real time on CUDA streams."""
+    rt = StreamRuntime(engines, backend, options, speed=speed)
+    for g, arrival in graphs_with_arrivals:
+        rt.submit_query(g, arrival, arrival_ms=arrival)
+    return rt, rt.run()
+
+
+class CapturedSearch:
+    """A fixed-shape search captured in a CUDA graph.
+
+    search(q) copies q into the captured input buffer and replays the graph; results land in
+    the captured output buffers (returned, valid until the next call)."""
+
+    def __init__(self, index, batch: int, k: int, row_range: tuple[int, int] | None = None,
+                 id_offset: int = 0, dtype=torch.bfloat16, warmup: int = 2):
+        self.index = index
+        dev = index.device
+        self.q = torch.zeros((batch, index.dim), dtype=dtype, device=dev)
+        self.scores = torch.empty((batch, k), dtype=torch.float32, device=dev)
+        self.ids = torch.empty((batch, k), dtype=torch.int32, device=dev)
+        self.k = k
+        self.row_range = row_range
+        self.id_offset = id_offset
+        stream = torch.cuda.Stream(dev)
+        with torch.cuda.stream(stream):
+            for _ in range(warmup):  # grows the per-stream workspace before capture
+                self._run(stream)
+        stream.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=stream, capture_error_mode="thread_local"):
+            self._run(torch.cuda.current_stream(dev))
+
+    def _run(self, stream):
+        self.index.search(self.q, self.k, row_range=self.row_range, id_offset=self.id_offset,
+                          stream=stream, out=(self.scores, self.ids))
+
+    def search(self, q: torch.Tensor):
+        self.q.copy_(q)
+        self.graph.replay()
+        return self.scores, self.ids
