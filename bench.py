@@ -45,6 +45,8 @@ def parse_args():
     ap.add_argument("--dim", type=int, default=1024)
     ap.add_argument("--batch", type=int, default=1024)
     ap.add_argument("--k", type=int, default=10)
+    ap.add_argument("--storage", choices=("bf16", "bf16_tiled", "f32"), default="bf16",
+                    help="f32 = fp32 mode (3xTF32 tensor-core products, scores within 1e-5)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU time of the bounded cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -199,8 +201,9 @@ def run_reference(args):
 
 def _config(args, shard_rows):
     return {
-        "workload": f"C4/metric: flat inner-product (cosine) search, {args.rows}x{args.dim} bf16 "
-                    f"corpus, batch {args.batch}, k={args.k}",
+        "workload": f"C4/metric: flat inner-product (cosine) search, {args.rows}x{args.dim} "
+                    f"{getattr(args, 'storage', 'bf16')} corpus, batch {args.batch}, k={args.k}",
+        "storage": getattr(args, "storage", "bf16"),
         "rows": args.rows, "dim": args.dim, "batch": args.batch, "k": args.k,
         "shard_rows": shard_rows, "parallelism": f"corpus-shard x{args.gpus}",
         "l2": "inputs larger than L2 (corpus streamed from HBM every step)",
@@ -208,13 +211,13 @@ def _config(args, shard_rows):
 
 
 # ---------------------------------------------------------------------- our arm
-def build_shard(idx_cls, rows, dim, lo, hi, device):
+def build_shard(idx_cls, rows, dim, lo, hi, device, storage="bf16"):
     """Corpus rows [lo, hi) of the global seeded corpus; chunk c of 2^20 rows is drawn from a
     generator seeded with c, so the corpus is identical for every sharding."""
     import torch
 
     chunk = 1 << 20
-    idx = idx_cls(dim, hi - lo, metric="cosine", device=device.index)
+    idx = idx_cls(dim, hi - lo, metric="cosine", device=device.index, storage=storage)
     c0 = lo // chunk
     while c0 * chunk < hi:
         a, b = c0 * chunk, min(rows, (c0 + 1) * chunk)
@@ -247,7 +250,7 @@ def run_ours(args):
 
     B, D, k, N = args.batch, args.dim, args.k, args.rows
     lo, hi = shard_range(N, rank, world)
-    idx = build_shard(DeviceIndex, N, D, lo, hi, dev)
+    idx = build_shard(DeviceIndex, N, D, lo, hi, dev, storage=args.storage)
 
     g = torch.Generator(device=dev).manual_seed(1)
     q_dev = normalize_rows(torch.randn((B, D), generator=g, device=dev))
@@ -318,6 +321,12 @@ def run_ours(args):
     achieved_gbs = bytes_alg / (avg_scan_ms / 1000.0) / 1e9
     peak_tf = float(peaks.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"]))
     peak_tf_sus = float(peaks.get("bf16_tflops_sustained", FALLBACK_PEAKS["bf16_tflops_sustained"]))
+    if args.storage == "f32":
+        # fp32 mode: 3 tf32 MMAs per product; tf32 dense rate is half the bf16 rate, so the
+        # algorithmic-fp32-flop ceiling is bf16 / 6 (no measured tf32 peak in MEASURED_PEAKS)
+        peak_tf /= 6.0
+        peak_tf_sus /= 6.0
+        bytes_alg = n_local * D * 8 + B * D * 4 + B * k * 8
     peak_bw = float(peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"]))
     t_tc = flops / (peak_tf * 1e12)
     t_bw = bytes_alg / (peak_bw * 1e9)
@@ -341,8 +350,10 @@ def run_ours(args):
                  "avg_launch_ms": avg_scan_ms, "launches_timed": scan_launches,
                  "algorithmic_flops_per_launch": flops,
                  "algorithmic_bytes_per_launch": bytes_alg,
-                 "peak_source": f"{peak_src} (MEASURED_PEAKS.json burst bf16 / copy GB/s)"
-                 if peak_src == "measured" else "fallback (B200_PROFILING.md)"})
+                 "peak_source": (f"{peak_src} (MEASURED_PEAKS.json burst bf16 / copy GB/s)"
+                                 if peak_src == "measured" else "fallback (B200_PROFILING.md)")
+                 + (" / 6 for fp32 mode (3 tf32 MMAs at half the bf16 rate)"
+                    if args.storage == "f32" else "")})
 
     value = B * args.steps / (dev_ms / 1000.0)
     e2e_value = B * args.steps / (e2e_ms / 1000.0)
@@ -362,7 +373,8 @@ def run_ours(args):
             "metric": "vector-search queries/s (10Mx1024 corpus, k=10)",
             "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32 (3xTF32)" if args.storage == "f32" else "bf16",
             "data": "synthetic (seeded N(0,1) rows and queries, L2-normalised on device)",
             "config": _config(args, n_local),
             "e2e": {"value": e2e_value, "unit": "queries/s",

@@ -45,6 +45,10 @@ enum {
 };
 
 enum { TSV_BF16 = 0, TSV_F32 = 1 };               /* element types */
+/* arena storage: TSV_BF16 (row-major), TSV_F32 (fp32 mode), TSV_BF16_TILED (row-major within
+ * contiguous 16 KB [128 rows x 64 elements] k-block tiles: the scan streams whole tiles; row
+ * ranges passed to the search calls must start at multiples of 128) */
+enum { TSV_BF16_TILED = 2 };
 enum { TSV_METRIC_IP = 0, TSV_METRIC_COSINE = 1 }; /* cosine = IP over L2-normalised rows */
 
 typedef struct tsv_index tsv_index;

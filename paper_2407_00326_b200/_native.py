@@ -18,6 +18,7 @@ LIB_PATH = Path(__file__).resolve().parent / "lib" / "libtsv.so"
 
 TSV_BF16 = 0
 TSV_F32 = 1
+TSV_BF16_TILED = 2
 TSV_METRIC_IP = 0
 TSV_METRIC_COSINE = 1
 

@@ -84,6 +84,24 @@ int encode_rows_map(CUtensorMap* map, const void* base, int64_t rows, int dim, i
   return TSV_OK;
 }
 
+// Tiled arena (TSV_BF16_TILED): 3-D view {64 elements, 128 rows, tiles * kblocks}; each box is
+// one contiguous 16 KB [128 x 64] k-block tile.
+int encode_tiled_map(CUtensorMap* map, const void* base, int64_t cap_rows, int dim) {
+  auto fn = get_encode_fn();
+  if (fn == nullptr) return fail(TSV_ERR_DEVICE, "cuTensorMapEncodeTiled unavailable");
+  const int64_t kbs = (dim + 63) / 64;
+  const int64_t tiles = (cap_rows + 127) / 128;
+  cuuint64_t gdim[3] = {64, 128, static_cast<cuuint64_t>(tiles * kbs)};
+  cuuint64_t gstride[2] = {128, 128 * 128};
+  cuuint32_t box[3] = {64, 128, 1};
+  cuuint32_t estride[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), gdim, gstride,
+                  box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(TSV_ERR_DEVICE, "cuTensorMapEncodeTiled (3d) failed (%d)", (int)r);
+  return TSV_OK;
+}
+
 template <typename T>
 struct DevBuf {
   T* ptr = nullptr;
@@ -289,8 +307,8 @@ int tsv_index_create2(int device, int dim, int metric, int storage, int64_t cap_
                       tsv_index** out) {
   int rc = create_common(device, dim, metric, out);
   if (rc) return rc;
-  rc = check_dtype(storage);
-  if (rc) return rc;
+  if (storage != TSV_BF16 && storage != TSV_F32 && storage != TSV_BF16_TILED)
+    return fail(TSV_ERR_CONFIG, "unknown storage %d", storage);
   if (cap_rows <= 0 || cap_rows > (int64_t(1) << 31) - 1)
     return fail(TSV_ERR_CAPACITY, "cap_rows out of range: %lld", (long long)cap_rows);
   DeviceGuard g(device);
@@ -302,15 +320,20 @@ int tsv_index_create2(int device, int dim, int metric, int storage, int64_t cap_
   idx->cap_rows = cap_rows;
   cudaDeviceGetAttribute(&idx->num_sms, cudaDevAttrMultiProcessorCount, device);
   const bool f32 = storage == TSV_F32;
-  const size_t bytes = static_cast<size_t>(cap_rows) * dim * (f32 ? 4 : 2);
+  const bool tiled = storage == TSV_BF16_TILED;
+  const size_t bytes = tiled ? static_cast<size_t>((cap_rows + 127) / 128) * 128 *
+                                   ((dim + 63) / 64) * 64 * 2
+                             : static_cast<size_t>(cap_rows) * dim * (f32 ? 4 : 2);
   cudaError_t e = cudaMalloc(&idx->arena, bytes);
   if (e == cudaSuccess && f32) e = cudaMalloc(&idx->arena_lo, bytes);
+  if (e == cudaSuccess && tiled) e = cudaMemset(idx->arena, 0, bytes);  // zero k padding
   if (e != cudaSuccess) {
     if (idx->arena) cudaFree(idx->arena);
     delete idx;
     return cuda_fail(e, "arena cudaMalloc");
   }
-  rc = encode_rows_map(&idx->tmap_c, idx->arena, cap_rows, dim, tsv::kBlockN, f32);
+  rc = tiled ? encode_tiled_map(&idx->tmap_c, idx->arena, cap_rows, dim)
+             : encode_rows_map(&idx->tmap_c, idx->arena, cap_rows, dim, tsv::kBlockN, f32);
   if (!rc && f32) rc = encode_rows_map(&idx->tmap_c_lo, idx->arena_lo, cap_rows, dim, tsv::kBlockN, true);
   if (rc) {
     cudaFree(idx->arena);
@@ -392,6 +415,14 @@ int tsv_index_append(tsv_index* idx, const void* rows_dev, int src_dtype, int64_
     idx->rows += n;
     return TSV_OK;
   }
+  if (idx->storage == TSV_BF16_TILED) {
+    int e = tsv::launch_scatter_tiled(rows_dev, src_dtype == TSV_F32, n, idx->dim,
+                                      idx->metric == TSV_METRIC_COSINE, idx->arena, idx->rows, st);
+    if (e) return cuda_fail(static_cast<cudaError_t>(e), "scatter rows");
+    g_launches++;
+    idx->rows += n;
+    return TSV_OK;
+  }
   void* dst = static_cast<uint8_t*>(idx->arena) + static_cast<size_t>(idx->rows) * idx->dim * 2;
   if (src_dtype == TSV_BF16 && idx->metric == TSV_METRIC_IP) {
     TSV_CUDA(cudaMemcpyAsync(dst, rows_dev, static_cast<size_t>(n) * idx->dim * 2,
@@ -467,6 +498,9 @@ int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   Workspace& w = idx->ws[st];
   const bool f32 = idx->storage == TSV_F32;
+  const bool tiled = idx->storage == TSV_BF16_TILED;
+  if (tiled && row_beg % 128 != 0)
+    return fail(TSV_ERR_CONFIG, "tiled index: row_beg must be a multiple of 128");
   if (f32 && kcap > tsv::kMaxKF32)
     return fail(TSV_ERR_CONFIG, "k=%d exceeds the fp32-mode maximum (%d)", k, tsv::kMaxKF32);
 
@@ -505,6 +539,7 @@ int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int
   p.row_end = row_end;
   const int kb_elems = f32 ? 32 : tsv::kBlockK;  // elements per 128-byte k-block row
   p.num_kb = (idx->dim + kb_elems - 1) / kb_elems;
+  if (tiled) p.flags |= tsv::kFlagTiled;
 
   if (pair && nqg <= 64 && env_flag("TSV_DYN")) {
     // Dynamic-unit pair kernel (experimental, opt-in): every pair keeps one list per query;
@@ -533,6 +568,13 @@ int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int
     if (e) return cuda_fail(static_cast<cudaError_t>(e), "merge launch");
     g_launches++;
     return TSV_OK;
+  }
+  if (pair && nqg > 1 && num_items <= units && !env_flag("TSV_NO_LOCKSTEP")) {
+    rc = w.counter.ensure(static_cast<size_t>(num_items));
+    if (rc) return rc;
+    TSV_CUDA(cudaMemsetAsync(w.counter.ptr, 0, sizeof(int32_t) * num_items, st), "progress reset");
+    p.counter = w.counter.ptr;
+    p.flags |= tsv::kFlagLockstep;
   }
   if (R == 1) {
     p.out_k = k;
@@ -586,6 +628,10 @@ int tsv_search_segmented(tsv_index* idx, const void* q_dev, int q_dtype, int nse
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   Workspace& w = idx->ws[st];
   const bool f32 = idx->storage == TSV_F32;
+  const bool tiled = idx->storage == TSV_BF16_TILED;
+  for (int s_ = 0; tiled && s_ < nseg; ++s_)
+    if (seg_row_beg[s_] % 128 != 0)
+      return fail(TSV_ERR_CONFIG, "tiled index: segment %d must start at a multiple of 128", s_);
   if (f32 && kcap > tsv::kMaxKF32)
     return fail(TSV_ERR_CONFIG, "k=%d exceeds the fp32-mode maximum (%d)", k, tsv::kMaxKF32);
   const void* qb = nullptr;
@@ -632,6 +678,7 @@ int tsv_search_segmented(tsv_index* idx, const void* q_dev, int q_dtype, int nse
   p.num_items = static_cast<int>(hi.size());
   const int kb_elems = f32 ? 32 : tsv::kBlockK;
   p.num_kb = (idx->dim + kb_elems - 1) / kb_elems;
+  if (tiled) p.flags |= tsv::kFlagTiled;
   const int grid = std::min(p.num_items, idx->num_sms);
   if (R == 1) {
     p.out_k = k;
@@ -689,7 +736,8 @@ int tsv_rerank(tsv_index* idx, const void* q_dev, int q_dtype, int B, const int3
   int e = tsv::launch_rerank(f32 ? nullptr : idx->arena,
                              f32 ? static_cast<const float*>(idx->arena) : nullptr,
                              f32 ? idx->arena_lo : nullptr, idx->rows, idx->dim, q, q_lo, q_f32,
-                             B, cand_ids_dev, C, k, scores_dev, ids_dev, st);
+                             B, cand_ids_dev, C, k, scores_dev, ids_dev, st,
+                             idx->storage == TSV_BF16_TILED);
   if (e) return cuda_fail(static_cast<cudaError_t>(e), "rerank launch");
   g_launches++;
   return TSV_OK;

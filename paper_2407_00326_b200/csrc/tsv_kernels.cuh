@@ -44,11 +44,18 @@ struct ScanParams {
   // are rows pair * B + query with out_k (a multiple of 4) entries each
   int32_t* counter;
   int32_t flags;  // bit 0: CTA-scope (not cluster-scope) unit/accumulator barrier waits
+                  // bit 1: corpus map is the tiled layout (3-D: 64 x 128 x tiles*kblocks)
   int32_t chunk;  // corpus tiles per dynamic unit
 };
 
 // `mb` argument selecting the dynamic-unit CTA-pair kernel (see tsv_scan.cu).
 constexpr int kPairDynMode = 5;
+constexpr int kFlagTiled = 2;
+constexpr int kFlagLockstep = 4;  // static pair kernel: bound drift between range partners
+// Tiled arena layout: row i, element d at ((i/128 * KB + d/64) * 128 + i%128) * 64 + d%64,
+// KB = ceil(dim/64): every [128 rows x 64 elements] k-block tile is one contiguous 16 KB block.
+int launch_scatter_tiled(const void* src, int src_is_f32, int64_t n, int dim, int do_normalize,
+                         void* arena, int64_t first_row, cudaStream_t stream);
 
 // `mb` argument of launch_scan_topk selecting the CTA-pair kernel: 256 queries x 256 corpus
 // rows per pair tile (tcgen05 cta_group::2); the tensor map for queries then uses 128-row
@@ -79,7 +86,7 @@ int launch_merge_topk(const float* in_s, const int32_t* in_id, int lists, int B,
 int launch_rerank(const void* arena, const float* arena_hi, const float* arena_lo, int64_t nrows,
                   int dim, const void* q, const float* q_lo, int q_is_f32, int B,
                   const int32_t* cand, int C, int k, float* out_s, int32_t* out_id,
-                  cudaStream_t stream);
+                  cudaStream_t stream, int tiled = 0);
 
 int launch_normalize(const void* src, int src_is_f32, int64_t n, int dim, int do_normalize,
                      void* dst_bf16, cudaStream_t stream);

@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(
     const __nv_bfloat16* __restrict__ arena, const float* __restrict__ arena_hi,
     const float* __restrict__ arena_lo, int64_t nrows, int dim, const void* __restrict__ q,
     const float* __restrict__ q_lo, int q_is_f32, const int32_t* __restrict__ cand, int C, int k,
-    float* __restrict__ out_s, int32_t* __restrict__ out_id) {
+    float* __restrict__ out_s, int32_t* __restrict__ out_id, int tiled) {
   extern __shared__ uint8_t sm[];
   float* qv = reinterpret_cast<float*>(sm);                       // dim floats
   uint64_t* keys = reinterpret_cast<uint64_t*>(sm + ((dim * 4 + 15) & ~15));
@@ -152,8 +152,12 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(
       }
     }
     const uint4* row = reinterpret_cast<const uint4*>(arena + static_cast<int64_t>(id) * dim);
+    // tiled layout: 16-byte chunk ch of row id lives in k-block tile (id/128, ch/8)
+    const uint4* trow = reinterpret_cast<const uint4*>(
+        arena + ((static_cast<int64_t>(id) >> 7) * ((dim + 63) >> 6) * 128 + (id & 127)) * 64);
     for (int ch = lane; arena_hi == nullptr && ch < chunks; ch += 32) {
-      const uint4 raw = __ldg(row + ch);
+      const uint4 raw = tiled ? __ldg(trow + static_cast<int64_t>(ch >> 3) * 1024 + (ch & 7))
+                              : __ldg(row + ch);
       const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
       const float* qq = qv + ch * 8;
 #pragma unroll
@@ -241,7 +245,46 @@ __global__ void split_f32_kernel(const void* __restrict__ src, int src_is_f32, i
   }
 }
 
+// Tiled-layout ingest: one warp per row, optional L2 normalisation, bf16 cast, and scatter of
+// the row's 64-element k-block pieces into their [128 x 64] tiles.
+__global__ void scatter_tiled_kernel(const void* __restrict__ src, int src_is_f32, int64_t n,
+                                     int dim, int do_normalize, __nv_bfloat16* __restrict__ arena,
+                                     int64_t first_row) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= n) return;
+  const float* sf = reinterpret_cast<const float*>(src) + r * dim;
+  const __nv_bfloat16* sb = reinterpret_cast<const __nv_bfloat16*>(src) + r * dim;
+  float ss = 0.f;
+  if (do_normalize) {
+    for (int d = lane; d < dim; d += 32) {
+      const float x = src_is_f32 ? sf[d] : __bfloat162float(sb[d]);
+      ss = fmaf(x, x, ss);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  }
+  const float scale = (do_normalize && ss > 0.f) ? rsqrtf(ss) : 1.f;
+  const int64_t row = first_row + r;
+  const int kbs = (dim + 63) >> 6;
+  __nv_bfloat16* base = arena + ((row >> 7) * kbs * 128 + (row & 127)) * 64;
+  for (int d = lane; d < dim; d += 32) {
+    const float x = src_is_f32 ? sf[d] : __bfloat162float(sb[d]);
+    base[static_cast<int64_t>(d >> 6) * 128 * 64 + (d & 63)] = __float2bfloat16_rn(x * scale);
+  }
+}
+
 }  // namespace
+
+int launch_scatter_tiled(const void* src, int src_is_f32, int64_t n, int dim, int do_normalize,
+                         void* arena, int64_t first_row, cudaStream_t stream) {
+  if (n <= 0) return 0;
+  constexpr int kWarps = 8;
+  const int64_t blocks = (n + kWarps - 1) / kWarps;
+  scatter_tiled_kernel<<<static_cast<unsigned>(blocks), kWarps * 32, 0, stream>>>(
+      src, src_is_f32, n, dim, do_normalize, reinterpret_cast<__nv_bfloat16*>(arena), first_row);
+  return static_cast<int>(cudaGetLastError());
+}
 
 int launch_split_f32(const void* src, int src_is_f32, int64_t n, int dim, int do_normalize,
                      float* hi, float* lo, cudaStream_t stream) {
@@ -275,7 +318,7 @@ int launch_merge_topk(const float* in_s, const int32_t* in_id, int lists, int B,
 int launch_rerank(const void* arena, const float* arena_hi, const float* arena_lo, int64_t nrows,
                   int dim, const void* q, const float* q_lo, int q_is_f32, int B,
                   const int32_t* cand, int C, int k, float* out_s, int32_t* out_id,
-                  cudaStream_t stream) {
+                  cudaStream_t stream, int tiled) {
   if (B <= 0) return 0;
   int np = 1;
   while (np < C) np <<= 1;
@@ -289,7 +332,7 @@ int launch_rerank(const void* arena, const float* arena_hi, const float* arena_l
   }
   rerank_kernel<kThreads><<<B, kThreads, smem, stream>>>(
       reinterpret_cast<const __nv_bfloat16*>(arena), arena_hi, arena_lo, nrows, dim, q, q_lo,
-      q_is_f32, cand, C, k, out_s, out_id);
+      q_is_f32, cand, C, k, out_s, out_id, tiled);
   return static_cast<int>(cudaGetLastError());
 }
 

@@ -259,6 +259,33 @@ __device__ __forceinline__ void mma2_commit_mc_warp(uint64_t* bar, uint16_t mask
 }
 // TMA load into this CTA's smem whose completion is reported to the pair leader's mbarrier
 // (bar_cluster_addr: shared::cluster address of the leader's barrier).
+// 3-D tiled loads (corpus in the tiled arena layout: coordinate z selects one contiguous
+// [128 rows x 128 B] block).
+__device__ __forceinline__ void tma_load_3d_warp(void* smem_dst, const CUtensorMap* map,
+                                                 uint64_t* bar, int32_t c0, int32_t c1, int32_t c2,
+                                                 uint64_t policy) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t.reg .b32 r;\n\t"
+      "elect.sync r|e, 0xffffffff;\n\t"
+      "@e cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;\n\t}" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2),
+      "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_pair_warp(void* smem_dst, const CUtensorMap* map,
+                                                      uint32_t bar_cluster_addr, int32_t c0,
+                                                      int32_t c1, int32_t c2, uint64_t policy) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t.reg .b32 r;\n\t"
+      "elect.sync r|e, 0xffffffff;\n\t"
+      "@e cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6;\n\t}" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster_addr), "r"(c0), "r"(c1), "r"(c2),
+      "l"(policy)
+      : "memory");
+}
+
 __device__ __forceinline__ void tma_load_2d_pair_warp(void* smem_dst, const CUtensorMap* map,
                                                       uint32_t bar_cluster_addr, int32_t c0,
                                                       int32_t c1, uint64_t policy) {

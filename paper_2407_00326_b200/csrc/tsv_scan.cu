@@ -229,8 +229,12 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
           for (int mb = 0; mb < MB; ++mb)
             ptx::tma_load_2d_warp(st + mb * Cfg::kABytes, &tmap_q, &full_bar[stage],
                                   kb * kElemsPerKb, it.q_begin + mb * kBlockM, pol_q);
-          ptx::tma_load_2d_warp(st + MB * Cfg::kABytes, &tmap_c, &full_bar[stage],
-                                kb * kElemsPerKb, row0, pol_c);
+          if (p.flags & kFlagTiled)  // row0 is a multiple of 128 in the tiled layout
+            ptx::tma_load_3d_warp(st + MB * Cfg::kABytes, &tmap_c, &full_bar[stage], 0, 0,
+                                  (row0 >> 7) * p.num_kb + kb, pol_c);
+          else
+            ptx::tma_load_2d_warp(st + MB * Cfg::kABytes, &tmap_c, &full_bar[stage],
+                                  kb * kElemsPerKb, row0, pol_c);
           if constexpr (TF32) {  // lo planes follow the hi planes in the stage
             uint8_t* lo = st + MB * Cfg::kABytes + Cfg::kBBytes;
             ptx::tma_load_2d_warp(lo, &tmap_q_lo, &full_bar[stage], kb * kElemsPerKb,
@@ -422,6 +426,8 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
 // issues tcgen05.mma.cta_group::2 and each CTA's TMEM receives its own 128 query rows x 256
 // columns. Per SM this halves the shared-memory operand bytes per MAC compared with the
 // single-CTA 128x128 tile, which is what keeps the tensor pipe fed.
+constexpr int kLockWindow = 4;  // tiles a pair may run ahead of its range partners
+
 struct Pair {
   static constexpr int kTileRows = 256;                 // corpus rows per pair tile (N)
   static constexpr int kQG = 256;                       // queries per pair (M)
@@ -485,11 +491,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
     const uint64_t pol_c = ptx::policy_evict_normal();
     int stage = 0;
     uint32_t phase = 0;
+    // Range lockstep (flag bit 2): the pairs that stream the same corpus range for different
+    // query groups publish their tile progress and none runs more than kLockWindow tiles ahead,
+    // so each corpus tile is fetched from HBM once and served to the others from L2.
+    const bool lockstep = (p.flags & kFlagLockstep) && p.items == nullptr && num_items <= npairs;
+    volatile int32_t* progress = p.counter;
     for (int i = pair; i < num_items; i += npairs) {
       ScanItem it;
       resolve_item(p, i, it, Pair::kQG, Pair::kTileRows);
       const int64_t ntiles = (it.row_end - it.row_begin + Pair::kTileRows - 1) / Pair::kTileRows;
+      const int my_qg = i / p.R, my_r = i - (i / p.R) * p.R;
+      const int nqg = num_items / p.R;
       for (int64_t t = 0; t < ntiles; ++t) {
+        if (lockstep && leader && lane == 0) {
+          if ((t & 1) == 0) progress[i] = static_cast<int32_t>(t);
+          if (t >= kLockWindow) {
+            for (int g = 0; g < nqg; ++g) {
+              if (g == my_qg) continue;
+              while (progress[g * p.R + my_r] < t - kLockWindow) __nanosleep(256);
+            }
+          }
+        }
+        __syncwarp();
         const int32_t row0 = static_cast<int32_t>(it.row_begin + t * Pair::kTileRows) + rank * 128;
         for (int kb = 0; kb < p.num_kb; ++kb) {
           ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -497,13 +520,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
           const uint32_t fb = ptx::mapa(ptx::smem_u32(&full_bar[stage]), 0);
           if (leader) ptx::mbar_arrive_expect_tx_warp(&full_bar[stage], 2 * Pair::kStageBytes);
           ptx::tma_load_2d_pair_warp(st, &tmap_q, fb, kb * kBlockK, it.q_begin + rank * 128, pol_q);
-          ptx::tma_load_2d_pair_warp(st + Pair::kHalfBytes, &tmap_c, fb, kb * kBlockK, row0, pol_c);
+          if (p.flags & kFlagTiled)
+            ptx::tma_load_3d_pair_warp(st + Pair::kHalfBytes, &tmap_c, fb, 0, 0,
+                                       (row0 >> 7) * p.num_kb + kb, pol_c);
+          else
+            ptx::tma_load_2d_pair_warp(st + Pair::kHalfBytes, &tmap_c, fb, kb * kBlockK, row0,
+                                       pol_c);
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
       }
+      if (lockstep && leader && lane == 0) progress[i] = 0x7fffffff;  // range done
     }
   } else if (warp == 1) {
     // ---- MMA issuer (leader CTA only)
@@ -741,7 +770,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
         const uint32_t fb = ptx::mapa(ptx::smem_u32(&full_bar[stage]), 0);
         if (leader) ptx::mbar_arrive_expect_tx_warp(&full_bar[stage], 2 * Pair::kStageBytes);
         ptx::tma_load_2d_pair_warp(st, &tmap_q, fb, kb * kBlockK, q0, pol_q);
-        ptx::tma_load_2d_pair_warp(st + Pair::kHalfBytes, &tmap_c, fb, kb * kBlockK, row0, pol_c);
+        if (p.flags & kFlagTiled)
+          ptx::tma_load_3d_pair_warp(st + Pair::kHalfBytes, &tmap_c, fb, 0, 0,
+                                     (row0 >> 7) * p.num_kb + kb, pol_c);
+        else
+          ptx::tma_load_2d_pair_warp(st + Pair::kHalfBytes, &tmap_c, fb, kb * kBlockK, row0, pol_c);
         if (++stage == kStages) {
           stage = 0;
           phase ^= 1;

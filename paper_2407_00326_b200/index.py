@@ -47,7 +47,7 @@ class _ArenaView:
         }
 
 
-STORAGE = {"bf16": nat.TSV_BF16, "f32": nat.TSV_F32}
+STORAGE = {"bf16": nat.TSV_BF16, "f32": nat.TSV_F32, "bf16_tiled": nat.TSV_BF16_TILED}
 
 
 class DeviceIndex:
@@ -74,7 +74,7 @@ class DeviceIndex:
                                             STORAGE[storage], int(capacity), ctypes.byref(h)))
             self._h = h
         self.dim = int(lib.tsv_index_dim(self._h))
-        self.storage = "f32" if lib.tsv_index_storage(self._h) == nat.TSV_F32 else "bf16"
+        self.storage = {v: k for k, v in STORAGE.items()}[lib.tsv_index_storage(self._h)]
 
     @classmethod
     def view(cls, rows: torch.Tensor, metric: str = "ip") -> "DeviceIndex":
@@ -112,6 +112,12 @@ class DeviceIndex:
             hi, lo = self.planes()
             return hi + lo
         ptr = nat.load().tsv_index_data(self._h)
+        if self.storage == "bf16_tiled":  # de-tile into a new [rows, dim] tensor
+            kbs = (self.dim + 63) // 64
+            tiles = (self.rows + 127) // 128
+            t = torch.as_tensor(_ArenaView(ptr, tiles * kbs * 128, 64), device=self.device)
+            t = t.view(torch.bfloat16).view(tiles, kbs, 128, 64).permute(0, 2, 1, 3)
+            return t.reshape(tiles * 128, kbs * 64)[: self.rows, : self.dim].contiguous()
         t = torch.as_tensor(_ArenaView(ptr, self.rows, self.dim), device=self.device)
         return t.view(torch.bfloat16)
 

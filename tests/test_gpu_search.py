@@ -279,3 +279,44 @@ def test_fp32_mode_rerank(cuda):
     s, i = idx.rerank(torch.from_numpy(q).to(cuda), torch.from_numpy(cand).to(cuda), 5)
     es, ei = orc.rerank(q.astype(np.float64), raw.astype(np.float64), cand, 5)
     np.testing.assert_allclose(from_dev(s), es, rtol=1e-5)
+
+
+@pytest.mark.parametrize("n,dim,b,k", [(20000, 768, 256, 10), (4099, 72, 1, 5), (30011, 1024, 300, 50),
+                                       (1000, 384, 1030, 16)])
+def test_tiled_layout_identical_to_row_major(cuda, n, dim, b, k):
+    """The tiled arena (contiguous 16 KB k-block tiles) feeds the same operands to the tensor
+    cores, so results are bit-identical to the row-major arena, and match the oracle."""
+    import torch
+    from paper_2407_00326_b200.index import DeviceIndex
+
+    c = orc.make_corpus(n, dim, seed=0)
+    q, _ = orc.make_queries(c, b, seed=1)
+    rm = _index_from(c, cuda)
+    tl = DeviceIndex(dim, n, device=cuda.index, storage="bf16_tiled")
+    tl.append(to_dev_bf16(c, cuda))
+    np.testing.assert_array_equal(from_dev(tl.data()), c)
+    qd = to_dev_bf16(q, cuda)
+    s1, i1 = rm.search(qd, k)
+    s2, i2 = tl.search(qd, k)
+    np.testing.assert_array_equal(from_dev(i1), from_dev(i2))
+    np.testing.assert_array_equal(from_dev(s1), from_dev(s2))
+    assert_topk(s2, i2, q, c, k, TOL)
+    cand = torch.from_numpy(np.random.default_rng(0).integers(0, n, (b, 40)).astype(np.int32)).to(cuda)
+    r1 = rm.rerank(qd, cand, 5)
+    r2 = tl.rerank(qd, cand, 5)
+    np.testing.assert_array_equal(from_dev(r1[1]), from_dev(r2[1]))
+
+
+def test_tiled_segmented_requires_aligned_segments(cuda):
+    from paper_2407_00326_b200.errors import ConfigParse
+    from paper_2407_00326_b200.index import DeviceIndex
+
+    c = orc.make_corpus(1024, 128, seed=0)
+    q = orc.make_corpus(3, 128, seed=1)
+    tl = DeviceIndex(128, 1024, device=cuda.index, storage="bf16_tiled")
+    tl.append(to_dev_bf16(c, cuda))
+    s, i = tl.search_segmented(to_dev_bf16(q, cuda), [0, 1, 3], [(0, 300), (384, 1024)], 7)
+    assert not orc.check_topk(from_dev(s)[:1], from_dev(i)[:1], q[:1], c[0:300], 7, TOL)
+    assert not orc.check_topk(from_dev(s)[1:], from_dev(i)[1:], q[1:], c[384:1024], 7, TOL)
+    with pytest.raises(ConfigParse):
+        tl.search_segmented(to_dev_bf16(q, cuda), [0, 3], [(5, 300)], 7)
