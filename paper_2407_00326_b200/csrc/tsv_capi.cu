@@ -569,7 +569,7 @@ int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int
     g_launches++;
     return TSV_OK;
   }
-  if (pair && nqg > 1 && num_items <= units && !env_flag("TSV_NO_LOCKSTEP")) {
+  if (nqg > 1 && num_items <= units && !env_flag("TSV_NO_LOCKSTEP")) {
     rc = w.counter.ensure(static_cast<size_t>(num_items));
     if (rc) return rc;
     TSV_CUDA(cudaMemsetAsync(w.counter.ptr, 0, sizeof(int32_t) * num_items, st), "progress reset");

@@ -23,6 +23,8 @@
 namespace tsv {
 namespace {
 
+constexpr int kLockWindow = 4;  // 256-row tiles a worker may run ahead of its range partners
+
 // Lists of more than kRegListMax entries live in shared memory (one column per query thread,
 // entry j of thread t at [j * 128 + t], so lock-step accesses are bank-conflict free).
 constexpr int kRegListMax = 32;
@@ -119,25 +121,53 @@ __device__ __forceinline__ void scan_chunk(const uint32_t (&v)[32], float (&s)[K
   }
 }
 
-// Shared-memory list variant (KCAP > 32): the list of thread t is the column t of
-// ls/li[KCAP][128]; `tau` caches the last entry (the admission threshold).
+// Shared-memory list variant (KCAP > 32), warp-cooperative: the list of query row q is
+// ls/li[q * K .. q * K + K) sorted by (score desc, id asc); every lane of a warp holds K/32
+// consecutive entries of the list being updated. One candidate is inserted by the whole warp:
+// its rank comes from a warp reduction, the tail shifts one slot via a shuffle, and the
+// admission threshold of the owner lane (`tau`, the last entry) is refreshed. This replaces a
+// K-long dependent chain of shared-memory moves with ~40 warp instructions.
 template <int K>
-__device__ __forceinline__ void smem_list_insert(float* ls, int32_t* li, int t, float x, int32_t xi,
-                                                 float& tau) {
-  int p = K - 1;
-  while (p > 0 && ls[(p - 1) * kBlockM + t] < x) {
-    ls[p * kBlockM + t] = ls[(p - 1) * kBlockM + t];
-    li[p * kBlockM + t] = li[(p - 1) * kBlockM + t];
-    --p;
+__device__ __forceinline__ float coop_list_insert(float* ls, int32_t* li, int qrow, float x,
+                                                  int32_t xi, int lane) {
+  constexpr int kPer = K / 32;
+  float* rs = ls + qrow * K + lane * kPer;
+  int32_t* ri = li + qrow * K + lane * kPer;
+  float e[kPer];
+  int32_t d[kPer];
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    e[i] = rs[i];
+    d[i] = ri[i];
   }
-  ls[p * kBlockM + t] = x;
-  li[p * kBlockM + t] = xi;
-  tau = ls[(K - 1) * kBlockM + t];
+  int ge = 0;
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) ge += e[i] >= x ? 1 : 0;
+  const int pos = __reduce_add_sync(0xffffffffu, ge);  // entries that stay ahead of x
+  const float prev_e = __shfl_up_sync(0xffffffffu, e[kPer - 1], 1);
+  const int32_t prev_d = __shfl_up_sync(0xffffffffu, d[kPer - 1], 1);
+  float ne[kPer];
+  int32_t nd[kPer];
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const int g = lane * kPer + i;
+    const float below = i == 0 ? prev_e : e[i - 1];
+    const int32_t below_d = i == 0 ? prev_d : d[i - 1];
+    ne[i] = g < pos ? e[i] : (g == pos ? x : below);
+    nd[i] = g < pos ? d[i] : (g == pos ? xi : below_d);
+  }
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    rs[i] = ne[i];
+    ri[i] = nd[i];
+  }
+  return __shfl_sync(0xffffffffu, ne[kPer - 1], 31);  // new last entry = new threshold
 }
 
 template <int K>
-__device__ __forceinline__ void scan_chunk_smem(const uint32_t (&v)[32], float* ls, int32_t* li,
-                                                int t, float& tau, int32_t id0, int valid) {
+__device__ __forceinline__ void scan_chunk_coop(const uint32_t (&v)[32], float* ls, int32_t* li,
+                                                int row_base, int lane, float& tau, int32_t id0,
+                                                int valid) {
   float m0 = fmaxf(__uint_as_float(v[0]), __uint_as_float(v[1]));
   float m1 = fmaxf(__uint_as_float(v[2]), __uint_as_float(v[3]));
 #pragma unroll
@@ -145,11 +175,17 @@ __device__ __forceinline__ void scan_chunk_smem(const uint32_t (&v)[32], float* 
     m0 = fmaxf(m0, fmaxf(__uint_as_float(v[j]), __uint_as_float(v[j + 1])));
     m1 = fmaxf(m1, fmaxf(__uint_as_float(v[j + 2]), __uint_as_float(v[j + 3])));
   }
-  if (fmaxf(m0, m1) > tau) {
+  if (!__any_sync(0xffffffffu, fmaxf(m0, m1) > tau)) return;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const float x = __uint_as_float(v[j]);
-      if (x > tau && j < valid) smem_list_insert<K>(ls, li, t, x, id0 + j, tau);
+  for (int j = 0; j < 32; ++j) {
+    const float x = __uint_as_float(v[j]);
+    unsigned want = __ballot_sync(0xffffffffu, x > tau && j < valid);
+    while (want) {
+      const int src = __ffs(want) - 1;
+      want &= want - 1;
+      const float xs = __shfl_sync(0xffffffffu, x, src);
+      const float t_new = coop_list_insert<K>(ls, li, row_base + src, xs, id0 + j, lane);
+      if (lane == src) tau = t_new;
     }
   }
 }
@@ -215,11 +251,26 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
     const uint64_t pol_c = ptx::policy_evict_normal();
     int stage = 0;
     uint32_t phase = 0;
+    // range lockstep between the CTAs that stream the same corpus range (see the pair kernel)
+    const bool lockstep = (p.flags & kFlagLockstep) && p.items == nullptr &&
+                          num_items <= static_cast<int>(gridDim.x);
+    volatile int32_t* progress = p.counter;
     for (int i = blockIdx.x; i < num_items; i += gridDim.x) {
       ScanItem it;
       resolve_item(p, i, it, kQG);
       const int64_t ntiles = (it.row_end - it.row_begin + kBlockN - 1) / kBlockN;
+      const int my_qg = p.R > 0 ? i / p.R : 0, my_r = p.R > 0 ? i - my_qg * p.R : 0;
+      const int nqg = p.R > 0 ? num_items / p.R : 1;
       for (int64_t t = 0; t < ntiles; ++t) {
+        if (lockstep && lane == 0) {
+          if ((t & 3) == 0) progress[i] = static_cast<int32_t>(t);
+          if (t >= 2 * kLockWindow) {
+            for (int g = 0; g < nqg; ++g)
+              if (g != my_qg)
+                while (progress[g * p.R + my_r] < t - 2 * kLockWindow) __nanosleep(256);
+          }
+        }
+        __syncwarp();
         const int32_t row0 = static_cast<int32_t>(it.row_begin + t * kBlockN);
         for (int kb = 0; kb < p.num_kb; ++kb) {
           ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -248,6 +299,7 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
           }
         }
       }
+      if (lockstep && lane == 0) progress[i] = 0x7fffffff;
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
@@ -335,9 +387,10 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
       }
       if constexpr (kSmemList) {
         for (int j = 0; j < KCAP; ++j) {
-          list_s[j * kBlockM + t_epi] = -FLT_MAX;
-          list_i[j * kBlockM + t_epi] = -1;
+          list_s[t_epi * KCAP + j] = -FLT_MAX;
+          list_i[t_epi * KCAP + j] = -1;
         }
+        __syncwarp();
       }
       const int64_t ntiles = (it.row_end - it.row_begin + kBlockN - 1) / kBlockN;
       for (int64_t t = 0; t < ntiles; ++t) {
@@ -362,7 +415,7 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
               va[j] = __float_as_uint(__uint_as_float(va[j]) + odd * __uint_as_float(vb[j]) +
                                       __uint_as_float(vc[j]));
             if constexpr (kSmemList)
-              scan_chunk_smem<KCAP>(va, list_s, list_i, t_epi, tau, id0 + c, valid - c);
+              scan_chunk_coop<KCAP>(va, list_s, list_i, quad * 32, lane, tau, id0 + c, valid - c);
             else
               scan_chunk<kRegK>(va, s, id, id0 + c, valid - c);
           }
@@ -374,8 +427,9 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
           ptx::tmem_ld_32x32b_x32(taddr + c + 32, vb);
           ptx::tmem_ld_wait();
           if constexpr (kSmemList) {
-            scan_chunk_smem<KCAP>(va, list_s, list_i, t_epi, tau, id0 + c, valid - c);
-            scan_chunk_smem<KCAP>(vb, list_s, list_i, t_epi, tau, id0 + c + 32, valid - c - 32);
+            scan_chunk_coop<KCAP>(va, list_s, list_i, quad * 32, lane, tau, id0 + c, valid - c);
+            scan_chunk_coop<KCAP>(vb, list_s, list_i, quad * 32, lane, tau, id0 + c + 32,
+                                  valid - c - 32);
           } else {
             scan_chunk<kRegK>(va, s, id, id0 + c, valid - c);
             scan_chunk<kRegK>(vb, s, id, id0 + c + 32, valid - c - 32);
@@ -394,8 +448,8 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
         int32_t* oi = p.out_ids + (it.out_row + lq) * p.out_k;
         if constexpr (kSmemList) {
           for (int j = 0; j < p.out_k; ++j) {
-            const int32_t v = list_i[j * kBlockM + t_epi];
-            os[j] = v < 0 ? -INFINITY : list_s[j * kBlockM + t_epi];
+            const int32_t v = list_i[t_epi * KCAP + j];
+            os[j] = v < 0 ? -INFINITY : list_s[t_epi * KCAP + j];
             oi[j] = v < 0 ? -1 : v;
           }
         } else {
@@ -426,8 +480,6 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
 // issues tcgen05.mma.cta_group::2 and each CTA's TMEM receives its own 128 query rows x 256
 // columns. Per SM this halves the shared-memory operand bytes per MAC compared with the
 // single-CTA 128x128 tile, which is what keeps the tensor pipe fed.
-constexpr int kLockWindow = 4;  // tiles a pair may run ahead of its range partners
-
 struct Pair {
   static constexpr int kTileRows = 256;                 // corpus rows per pair tile (N)
   static constexpr int kQG = 256;                       // queries per pair (M)
