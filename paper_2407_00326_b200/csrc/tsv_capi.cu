@@ -127,6 +127,8 @@ struct Workspace {
   DevBuf<int32_t> counter;     // dynamic-unit scheduler counter
   DevBuf<uint16_t> qbuf;       // bf16 staged queries
   DevBuf<float> qhi, qlo;      // fp32-mode query planes
+  DevBuf<float> seed_s, tau0;  // threshold seeding for k > 32
+  DevBuf<int32_t> seed_i;
   DevBuf<float> part_s;        // partial lists
   DevBuf<int32_t> part_i;
   DevBuf<tsv::ScanItem> items;
@@ -136,6 +138,9 @@ struct Workspace {
     qbuf.release();
     qhi.release();
     qlo.release();
+    seed_s.release();
+    tau0.release();
+    seed_i.release();
     part_s.release();
     part_i.release();
     items.release();
@@ -479,9 +484,9 @@ int tsv_index_scan_time(tsv_index* idx, double* total_ms, int64_t* launches) {
   return TSV_OK;
 }
 
-int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int64_t row_beg,
-               int64_t row_end, int32_t id_offset, float* scores_dev, int32_t* ids_dev,
-               void* stream) {
+static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k,
+                       int64_t row_beg, int64_t row_end, int32_t id_offset, float* scores_dev,
+                       int32_t* ids_dev, void* stream, const float* tau0) {
   if (idx == nullptr) return fail(TSV_ERR_ARGUMENT, "index is null");
   int rc = check_dtype(q_dtype);
   if (rc) return rc;
@@ -511,7 +516,7 @@ int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int
 
   // B > 128: CTA-pair kernel (256 queries x 256 rows per pair tile); otherwise one CTA per
   // 128-query group with 128-row tiles.
-  const bool pair = !f32 && B > tsv::kBlockM && kcap <= tsv::kMaxRegK && !env_flag("TSV_NO_PAIR");
+  const bool pair = !f32 && B > tsv::kBlockM && !env_flag("TSV_NO_PAIR");
   const int mb = pair ? tsv::kPairMode : 1;
   const int qg = pair ? tsv::kPairQG : tsv::kBlockM;
   const int tile_rows = pair ? tsv::kPairTileRows : tsv::kBlockN;
@@ -537,11 +542,12 @@ int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int
   p.id_offset = id_offset;
   p.row_beg = row_beg;
   p.row_end = row_end;
+  p.tau0 = tau0;
   const int kb_elems = f32 ? 32 : tsv::kBlockK;  // elements per 128-byte k-block row
   p.num_kb = (idx->dim + kb_elems - 1) / kb_elems;
   if (tiled) p.flags |= tsv::kFlagTiled;
 
-  if (pair && nqg <= 64 && env_flag("TSV_DYN")) {
+  if (pair && nqg <= 64 && kcap <= tsv::kMaxRegK && env_flag("TSV_DYN")) {
     // Dynamic-unit pair kernel (experimental, opt-in): every pair keeps one list per query;
     // K4 merges the pairs. Streams the corpus from HBM once for any B, but is slower than the
     // static range kernel today ("dynamic units").
@@ -598,6 +604,41 @@ int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int
   if (e) return cuda_fail(static_cast<cudaError_t>(e), "merge launch");
   g_launches++;
   return TSV_OK;
+}
+
+int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int64_t row_beg,
+               int64_t row_end, int32_t id_offset, float* scores_dev, int32_t* ids_dev,
+               void* stream) {
+  // k > 32 keeps shared-memory lists whose cost is the number of admitted candidates. A top-k
+  // over a 1/16 sample of the rows bounds every query's final k-th score from below; seeding
+  // the main scan with it keeps the result exact and skips most insertions.
+  const int kcap = tsv::scan_kcap_for(k);
+  const int64_t n = row_end - row_beg;
+  if (idx != nullptr && kcap > tsv::kMaxRegK && idx->storage != TSV_F32 && B > 0 &&
+      n >= 64 * 4096 && !env_flag("TSV_NO_SEED")) {
+    int frac = 16;
+    if (const char* e = getenv("TSV_SEED_FRAC")) frac = std::max(2, atoi(e));
+    const int64_t sample = ((n / frac + 255) / 256) * 256;
+    DeviceGuard g(idx->device);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    Workspace& w = idx->ws[st];
+    int rc = w.seed_s.ensure(static_cast<size_t>(B) * k);
+    if (!rc) rc = w.seed_i.ensure(static_cast<size_t>(B) * k);
+    if (!rc) rc = w.tau0.ensure(static_cast<size_t>(B));
+    if (rc) return rc;
+    // the sample pass is itself seeded from a smaller sample when it is large enough; it
+    // reuses the seed buffers only after its own floor has been consumed (same stream order)
+    rc = tsv_search(idx, q_dev, q_dtype, B, k, row_beg, row_beg + sample, 0, w.seed_s.ptr,
+                    w.seed_i.ptr, stream);
+    if (rc) return rc;
+    int e = tsv::launch_seed_floor(w.seed_s.ptr, w.seed_i.ptr, B, k, w.tau0.ptr, st);
+    if (e) return cuda_fail(static_cast<cudaError_t>(e), "seed floor");
+    g_launches++;
+    return search_impl(idx, q_dev, q_dtype, B, k, row_beg, row_end, id_offset, scores_dev,
+                       ids_dev, stream, w.tau0.ptr);
+  }
+  return search_impl(idx, q_dev, q_dtype, B, k, row_beg, row_end, id_offset, scores_dev, ids_dev,
+                     stream, nullptr);
 }
 
 int tsv_search_segmented(tsv_index* idx, const void* q_dev, int q_dtype, int nseg,

@@ -46,6 +46,9 @@ struct ScanParams {
   int32_t flags;  // bit 0: CTA-scope (not cluster-scope) unit/accumulator barrier waits
                   // bit 1: corpus map is the tiled layout (3-D: 64 x 128 x tiles*kblocks)
   int32_t chunk;  // corpus tiles per dynamic unit
+  // Optional per-query admission floor (k > 32 lists): a lower bound of the query's final k-th
+  // score (from a sample pass); candidates at or below it can never be in the result.
+  const float* tau0;
 };
 
 // `mb` argument selecting the dynamic-unit CTA-pair kernel (see tsv_scan.cu).
@@ -54,6 +57,8 @@ constexpr int kFlagTiled = 2;
 constexpr int kFlagLockstep = 4;  // static pair kernel: bound drift between range partners
 // Tiled arena layout: row i, element d at ((i/128 * KB + d/64) * 128 + i%128) * 64 + d%64,
 // KB = ceil(dim/64): every [128 rows x 64 elements] k-block tile is one contiguous 16 KB block.
+int launch_seed_floor(const float* s, const int32_t* id, int B, int k, float* floor_out,
+                      cudaStream_t stream);
 int launch_scatter_tiled(const void* src, int src_is_f32, int64_t n, int dim, int do_normalize,
                          void* arena, int64_t first_row, cudaStream_t stream);
 

@@ -274,7 +274,24 @@ __global__ void scatter_tiled_kernel(const void* __restrict__ src, int src_is_f3
   }
 }
 
+// Admission floor from a sample pass: one below the sample's k-th score (so ties at the final
+// boundary stay admissible), or -FLT_MAX when the sample had fewer than k rows.
+__global__ void seed_floor_kernel(const float* __restrict__ s, const int32_t* __restrict__ id,
+                                  int B, int k, float* __restrict__ floor_out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int64_t o = static_cast<int64_t>(b) * k + (k - 1);
+  floor_out[b] = id[o] >= 0 ? nextafterf(s[o], -INFINITY) : -FLT_MAX;
+}
+
 }  // namespace
+
+int launch_seed_floor(const float* s, const int32_t* id, int B, int k, float* floor_out,
+                      cudaStream_t stream) {
+  if (B <= 0) return 0;
+  seed_floor_kernel<<<(B + 255) / 256, 256, 0, stream>>>(s, id, B, k, floor_out);
+  return static_cast<int>(cudaGetLastError());
+}
 
 int launch_scatter_tiled(const void* src, int src_is_f32, int64_t n, int dim, int do_normalize,
                          void* arena, int64_t first_row, cudaStream_t stream) {

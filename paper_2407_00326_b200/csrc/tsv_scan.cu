@@ -167,7 +167,7 @@ __device__ __forceinline__ float coop_list_insert(float* ls, int32_t* li, int qr
 template <int K>
 __device__ __forceinline__ void scan_chunk_coop(const uint32_t (&v)[32], float* ls, int32_t* li,
                                                 int row_base, int lane, float& tau, int32_t id0,
-                                                int valid) {
+                                                int valid, float floor_tau) {
   float m0 = fmaxf(__uint_as_float(v[0]), __uint_as_float(v[1]));
   float m1 = fmaxf(__uint_as_float(v[2]), __uint_as_float(v[3]));
 #pragma unroll
@@ -185,7 +185,7 @@ __device__ __forceinline__ void scan_chunk_coop(const uint32_t (&v)[32], float* 
       want &= want - 1;
       const float xs = __shfl_sync(0xffffffffu, x, src);
       const float t_new = coop_list_insert<K>(ls, li, row_base + src, xs, id0 + j, lane);
-      if (lane == src) tau = t_new;
+      if (lane == src) tau = fmaxf(t_new, floor_tau);
     }
   }
 }
@@ -378,8 +378,10 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
       resolve_item(p, i, it, kQG);
       float s[kRegK];
       int32_t id[kRegK];
-      float tau = -FLT_MAX;
-      const int t_epi = quad * 32 + lane;  // column of this thread's shared-memory list
+      const int t_epi = quad * 32 + lane;  // row of this thread's shared-memory list
+      const float tau_floor = (p.tau0 != nullptr && lq < it.q_count) ? p.tau0[it.q_begin + lq]
+                                                                      : -FLT_MAX;
+      float tau = tau_floor;
 #pragma unroll
       for (int j = 0; j < kRegK; ++j) {
         s[j] = -FLT_MAX;
@@ -415,7 +417,8 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
               va[j] = __float_as_uint(__uint_as_float(va[j]) + odd * __uint_as_float(vb[j]) +
                                       __uint_as_float(vc[j]));
             if constexpr (kSmemList)
-              scan_chunk_coop<KCAP>(va, list_s, list_i, quad * 32, lane, tau, id0 + c, valid - c);
+              scan_chunk_coop<KCAP>(va, list_s, list_i, quad * 32, lane, tau, id0 + c, valid - c,
+                                  tau_floor);
             else
               scan_chunk<kRegK>(va, s, id, id0 + c, valid - c);
           }
@@ -427,9 +430,10 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
           ptx::tmem_ld_32x32b_x32(taddr + c + 32, vb);
           ptx::tmem_ld_wait();
           if constexpr (kSmemList) {
-            scan_chunk_coop<KCAP>(va, list_s, list_i, quad * 32, lane, tau, id0 + c, valid - c);
+            scan_chunk_coop<KCAP>(va, list_s, list_i, quad * 32, lane, tau, id0 + c, valid - c,
+                                  tau_floor);
             scan_chunk_coop<KCAP>(vb, list_s, list_i, quad * 32, lane, tau, id0 + c + 32,
-                                  valid - c - 32);
+                                  valid - c - 32, tau_floor);
           } else {
             scan_chunk<kRegK>(va, s, id, id0 + c, valid - c);
             scan_chunk<kRegK>(vb, s, id, id0 + c + 32, valid - c - 32);
@@ -494,14 +498,29 @@ struct Pair {
 };
 
 template <int KCAP>
+struct PairStages {
+  static constexpr int value =
+      KCAP > kRegListMax ? (227 * 1024 - 2048 - 128 * KCAP * 8) / Pair::kStageBytes : Pair::kStages;
+  static constexpr int smem =
+      value * Pair::kStageBytes + (KCAP > kRegListMax ? 128 * KCAP * 8 : 0) + 256 + 1024;
+};
+
+template <int KCAP>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
     scan_topk_pair_kernel(const __grid_constant__ CUtensorMap tmap_q,
                           const __grid_constant__ CUtensorMap tmap_c, const ScanParams p) {
-  constexpr int kStages = Pair::kStages;
+  // k > 32: warp-cooperative lists in shared memory (128 query rows x KCAP), fewer stages
+  constexpr bool kSmemList = KCAP > kRegListMax;
+  constexpr int kListBytes = kSmemList ? 128 * KCAP * 8 : 0;
+  constexpr int kStages = PairStages<KCAP>::value;
+  constexpr int kRegK = kSmemList ? 1 : KCAP;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * Pair::kStageBytes);
+  float* list_s = reinterpret_cast<float*>(smem + kStages * Pair::kStageBytes);
+  int32_t* list_i = reinterpret_cast<int32_t*>(list_s + (kSmemList ? 128 * KCAP : 0));
+  uint64_t* full_bar =
+      reinterpret_cast<uint64_t*>(smem + kStages * Pair::kStageBytes + kListBytes);
   uint64_t* empty_bar = full_bar + kStages;
   uint64_t* tfull_bar = empty_bar + kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
@@ -635,12 +654,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
     for (int i = pair; i < num_items; i += npairs) {
       ScanItem it;
       resolve_item(p, i, it, Pair::kQG, Pair::kTileRows);
-      float s[KCAP];
-      int32_t id[KCAP];
+      float s[kRegK];
+      int32_t id[kRegK];
+      const int t_epi = quad * 32 + lane;
+      const float tau_floor = (p.tau0 != nullptr && lq < it.q_count) ? p.tau0[it.q_begin + lq]
+                                                                      : -FLT_MAX;
+      float tau = tau_floor;
 #pragma unroll
-      for (int j = 0; j < KCAP; ++j) {
+      for (int j = 0; j < kRegK; ++j) {
         s[j] = -FLT_MAX;
         id[j] = -1;
+      }
+      if constexpr (kSmemList) {
+        for (int j = 0; j < KCAP; ++j) {
+          list_s[t_epi * KCAP + j] = -FLT_MAX;
+          list_i[t_epi * KCAP + j] = -1;
+        }
+        __syncwarp();
       }
       const int64_t ntiles = (it.row_end - it.row_begin + Pair::kTileRows - 1) / Pair::kTileRows;
       for (int64_t t = 0; t < ntiles; ++t) {
@@ -657,8 +687,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
           ptx::tmem_ld_32x32b_x32(taddr + c, va);
           ptx::tmem_ld_32x32b_x32(taddr + c + 32, vb);
           ptx::tmem_ld_wait();
-          scan_chunk<KCAP>(va, s, id, id0 + c, valid - c);
-          scan_chunk<KCAP>(vb, s, id, id0 + c + 32, valid - c - 32);
+          if constexpr (kSmemList) {
+            scan_chunk_coop<KCAP>(va, list_s, list_i, quad * 32, lane, tau, id0 + c, valid - c,
+                                  tau_floor);
+            scan_chunk_coop<KCAP>(vb, list_s, list_i, quad * 32, lane, tau, id0 + c + 32,
+                                  valid - c - 32, tau_floor);
+          } else {
+            scan_chunk<kRegK>(va, s, id, id0 + c, valid - c);
+            scan_chunk<kRegK>(vb, s, id, id0 + c + 32, valid - c - 32);
+          }
         }
         ptx::tc_fence_before();
         __syncwarp();
@@ -669,12 +706,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
       if (lq < it.q_count) {
         float* os = p.out_scores + (it.out_row + lq) * p.out_k;
         int32_t* oi = p.out_ids + (it.out_row + lq) * p.out_k;
+        if constexpr (kSmemList) {
+          for (int j = 0; j < p.out_k; ++j) {
+            const int32_t v = list_i[t_epi * KCAP + j];
+            os[j] = v < 0 ? -INFINITY : list_s[t_epi * KCAP + j];
+            oi[j] = v < 0 ? -1 : v;
+          }
+        } else {
 #pragma unroll
-        for (int j = 0; j < KCAP; ++j) {
-          if (j < p.out_k) {
-            const bool pad = id[j] < 0;
-            os[j] = pad ? -INFINITY : s[j];
-            oi[j] = pad ? -1 : id[j];
+          for (int j = 0; j < kRegK; ++j) {
+            if (j < p.out_k) {
+              const bool pad = id[j] < 0;
+              os[j] = pad ? -INFINITY : s[j];
+              oi[j] = pad ? -1 : id[j];
+            }
           }
         }
       }
@@ -1017,10 +1062,10 @@ template <int KCAP>
 int launch_pair_impl(const CUtensorMap& tq, const CUtensorMap& tc, const ScanParams& p, int grid,
                      cudaStream_t stream) {
   auto kern = scan_topk_pair_kernel<KCAP>;
-  cudaError_t err =
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Pair::kSmemBytes);
+  constexpr int smem = PairStages<KCAP>::smem;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (err != cudaSuccess) return static_cast<int>(err);
-  kern<<<grid, Pair::kThreads, Pair::kSmemBytes, stream>>>(tq, tc, p);
+  kern<<<grid, Pair::kThreads, smem, stream>>>(tq, tc, p);
   return static_cast<int>(cudaGetLastError());
 }
 
@@ -1067,6 +1112,8 @@ int dispatch_pair(int kcap, const CUtensorMap& tq, const CUtensorMap& tc, const 
     case 10: return launch_pair_impl<10>(tq, tc, p, grid, stream);
     case 16: return launch_pair_impl<16>(tq, tc, p, grid, stream);
     case 32: return launch_pair_impl<32>(tq, tc, p, grid, stream);
+    case 64: return launch_pair_impl<64>(tq, tc, p, grid, stream);
+    case 128: return launch_pair_impl<128>(tq, tc, p, grid, stream);
     default: return static_cast<int>(cudaErrorInvalidValue);
   }
 }

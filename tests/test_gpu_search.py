@@ -320,3 +320,28 @@ def test_tiled_segmented_requires_aligned_segments(cuda):
     assert not orc.check_topk(from_dev(s)[1:], from_dev(i)[1:], q[1:], c[384:1024], 7, TOL)
     with pytest.raises(ConfigParse):
         tl.search_segmented(to_dev_bf16(q, cuda), [0, 3], [(5, 300)], 7)
+
+
+def test_seeded_large_k_is_exact(cuda):
+    """k > 32 on >= 262144 rows runs a 1/64-sample pass first and admits only candidates above
+    the sample's k-th score; the result must equal the unseeded search and the oracle."""
+    import os
+
+    import torch
+
+    n, dim, b, k = 300_000, 256, 300, 100
+    c = orc.make_corpus(n, dim, seed=0)
+    q, _ = orc.make_queries(c, b, seed=1)
+    idx = _index_from(c, cuda)
+    qd = to_dev_bf16(q, cuda)
+    s1, i1 = idx.search(qd, k)
+    os.environ["TSV_NO_SEED"] = "1"
+    try:
+        s2, i2 = idx.search(qd, k)
+    finally:
+        del os.environ["TSV_NO_SEED"]
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(from_dev(i1), from_dev(i2))
+    np.testing.assert_array_equal(from_dev(s1), from_dev(s2))
+    sub = np.r_[0:20, 150:170]
+    assert_topk(s1[sub], i1[sub], q[sub], c, k, TOL)
