@@ -133,7 +133,16 @@ struct Workspace {
   DevBuf<int32_t> part_i;
   DevBuf<tsv::ScanItem> items;
   std::vector<tsv::ScanItem> host_items;
+  // pinned staging for the item table so its upload is a true async copy; the event marks
+  // when the previous upload has drained so the staging buffer can be rewritten
+  tsv::ScanItem* pinned = nullptr;
+  size_t pinned_cap = 0;
+  cudaEvent_t pinned_done = nullptr;
   void release() {
+    if (pinned) cudaFreeHost(pinned);
+    if (pinned_done) cudaEventDestroy(pinned_done);
+    pinned = nullptr;
+    pinned_done = nullptr;
     counter.release();
     qbuf.release();
     qhi.release();
@@ -198,6 +207,7 @@ int check_dtype(int dt) {
 }
 
 constexpr int kMergeCap = 8192;  // candidates per query the merge kernel sorts in smem
+constexpr int kMinTilesPerRange = 1;
 
 bool env_flag(const char* name) {
   const char* v = getenv(name);
@@ -225,10 +235,36 @@ int stage_queries(tsv_index* idx, Workspace& w, const void* q, int q_dtype, int6
   return TSV_OK;
 }
 
+// Query tensor maps are cached per (pointer, rows, dim): staged queries live in a stable
+// per-stream workspace buffer, so repeated searches skip the host-side encode.
+int query_map(const void* qb, int64_t B, int dim, CUtensorMap* out) {
+  struct Key {
+    const void* p;
+    int64_t b;
+    int d;
+    bool operator<(const Key& o) const {
+      return p != o.p ? p < o.p : (b != o.b ? b < o.b : d < o.d);
+    }
+  };
+  static std::mutex mu;
+  static std::map<Key, CUtensorMap> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(Key{qb, B, dim});
+  if (it != cache.end()) {
+    *out = it->second;
+    return TSV_OK;
+  }
+  int rc = encode_rows_map(out, qb, B, dim, tsv::kBlockM);
+  if (rc) return rc;
+  if (cache.size() > 4096) cache.clear();
+  cache.emplace(Key{qb, B, dim}, *out);
+  return TSV_OK;
+}
+
 int run_scan(tsv_index* idx, int mb, int kcap, const void* qb, int64_t B, tsv::ScanParams& p,
              int grid, cudaStream_t st) {
   CUtensorMap tq;
-  int rc = encode_rows_map(&tq, qb, B, idx->dim, tsv::kBlockM);
+  int rc = query_map(qb, B, idx->dim, &tq);
   if (rc) return rc;
   TimedLaunch tl{};
   if (idx->timing) {
@@ -529,7 +565,9 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
   int R = std::max(1, units / nqg);
   if (nqg * R < units * 97 / 100 && (2 * units) % nqg == 0) R = 2 * units / nqg;
   if (const char* e = getenv("TSV_SCAN_RANGES")) R = std::max(1, atoi(e));
-  R = static_cast<int>(std::min<int64_t>(R, tiles));
+  // at least kMinTilesPerRange tiles per range: tiny scans gain nothing from more workers, and
+  // every extra range is one more list for the merge
+  R = static_cast<int>(std::min<int64_t>(R, std::max<int64_t>(1, tiles / kMinTilesPerRange)));
   R = std::min(R, kMergeCap / kcap);  // the range merge holds R * kcap candidates per query
   const int num_items = nqg * R;
   const int grid = pair ? 2 * std::min(num_items, units) : std::min(num_items, units);
@@ -686,7 +724,7 @@ int tsv_search_segmented(tsv_index* idx, const void* q_dev, int q_dtype, int nse
   for (int s = 0; s < nseg; ++s) units += (seg_q_beg[s + 1] - seg_q_beg[s] + qg - 1) / qg;
   const int64_t max_tiles = std::max<int64_t>(1, (max_rows + tsv::kBlockN - 1) / tsv::kBlockN);
   int R = std::max(1, idx->num_sms / std::max(1, units));
-  R = static_cast<int>(std::min<int64_t>(R, max_tiles));
+  R = static_cast<int>(std::min<int64_t>(R, std::max<int64_t>(1, max_tiles / kMinTilesPerRange)));
   R = std::min(R, kMergeCap / kcap);
 
   auto& hi = w.host_items;
@@ -711,9 +749,21 @@ int tsv_search_segmented(tsv_index* idx, const void* q_dev, int q_dtype, int nse
   }
   rc = w.items.ensure(hi.size());
   if (rc) return rc;
-  TSV_CUDA(cudaMemcpyAsync(w.items.ptr, hi.data(), hi.size() * sizeof(tsv::ScanItem),
+  if (w.pinned_done == nullptr)
+    TSV_CUDA(cudaEventCreateWithFlags(&w.pinned_done, cudaEventDisableTiming), "cudaEventCreate");
+  else
+    TSV_CUDA(cudaEventSynchronize(w.pinned_done), "cudaEventSynchronize");
+  if (hi.size() > w.pinned_cap) {
+    if (w.pinned) cudaFreeHost(w.pinned);
+    w.pinned = nullptr;
+    TSV_CUDA(cudaMallocHost(&w.pinned, hi.size() * 2 * sizeof(tsv::ScanItem)), "cudaMallocHost");
+    w.pinned_cap = hi.size() * 2;
+  }
+  std::memcpy(w.pinned, hi.data(), hi.size() * sizeof(tsv::ScanItem));
+  TSV_CUDA(cudaMemcpyAsync(w.items.ptr, w.pinned, hi.size() * sizeof(tsv::ScanItem),
                            cudaMemcpyHostToDevice, st),
            "items upload");
+  TSV_CUDA(cudaEventRecord(w.pinned_done, st), "cudaEventRecord");
   tsv::ScanParams p{};
   p.items = w.items.ptr;
   p.num_items = static_cast<int>(hi.size());

@@ -4,7 +4,18 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 namespace tsv {
+
+// True the first time it is called on the current device for a given mask (kernel function
+// attributes are per device; setting them on every launch costs a driver call).
+inline bool first_on_device(std::atomic<uint64_t>& mask) {
+  int d = 0;
+  cudaGetDevice(&d);
+  const uint64_t bit = 1ull << (d & 63);
+  return (mask.fetch_or(bit) & bit) == 0;
+}
 
 // Geometry of the fused scan (K1). Queries sit on the UMMA M side (one TMEM lane per query),
 // corpus rows on the N side; K is the embedding dimension, streamed 64 bf16 (one 128 B swizzle

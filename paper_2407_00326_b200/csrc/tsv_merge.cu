@@ -321,12 +321,13 @@ int launch_merge_topk(const float* in_s, const int32_t* in_id, int lists, int B,
   while (np < lists * kin) np <<= 1;
   if (np > 8192) return static_cast<int>(cudaErrorInvalidValue);
   const size_t smem = static_cast<size_t>(np) * sizeof(uint64_t);
-  if (smem > 48 * 1024) {
+  static std::atomic<uint64_t> configured{0};
+  if (smem > 48 * 1024 && first_on_device(configured)) {
     cudaError_t e = cudaFuncSetAttribute(merge_topk_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     if (e != cudaSuccess) return static_cast<int>(e);
   }
-  const int threads = np >= 512 ? 256 : 128;
+  const int threads = np >= 1024 ? 256 : (np >= 256 ? 128 : 64);
   merge_topk_kernel<<<B, threads, smem, stream>>>(in_s, in_id, lists, B, kin, list_stride_rows,
                                                   kout, out_s, out_id, dedup);
   return static_cast<int>(cudaGetLastError());
@@ -342,9 +343,10 @@ int launch_rerank(const void* arena, const float* arena_hi, const float* arena_l
   const size_t smem = ((static_cast<size_t>(dim) * 4 + 15) & ~size_t(15)) + np * sizeof(uint64_t);
   if (smem > 200 * 1024) return static_cast<int>(cudaErrorInvalidValue);
   constexpr int kThreads = 256;
-  if (smem > 48 * 1024) {
+  static std::atomic<uint64_t> configured{0};
+  if (smem > 48 * 1024 && first_on_device(configured)) {
     cudaError_t e = cudaFuncSetAttribute(rerank_kernel<kThreads>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return static_cast<int>(e);
   }
   rerank_kernel<kThreads><<<B, kThreads, smem, stream>>>(

@@ -1063,8 +1063,11 @@ int launch_pair_impl(const CUtensorMap& tq, const CUtensorMap& tc, const ScanPar
                      cudaStream_t stream) {
   auto kern = scan_topk_pair_kernel<KCAP>;
   constexpr int smem = PairStages<KCAP>::smem;
-  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (err != cudaSuccess) return static_cast<int>(err);
+  static std::atomic<uint64_t> configured{0};
+  if (first_on_device(configured)) {
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (err != cudaSuccess) return static_cast<int>(err);
+  }
   kern<<<grid, Pair::kThreads, smem, stream>>>(tq, tc, p);
   return static_cast<int>(cudaGetLastError());
 }
@@ -1075,9 +1078,12 @@ int launch_impl(const CUtensorMap& tq, const CUtensorMap& tc, const ScanParams& 
                 const CUtensorMap* tc_lo = nullptr) {
   using Cfg = ScanCfg<MB, KCAP, TF32>;
   auto kern = scan_topk_kernel<MB, KCAP, TF32>;
-  cudaError_t err =
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
-  if (err != cudaSuccess) return static_cast<int>(err);
+  static std::atomic<uint64_t> configured{0};  // per instantiation and device
+  if (first_on_device(configured)) {
+    cudaError_t err =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
+    if (err != cudaSuccess) return static_cast<int>(err);
+  }
   kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, stream>>>(tq, tc, tq_lo ? *tq_lo : tq,
                                                           tc_lo ? *tc_lo : tc, p);
   return static_cast<int>(cudaGetLastError());

@@ -56,12 +56,15 @@ def _check_outputs(sim, backend):
             seg = backend.segments[(ctx.query_id, idx_key, backend.home(ctx.query_id))]
             rep = backend.replicas[seg.replica]
             rows = from_dev(rep.arena.data()[seg.row_beg:seg.row_end])
-            src = next(ctx.data[(e.src, e.key)] for e in ctx.graph.edges
-                       if e.dst == nid and e.key == "query_vectors")
+            srcs = [ctx.data[(e.src, e.key)] for e in ctx.graph.edges
+                    if e.dst == nid and e.key == "query_vectors"]
             k = node.meta.outputs[key].items // node.meta.batch_items
-            q = from_dev(backend.data.queries(rep.device, ctx.query_id, src[1], res.q_lo,
-                                              res.q_hi, src[4], seg.row_end - seg.row_beg, idx_key)
-                         .to("cuda").bfloat16())
+            # the vectors the embedding stages materialised, rows [q_lo, q_hi)
+            full = {}
+            for d in srcs:
+                for r_, row in enumerate(from_dev(d[5].bfloat16()), start=d[2]):
+                    full[r_] = row
+            q = np.stack([full[r_] for r_ in range(res.q_lo, res.q_hi)])
             probs = orc.check_topk(from_dev(res.scores), from_dev(res.ids), q, rows, k, TOL)
             assert not probs, (nid, probs[:3])
             checked += 1
