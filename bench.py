@@ -50,6 +50,8 @@ def parse_args():
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU time of the bounded cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", choices=("p2p", "nccl"), default="p2p",
+                    help="N>1: fused peer all-gather + merge over NVLink, or NCCL all-gather + K4")
     return ap.parse_args()
 
 
@@ -258,7 +260,7 @@ def run_ours(args):
     q_host.copy_(q_dev)
     s_host = torch.empty((B, k), dtype=torch.float32, pin_memory=True)
     i_host = torch.empty((B, k), dtype=torch.int32, pin_memory=True)
-    sharded = ShardedSearch(idx, N, rank=rank, world=world)
+    sharded = ShardedSearch(idx, N, rank=rank, world=world, exchange=args.exchange)
 
     def step(q):
         return sharded.search(q, k)
@@ -379,13 +381,16 @@ def run_ours(args):
             "scaling": "strong", "vs_baseline": None,
             "dtype": "f32 (3xTF32)" if args.storage == "f32" else "bf16",
             "data": "synthetic (seeded N(0,1) rows and queries, L2-normalised on device)",
-            "config": _config(args, n_local),
+            "config": {**_config(args, n_local),
+                       "exchange": (None if world == 1 else sharded.exchange
+                                    + (f" (p2p unavailable: {sharded.p2p_error})"
+                                       if sharded.p2p_error else ""))},
             "e2e": {"value": e2e_value, "unit": "queries/s",
                     "h2d_bytes_per_step": B * D * 2, "d2h_bytes_per_step": B * k * 8,
                     "ms_per_step": e2e_ms / args.steps,
                     "path": "ShardedSearch.search -> DeviceIndex.search (C ABI tsv_search) "
-                            "[+ NCCL all-gather + tsv_merge_topk when sharded], pinned host "
-                            "buffers"},
+                            "[+ tsv_peer_allgather_merge over NVLink (or NCCL all-gather + "
+                            "tsv_merge_topk) when sharded], pinned host buffers"},
             "roofline": roof,
             "cpu_baseline": cpu,
             "gpu_launches": launches,

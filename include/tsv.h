@@ -122,6 +122,21 @@ TSV_API int tsv_rerank(tsv_index* idx, const void* q_dev, int q_dtype, int B, co
 TSV_API int tsv_merge_topk(const float* in_scores, const int32_t* in_ids, int lists, int B, int kin,
                    int kout, int dedup, float* out_scores, int32_t* out_ids, void* stream);
 
+/* ---- Sharded mode over NVLink: all-gather of the per-rank [B, k] lists fused with the
+ * cross-shard merge (replaces ncclAllGather + tsv_merge_topk). One process per GPU; each
+ * rank creates a symmetric buffer, exports its IPC handle, opens every peer's handle (handles
+ * travel over any side channel, e.g. torch.distributed), then calls allgather_merge with the
+ * same B, k on every rank. Ranks push their lists into peers' memory and merge on arrival. ---- */
+typedef struct tsv_peer_group tsv_peer_group;
+TSV_API int tsv_peer_create(int device, int world, int rank, int max_b, int max_k,
+                            tsv_peer_group** out);
+TSV_API int tsv_peer_handle(tsv_peer_group* g, void* handle_out /* 64 bytes */, int* handle_bytes);
+TSV_API int tsv_peer_open(tsv_peer_group* g, int peer, const void* handle);
+TSV_API int tsv_peer_allgather_merge(tsv_peer_group* g, const float* local_scores,
+                                     const int32_t* local_ids, int B, int k, float* out_scores,
+                                     int32_t* out_ids, void* stream);
+TSV_API int tsv_peer_destroy(tsv_peer_group* g);
+
 /* ---- K5: L2-normalise (normalize != 0) and cast rows to bf16. ---- */
 TSV_API int tsv_normalize_rows(const void* src_dev, int src_dtype, int64_t n, int dim, int normalize,
                        void* dst_bf16_dev, void* stream);

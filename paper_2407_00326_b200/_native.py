@@ -54,6 +54,11 @@ SIGNATURES = {
     "tsv_rerank": (c_int, [c_vp, c_vp, c_int, c_int, c_vp, c_int, c_int, c_vp, c_vp, c_vp]),
     "tsv_merge_topk": (c_int, [c_vp, c_vp, c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp]),
     "tsv_normalize_rows": (c_int, [c_vp, c_int, c_i64, c_int, c_int, c_vp, c_vp]),
+    "tsv_peer_create": (c_int, [c_int, c_int, c_int, c_int, c_int, ctypes.POINTER(c_vp)]),
+    "tsv_peer_handle": (c_int, [c_vp, c_vp, ctypes.POINTER(c_int)]),
+    "tsv_peer_open": (c_int, [c_vp, c_int, c_vp]),
+    "tsv_peer_allgather_merge": (c_int, [c_vp, c_vp, c_vp, c_int, c_int, c_vp, c_vp, c_vp]),
+    "tsv_peer_destroy": (c_int, [c_vp]),
 }
 
 _lib = None

@@ -847,6 +847,115 @@ int tsv_merge_topk(const float* in_scores, const int32_t* in_ids, int lists, int
   return TSV_OK;
 }
 
+}  // extern "C"
+
+struct tsv_peer_group {
+  int device = 0, world = 1, rank = 0, max_b = 0, max_k = 0, num_sms = 148;
+  void* buf = nullptr;
+  std::vector<void*> peers;     // mapped base of every rank's buffer (own = buf)
+  std::vector<bool> opened;     // peers mapped through IPC (closed on destroy)
+  void** d_peers = nullptr;     // device copy of `peers`
+  bool dirty = true;
+  int epoch = 0;
+};
+
+extern "C" {
+
+int tsv_peer_create(int device, int world, int rank, int max_b, int max_k, tsv_peer_group** out) {
+  if (out == nullptr) return fail(TSV_ERR_ARGUMENT, "out is null");
+  *out = nullptr;
+  if (world < 1 || world > 64 || rank < 0 || rank >= world)
+    return fail(TSV_ERR_CONFIG, "bad world/rank %d/%d", world, rank);
+  if (max_b <= 0 || max_k <= 0 || max_k > tsv::kMaxK)
+    return fail(TSV_ERR_CAPACITY, "bad max_b/max_k %d/%d", max_b, max_k);
+  DeviceGuard g(device);
+  auto* pg = new tsv_peer_group();
+  pg->device = device;
+  pg->world = world;
+  pg->rank = rank;
+  pg->max_b = max_b;
+  pg->max_k = max_k;
+  cudaDeviceGetAttribute(&pg->num_sms, cudaDevAttrMultiProcessorCount, device);
+  const size_t bytes = tsv::peer_buffer_bytes(world, max_b, max_k);
+  cudaError_t e = cudaMalloc(&pg->buf, bytes);
+  if (e == cudaSuccess) e = cudaMemset(pg->buf, 0, bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&pg->d_peers, sizeof(void*) * world);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    if (pg->buf) cudaFree(pg->buf);
+    delete pg;
+    return cuda_fail(e, "peer buffer");
+  }
+  pg->peers.assign(world, nullptr);
+  pg->opened.assign(world, false);
+  pg->peers[rank] = pg->buf;
+  *out = pg;
+  return TSV_OK;
+}
+
+int tsv_peer_handle(tsv_peer_group* pg, void* handle_out, int* handle_bytes) {
+  if (pg == nullptr || handle_out == nullptr) return fail(TSV_ERR_ARGUMENT, "null argument");
+  DeviceGuard g(pg->device);
+  cudaIpcMemHandle_t h;
+  TSV_CUDA(cudaIpcGetMemHandle(&h, pg->buf), "cudaIpcGetMemHandle");
+  std::memcpy(handle_out, &h, sizeof(h));
+  if (handle_bytes) *handle_bytes = static_cast<int>(sizeof(h));
+  return TSV_OK;
+}
+
+int tsv_peer_open(tsv_peer_group* pg, int peer, const void* handle) {
+  if (pg == nullptr || handle == nullptr) return fail(TSV_ERR_ARGUMENT, "null argument");
+  if (peer < 0 || peer >= pg->world) return fail(TSV_ERR_CONFIG, "bad peer %d", peer);
+  if (peer == pg->rank) return TSV_OK;
+  DeviceGuard g(pg->device);
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  void* ptr = nullptr;
+  TSV_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  pg->peers[peer] = ptr;
+  pg->opened[peer] = true;
+  pg->dirty = true;
+  return TSV_OK;
+}
+
+int tsv_peer_allgather_merge(tsv_peer_group* pg, const float* local_s, const int32_t* local_i,
+                             int B, int k, float* out_s, int32_t* out_i, void* stream) {
+  if (pg == nullptr) return fail(TSV_ERR_ARGUMENT, "peer group is null");
+  if (B <= 0 || k <= 0) return fail(TSV_ERR_CAPACITY, "empty exchange");
+  if (B > pg->max_b || k > pg->max_k) return fail(TSV_ERR_CAPACITY, "exchange exceeds buffer");
+  if (!local_s || !local_i || !out_s || !out_i) return fail(TSV_ERR_ARGUMENT, "null buffer");
+  for (int r = 0; r < pg->world; ++r)
+    if (pg->peers[r] == nullptr) return fail(TSV_ERR_CONFIG, "peer %d not opened", r);
+  DeviceGuard g(pg->device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (pg->dirty) {
+    TSV_CUDA(cudaMemcpyAsync(pg->d_peers, pg->peers.data(), sizeof(void*) * pg->world,
+                             cudaMemcpyHostToDevice, st),
+             "peer table upload");
+    TSV_CUDA(cudaStreamSynchronize(st), "peer table upload");
+    pg->dirty = false;
+  }
+  pg->epoch++;
+  int e = tsv::launch_peer_exchange_merge(pg->d_peers, pg->rank, pg->world, B, k, pg->max_b,
+                                          pg->max_k, pg->epoch, local_s, local_i, out_s, out_i,
+                                          pg->num_sms, st);
+  if (e) return cuda_fail(static_cast<cudaError_t>(e), "peer exchange launch");
+  g_launches++;
+  return TSV_OK;
+}
+
+int tsv_peer_destroy(tsv_peer_group* pg) {
+  if (pg == nullptr) return TSV_OK;
+  DeviceGuard g(pg->device);
+  cudaDeviceSynchronize();
+  for (int r = 0; r < pg->world; ++r)
+    if (pg->opened[r]) cudaIpcCloseMemHandle(pg->peers[r]);
+  if (pg->d_peers) cudaFree(pg->d_peers);
+  if (pg->buf) cudaFree(pg->buf);
+  delete pg;
+  return TSV_OK;
+}
+
 int tsv_normalize_rows(const void* src_dev, int src_dtype, int64_t n, int dim, int normalize,
                        void* dst_bf16_dev, void* stream) {
   int rc = check_dtype(src_dtype);

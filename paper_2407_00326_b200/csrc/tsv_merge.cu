@@ -284,7 +284,111 @@ __global__ void seed_floor_kernel(const float* __restrict__ s, const int32_t* __
   floor_out[b] = id[o] >= 0 ? nextafterf(s[o], -INFINITY) : -FLT_MAX;
 }
 
+// ---------------------------------------------------------------------------------------------
+// Peer exchange fused with the cross-shard merge (sharded mode over NVLink / NVSwitch).
+// Every rank owns a symmetric buffer: flags[max_b] (cumulative arrival counters), then
+// recv_s / recv_i [2 parities][world][max_b][max_k]. A call (epoch e, parity e & 1):
+//   phase 1  each CTA pushes its queries' local top-k into slot [parity][rank][b] of every
+//            peer's buffer (stores through mapped peer memory), fences at system scope and
+//            bumps the peer's flags[b];
+//   phase 2  each CTA waits until its own flags[b] reach e * world (all ranks delivered),
+//            then merges the world lists of query b and writes the global top-k.
+// Every CTA sends everything before it waits and the grid is at most one CTA per SM, so no
+// CTA can wait on data that a non-resident CTA still has to send.
+struct PeerArgs {
+  void* const* peers;  // device array: base of each rank's symmetric buffer
+  int rank, world, B, k, max_b, max_k, parity;
+  uint32_t expected;
+  const float* local_s;
+  const int32_t* local_i;
+  float* out_s;
+  int32_t* out_i;
+};
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void peer_exchange_merge_kernel(const PeerArgs a) {
+  extern __shared__ uint64_t keys[];
+  const size_t flags_bytes = ((static_cast<size_t>(a.max_b) * 4 + 255) / 256) * 256;
+  const size_t plane = static_cast<size_t>(a.world) * a.max_b * a.max_k;  // entries per parity
+  auto recv_s = [&](void* base) {
+    return reinterpret_cast<float*>(static_cast<uint8_t*>(base) + flags_bytes);
+  };
+  auto recv_i = [&](void* base) {
+    return reinterpret_cast<int32_t*>(static_cast<uint8_t*>(base) + flags_bytes + 2 * plane * 4);
+  };
+  // phase 1: push
+  for (int b = blockIdx.x; b < a.B; b += gridDim.x) {
+    for (int p = 0; p < a.world; ++p) {
+      void* base = a.peers[p];
+      const size_t slot = ((static_cast<size_t>(a.parity) * a.world + a.rank) * a.max_b + b) * a.max_k;
+      for (int j = threadIdx.x; j < a.k; j += blockDim.x) {
+        recv_s(base)[slot + j] = a.local_s[static_cast<int64_t>(b) * a.k + j];
+        recv_i(base)[slot + j] = a.local_i[static_cast<int64_t>(b) * a.k + j];
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      for (int p = 0; p < a.world; ++p)
+        atomicAdd_system(reinterpret_cast<uint32_t*>(a.peers[p]) + b, 1u);
+    }
+  }
+  // phase 2: wait for every rank's contribution, merge
+  void* own = a.peers[a.rank];
+  const uint32_t* flags = reinterpret_cast<const uint32_t*>(own);
+  const int n = a.world * a.k;
+  const int np = pow2_ceil(n);
+  for (int b = blockIdx.x; b < a.B; b += gridDim.x) {
+    if (threadIdx.x == 0) {
+      while (ld_acquire_sys(flags + b) < a.expected) __nanosleep(128);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < np; i += blockDim.x) {
+      uint64_t key = pad_key();
+      if (i < n) {
+        const int r = i / a.k, j = i - (i / a.k) * a.k;
+        const size_t o = ((static_cast<size_t>(a.parity) * a.world + r) * a.max_b + b) * a.max_k + j;
+        const int32_t id = reinterpret_cast<volatile int32_t*>(recv_i(own))[o];
+        if (id >= 0) key = make_key(reinterpret_cast<volatile float*>(recv_s(own))[o], id);
+      }
+      keys[i] = key;
+    }
+    bitonic_sort_desc(keys, np);
+    for (int j = threadIdx.x; j < a.k; j += blockDim.x) {
+      const uint64_t key = keys[j];
+      const int32_t id = key_id(key);
+      a.out_s[static_cast<int64_t>(b) * a.k + j] = id < 0 ? -INFINITY : key_score(key);
+      a.out_i[static_cast<int64_t>(b) * a.k + j] = id;
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
+
+size_t peer_buffer_bytes(int world, int max_b, int max_k) {
+  const size_t flags_bytes = ((static_cast<size_t>(max_b) * 4 + 255) / 256) * 256;
+  return flags_bytes + 2 * 2 * static_cast<size_t>(world) * max_b * max_k * 4;
+}
+
+int launch_peer_exchange_merge(void* const* peers_dev, int rank, int world, int B, int k,
+                               int max_b, int max_k, int epoch, const float* local_s,
+                               const int32_t* local_i, float* out_s, int32_t* out_i,
+                               int num_sms, cudaStream_t stream) {
+  PeerArgs a{peers_dev, rank, world, B, k, max_b, max_k, epoch & 1,
+             static_cast<uint32_t>(epoch) * static_cast<uint32_t>(world), local_s, local_i,
+             out_s, out_i};
+  int np = 1;
+  while (np < world * k) np <<= 1;
+  const int grid = B < num_sms ? B : num_sms;
+  peer_exchange_merge_kernel<<<grid, 128, np * sizeof(uint64_t), stream>>>(a);
+  return static_cast<int>(cudaGetLastError());
+}
 
 int launch_seed_floor(const float* s, const int32_t* id, int B, int k, float* floor_out,
                       cudaStream_t stream) {

@@ -13,11 +13,18 @@ replica mode of backend.py, this module is the corpus-sharded mode (SURVEY.md §
 
 `search_fn` / `merge_fn` default to the device kernels; tests inject CPU doubles to exercise
 the shard arithmetic and collective wiring on the gloo backend.
+
+exchange="p2p" replaces steps 2-3 with one kernel (`tsv_peer_allgather_merge`): every rank
+pushes its [B, k] lists straight into the peers' symmetric buffers over NVLink (CUDA IPC
+mappings) and merges as soon as all ranks' lists have arrived — the collective and the merge
+are one launch, no NCCL call on the data path.
 """
 
 from __future__ import annotations
 
 from typing import Callable
+
+import ctypes
 
 import torch
 import torch.distributed as dist
@@ -28,9 +35,61 @@ def shard_range(n_rows: int, rank: int, world: int) -> tuple[int, int]:
     return n_rows * rank // world, n_rows * (rank + 1) // world
 
 
+class PeerExchange:
+    """Symmetric peer buffers across the ranks of a process group (collective constructor)."""
+
+    def __init__(self, device: torch.device, max_b: int, max_k: int, group=None):
+        from . import _native as nat
+
+        self.lib = nat.load()
+        self.check = nat.check
+        self.device = device
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.max_b, self.max_k = max_b, max_k
+        h = ctypes.c_void_p()
+        self.check(self.lib.tsv_peer_create(device.index, self.world, self.rank, max_b, max_k,
+                                            ctypes.byref(h)))
+        self._h = h
+        raw = (ctypes.c_ubyte * 64)()
+        n = ctypes.c_int()
+        self.check(self.lib.tsv_peer_handle(h, raw, ctypes.byref(n)))
+        mine = torch.tensor(list(bytes(raw)), dtype=torch.uint8)
+        if dist.get_backend(group) == "nccl":
+            mine = mine.to(device)
+        got = [torch.empty_like(mine) for _ in range(self.world)]
+        dist.all_gather(got, mine, group=group)
+        for p, t in enumerate(got):
+            buf = (ctypes.c_ubyte * 64)(*t.cpu().tolist())
+            self.check(self.lib.tsv_peer_open(h, p, buf))
+        dist.barrier(group)
+
+    def allgather_merge(self, s_loc: torch.Tensor, i_loc: torch.Tensor, k: int,
+                        stream: torch.cuda.Stream | None = None):
+        B = s_loc.shape[0]
+        out_s = torch.empty((B, k), dtype=torch.float32, device=self.device)
+        out_i = torch.empty((B, k), dtype=torch.int32, device=self.device)
+        st = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        self.check(self.lib.tsv_peer_allgather_merge(self._h, s_loc.data_ptr(), i_loc.data_ptr(),
+                                                     B, k, out_s.data_ptr(), out_i.data_ptr(),
+                                                     st))
+        return out_s, out_i
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self.lib.tsv_peer_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+
 class ShardedSearch:
     def __init__(self, index, n_rows: int, rank: int | None = None, world: int | None = None,
-                 group=None, search_fn: Callable | None = None, merge_fn: Callable | None = None):
+                 group=None, search_fn: Callable | None = None, merge_fn: Callable | None = None,
+                 exchange: str = "nccl"):
+        if exchange not in ("nccl", "p2p"):
+            raise ValueError(f"unknown exchange {exchange!r}")
+        self.exchange = exchange
+        self.p2p_error: str | None = None
+        self._peer: PeerExchange | None = None
         self.index = index
         self.group = group
         self.rank = dist.get_rank(group) if rank is None else rank
@@ -63,6 +122,15 @@ class ShardedSearch:
         self.search_fn(q, k, id_offset=self.lo, out=(s_loc, i_loc))
         if self.world == 1:
             return s_loc, i_loc
+        if self.exchange == "p2p":
+            if self._peer is None or self._peer.max_b < q.shape[0] or self._peer.max_k < k:
+                try:
+                    self._peer = PeerExchange(q.device, q.shape[0], k, self.group)
+                except Exception as exc:  # no peer mapping on this node: use NCCL instead
+                    self.exchange = "nccl"
+                    self.p2p_error = f"{type(exc).__name__}: {exc}"
+                    return self.search(q, k)
+            return self._peer.allgather_merge(s_loc, i_loc, k)
         if dist.get_backend(self.group) == "nccl":
             dist.all_gather_into_tensor(s_all, s_loc, group=self.group)
             dist.all_gather_into_tensor(i_all, i_loc, group=self.group)
