@@ -619,6 +619,7 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
     TSV_CUDA(cudaMemsetAsync(w.counter.ptr, 0, sizeof(int32_t) * num_items, st), "progress reset");
     p.counter = w.counter.ptr;
     p.flags |= tsv::kFlagLockstep;
+    if (const char* e = getenv("TSV_LOCK_WINDOW")) p.lock_window = std::max(1, atoi(e));
   }
   if (R == 1) {
     p.out_k = k;

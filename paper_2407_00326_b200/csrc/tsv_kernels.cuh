@@ -60,6 +60,7 @@ struct ScanParams {
   // Optional per-query admission floor (k > 32 lists): a lower bound of the query's final k-th
   // score (from a sample pass); candidates at or below it can never be in the result.
   const float* tau0;
+  int32_t lock_window;  // lockstep: max tiles ahead of range partners (0 = default)
 };
 
 // `mb` argument selecting the dynamic-unit CTA-pair kernel (see tsv_scan.cu).

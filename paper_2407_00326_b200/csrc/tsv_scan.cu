@@ -23,7 +23,7 @@
 namespace tsv {
 namespace {
 
-constexpr int kLockWindow = 4;  // 256-row tiles a worker may run ahead of its range partners
+constexpr int kLockWindow = 2;  // 256-row tiles a worker may run ahead of its range partners
 
 // Lists of more than kRegListMax entries live in shared memory (one column per query thread,
 // entry j of thread t at [j * 128 + t], so lock-step accesses are bank-conflict free).
@@ -575,11 +575,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
       const int nqg = num_items / p.R;
       for (int64_t t = 0; t < ntiles; ++t) {
         if (lockstep && leader && lane == 0) {
+          const int w = p.lock_window > 0 ? p.lock_window : kLockWindow;
           if ((t & 1) == 0) progress[i] = static_cast<int32_t>(t);
-          if (t >= kLockWindow) {
+          if (t >= w) {
             for (int g = 0; g < nqg; ++g) {
               if (g == my_qg) continue;
-              while (progress[g * p.R + my_r] < t - kLockWindow) __nanosleep(256);
+              while (progress[g * p.R + my_r] < t - w) __nanosleep(256);
             }
           }
         }
