@@ -84,6 +84,8 @@ def run_config(name: str, cfg: dict, profiles: dict, limit: int | None, devices)
     backend.warmup()
     sim, trace = R.run_queries(es, subs, R.RuntimeOptions(scheduler="topo"), backend=backend)
     torch.cuda.synchronize()
+    from paper_2407_00326_b200.report import retrieval_report
+
     lat = [c.latency_ms for c in sim.contexts.values() if c.latency_ms is not None]
     out = {"config": name, "queries": len(subs), "completed": len(lat),
            "e2e_ms": {"mean": float(np.mean(lat)) if lat else None, "p50": pct(lat, 50),
@@ -100,6 +102,7 @@ def run_config(name: str, cfg: dict, profiles: dict, limit: int | None, devices)
             "device_ms": {"p50": pct(dev, 50), "p95": pct(dev, 95), "mean": float(np.mean(dev))},
             "simulated_profile_ms": {"p50": pct(sim_ms, 50), "mean": float(np.mean(sim_ms))},
         }
+    out["device_report"] = retrieval_report(backend)
     return out
 
 

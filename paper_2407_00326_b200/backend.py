@@ -118,6 +118,28 @@ class SearchResult:
 
 
 @dataclass
+class LaunchRecord:
+    """Per-batch device record (SURVEY.md §5 tracing): what one retrieval batch moved and
+    computed, and how long the device took."""
+
+    engine_id: str
+    replica: int
+    kind: str          # "search" | "rerank"
+    queries: int       # queries (search) or questions (rerank)
+    rows: int          # corpus rows scanned (search) or candidate rows gathered (rerank)
+    k: int
+    dim: int
+    bytes: int         # algorithmic bytes: rows + queries read, results written
+    flops: int         # algorithmic flops (2 per multiply-add)
+    start: object = None
+    end: object = None
+
+    @property
+    def device_ms(self) -> float:
+        return self.start.elapsed_time(self.end)
+
+
+@dataclass
 class Replica:
     device: torch.device
     stream: torch.cuda.Stream
@@ -155,6 +177,7 @@ class RetrievalBackend:
         self.acc: dict[tuple[str, str], list] = {}
         self.launches = 0
         self.device_ms_total = 0.0
+        self.records: list[LaunchRecord] = []
 
     # -- binding ---------------------------------------------------------------------
     def serves(self, profile: EngineProfile) -> bool:
@@ -304,11 +327,14 @@ class RetrievalBackend:
             # inputs are assembled first; `start` is recorded right before the library calls,
             # so the measured window is the device work of the batch
             if profile.category == "search":
-                self._search_batch(rep, plan, start)
+                rec = self._search_batch(rep, plan, start)
             else:
-                self._rerank_batch(rep, plan, start)
+                rec = self._rerank_batch(rep, plan, start)
             end.record(rep.stream)
         self.launches += 1
+        rec.engine_id, rec.replica, rec.start, rec.end = (profile.engine_id,
+                                                          self.replicas.index(rep), start, end)
+        self.records.append(rec)
         return start, end
 
     def execute(self, profile: EngineProfile, plan, t: float, instance) -> tuple[float, float | None]:
@@ -389,6 +415,12 @@ class RetrievalBackend:
         for (task, lo, n, k), a in zip(metas, q_off[:-1]):
             self.acc.setdefault((task.ctx.query_id, task.node_id), []).append(
                 (lo, scores[a:a + n, :k], ids[a:a + n, :k], ready, r))
+        nq = q_off[-1]
+        rows = sum(b - a for a, b in ranges)
+        pairs = sum((q_off[i + 1] - q_off[i]) * (b - a) for i, (a, b) in enumerate(ranges))
+        return LaunchRecord("", 0, "search", nq, rows, kmax, self.dim,
+                            bytes=rows * self.dim * 2 + nq * self.dim * 2 + nq * kmax * 8,
+                            flops=2 * pairs * self.dim)
 
     def _rerank_batch(self, rep: Replica, plan, start: torch.cuda.Event) -> None:
         jobs = []
@@ -416,6 +448,11 @@ class RetrievalBackend:
             i = torch.where(i >= 0, i - seg.row_beg, i).to(torch.int32)
             self.acc.setdefault((task.ctx.query_id, task.node_id), []).append(
                 (lo, s, i, self._record(rep), self.replicas.index(rep)))
+        n_rows = sum(j[5].shape[1] for j in jobs)
+        k_out = max(j[2] for j in jobs)
+        return LaunchRecord("", 0, "rerank", len(jobs), n_rows, k_out, self.dim,
+                            bytes=n_rows * (self.dim * 2 + 4) + len(jobs) * (self.dim * 2 + k_out * 8),
+                            flops=2 * n_rows * self.dim)
 
     def _index_of_search(self, ctx, producer: str):
         """Walk back from an Aggregate / Searching producer to the Searching node's index input."""

@@ -117,3 +117,34 @@ def test_measured_timing_reports_device_time(cuda):
     gpu = [b for b in trace.batches if b.engine_id in ("vdb-search0", "rerank0")]
     assert gpu and all(b.device_ms is not None and b.device_ms > 0 for b in gpu)
     assert all(abs((b.end_ms - b.start_ms) - b.device_ms) < 1e-9 for b in gpu)
+
+
+def test_launch_records_and_report(cuda):
+    from paper_2407_00326_b200.report import retrieval_report, write_launch_csv
+
+    traces, prof = _fixture()
+    case = next(c for c in traces if c["case"] == "advanced_c3" and c["scheduler"] == "topo")
+    sim, trace, backend = _run(case, prof)
+    assert len(backend.records) == backend.launches > 0
+    rep = retrieval_report(backend)
+    assert set(rep) == {"vdb-search0", "rerank0"}
+    assert all(v["device_ms_total"] > 0 and v["achieved_gbs"] > 0 for v in rep.values())
+    import tempfile
+
+    with tempfile.NamedTemporaryFile(suffix=".csv") as f:
+        write_launch_csv(backend, f.name)
+        assert open(f.name).read().count("\n") == len(backend.records) + 1
+
+
+def test_measured_profile_gives_gpu_true_beff(cuda):
+    from paper_2407_00326_b200.engines import max_efficient_batch
+    from paper_2407_00326_b200.profiler import measure_rerank_profile, measure_search_profile
+
+    s, samples = measure_search_profile(rows=200_000, dim=256, batches=(1, 4, 16, 64, 256))
+    assert [b for b, _ in samples] == [1, 4, 16, 64, 256]
+    assert all(ms > 0 for _, ms in samples)
+    # per-query cost falls with batch size until the scan stops being memory-bound
+    assert samples[-1][1] / 256 < samples[0][1]
+    assert max_efficient_batch(s) >= 16
+    r, _ = measure_rerank_profile(rows=20_000, dim=256, candidates=(8, 32, 128))
+    assert r.category == "rerank" and len(r.latency_table) == 3

@@ -208,3 +208,24 @@ def test_determinism_identical_traces(profiles):
         subs = [(parse_graph(g), a, b) for g, a, b in case["graphs"]]
         runs.append(R.run_queries(es, subs)[1].rows())
     assert runs[0] == runs[1]
+
+
+def test_b200_measured_profiles_change_the_split(profiles):
+    """With the reference profile a 1024-query Searching node splits into 64 stages of 16
+    (B_eff 16); with the B200-measured profile (profiles/b200_engines.json,
+    written by paper_2407_00326_b200/profiler.py on a B200) it stays one launch."""
+    from pathlib import Path
+
+    from paper_2407_00326_b200.graph import PGraph
+
+    ref = E.EngineSet.from_dict(profiles["default"]["profiles"])
+    b200 = E.EngineSet.from_dict(json.loads(
+        (Path(__file__).resolve().parents[1] / "profiles" / "b200_engines.json").read_text()))
+    node = S.searching_node("search", "vdb-search0", {"query_count": 1024, "per_query_top_k": 10},
+                            (), "top")
+    g = PGraph(nodes={node.node_id: node}, edges=[], query_id="q")
+    out_ref, _ = S.stage_decompose(g, ref)
+    out_b200, fired = S.stage_decompose(g, b200)
+    assert len(out_ref.nodes) == 64
+    assert E.max_efficient_batch(b200["vdb-search0"]) >= 256
+    assert len(out_b200.nodes) == 1024 // int(E.max_efficient_batch(b200["vdb-search0"]))
