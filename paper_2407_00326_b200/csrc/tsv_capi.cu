@@ -237,34 +237,40 @@ int stage_queries(tsv_index* idx, Workspace& w, const void* q, int q_dtype, int6
 
 // Query tensor maps are cached per (pointer, rows, dim): staged queries live in a stable
 // per-stream workspace buffer, so repeated searches skip the host-side encode.
-int query_map(const void* qb, int64_t B, int dim, CUtensorMap* out) {
+int query_map(const void* qb, int64_t B, int dim, CUtensorMap* out, int box_rows = tsv::kBlockM) {
   struct Key {
     const void* p;
     int64_t b;
     int d;
+    int box;
     bool operator<(const Key& o) const {
-      return p != o.p ? p < o.p : (b != o.b ? b < o.b : d < o.d);
+      return p != o.p ? p < o.p : (b != o.b ? b < o.b : (d != o.d ? d < o.d : box < o.box));
     }
   };
   static std::mutex mu;
   static std::map<Key, CUtensorMap> cache;
   std::lock_guard<std::mutex> lock(mu);
-  auto it = cache.find(Key{qb, B, dim});
+  auto it = cache.find(Key{qb, B, dim, box_rows});
   if (it != cache.end()) {
     *out = it->second;
     return TSV_OK;
   }
-  int rc = encode_rows_map(out, qb, B, dim, tsv::kBlockM);
+  int rc = encode_rows_map(out, qb, B, dim, box_rows);
   if (rc) return rc;
   if (cache.size() > 4096) cache.clear();
-  cache.emplace(Key{qb, B, dim}, *out);
+  cache.emplace(Key{qb, B, dim, box_rows}, *out);
   return TSV_OK;
 }
 
 int run_scan(tsv_index* idx, int mb, int kcap, const void* qb, int64_t B, tsv::ScanParams& p,
              int grid, cudaStream_t st) {
+  // One query group of fewer than 128 queries: load only its rows (TMA out-of-bounds fill of
+  // the rest of a 128-row box costs as much as real rows and halves the HBM-bound scan rate).
+  p.a_rows = (mb == 1 && p.items == nullptr && B < tsv::kBlockM && !getenv("TSV_FULL_QBOX"))
+                 ? static_cast<int>((B + 7) & ~7)
+                 : 0;
   CUtensorMap tq;
-  int rc = query_map(qb, B, idx->dim, &tq);
+  int rc = query_map(qb, B, idx->dim, &tq, p.a_rows ? p.a_rows : tsv::kBlockM);
   if (rc) return rc;
   TimedLaunch tl{};
   if (idx->timing) {

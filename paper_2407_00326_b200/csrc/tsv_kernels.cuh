@@ -61,6 +61,10 @@ struct ScanParams {
   // score (from a sample pass); candidates at or below it can never be in the result.
   const float* tau0;
   int32_t lock_window;  // lockstep: max tiles ahead of range partners (0 = default)
+  // Single-CTA bf16 kernel: query rows per A-tile TMA box (0 = kBlockM). With B < 128 the box
+  // covers only the real queries (rounded up to the 8-row swizzle atom); the TMEM lanes of the
+  // rows it leaves untouched are never emitted.
+  int32_t a_rows;
 };
 
 // `mb` argument selecting the dynamic-unit CTA-pair kernel (see tsv_scan.cu).

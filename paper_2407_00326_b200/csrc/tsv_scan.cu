@@ -255,6 +255,9 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
     const bool lockstep = (p.flags & kFlagLockstep) && p.items == nullptr &&
                           num_items <= static_cast<int>(gridDim.x);
     volatile int32_t* progress = p.counter;
+    const uint32_t stage_tx = (!TF32 && p.a_rows > 0)
+                                  ? static_cast<uint32_t>(MB * p.a_rows * 128 + Cfg::kBBytes)
+                                  : static_cast<uint32_t>(Cfg::kStageBytes);
     for (int i = blockIdx.x; i < num_items; i += gridDim.x) {
       ScanItem it;
       resolve_item(p, i, it, kQG);
@@ -275,7 +278,7 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
         for (int kb = 0; kb < p.num_kb; ++kb) {
           ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* st = smem + stage * Cfg::kStageBytes;
-          ptx::mbar_arrive_expect_tx_warp(&full_bar[stage], Cfg::kStageBytes);
+          ptx::mbar_arrive_expect_tx_warp(&full_bar[stage], stage_tx);
 #pragma unroll
           for (int mb = 0; mb < MB; ++mb)
             ptx::tma_load_2d_warp(st + mb * Cfg::kABytes, &tmap_q, &full_bar[stage],
