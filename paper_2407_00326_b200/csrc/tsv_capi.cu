@@ -206,7 +206,7 @@ int check_dtype(int dt) {
   return TSV_OK;
 }
 
-constexpr int kMergeCap = 8192;  // candidates per query the merge kernel sorts in smem
+constexpr int kMergeCap = 16384;  // candidates per query the merge kernel sorts in smem
 constexpr int kMinTilesPerRange = 1;
 
 bool env_flag(const char* name) {
@@ -528,14 +528,17 @@ int tsv_index_scan_time(tsv_index* idx, double* total_ms, int64_t* launches) {
 
 static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k,
                        int64_t row_beg, int64_t row_end, int32_t id_offset, float* scores_dev,
-                       int32_t* ids_dev, void* stream, const float* tau0) {
+                       int32_t* ids_dev, void* stream, const float* tau0, int list_cap = 0) {
+  // list_cap > 0 (sample pass of a seeded search): per-range lists of list_cap < k entries;
+  // the merge then returns the best k of the union of those lists.
   if (idx == nullptr) return fail(TSV_ERR_ARGUMENT, "index is null");
   int rc = check_dtype(q_dtype);
   if (rc) return rc;
   if (B <= 0) return fail(TSV_ERR_CAPACITY, "empty batch");
   if (k <= 0) return fail(TSV_ERR_CONFIG, "k must be >= 1");
-  const int kcap = tsv::scan_kcap_for(k);
-  if (kcap == 0) return fail(TSV_ERR_CONFIG, "k=%d exceeds the supported maximum (128)", k);
+  if (tsv::scan_kcap_for(k) == 0)
+    return fail(TSV_ERR_CONFIG, "k=%d exceeds the supported maximum (128)", k);
+  const int kcap = list_cap > 0 ? tsv::scan_kcap_for(list_cap) : tsv::scan_kcap_for(k);
   if (q_dev == nullptr || scores_dev == nullptr || ids_dev == nullptr)
     return fail(TSV_ERR_ARGUMENT, "null buffer");
   if (row_beg < 0 || row_end > idx->rows || row_beg > row_end)
@@ -619,15 +622,22 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
     g_launches++;
     return TSV_OK;
   }
-  if (nqg > 1 && num_items <= units && !env_flag("TSV_NO_LOCKSTEP")) {
-    rc = w.counter.ensure(static_cast<size_t>(num_items));
+  const bool lock = nqg > 1 && num_items <= units && !env_flag("TSV_NO_LOCKSTEP");
+  const bool floor = R > 1 && !env_flag("TSV_NO_FLOOR");
+  if (lock || floor) {  // one zeroed buffer: [progress counters][per-query floors]
+    const size_t nc = lock ? static_cast<size_t>(num_items) : 0;
+    const size_t n = nc + (floor ? static_cast<size_t>(B) : 0);
+    rc = w.counter.ensure(n);
     if (rc) return rc;
-    TSV_CUDA(cudaMemsetAsync(w.counter.ptr, 0, sizeof(int32_t) * num_items, st), "progress reset");
-    p.counter = w.counter.ptr;
-    p.flags |= tsv::kFlagLockstep;
-    if (const char* e = getenv("TSV_LOCK_WINDOW")) p.lock_window = std::max(1, atoi(e));
+    TSV_CUDA(cudaMemsetAsync(w.counter.ptr, 0, sizeof(int32_t) * n, st), "progress reset");
+    if (lock) {
+      p.counter = w.counter.ptr;
+      p.flags |= tsv::kFlagLockstep;
+      if (const char* e = getenv("TSV_LOCK_WINDOW")) p.lock_window = std::max(1, atoi(e));
+    }
+    if (floor) p.floor_g = reinterpret_cast<uint32_t*>(w.counter.ptr + nc);
   }
-  if (R == 1) {
+  if (R == 1 && kcap >= k) {
     p.out_k = k;
     p.out_scores = scores_dev;
     p.out_ids = ids_dev;
@@ -671,10 +681,13 @@ int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int
     if (!rc) rc = w.seed_i.ensure(static_cast<size_t>(B) * k);
     if (!rc) rc = w.tau0.ensure(static_cast<size_t>(B));
     if (rc) return rc;
-    // the sample pass is itself seeded from a smaller sample when it is large enough; it
-    // reuses the seed buffers only after its own floor has been consumed (same stream order)
-    rc = tsv_search(idx, q_dev, q_dtype, B, k, row_beg, row_beg + sample, 0, w.seed_s.ptr,
-                    w.seed_i.ptr, stream);
+    // Sample pass with 32-entry register lists per corpus range: the k-th best of the union
+    // of those lists is still a lower bound of the sample's k-th best (the union holds k
+    // distinct rows scoring at least that much) and, with the top rows spread over many
+    // ranges, usually equal to it; the k-entry shared-memory lists of the main pass then see
+    // few insertions.
+    rc = search_impl(idx, q_dev, q_dtype, B, k, row_beg, row_beg + sample, 0, w.seed_s.ptr,
+                     w.seed_i.ptr, stream, nullptr, tsv::kMaxRegK);
     if (rc) return rc;
     int e = tsv::launch_seed_floor(w.seed_s.ptr, w.seed_i.ptr, B, k, w.tau0.ptr, st);
     if (e) return cuda_fail(static_cast<cudaError_t>(e), "seed floor");
@@ -778,6 +791,12 @@ int tsv_search_segmented(tsv_index* idx, const void* q_dev, int q_dtype, int nse
   p.num_kb = (idx->dim + kb_elems - 1) / kb_elems;
   if (tiled) p.flags |= tsv::kFlagTiled;
   const int grid = std::min(p.num_items, idx->num_sms);
+  if (R > 1 && !env_flag("TSV_NO_FLOOR")) {  // shared admission floors (see ScanParams)
+    rc = w.counter.ensure(static_cast<size_t>(B));
+    if (rc) return rc;
+    TSV_CUDA(cudaMemsetAsync(w.counter.ptr, 0, sizeof(int32_t) * B, st), "floor reset");
+    p.floor_g = reinterpret_cast<uint32_t*>(w.counter.ptr);
+  }
   if (R == 1) {
     p.out_k = k;
     p.out_scores = scores_dev;

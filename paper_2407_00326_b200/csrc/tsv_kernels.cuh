@@ -65,6 +65,13 @@ struct ScanParams {
   // covers only the real queries (rounded up to the 8-row swizzle atom); the TMEM lanes of the
   // rows it leaves untouched are never emitted.
   int32_t a_rows;
+  // Shared admission floor (nullptr = off), one order-preserving key per query row, zeroed
+  // before the launch. Every corpus range of a query publishes the k-th score of its full list
+  // (atomicMax) and admits only candidates at or above the best published one: that range's
+  // list already holds k rows scoring at least that much, so nothing below it can reach the
+  // merged top-k. Without it each range's threshold starts from scratch and the insertions
+  // of the first tiles of every range dominate short scans.
+  uint32_t* floor_g;
 };
 
 // `mb` argument selecting the dynamic-unit CTA-pair kernel (see tsv_scan.cu).

@@ -66,20 +66,25 @@ __global__ void merge_topk_kernel(const float* __restrict__ in_s, const int32_t*
                                   float* __restrict__ out_s, int32_t* __restrict__ out_id,
                                   int dedup) {
   extern __shared__ uint64_t keys[];
+  __shared__ int count;
   const int b = blockIdx.x;
   const int n = lists * kin;
-  const int np = pow2_ceil(n);
-  for (int i = threadIdx.x; i < np; i += blockDim.x) {
-    uint64_t key = pad_key();
-    if (i < n) {
-      const int r = i / kin;
-      const int j = i - r * kin;
-      const int64_t off = (static_cast<int64_t>(r) * list_stride_rows + b) * kin + j;
-      const int32_t id = in_id[off];
-      if (id >= 0) key = make_key(in_s[off], id);
-    }
-    keys[i] = key;
+  // Compact the real entries first: seeded / floored scans leave most partial lists mostly
+  // padding, and the sort cost follows the compacted size (the key order makes the result
+  // independent of the compaction order).
+  if (threadIdx.x == 0) count = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int r = i / kin;
+    const int j = i - r * kin;
+    const int64_t off = (static_cast<int64_t>(r) * list_stride_rows + b) * kin + j;
+    const int32_t id = in_id[off];
+    if (id >= 0) keys[atomicAdd(&count, 1)] = make_key(in_s[off], id);
   }
+  __syncthreads();
+  const int m = count;
+  const int np = pow2_ceil(m > 0 ? m : 1);
+  for (int i = m + threadIdx.x; i < np; i += blockDim.x) keys[i] = pad_key();
   bitonic_sort_desc(keys, np);
   if (dedup) {
     // Copies of one id carry identical scores, so they are adjacent after the sort.
@@ -423,12 +428,12 @@ int launch_merge_topk(const float* in_s, const int32_t* in_id, int lists, int B,
   if (B <= 0) return 0;
   int np = 1;
   while (np < lists * kin) np <<= 1;
-  if (np > 8192) return static_cast<int>(cudaErrorInvalidValue);
+  if (np > 16384) return static_cast<int>(cudaErrorInvalidValue);
   const size_t smem = static_cast<size_t>(np) * sizeof(uint64_t);
   static std::atomic<uint64_t> configured{0};
   if (smem > 48 * 1024 && first_on_device(configured)) {
     cudaError_t e = cudaFuncSetAttribute(merge_topk_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
     if (e != cudaSuccess) return static_cast<int>(e);
   }
   const int threads = np >= 1024 ? 256 : (np >= 256 ? 128 : 64);

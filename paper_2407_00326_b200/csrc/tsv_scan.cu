@@ -78,6 +78,24 @@ __device__ __forceinline__ void resolve_item(const ScanParams& p, int i, ScanIte
   it.id_offset = p.id_offset;
 }
 
+// Order-preserving float <-> uint32 keys for the shared admission floor (atomicMax).
+__device__ __forceinline__ uint32_t ord_key(float f) {
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+// Admission bound for a published k-th score f: admit x >= f, i.e. x > nextafter(f, -inf).
+// Key 0 (nothing published yet) admits everything.
+__device__ __forceinline__ float floor_admit(uint32_t key) {
+  if (key == 0) return -FLT_MAX;
+  const float f = __uint_as_float((key & 0x80000000u) ? (key & 0x7fffffffu) : ~key);
+  return nextafterf(f, -INFINITY);
+}
+__device__ __forceinline__ uint32_t floor_load(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
 // Insert (x, xi) into a list sorted by (score desc, id asc). Precondition: x > s[K-1].
 // Elements with score >= x keep their place (they were seen earlier, so their ids are
 // smaller), the rest shift down one slot and the last one drops out.
@@ -98,9 +116,31 @@ __device__ __forceinline__ void list_insert(float (&s)[K], int32_t (&id)[K], flo
   }
 }
 
-template <int K>
-__device__ __forceinline__ void scan_chunk(const uint32_t (&v)[32], float (&s)[K], int32_t (&id)[K],
-                                           int32_t id0, int valid) {
+// v[j] for a run-time j via a 5-level tree of constant-index selects: indexing the chunk
+// dynamically would spill it to local memory.
+__device__ __forceinline__ float pick32(const uint32_t (&v)[32], int j) {
+  uint32_t a[16], b[8], c[4], d[2];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = (j & 1) ? v[2 * i + 1] : v[2 * i];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) b[i] = (j & 2) ? a[2 * i + 1] : a[2 * i];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) c[i] = (j & 4) ? b[2 * i + 1] : b[2 * i];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) d[i] = (j & 8) ? c[2 * i + 1] : c[2 * i];
+  return __uint_as_float((j & 16) ? d[1] : d[0]);
+}
+
+// Candidate bit mask of a 32-score chunk: bit j set iff v[j] > thr and j < valid.
+__device__ __forceinline__ uint32_t chunk_mask(const uint32_t (&v)[32], float thr, int valid) {
+  uint32_t mask = 0;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) mask |= (__uint_as_float(v[j]) > thr ? 1u : 0u) << j;
+  if (valid < 32) mask &= valid > 0 ? (0xffffffffu >> (32 - valid)) : 0u;
+  return mask;
+}
+
+__device__ __forceinline__ float chunk_max(const uint32_t (&v)[32]) {
   float m0 = fmaxf(__uint_as_float(v[0]), __uint_as_float(v[1]));
   float m1 = fmaxf(__uint_as_float(v[2]), __uint_as_float(v[3]));
 #pragma unroll
@@ -108,15 +148,26 @@ __device__ __forceinline__ void scan_chunk(const uint32_t (&v)[32], float (&s)[K
     m0 = fmaxf(m0, fmaxf(__uint_as_float(v[j]), __uint_as_float(v[j + 1])));
     m1 = fmaxf(m1, fmaxf(__uint_as_float(v[j + 2]), __uint_as_float(v[j + 3])));
   }
-  const float m = fmaxf(m0, m1);
-  if (m > s[K - 1]) {
-    // Rare path, fully unrolled so the chunk stays in registers (a rolled loop would index
-    // v[] dynamically and spill it to local memory, whose L1 traffic competes with the
-    // tensor core's shared-memory operand reads).
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const float x = __uint_as_float(v[j]);
-      if (x > s[K - 1] && j < valid) list_insert<K>(s, id, x, id0 + j);
+  return fmaxf(m0, m1);
+}
+
+// Filter one 32-score chunk (this thread's query x 32 corpus rows) into its register list.
+// Common case: one max-reduce and a compare. Rare case (the chunk beats the admission bound
+// max(k-th, fl)): a candidate bit mask, then a rolled loop over its set bits in ascending
+// row order (so equal scores keep the smaller id first). The rare path is deliberately small:
+// a fully unrolled 32-way insertion body per chunk overflows the instruction cache, and with
+// 32 queries per warp the "rare" path runs for most chunks of a short scan.
+template <int K>
+__device__ __forceinline__ void scan_chunk(const uint32_t (&v)[32], float (&s)[K], int32_t (&id)[K],
+                                           int32_t id0, int valid, float fl) {
+  const float thr = fmaxf(s[K - 1], fl);
+  if (chunk_max(v) > thr) {
+    uint32_t mask = chunk_mask(v, thr, valid);
+    while (mask) {
+      const int j = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const float x = pick32(v, j);
+      if (x > fmaxf(s[K - 1], fl)) list_insert<K>(s, id, x, id0 + j);
     }
   }
 }
@@ -168,25 +219,50 @@ template <int K>
 __device__ __forceinline__ void scan_chunk_coop(const uint32_t (&v)[32], float* ls, int32_t* li,
                                                 int row_base, int lane, float& tau, int32_t id0,
                                                 int valid, float floor_tau) {
-  float m0 = fmaxf(__uint_as_float(v[0]), __uint_as_float(v[1]));
-  float m1 = fmaxf(__uint_as_float(v[2]), __uint_as_float(v[3]));
-#pragma unroll
-  for (int j = 4; j < 32; j += 4) {
-    m0 = fmaxf(m0, fmaxf(__uint_as_float(v[j]), __uint_as_float(v[j + 1])));
-    m1 = fmaxf(m1, fmaxf(__uint_as_float(v[j + 2]), __uint_as_float(v[j + 3])));
-  }
-  if (!__any_sync(0xffffffffu, fmaxf(m0, m1) > tau)) return;
-#pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const float x = __uint_as_float(v[j]);
-    unsigned want = __ballot_sync(0xffffffffu, x > tau && j < valid);
-    while (want) {
-      const int src = __ffs(want) - 1;
-      want &= want - 1;
-      const float xs = __shfl_sync(0xffffffffu, x, src);
-      const float t_new = coop_list_insert<K>(ls, li, row_base + src, xs, id0 + j, lane);
+  if (!__any_sync(0xffffffffu, chunk_max(v) > tau)) return;
+  uint32_t mask = chunk_mask(v, tau, valid);
+  // one candidate per iteration, lowest lane first; each lane's candidates in ascending row
+  // order (its list keeps equal scores in id order)
+  while (true) {
+    const unsigned lanes = __ballot_sync(0xffffffffu, mask != 0);
+    if (lanes == 0) break;
+    const int src = __ffs(lanes) - 1;
+    const int j = (__ffs(mask) - 1) & 31;
+    const float x = pick32(v, j);
+    if (lane == src) mask &= mask - 1;
+    const int js = __shfl_sync(0xffffffffu, j, src);
+    const float xs = __shfl_sync(0xffffffffu, x, src);
+    const float ts = __shfl_sync(0xffffffffu, tau, src);
+    if (xs > ts) {
+      const float t_new = coop_list_insert<K>(ls, li, row_base + src, xs, id0 + js, lane);
       if (lane == src) tau = fmaxf(t_new, floor_tau);
     }
+  }
+}
+
+// After each tile: adopt the best k-th score published by the other ranges of this query
+// (`fkey`, loaded before the tile so the L2 latency is hidden) and publish our own once the
+// list is full and has improved. `fl` is the admission bound scan_chunk(_coop) applies.
+template <int KCAP, bool kSmemList, int kRegK>
+__device__ __forceinline__ void share_floor(uint32_t* fslot, uint32_t fkey, const float (&s)[kRegK],
+                                            const int32_t (&id)[kRegK], const float* list_s,
+                                            const int32_t* list_i, int t_epi, float& fl,
+                                            float& tau, float& published) {
+  fl = fmaxf(fl, floor_admit(fkey));
+  float kth;
+  bool full;
+  if constexpr (kSmemList) {
+    __syncwarp();  // the list tail may have been written by another lane
+    kth = list_s[t_epi * KCAP + KCAP - 1];
+    full = list_i[t_epi * KCAP + KCAP - 1] >= 0;
+    tau = fmaxf(tau, fl);
+  } else {
+    kth = s[kRegK - 1];
+    full = id[kRegK - 1] >= 0;
+  }
+  if (fslot != nullptr && full && kth > published) {
+    atomicMax(fslot, ord_key(kth));
+    published = kth;
   }
 }
 
@@ -385,6 +461,9 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
       const float tau_floor = (p.tau0 != nullptr && lq < it.q_count) ? p.tau0[it.q_begin + lq]
                                                                       : -FLT_MAX;
       float tau = tau_floor;
+      uint32_t* const fslot =
+          (p.floor_g != nullptr && lq < it.q_count) ? p.floor_g + it.q_begin + lq : nullptr;
+      float fl = tau_floor, published = -FLT_MAX;
 #pragma unroll
       for (int j = 0; j < kRegK; ++j) {
         s[j] = -FLT_MAX;
@@ -402,6 +481,7 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
         const int64_t row0 = it.row_begin + t * kBlockN;
         const int valid = static_cast<int>(it.row_end - row0 < kBlockN ? it.row_end - row0 : kBlockN);
         const int32_t id0 = static_cast<int32_t>(row0) + it.id_offset;
+        const uint32_t fkey = fslot != nullptr ? floor_load(fslot) : 0u;  // used after this tile
         ptx::mbar_wait(&tfull_bar[abuf], aphase);
         ptx::tc_fence_after();
         const uint32_t taddr = lane_addr + abuf * Cfg::kAccCols;
@@ -421,9 +501,9 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
                                       __uint_as_float(vc[j]));
             if constexpr (kSmemList)
               scan_chunk_coop<KCAP>(va, list_s, list_i, quad * 32, lane, tau, id0 + c, valid - c,
-                                  tau_floor);
+                                  fl);
             else
-              scan_chunk<kRegK>(va, s, id, id0 + c, valid - c);
+              scan_chunk<kRegK>(va, s, id, id0 + c, valid - c, fl);
           }
         } else {
 #pragma unroll 1
@@ -434,17 +514,20 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
           ptx::tmem_ld_wait();
           if constexpr (kSmemList) {
             scan_chunk_coop<KCAP>(va, list_s, list_i, quad * 32, lane, tau, id0 + c, valid - c,
-                                  tau_floor);
+                                  fl);
             scan_chunk_coop<KCAP>(vb, list_s, list_i, quad * 32, lane, tau, id0 + c + 32,
-                                  valid - c - 32, tau_floor);
+                                  valid - c - 32, fl);
           } else {
-            scan_chunk<kRegK>(va, s, id, id0 + c, valid - c);
-            scan_chunk<kRegK>(vb, s, id, id0 + c + 32, valid - c - 32);
+            scan_chunk<kRegK>(va, s, id, id0 + c, valid - c, fl);
+            scan_chunk<kRegK>(vb, s, id, id0 + c + 32, valid - c - 32, fl);
           }
         }
         }
         ptx::tc_fence_before();
         ptx::mbar_arrive(&tempty_bar[abuf]);
+        if (p.floor_g != nullptr)  // warp-uniform (the smem-list variant syncs the warp)
+          share_floor<KCAP, kSmemList>(fslot, fkey, s, id, list_s, list_i, t_epi, fl, tau,
+                                       published);
         if (++abuf == Cfg::kAccBufs) {
           abuf = 0;
           aphase ^= 1;
@@ -664,6 +747,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
       const float tau_floor = (p.tau0 != nullptr && lq < it.q_count) ? p.tau0[it.q_begin + lq]
                                                                       : -FLT_MAX;
       float tau = tau_floor;
+      uint32_t* const fslot =
+          (p.floor_g != nullptr && lq < it.q_count) ? p.floor_g + it.q_begin + lq : nullptr;
+      float fl = tau_floor, published = -FLT_MAX;
 #pragma unroll
       for (int j = 0; j < kRegK; ++j) {
         s[j] = -FLT_MAX;
@@ -682,6 +768,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
         const int valid = static_cast<int>(
             it.row_end - row0 < Pair::kTileRows ? it.row_end - row0 : Pair::kTileRows);
         const int32_t id0 = static_cast<int32_t>(row0) + it.id_offset;
+        const uint32_t fkey = fslot != nullptr ? floor_load(fslot) : 0u;  // used after this tile
         ptx::mbar_wait(&tfull_bar[abuf], aphase);
         ptx::tc_fence_after();
         const uint32_t taddr = lane_addr + abuf * Pair::kAccCols;
@@ -693,17 +780,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
           ptx::tmem_ld_wait();
           if constexpr (kSmemList) {
             scan_chunk_coop<KCAP>(va, list_s, list_i, quad * 32, lane, tau, id0 + c, valid - c,
-                                  tau_floor);
+                                  fl);
             scan_chunk_coop<KCAP>(vb, list_s, list_i, quad * 32, lane, tau, id0 + c + 32,
-                                  valid - c - 32, tau_floor);
+                                  valid - c - 32, fl);
           } else {
-            scan_chunk<kRegK>(va, s, id, id0 + c, valid - c);
-            scan_chunk<kRegK>(vb, s, id, id0 + c + 32, valid - c - 32);
+            scan_chunk<kRegK>(va, s, id, id0 + c, valid - c, fl);
+            scan_chunk<kRegK>(vb, s, id, id0 + c + 32, valid - c - 32, fl);
           }
         }
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader0 + abuf * 8);
+        if (p.floor_g != nullptr)  // warp-uniform (the smem-list variant syncs the warp)
+          share_floor<KCAP, kSmemList>(fslot, fkey, s, id, list_s, list_i, t_epi, fl, tau,
+                                       published);
         abuf ^= 1;
         if (abuf == 0) aphase ^= 1;
       }
@@ -1001,8 +1091,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
         ptx::tmem_ld_32x32b_x32(taddr + c, va);
         ptx::tmem_ld_32x32b_x32(taddr + c + 32, vb);
         ptx::tmem_ld_wait();
-        scan_chunk<KCAP>(va, s, id, id0 + c, valid - c);
-        scan_chunk<KCAP>(vb, s, id, id0 + c + 32, valid - c - 32);
+        scan_chunk<KCAP>(va, s, id, id0 + c, valid - c, -FLT_MAX);
+        scan_chunk<KCAP>(vb, s, id, id0 + c + 32, valid - c - 32, -FLT_MAX);
       }
       ptx::tc_fence_before();
       __syncwarp();
