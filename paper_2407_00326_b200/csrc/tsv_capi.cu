@@ -863,8 +863,8 @@ int tsv_rerank(tsv_index* idx, const void* q_dev, int q_dtype, int B, const int3
 int tsv_merge_topk(const float* in_scores, const int32_t* in_ids, int lists, int B, int kin,
                    int kout, int dedup, float* out_scores, int32_t* out_ids, void* stream) {
   if (lists <= 0 || B <= 0 || kin <= 0 || kout <= 0) return fail(TSV_ERR_CAPACITY, "empty merge");
-  if (static_cast<int64_t>(lists) * kin > 8192)
-    return fail(TSV_ERR_CAPACITY, "merge of %d x %d candidates exceeds 8192", lists, kin);
+  if (static_cast<int64_t>(lists) * kin > 16384)
+    return fail(TSV_ERR_CAPACITY, "merge of %d x %d candidates exceeds 16384", lists, kin);
   if (!in_scores || !in_ids || !out_scores || !out_ids) return fail(TSV_ERR_ARGUMENT, "null buffer");
   int e = tsv::launch_merge_topk(in_scores, in_ids, lists, B, kin, B, kout, out_scores, out_ids,
                                  reinterpret_cast<cudaStream_t>(stream), dedup);

@@ -54,10 +54,144 @@ __device__ void bitonic_sort_desc(uint64_t* keys, int n) {
   __syncthreads();
 }
 
+// Register-resident bitonic stages: a warp holds a 64-key chunk as a (index lane) and b (index
+// lane + 32); strides below 32 exchange through shuffles, stride 32 is in-lane.
+__device__ __forceinline__ void cas_shfl(uint64_t& v, int lane, int s, bool desc) {
+  const uint64_t o = __shfl_xor_sync(0xffffffffu, v, s);
+  const bool take_max = ((lane & s) == 0) == desc;
+  v = take_max ? (v > o ? v : o) : (v < o ? v : o);
+}
+// All stages of merge size `size` with stride <= 32, on the chunk starting at index g0.
+__device__ __forceinline__ void chunk_stages(uint64_t& a, uint64_t& b, int g0, int lane, int size) {
+  const bool da = ((g0 + lane) & size) == 0;
+  const bool db = ((g0 + lane + 32) & size) == 0;
+  if (size >= 64) {
+    const uint64_t hi = a > b ? a : b, lo = a > b ? b : a;
+    a = da ? hi : lo;
+    b = da ? lo : hi;
+  }
+  for (int st = min(size >> 1, 16); st > 0; st >>= 1) {
+    cas_shfl(a, lane, st, da);
+    cas_shfl(b, lane, st, db);
+  }
+}
+
+// Descending bitonic sort of n (power of two) keys in shared memory with the short-stride
+// stages in registers: 2 + log2(n / 64) block barriers per merge size instead of log2(size).
+__device__ void bitonic_sort_desc_fast(uint64_t* keys, int n) {
+  if (n < 64) {
+    bitonic_sort_desc(keys, n);
+    return;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  for (int c = warp; c < (n >> 6); c += nw) {
+    uint64_t a = keys[c * 64 + lane], b = keys[c * 64 + 32 + lane];
+    for (int size = 2; size <= 64; size <<= 1) chunk_stages(a, b, c * 64, lane, size);
+    keys[c * 64 + lane] = a;
+    keys[c * 64 + 32 + lane] = b;
+  }
+  for (int size = 128; size <= n; size <<= 1) {
+    for (int stride = size >> 1; stride >= 64; stride >>= 1) {
+      __syncthreads();
+      for (int i = threadIdx.x; i < (n >> 1); i += blockDim.x) {
+        const int lo = 2 * i - (i & (stride - 1));
+        const int hi = lo + stride;
+        const bool desc = ((lo & size) == 0);
+        const uint64_t x = keys[lo], y = keys[hi];
+        if ((x < y) == desc) {
+          keys[lo] = y;
+          keys[hi] = x;
+        }
+      }
+    }
+    __syncthreads();
+    for (int c = warp; c < (n >> 6); c += nw) {
+      uint64_t a = keys[c * 64 + lane], b = keys[c * 64 + 32 + lane];
+      chunk_stages(a, b, c * 64, lane, size);
+      keys[c * 64 + lane] = a;
+      keys[c * 64 + 32 + lane] = b;
+    }
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ int pow2_ceil(int n) {
   int p = 1;
   while (p < n) p <<= 1;
   return p;
+}
+
+// Copy the `need` largest of keys[0, m) into sel (capacity cap >= need) in any order, with an
+// MSB-first 8-bit radix select: each pass histograms the digit below the fixed prefix and
+// keeps the bin that holds the need-th largest key; it stops once that bin is taken whole.
+// Returns the number of keys written. Keys are unique except for exact duplicates, which are
+// interchangeable.
+__device__ int radix_select_top(const uint64_t* keys, int m, int need, uint64_t* sel, int cap) {
+  __shared__ int hist[256];
+  __shared__ int sel_d, sel_above, sel_cnt, nsel;
+  uint64_t prefix = 0, pmask = 0;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+      const uint64_t k = keys[i];
+      if ((k & pmask) == prefix) atomicAdd(&hist[(k >> shift) & 255], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // digit holding the need-th largest (bins scanned high to low)
+      const int lane = threadIdx.x;
+      int c[8], tot = 0;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        c[t] = hist[255 - (lane * 8 + t)];
+        tot += c[t];
+      }
+      int incl = tot;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += v;
+      }
+      const int excl = incl - tot;
+      if (excl < need && need <= incl) {
+        int run = excl;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          if (run + c[t] >= need) {
+            sel_d = 255 - (lane * 8 + t);
+            sel_above = run;
+            sel_cnt = c[t];
+            break;
+          }
+          run += c[t];
+        }
+      }
+    }
+    __syncthreads();
+    need -= sel_above;
+    prefix |= static_cast<uint64_t>(sel_d) << shift;
+    pmask |= 255ull << shift;
+    const bool whole = sel_cnt == need;
+    __syncthreads();  // sel_* are rewritten by the next pass
+    if (whole) break;
+  }
+  if (threadIdx.x == 0) nsel = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {  // strictly above the prefix: all in
+    const uint64_t k = keys[i];
+    if ((k & pmask) > prefix) sel[atomicAdd(&nsel, 1)] = k;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {  // on the prefix: as many as fit
+    const uint64_t k = keys[i];
+    if ((k & pmask) == prefix) {
+      const int slot = atomicAdd(&nsel, 1);
+      if (slot < cap) sel[slot] = k;
+    }
+  }
+  __syncthreads();
+  return nsel < cap ? nsel : cap;
 }
 
 // One block per query: gather lists * kin candidates, sort, keep kout.
@@ -74,18 +208,46 @@ __global__ void merge_topk_kernel(const float* __restrict__ in_s, const int32_t*
   // independent of the compaction order).
   if (threadIdx.x == 0) count = 0;
   __syncthreads();
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const int r = i / kin;
-    const int j = i - r * kin;
-    const int64_t off = (static_cast<int64_t>(r) * list_stride_rows + b) * kin + j;
-    const int32_t id = in_id[off];
-    if (id >= 0) keys[atomicAdd(&count, 1)] = make_key(in_s[off], id);
+  // eight independent loads in flight per thread (the lists are L2-resident, latency-bound)
+  constexpr int kBatch = 8;
+  for (int base = 0; base < n; base += kBatch * blockDim.x) {
+    int32_t id[kBatch];
+    float sc[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const int i = base + u * blockDim.x + threadIdx.x;
+      id[u] = -1;
+      if (i < n) {
+        const int r = i / kin;
+        const int64_t off = (static_cast<int64_t>(r) * list_stride_rows + b) * kin + (i - r * kin);
+        id[u] = __ldg(in_id + off);
+        sc[u] = __ldg(in_s + off);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u)
+      if (id[u] >= 0) keys[atomicAdd(&count, 1)] = make_key(sc[u], id[u]);
   }
   __syncthreads();
   const int m = count;
+  const int kp = pow2_ceil(kout);
+  if (!dedup && m > 2 * kp && m > 256) {
+    // Many more candidates than outputs: radix-select the kout best keys, sort only those.
+    uint64_t* sel = keys + pow2_ceil(n);
+    const int got = radix_select_top(keys, m, kout, sel, kp);
+    for (int i = got + threadIdx.x; i < kp; i += blockDim.x) sel[i] = pad_key();
+    bitonic_sort_desc_fast(sel, kp);
+    for (int j = threadIdx.x; j < kout; j += blockDim.x) {
+      const uint64_t key = sel[j];
+      const int32_t id = key_id(key);
+      out_s[static_cast<int64_t>(b) * kout + j] = id < 0 ? -INFINITY : key_score(key);
+      out_id[static_cast<int64_t>(b) * kout + j] = id;
+    }
+    return;
+  }
   const int np = pow2_ceil(m > 0 ? m : 1);
   for (int i = m + threadIdx.x; i < np; i += blockDim.x) keys[i] = pad_key();
-  bitonic_sort_desc(keys, np);
+  bitonic_sort_desc_fast(keys, np);
   if (dedup) {
     // Copies of one id carry identical scores, so they are adjacent after the sort.
     if (threadIdx.x == 0) {
@@ -176,7 +338,7 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) keys[c] = make_key(acc, id);
   }
-  bitonic_sort_desc(keys, np);
+  bitonic_sort_desc_fast(keys, np);
   // Dedup: duplicates of one id carry identical scores, so they are adjacent after the sort.
   if (threadIdx.x == 0) {
     int w = 0;
@@ -363,7 +525,7 @@ __global__ void peer_exchange_merge_kernel(const PeerArgs a) {
       }
       keys[i] = key;
     }
-    bitonic_sort_desc(keys, np);
+    bitonic_sort_desc_fast(keys, np);
     for (int j = threadIdx.x; j < a.k; j += blockDim.x) {
       const uint64_t key = keys[j];
       const int32_t id = key_id(key);
@@ -429,11 +591,13 @@ int launch_merge_topk(const float* in_s, const int32_t* in_id, int lists, int B,
   int np = 1;
   while (np < lists * kin) np <<= 1;
   if (np > 16384) return static_cast<int>(cudaErrorInvalidValue);
-  const size_t smem = static_cast<size_t>(np) * sizeof(uint64_t);
+  int kp = 1;
+  while (kp < kout) kp <<= 1;
+  const size_t smem = static_cast<size_t>(np + kp) * sizeof(uint64_t);  // keys + selection
   static std::atomic<uint64_t> configured{0};
   if (smem > 48 * 1024 && first_on_device(configured)) {
     cudaError_t e = cudaFuncSetAttribute(merge_topk_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 132 * 1024);
     if (e != cudaSuccess) return static_cast<int>(e);
   }
   const int threads = np >= 1024 ? 256 : (np >= 256 ? 128 : 64);

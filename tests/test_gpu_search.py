@@ -184,6 +184,36 @@ def test_merge_matches_oracle(cuda):
     np.testing.assert_array_equal(from_dev(s), es.astype(np.float32))
 
 
+@pytest.mark.parametrize("L,kin,k", [(64, 32, 100), (100, 10, 10), (74, 128, 100), (3, 128, 128)])
+def test_merge_many_lists_radix_select(cuda, L, kin, k):
+    """Merges with many more candidates than outputs take the radix-select path: exact ties,
+    exact duplicate entries, padding-heavy lists and fewer candidates than k."""
+    import torch
+    from paper_2407_00326_b200.index import merge_topk
+
+    rng = np.random.default_rng(L * 1000 + kin)
+    B = 37
+    sc = (rng.integers(-400, 400, (L, B, kin)) / 128.0).astype(np.float32)  # many equal scores
+    sc = -np.sort(-sc, axis=2)
+    ids = rng.permutation(L * B * kin).reshape(L, B, kin).astype(np.int32)
+    real = rng.integers(0, kin + 1, (L, B))  # each list keeps a random-length real prefix
+    pad = np.arange(kin)[None, None, :] >= real[:, :, None]
+    ids[pad] = -1
+    sc[pad] = -np.inf
+    if L > 2:  # an exact duplicate of list 0's head in list 1 (same id, same score)
+        sc[1, :, 0] = np.maximum(sc[1, :, 0], sc[0, :, 0])
+        keep = ids[0, :, 0] >= 0
+        sc[1, keep, 0] = sc[0, keep, 0]
+        ids[1, keep, 0] = ids[0, keep, 0]
+        order = np.argsort(-sc[1], axis=1, kind="stable")
+        sc[1] = np.take_along_axis(sc[1], order, axis=1)
+        ids[1] = np.take_along_axis(ids[1], order, axis=1)
+    s, i = merge_topk(torch.from_numpy(sc).cuda(), torch.from_numpy(ids).cuda(), k)
+    es, ei = orc.merge(sc, ids, k)
+    np.testing.assert_array_equal(from_dev(s), es.astype(np.float32))
+    np.testing.assert_array_equal(from_dev(i), ei)
+
+
 def test_normalize_rows_matches_oracle(cuda):
     import torch
     from paper_2407_00326_b200.index import normalize_rows
