@@ -1,0 +1,39 @@
+"""Small search / segmented search / rerank / merge / normalize calls for compute-sanitizer
+(memcheck, racecheck, synccheck) on the GPU box:
+
+    compute-sanitizer --tool memcheck python scripts/sanitize.py
+"""
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+from paper_2407_00326_b200.index import DeviceIndex, merge_topk, normalize_rows  # noqa: E402
+
+
+def main():
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device=dev).manual_seed(0)
+    idx = DeviceIndex(256, 40_000, metric="cosine", device=0)
+    idx.append(torch.randn((40_000, 256), generator=g, device=dev))
+    for B, k in ((1, 5), (100, 10), (300, 10), (64, 100)):
+        q = normalize_rows(torch.randn((B, 256), generator=g, device=dev))
+        idx.search(q, k)
+    q = normalize_rows(torch.randn((40, 256), generator=g, device=dev))
+    idx.search_segmented(q, [0, 10, 25, 40], [(0, 48), (48, 3000), (3000, 40_000)], 8)
+    cand = torch.randint(0, 40_000, (4, 200), generator=g, device=dev, dtype=torch.int32)
+    idx.rerank(q[:4], cand, 10)
+    s = torch.sort(torch.randn((8, 37, 16), generator=g, device=dev), dim=2, descending=True)[0]
+    i = torch.arange(8 * 37 * 16, device=dev, dtype=torch.int32).reshape(8, 37, 16)
+    merge_topk(s, i, 10)
+    f32 = DeviceIndex(64, 5000, metric="ip", device=0, storage="f32")
+    f32.append(torch.randn((5000, 64), generator=g, device=dev))
+    f32.search(torch.randn((20, 64), generator=g, device=dev), 10)
+    torch.cuda.synchronize()
+    print("sanitize workload done")
+
+
+if __name__ == "__main__":
+    main()
