@@ -133,16 +133,22 @@ struct Workspace {
   DevBuf<int32_t> part_i;
   DevBuf<tsv::ScanItem> items;
   std::vector<tsv::ScanItem> host_items;
-  // pinned staging for the item table so its upload is a true async copy; the event marks
-  // when the previous upload has drained so the staging buffer can be rewritten
-  tsv::ScanItem* pinned = nullptr;
-  size_t pinned_cap = 0;
-  cudaEvent_t pinned_done = nullptr;
+  // Pinned staging for the item table so its upload is a true async copy. A ring of slots,
+  // each with an event marking when its upload drained: the host only waits when it laps a
+  // slot whose copy is still queued, so back-to-back segmented searches stay asynchronous.
+  static constexpr int kPinnedSlots = 4;
+  struct Pinned {
+    tsv::ScanItem* ptr = nullptr;
+    size_t cap = 0;
+    cudaEvent_t done = nullptr;
+  } pinned[kPinnedSlots];
+  int pinned_next = 0;
   void release() {
-    if (pinned) cudaFreeHost(pinned);
-    if (pinned_done) cudaEventDestroy(pinned_done);
-    pinned = nullptr;
-    pinned_done = nullptr;
+    for (auto& s : pinned) {
+      if (s.ptr) cudaFreeHost(s.ptr);
+      if (s.done) cudaEventDestroy(s.done);
+      s = Pinned{};
+    }
     counter.release();
     qbuf.release();
     qhi.release();
@@ -266,9 +272,11 @@ int run_scan(tsv_index* idx, int mb, int kcap, const void* qb, int64_t B, tsv::S
              int grid, cudaStream_t st) {
   // One query group of fewer than 128 queries: load only its rows (TMA out-of-bounds fill of
   // the rest of a 128-row box costs as much as real rows and halves the HBM-bound scan rate).
-  p.a_rows = (mb == 1 && p.items == nullptr && B < tsv::kBlockM && !getenv("TSV_FULL_QBOX"))
-                 ? static_cast<int>((B + 7) & ~7)
-                 : 0;
+  // (Segmented searches set a_rows from their largest query group before the call.)
+  if (p.a_rows == 0 && mb == 1 && p.items == nullptr && B < tsv::kBlockM &&
+      !getenv("TSV_FULL_QBOX"))
+    p.a_rows = static_cast<int>((B + 7) & ~7);
+  if (getenv("TSV_FULL_QBOX")) p.a_rows = 0;
   CUtensorMap tq;
   int rc = query_map(qb, B, idx->dim, &tq, p.a_rows ? p.a_rows : tsv::kBlockM);
   if (rc) return rc;
@@ -769,24 +777,28 @@ int tsv_search_segmented(tsv_index* idx, const void* q_dev, int q_dtype, int nse
   }
   rc = w.items.ensure(hi.size());
   if (rc) return rc;
-  if (w.pinned_done == nullptr)
-    TSV_CUDA(cudaEventCreateWithFlags(&w.pinned_done, cudaEventDisableTiming), "cudaEventCreate");
+  Workspace::Pinned& slot = w.pinned[w.pinned_next];
+  w.pinned_next = (w.pinned_next + 1) % Workspace::kPinnedSlots;
+  if (slot.done == nullptr)
+    TSV_CUDA(cudaEventCreateWithFlags(&slot.done, cudaEventDisableTiming), "cudaEventCreate");
   else
-    TSV_CUDA(cudaEventSynchronize(w.pinned_done), "cudaEventSynchronize");
-  if (hi.size() > w.pinned_cap) {
-    if (w.pinned) cudaFreeHost(w.pinned);
-    w.pinned = nullptr;
-    TSV_CUDA(cudaMallocHost(&w.pinned, hi.size() * 2 * sizeof(tsv::ScanItem)), "cudaMallocHost");
-    w.pinned_cap = hi.size() * 2;
+    TSV_CUDA(cudaEventSynchronize(slot.done), "cudaEventSynchronize");
+  if (hi.size() > slot.cap) {
+    if (slot.ptr) cudaFreeHost(slot.ptr);
+    slot.ptr = nullptr;
+    TSV_CUDA(cudaMallocHost(&slot.ptr, hi.size() * 2 * sizeof(tsv::ScanItem)), "cudaMallocHost");
+    slot.cap = hi.size() * 2;
   }
-  std::memcpy(w.pinned, hi.data(), hi.size() * sizeof(tsv::ScanItem));
-  TSV_CUDA(cudaMemcpyAsync(w.items.ptr, w.pinned, hi.size() * sizeof(tsv::ScanItem),
+  std::memcpy(slot.ptr, hi.data(), hi.size() * sizeof(tsv::ScanItem));
+  TSV_CUDA(cudaMemcpyAsync(w.items.ptr, slot.ptr, hi.size() * sizeof(tsv::ScanItem),
                            cudaMemcpyHostToDevice, st),
            "items upload");
-  TSV_CUDA(cudaEventRecord(w.pinned_done, st), "cudaEventRecord");
+  TSV_CUDA(cudaEventRecord(slot.done, st), "cudaEventRecord");
   tsv::ScanParams p{};
   p.items = w.items.ptr;
   p.num_items = static_cast<int>(hi.size());
+  // query box = the largest query group (rows past an item's own queries are never emitted)
+  if (mb == 1 && !f32 && max_q < tsv::kBlockM) p.a_rows = (max_q + 7) & ~7;
   const int kb_elems = f32 ? 32 : tsv::kBlockK;
   p.num_kb = (idx->dim + kb_elems - 1) / kb_elems;
   if (tiled) p.flags |= tsv::kFlagTiled;

@@ -302,41 +302,68 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(
   __syncthreads();
 
   const int chunks = dim >> 3;  // 8 bf16 (16 B) per chunk; dim % 8 == 0 enforced by the host
-  for (int c = warp; c < C; c += kWarps) {
-    const int32_t id = cand[static_cast<int64_t>(b) * C + c];
-    if (id < 0 || id >= nrows) continue;  // warp-uniform
-    float acc = 0.f;
+  const int64_t kb_per_row = (dim + 63) >> 6;
+  // Two candidates per warp iteration with independent loads and accumulators (the gather is
+  // latency-bound: one row is only 2 KB at D=1024).
+  for (int c0 = 2 * warp; c0 < C; c0 += 2 * kWarps) {
+    int32_t id[2];
+    bool ok[2];
+    float acc[2] = {0.f, 0.f};
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      id[u] = c0 + u < C ? cand[static_cast<int64_t>(b) * C + c0 + u] : -1;
+      ok[u] = id[u] >= 0 && id[u] < nrows;  // warp-uniform
+    }
     if (arena_hi != nullptr) {  // fp32 storage: row = hi + lo, fp32 FMA
-      const float4* hi = reinterpret_cast<const float4*>(arena_hi + static_cast<int64_t>(id) * dim);
-      const float4* lo = reinterpret_cast<const float4*>(arena_lo + static_cast<int64_t>(id) * dim);
-      for (int ch = lane; ch < (dim >> 2); ch += 32) {
-        const float4 h = __ldg(hi + ch), l = __ldg(lo + ch);
-        const float* qq = qv + ch * 4;
-        acc = fmaf(h.x + l.x, qq[0], acc);
-        acc = fmaf(h.y + l.y, qq[1], acc);
-        acc = fmaf(h.z + l.z, qq[2], acc);
-        acc = fmaf(h.w + l.w, qq[3], acc);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (!ok[u]) continue;
+        const float4* hi = reinterpret_cast<const float4*>(arena_hi + static_cast<int64_t>(id[u]) * dim);
+        const float4* lo = reinterpret_cast<const float4*>(arena_lo + static_cast<int64_t>(id[u]) * dim);
+        for (int ch = lane; ch < (dim >> 2); ch += 32) {
+          const float4 h = __ldg(hi + ch), l = __ldg(lo + ch);
+          const float* qq = qv + ch * 4;
+          acc[u] = fmaf(h.x + l.x, qq[0], acc[u]);
+          acc[u] = fmaf(h.y + l.y, qq[1], acc[u]);
+          acc[u] = fmaf(h.z + l.z, qq[2], acc[u]);
+          acc[u] = fmaf(h.w + l.w, qq[3], acc[u]);
+        }
+      }
+    } else {
+      const uint4* row[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int64_t r = ok[u] ? id[u] : 0;
+        // tiled layout: 16-byte chunk ch of row r lives in k-block tile (r/128, ch/8)
+        row[u] = tiled ? reinterpret_cast<const uint4*>(
+                             arena + ((r >> 7) * kb_per_row * 128 + (r & 127)) * 64)
+                       : reinterpret_cast<const uint4*>(arena + r * dim);
+      }
+#pragma unroll 2
+      for (int ch = lane; ch < chunks; ch += 32) {
+        const int64_t off = tiled ? static_cast<int64_t>(ch >> 3) * 1024 + (ch & 7) : ch;
+        uint4 raw[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) raw[u] = ok[u] ? __ldg(row[u] + off) : make_uint4(0, 0, 0, 0);
+        const float* qq = qv + ch * 8;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw[u]);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const float2 f = __bfloat1622float2(h[t]);
+            acc[u] = fmaf(f.x, qq[2 * t], acc[u]);
+            acc[u] = fmaf(f.y, qq[2 * t + 1], acc[u]);
+          }
+        }
       }
     }
-    const uint4* row = reinterpret_cast<const uint4*>(arena + static_cast<int64_t>(id) * dim);
-    // tiled layout: 16-byte chunk ch of row id lives in k-block tile (id/128, ch/8)
-    const uint4* trow = reinterpret_cast<const uint4*>(
-        arena + ((static_cast<int64_t>(id) >> 7) * ((dim + 63) >> 6) * 128 + (id & 127)) * 64);
-    for (int ch = lane; arena_hi == nullptr && ch < chunks; ch += 32) {
-      const uint4 raw = tiled ? __ldg(trow + static_cast<int64_t>(ch >> 3) * 1024 + (ch & 7))
-                              : __ldg(row + ch);
-      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
-      const float* qq = qv + ch * 8;
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const float2 f = __bfloat1622float2(h[t]);
-        acc = fmaf(f.x, qq[2 * t], acc);
-        acc = fmaf(f.y, qq[2 * t + 1], acc);
-      }
+    for (int u = 0; u < 2; ++u) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
+      if (lane == 0 && ok[u]) keys[c0 + u] = make_key(acc[u], id[u]);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) keys[c] = make_key(acc, id);
   }
   bitonic_sort_desc_fast(keys, np);
   // Dedup: duplicates of one id carry identical scores, so they are adjacent after the sort.
@@ -615,7 +642,7 @@ int launch_rerank(const void* arena, const float* arena_hi, const float* arena_l
   while (np < C) np <<= 1;
   const size_t smem = ((static_cast<size_t>(dim) * 4 + 15) & ~size_t(15)) + np * sizeof(uint64_t);
   if (smem > 200 * 1024) return static_cast<int>(cudaErrorInvalidValue);
-  constexpr int kThreads = 256;
+  constexpr int kThreads = 512;
   static std::atomic<uint64_t> configured{0};
   if (smem > 48 * 1024 && first_on_device(configured)) {
     cudaError_t e = cudaFuncSetAttribute(rerank_kernel<kThreads>,
