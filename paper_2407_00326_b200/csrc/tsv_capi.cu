@@ -131,6 +131,9 @@ struct Workspace {
   DevBuf<int32_t> seed_i;
   DevBuf<float> part_s;        // partial lists
   DevBuf<int32_t> part_i;
+  DevBuf<float> cand_s;        // append mode: candidate rows [B][kCandCap]
+  DevBuf<int32_t> cand_i;
+  DevBuf<int32_t> cand_cnt;    // [B] candidate counts, then the overflow flag
   DevBuf<tsv::ScanItem> items;
   std::vector<tsv::ScanItem> host_items;
   // Pinned staging for the item table so its upload is a true async copy. A ring of slots,
@@ -158,6 +161,9 @@ struct Workspace {
     seed_i.release();
     part_s.release();
     part_i.release();
+    cand_s.release();
+    cand_i.release();
+    cand_cnt.release();
     items.release();
   }
 };
@@ -536,9 +542,14 @@ int tsv_index_scan_time(tsv_index* idx, double* total_ms, int64_t* launches) {
 
 static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k,
                        int64_t row_beg, int64_t row_end, int32_t id_offset, float* scores_dev,
-                       int32_t* ids_dev, void* stream, const float* tau0, int list_cap = 0) {
+                       int32_t* ids_dev, void* stream, const float* tau0, int list_cap = 0,
+                       const int32_t* gate = nullptr, bool append = false) {
   // list_cap > 0 (sample pass of a seeded search): per-range lists of list_cap < k entries;
   // the merge then returns the best k of the union of those lists.
+  // gate != nullptr: every launch is skipped on the device unless *gate != 0.
+  // append (requires tau0): candidate mode — rows above tau0 go to per-query candidate rows and
+  // a select kernel writes the top k; a candidate row overflow sets the flag at
+  // cand_cnt[B], which the caller passes as the gate of a list-mode fallback pass.
   if (idx == nullptr) return fail(TSV_ERR_ARGUMENT, "index is null");
   int rc = check_dtype(q_dtype);
   if (rc) return rc;
@@ -585,7 +596,7 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
   // at least kMinTilesPerRange tiles per range: tiny scans gain nothing from more workers, and
   // every extra range is one more list for the merge
   R = static_cast<int>(std::min<int64_t>(R, std::max<int64_t>(1, tiles / kMinTilesPerRange)));
-  R = std::min(R, kMergeCap / kcap);  // the range merge holds R * kcap candidates per query
+  if (!append) R = std::min(R, kMergeCap / kcap);  // the range merge holds R * kcap per query
   const int num_items = nqg * R;
   const int grid = pair ? 2 * std::min(num_items, units) : std::min(num_items, units);
 
@@ -598,10 +609,39 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
   p.row_beg = row_beg;
   p.row_end = row_end;
   p.tau0 = tau0;
+  p.gate = gate;
   const int kb_elems = f32 ? 32 : tsv::kBlockK;  // elements per 128-byte k-block row
   p.num_kb = (idx->dim + kb_elems - 1) / kb_elems;
   if (tiled) p.flags |= tsv::kFlagTiled;
 
+  if (append) {
+    const bool lock = nqg > 1 && num_items <= units && !env_flag("TSV_NO_LOCKSTEP");
+    const size_t nc = lock ? static_cast<size_t>(num_items) : 0;
+    rc = w.cand_s.ensure(static_cast<size_t>(B) * tsv::kCandCap);
+    if (!rc) rc = w.cand_i.ensure(static_cast<size_t>(B) * tsv::kCandCap);
+    if (!rc) rc = w.cand_cnt.ensure(static_cast<size_t>(B) + 1);
+    if (!rc && lock) rc = w.counter.ensure(nc);
+    if (rc) return rc;
+    TSV_CUDA(cudaMemsetAsync(w.cand_cnt.ptr, 0, sizeof(int32_t) * (B + 1), st), "count reset");
+    if (lock) {
+      TSV_CUDA(cudaMemsetAsync(w.counter.ptr, 0, sizeof(int32_t) * nc, st), "progress reset");
+      p.counter = w.counter.ptr;
+      p.flags |= tsv::kFlagLockstep;
+      if (const char* e = getenv("TSV_LOCK_WINDOW")) p.lock_window = std::max(1, atoi(e));
+    }
+    p.out_k = 0;
+    p.out_scores = w.cand_s.ptr;
+    p.out_ids = w.cand_i.ptr;
+    p.cand_count = w.cand_cnt.ptr;
+    p.cand_cap = tsv::kCandCap;
+    rc = run_scan(idx, mb, tsv::kAppendCap, qb, B, p, grid, st);
+    if (rc) return rc;
+    int e = tsv::launch_cand_select(w.cand_s.ptr, w.cand_i.ptr, w.cand_cnt.ptr, tsv::kCandCap, B,
+                                    k, scores_dev, ids_dev, w.cand_cnt.ptr + B, st);
+    if (e) return cuda_fail(static_cast<cudaError_t>(e), "candidate select launch");
+    g_launches++;
+    return TSV_OK;
+  }
   if (pair && nqg <= 64 && kcap <= tsv::kMaxRegK && env_flag("TSV_DYN")) {
     // Dynamic-unit pair kernel (experimental, opt-in): every pair keeps one list per query;
     // K4 merges the pairs. Streams the corpus from HBM once for any B, but is slower than the
@@ -663,7 +703,7 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
            : run_scan(idx, mb, kcap, qb, B, p, grid, st);
   if (rc) return rc;
   int e = tsv::launch_merge_topk(w.part_s.ptr, w.part_i.ptr, R, B, kcap, B, k, scores_dev, ids_dev,
-                                 st);
+                                 st, 0, gate);
   if (e) return cuda_fail(static_cast<cudaError_t>(e), "merge launch");
   g_launches++;
   return TSV_OK;
@@ -700,8 +740,18 @@ int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int
     int e = tsv::launch_seed_floor(w.seed_s.ptr, w.seed_i.ptr, B, k, w.tau0.ptr, st);
     if (e) return cuda_fail(static_cast<cudaError_t>(e), "seed floor");
     g_launches++;
+    if (env_flag("TSV_NO_APPEND"))
+      return search_impl(idx, q_dev, q_dtype, B, k, row_beg, row_end, id_offset, scores_dev,
+                         ids_dev, stream, w.tau0.ptr);
+    // Main pass in candidate mode: the register-list pipeline depth (no shared-memory lists),
+    // every row above tau0 appended to its query's candidate row, exact top-k selected from
+    // those. If any candidate row overflowed, the device-gated list-mode pass recomputes the
+    // batch (exact either way; no host round trip decides it).
+    rc = search_impl(idx, q_dev, q_dtype, B, k, row_beg, row_end, id_offset, scores_dev, ids_dev,
+                     stream, w.tau0.ptr, 0, nullptr, true);
+    if (rc) return rc;
     return search_impl(idx, q_dev, q_dtype, B, k, row_beg, row_end, id_offset, scores_dev,
-                       ids_dev, stream, w.tau0.ptr);
+                       ids_dev, stream, w.tau0.ptr, 0, w.cand_cnt.ptr + B);
   }
   return search_impl(idx, q_dev, q_dtype, B, k, row_beg, row_end, id_offset, scores_dev, ids_dev,
                      stream, nullptr);

@@ -72,7 +72,25 @@ struct ScanParams {
   // merged top-k. Without it each range's threshold starts from scratch and the insertions
   // of the first tiles of every range dominate short scans.
   uint32_t* floor_g;
+  // Candidate mode (KCAP == kAppendCap, k > 32 after a seeding pass): every row scoring above
+  // the query's tau0 is appended to its candidate row out_scores/out_ids[q * cand_cap, ...);
+  // cand_count[q] (zeroed before the launch) counts them, and may exceed cand_cap (overflow:
+  // the entries past cand_cap are dropped and the caller's gated fallback reruns the query set).
+  int32_t* cand_count;
+  int32_t cand_cap;
+  // Device-side gate (nullptr = always run): the kernel returns at once unless *gate != 0. Used
+  // for the overflow fallback, so the decision needs no host round trip.
+  const int32_t* gate;
 };
+
+// List-capacity value selecting candidate (append) mode in launch_scan_topk.
+constexpr int kAppendCap = 0;
+// Candidate-row capacity per query in append mode. Seeding from a 1/16 sample leaves about
+// 16 k rows above tau0 for a uniformly spread corpus (k = 128: ~2k +- 0.2k).
+constexpr int kCandCap = 8192;
+int launch_cand_select(const float* buf_s, const int32_t* buf_i, const int32_t* cnt, int cap,
+                       int B, int kout, float* out_s, int32_t* out_id, int32_t* overflow,
+                       cudaStream_t stream);
 
 // `mb` argument selecting the dynamic-unit CTA-pair kernel (see tsv_scan.cu).
 constexpr int kPairDynMode = 5;
@@ -114,7 +132,7 @@ constexpr int kMaxK = 128;
 
 int launch_merge_topk(const float* in_s, const int32_t* in_id, int lists, int B, int kin,
                       int64_t list_stride_rows, int kout, float* out_s, int32_t* out_id,
-                      cudaStream_t stream, int dedup = 0);
+                      cudaStream_t stream, int dedup = 0, const int32_t* gate = nullptr);
 
 int launch_rerank(const void* arena, const float* arena_hi, const float* arena_lo, int64_t nrows,
                   int dim, const void* q, const float* q_lo, int q_is_f32, int B,

@@ -194,13 +194,45 @@ __device__ int radix_select_top(const uint64_t* keys, int m, int need, uint64_t*
   return nsel < cap ? nsel : cap;
 }
 
+// The kout best of the m keys in keys[0, m) (any order), written sorted (score desc, id asc)
+// with (-inf, -1) padding to os / oi. keys has room for n_alloc >= pow2_ceil(m) keys plus
+// pow2_ceil(kout) selection slots behind them. Block-wide.
+__device__ void write_topk_of_keys(uint64_t* keys, int m, int n_alloc, int kout,
+                                   float* __restrict__ os, int32_t* __restrict__ oi) {
+  const int kp = pow2_ceil(kout);
+  if (m > 2 * kp && m > 256) {
+    // Many more candidates than outputs: radix-select the kout best keys, sort only those.
+    uint64_t* sel = keys + n_alloc;
+    const int got = radix_select_top(keys, m, kout, sel, kp);
+    for (int i = got + threadIdx.x; i < kp; i += blockDim.x) sel[i] = pad_key();
+    bitonic_sort_desc_fast(sel, kp);
+    for (int j = threadIdx.x; j < kout; j += blockDim.x) {
+      const uint64_t key = sel[j];
+      const int32_t id = key_id(key);
+      os[j] = id < 0 ? -INFINITY : key_score(key);
+      oi[j] = id;
+    }
+    return;
+  }
+  const int np = pow2_ceil(m > 0 ? m : 1);
+  for (int i = m + threadIdx.x; i < np; i += blockDim.x) keys[i] = pad_key();
+  bitonic_sort_desc_fast(keys, np);
+  for (int j = threadIdx.x; j < kout; j += blockDim.x) {
+    const uint64_t key = j < np ? keys[j] : pad_key();
+    const int32_t id = key_id(key);
+    os[j] = id < 0 ? -INFINITY : key_score(key);
+    oi[j] = id;
+  }
+}
+
 // One block per query: gather lists * kin candidates, sort, keep kout.
 __global__ void merge_topk_kernel(const float* __restrict__ in_s, const int32_t* __restrict__ in_id,
                                   int lists, int B, int kin, int64_t list_stride_rows, int kout,
                                   float* __restrict__ out_s, int32_t* __restrict__ out_id,
-                                  int dedup) {
+                                  int dedup, const int32_t* __restrict__ gate) {
   extern __shared__ uint64_t keys[];
   __shared__ int count;
+  if (gate != nullptr && *gate == 0) return;
   const int b = blockIdx.x;
   const int n = lists * kin;
   // Compact the real entries first: seeded / floored scans leave most partial lists mostly
@@ -230,51 +262,55 @@ __global__ void merge_topk_kernel(const float* __restrict__ in_s, const int32_t*
   }
   __syncthreads();
   const int m = count;
-  const int kp = pow2_ceil(kout);
-  if (!dedup && m > 2 * kp && m > 256) {
-    // Many more candidates than outputs: radix-select the kout best keys, sort only those.
-    uint64_t* sel = keys + pow2_ceil(n);
-    const int got = radix_select_top(keys, m, kout, sel, kp);
-    for (int i = got + threadIdx.x; i < kp; i += blockDim.x) sel[i] = pad_key();
-    bitonic_sort_desc_fast(sel, kp);
-    for (int j = threadIdx.x; j < kout; j += blockDim.x) {
-      const uint64_t key = sel[j];
-      const int32_t id = key_id(key);
-      out_s[static_cast<int64_t>(b) * kout + j] = id < 0 ? -INFINITY : key_score(key);
-      out_id[static_cast<int64_t>(b) * kout + j] = id;
-    }
+  if (!dedup) {
+    write_topk_of_keys(keys, m, pow2_ceil(n), kout, out_s + static_cast<int64_t>(b) * kout,
+                       out_id + static_cast<int64_t>(b) * kout);
     return;
   }
   const int np = pow2_ceil(m > 0 ? m : 1);
   for (int i = m + threadIdx.x; i < np; i += blockDim.x) keys[i] = pad_key();
   bitonic_sort_desc_fast(keys, np);
-  if (dedup) {
-    // Copies of one id carry identical scores, so they are adjacent after the sort.
-    if (threadIdx.x == 0) {
-      int w = 0;
-      int32_t last = -2;
-      for (int i = 0; i < np && w < kout; ++i) {
-        const int32_t id = key_id(keys[i]);
-        if (id < 0) break;
-        if (id == last) continue;
-        last = id;
-        out_s[static_cast<int64_t>(b) * kout + w] = key_score(keys[i]);
-        out_id[static_cast<int64_t>(b) * kout + w] = id;
-        ++w;
-      }
-      for (; w < kout; ++w) {
-        out_s[static_cast<int64_t>(b) * kout + w] = -INFINITY;
-        out_id[static_cast<int64_t>(b) * kout + w] = -1;
-      }
+  // Copies of one id carry identical scores, so they are adjacent after the sort.
+  if (threadIdx.x == 0) {
+    int w = 0;
+    int32_t last = -2;
+    for (int i = 0; i < np && w < kout; ++i) {
+      const int32_t id = key_id(keys[i]);
+      if (id < 0) break;
+      if (id == last) continue;
+      last = id;
+      out_s[static_cast<int64_t>(b) * kout + w] = key_score(keys[i]);
+      out_id[static_cast<int64_t>(b) * kout + w] = id;
+      ++w;
     }
+    for (; w < kout; ++w) {
+      out_s[static_cast<int64_t>(b) * kout + w] = -INFINITY;
+      out_id[static_cast<int64_t>(b) * kout + w] = -1;
+    }
+  }
+}
+
+// Candidate select (append mode, k > 32): one block per query; the query's candidate row holds
+// every corpus row that scored above its seeded floor, in arrival order. Exact top-k of those
+// (the floor is a lower bound of the final k-th score, so they include the whole result), or,
+// when the row overflowed, nothing but the overflow flag that gates the fallback pass.
+__global__ void cand_select_kernel(const float* __restrict__ buf_s, const int32_t* __restrict__ buf_i,
+                                   const int32_t* __restrict__ cnt, int cap, int kout,
+                                   float* __restrict__ out_s, int32_t* __restrict__ out_id,
+                                   int32_t* __restrict__ overflow) {
+  extern __shared__ uint64_t keys[];
+  const int b = blockIdx.x;
+  const int m = cnt[b];
+  if (m > cap) {
+    if (threadIdx.x == 0) atomicExch(overflow, 1);
     return;
   }
-  for (int j = threadIdx.x; j < kout; j += blockDim.x) {
-    const uint64_t key = j < np ? keys[j] : pad_key();
-    const int32_t id = key_id(key);
-    out_s[static_cast<int64_t>(b) * kout + j] = id < 0 ? -INFINITY : key_score(key);
-    out_id[static_cast<int64_t>(b) * kout + j] = id;
-  }
+  const int64_t row = static_cast<int64_t>(b) * cap;
+  for (int i = threadIdx.x; i < m; i += blockDim.x)
+    keys[i] = make_key(__ldg(buf_s + row + i), __ldg(buf_i + row + i));
+  __syncthreads();
+  write_topk_of_keys(keys, m, pow2_ceil(cap), kout, out_s + static_cast<int64_t>(b) * kout,
+                     out_id + static_cast<int64_t>(b) * kout);
 }
 
 // One block per question: score C candidate rows (gathered by id from the arena) against the
@@ -611,9 +647,30 @@ int launch_split_f32(const void* src, int src_is_f32, int64_t n, int dim, int do
   return static_cast<int>(cudaGetLastError());
 }
 
+int launch_cand_select(const float* buf_s, const int32_t* buf_i, const int32_t* cnt, int cap,
+                       int B, int kout, float* out_s, int32_t* out_id, int32_t* overflow,
+                       cudaStream_t stream) {
+  if (B <= 0) return 0;
+  int np = 1;
+  while (np < cap) np <<= 1;
+  int kp = 1;
+  while (kp < kout) kp <<= 1;
+  const size_t smem = static_cast<size_t>(np + kp) * sizeof(uint64_t);
+  if (smem > 200 * 1024) return static_cast<int>(cudaErrorInvalidValue);
+  static std::atomic<uint64_t> configured{0};
+  if (smem > 48 * 1024 && first_on_device(configured)) {
+    cudaError_t e = cudaFuncSetAttribute(cand_select_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return static_cast<int>(e);
+  }
+  cand_select_kernel<<<B, 256, smem, stream>>>(buf_s, buf_i, cnt, cap, kout, out_s, out_id,
+                                               overflow);
+  return static_cast<int>(cudaGetLastError());
+}
+
 int launch_merge_topk(const float* in_s, const int32_t* in_id, int lists, int B, int kin,
                       int64_t list_stride_rows, int kout, float* out_s, int32_t* out_id,
-                      cudaStream_t stream, int dedup) {
+                      cudaStream_t stream, int dedup, const int32_t* gate) {
   if (B <= 0) return 0;
   int np = 1;
   while (np < lists * kin) np <<= 1;
@@ -629,7 +686,7 @@ int launch_merge_topk(const float* in_s, const int32_t* in_id, int lists, int B,
   }
   const int threads = np >= 1024 ? 256 : (np >= 256 ? 128 : 64);
   merge_topk_kernel<<<B, threads, smem, stream>>>(in_s, in_id, lists, B, kin, list_stride_rows,
-                                                  kout, out_s, out_id, dedup);
+                                                  kout, out_s, out_id, dedup, gate);
   return static_cast<int>(cudaGetLastError());
 }
 

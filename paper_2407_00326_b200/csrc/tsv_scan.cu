@@ -172,6 +172,27 @@ __device__ __forceinline__ void scan_chunk(const uint32_t (&v)[32], float (&s)[K
   }
 }
 
+// Candidate (append) mode: every score of the chunk above thr goes to the query's candidate
+// row; one atomic per chunk reserves the slots. Same cheap common path as scan_chunk.
+__device__ __forceinline__ void scan_chunk_append(const uint32_t (&v)[32], float thr, int32_t id0,
+                                                  int valid, int32_t* cnt, float* cs, int32_t* ci,
+                                                  int cap) {
+  if (chunk_max(v) > thr) {
+    uint32_t mask = chunk_mask(v, thr, valid);
+    if (mask == 0) return;
+    int pos = atomicAdd(cnt, __popc(mask));
+    while (mask) {
+      const int j = __ffs(mask) - 1;
+      mask &= mask - 1;
+      if (pos < cap) {
+        cs[pos] = pick32(v, j);
+        ci[pos] = id0 + j;
+      }
+      ++pos;
+    }
+  }
+}
+
 // Shared-memory list variant (KCAP > 32), warp-cooperative: the list of query row q is
 // ls/li[q * K .. q * K + K) sorted by (score desc, id asc); every lane of a warp holds K/32
 // consecutive entries of the list being updated. One candidate is inserted by the whole warp:
@@ -277,7 +298,9 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
   constexpr int kStages = Cfg::kStages;
   constexpr int kQG = MB * kBlockM;
   constexpr bool kSmemList = Cfg::kSmemList;
-  constexpr int kRegK = kSmemList ? 1 : KCAP;
+  constexpr bool kAppend = KCAP == kAppendCap;
+  constexpr int kRegK = (kSmemList || kAppend) ? 1 : KCAP;
+  if (p.gate != nullptr && *p.gate == 0) return;
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -464,6 +487,12 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
       uint32_t* const fslot =
           (p.floor_g != nullptr && lq < it.q_count) ? p.floor_g + it.q_begin + lq : nullptr;
       float fl = tau_floor, published = -FLT_MAX;
+      // append mode: admit scores above tau0 (padding query rows admit nothing)
+      const float athr = lq < it.q_count ? tau_floor : INFINITY;
+      const int64_t qrow = static_cast<int64_t>(it.q_begin) + (lq < it.q_count ? lq : 0);
+      int32_t* const ccnt = kAppend ? p.cand_count + qrow : nullptr;
+      float* const cbs = kAppend ? p.out_scores + qrow * p.cand_cap : nullptr;
+      int32_t* const cbi = kAppend ? p.out_ids + qrow * p.cand_cap : nullptr;
 #pragma unroll
       for (int j = 0; j < kRegK; ++j) {
         s[j] = -FLT_MAX;
@@ -512,7 +541,10 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
           ptx::tmem_ld_32x32b_x32(taddr + c, va);
           ptx::tmem_ld_32x32b_x32(taddr + c + 32, vb);
           ptx::tmem_ld_wait();
-          if constexpr (kSmemList) {
+          if constexpr (kAppend) {
+            scan_chunk_append(va, athr, id0 + c, valid - c, ccnt, cbs, cbi, p.cand_cap);
+            scan_chunk_append(vb, athr, id0 + c + 32, valid - c - 32, ccnt, cbs, cbi, p.cand_cap);
+          } else if constexpr (kSmemList) {
             scan_chunk_coop<KCAP>(va, list_s, list_i, quad * 32, lane, tau, id0 + c, valid - c,
                                   fl);
             scan_chunk_coop<KCAP>(vb, list_s, list_i, quad * 32, lane, tau, id0 + c + 32,
@@ -533,7 +565,7 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
           aphase ^= 1;
         }
       }
-      if (lq < it.q_count) {
+      if (!kAppend && lq < it.q_count) {
         float* os = p.out_scores + (it.out_row + lq) * p.out_k;
         int32_t* oi = p.out_ids + (it.out_row + lq) * p.out_k;
         if constexpr (kSmemList) {
@@ -599,7 +631,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
   constexpr bool kSmemList = KCAP > kRegListMax;
   constexpr int kListBytes = kSmemList ? 128 * KCAP * 8 : 0;
   constexpr int kStages = PairStages<KCAP>::value;
-  constexpr int kRegK = kSmemList ? 1 : KCAP;
+  constexpr bool kAppend = KCAP == kAppendCap;
+  constexpr int kRegK = (kSmemList || kAppend) ? 1 : KCAP;
+  if (p.gate != nullptr && *p.gate == 0) return;  // both CTAs of the pair see the same gate
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -750,6 +784,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
       uint32_t* const fslot =
           (p.floor_g != nullptr && lq < it.q_count) ? p.floor_g + it.q_begin + lq : nullptr;
       float fl = tau_floor, published = -FLT_MAX;
+      // append mode: admit scores above tau0 (padding query rows admit nothing)
+      const float athr = lq < it.q_count ? tau_floor : INFINITY;
+      const int64_t qrow = static_cast<int64_t>(it.q_begin) + (lq < it.q_count ? lq : 0);
+      int32_t* const ccnt = kAppend ? p.cand_count + qrow : nullptr;
+      float* const cbs = kAppend ? p.out_scores + qrow * p.cand_cap : nullptr;
+      int32_t* const cbi = kAppend ? p.out_ids + qrow * p.cand_cap : nullptr;
 #pragma unroll
       for (int j = 0; j < kRegK; ++j) {
         s[j] = -FLT_MAX;
@@ -778,7 +818,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
           ptx::tmem_ld_32x32b_x32(taddr + c, va);
           ptx::tmem_ld_32x32b_x32(taddr + c + 32, vb);
           ptx::tmem_ld_wait();
-          if constexpr (kSmemList) {
+          if constexpr (kAppend) {
+            scan_chunk_append(va, athr, id0 + c, valid - c, ccnt, cbs, cbi, p.cand_cap);
+            scan_chunk_append(vb, athr, id0 + c + 32, valid - c - 32, ccnt, cbs, cbi, p.cand_cap);
+          } else if constexpr (kSmemList) {
             scan_chunk_coop<KCAP>(va, list_s, list_i, quad * 32, lane, tau, id0 + c, valid - c,
                                   fl);
             scan_chunk_coop<KCAP>(vb, list_s, list_i, quad * 32, lane, tau, id0 + c + 32,
@@ -797,7 +840,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
         abuf ^= 1;
         if (abuf == 0) aphase ^= 1;
       }
-      if (lq < it.q_count) {
+      if (!kAppend && lq < it.q_count) {
         float* os = p.out_scores + (it.out_row + lq) * p.out_k;
         int32_t* oi = p.out_ids + (it.out_row + lq) * p.out_k;
         if constexpr (kSmemList) {
@@ -1187,6 +1230,9 @@ template <int MB>
 int dispatch_kcap(int kcap, const CUtensorMap& tq, const CUtensorMap& tc, const ScanParams& p,
                   int grid, cudaStream_t stream) {
   switch (kcap) {
+    case kAppendCap:
+      if constexpr (MB == 1) return launch_impl<1, kAppendCap>(tq, tc, p, grid, stream);
+      return static_cast<int>(cudaErrorInvalidValue);
     case 1: return launch_impl<MB, 1>(tq, tc, p, grid, stream);
     case 4: return launch_impl<MB, 4>(tq, tc, p, grid, stream);
     case 8: return launch_impl<MB, 8>(tq, tc, p, grid, stream);
@@ -1206,6 +1252,7 @@ int dispatch_kcap(int kcap, const CUtensorMap& tq, const CUtensorMap& tc, const 
 int dispatch_pair(int kcap, const CUtensorMap& tq, const CUtensorMap& tc, const ScanParams& p,
                   int grid, cudaStream_t stream) {
   switch (kcap) {
+    case kAppendCap: return launch_pair_impl<kAppendCap>(tq, tc, p, grid, stream);
     case 1: return launch_pair_impl<1>(tq, tc, p, grid, stream);
     case 4: return launch_pair_impl<4>(tq, tc, p, grid, stream);
     case 8: return launch_pair_impl<8>(tq, tc, p, grid, stream);

@@ -18,6 +18,8 @@ def to_dev_bf16(x: np.ndarray, device):
 def from_dev(t) -> np.ndarray:
     import torch
 
+    if isinstance(t, np.ndarray):
+        return t
     if t.dtype == torch.bfloat16:
         return orc.bf16_to_f32(t.view(torch.int16).cpu().numpy().view(np.uint16))
     return t.cpu().numpy()

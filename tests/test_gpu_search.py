@@ -352,26 +352,62 @@ def test_tiled_segmented_requires_aligned_segments(cuda):
         tl.search_segmented(to_dev_bf16(q, cuda), [0, 3], [(5, 300)], 7)
 
 
-def test_seeded_large_k_is_exact(cuda):
-    """k > 32 on >= 262144 rows runs a 1/64-sample pass first and admits only candidates above
-    the sample's k-th score; the result must equal the unseeded search and the oracle."""
+def _search_env(idx, qd, k, **env):
     import os
 
     import torch
 
-    n, dim, b, k = 300_000, 256, 300, 100
+    old = {key: os.environ.get(key) for key in env}
+    os.environ.update({key: str(v) for key, v in env.items()})
+    try:
+        s, i = idx.search(qd, k)
+        torch.cuda.synchronize()
+    finally:
+        for key, v in old.items():
+            if v is None:
+                del os.environ[key]
+            else:
+                os.environ[key] = v
+    return from_dev(s), from_dev(i)
+
+
+@pytest.mark.parametrize("b,k", [(300, 100), (64, 100), (1024, 50), (200, 128)])
+def test_seeded_large_k_is_exact(cuda, b, k):
+    """k > 32 on >= 262144 rows runs a 1/16-sample pass first; the main pass then appends every
+    row above the sample's k-th score to a per-query candidate row and selects the top k (pair
+    kernel for B > 128, single-CTA kernel below). The result must equal the seeded list-mode
+    search, the unseeded search and the oracle, bit for bit."""
+    n, dim = 300_000, 256
     c = orc.make_corpus(n, dim, seed=0)
     q, _ = orc.make_queries(c, b, seed=1)
     idx = _index_from(c, cuda)
     qd = to_dev_bf16(q, cuda)
-    s1, i1 = idx.search(qd, k)
-    os.environ["TSV_NO_SEED"] = "1"
-    try:
-        s2, i2 = idx.search(qd, k)
-    finally:
-        del os.environ["TSV_NO_SEED"]
-    torch.cuda.synchronize()
-    np.testing.assert_array_equal(from_dev(i1), from_dev(i2))
-    np.testing.assert_array_equal(from_dev(s1), from_dev(s2))
-    sub = np.r_[0:20, 150:170]
+    s1, i1 = _search_env(idx, qd, k)
+    s2, i2 = _search_env(idx, qd, k, TSV_NO_SEED=1)
+    s3, i3 = _search_env(idx, qd, k, TSV_NO_APPEND=1)
+    np.testing.assert_array_equal(i1, i2)
+    np.testing.assert_array_equal(s1, s2)
+    np.testing.assert_array_equal(i1, i3)
+    np.testing.assert_array_equal(s1, s3)
+    sub = np.r_[0:20, b // 2:b // 2 + 20]
     assert_topk(s1[sub], i1[sub], q[sub], c, k, TOL)
+
+
+def test_candidate_overflow_falls_back_exactly(cuda):
+    """Degenerate corpus: half the rows are copies of one vector v. Queries equal to v tie with
+    150,000 rows, so their candidate rows overflow (cap 8192) and the device-gated list-mode
+    pass must recompute the batch; ties break by ascending id."""
+    n, dim, b, k = 300_000, 256, 256, 100
+    c = orc.make_corpus(n, dim, seed=0)
+    v = c[7].copy()
+    c[1::2] = v
+    q, _ = orc.make_queries(c, b, seed=1)
+    q[::4] = v  # every 4th query overflows, the others do not
+    idx = _index_from(c, cuda)
+    qd = to_dev_bf16(q, cuda)
+    s1, i1 = _search_env(idx, qd, k)
+    s2, i2 = _search_env(idx, qd, k, TSV_NO_SEED=1)
+    np.testing.assert_array_equal(i1, i2)
+    np.testing.assert_array_equal(s1, s2)
+    # the tied block: row 1, 3, 5, ... (all equal v; row 7 is v too but odd, so included)
+    np.testing.assert_array_equal(i1[0], np.arange(1, 2 * k, 2))
