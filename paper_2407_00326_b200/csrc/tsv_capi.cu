@@ -543,10 +543,12 @@ int tsv_index_scan_time(tsv_index* idx, double* total_ms, int64_t* launches) {
 static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k,
                        int64_t row_beg, int64_t row_end, int32_t id_offset, float* scores_dev,
                        int32_t* ids_dev, void* stream, const float* tau0, int list_cap = 0,
-                       const int32_t* gate = nullptr, bool append = false) {
+                       const int32_t* gate = nullptr, bool append = false,
+                       bool staged = false) {
   // list_cap > 0 (sample pass of a seeded search): per-range lists of list_cap < k entries;
   // the merge then returns the best k of the union of those lists.
   // gate != nullptr: every launch is skipped on the device unless *gate != 0.
+  // staged: q_dev is already the bf16 (normalised for cosine) matrix the scan reads.
   // append (requires tau0): candidate mode — rows above tau0 go to per-query candidate rows and
   // a select kernel writes the top k; a candidate row overflow sets the flag at
   // cand_cnt[B], which the caller passes as the gate of a list-mode fallback pass.
@@ -573,10 +575,12 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
   if (f32 && kcap > tsv::kMaxKF32)
     return fail(TSV_ERR_CONFIG, "k=%d exceeds the fp32-mode maximum (%d)", k, tsv::kMaxKF32);
 
-  const void* qb = nullptr;
-  rc = f32 ? stage_queries_f32(idx, w, q_dev, q_dtype, B, st)
-           : stage_queries(idx, w, q_dev, q_dtype, B, st, &qb);
-  if (rc) return rc;
+  const void* qb = staged ? q_dev : nullptr;
+  if (!staged) {
+    rc = f32 ? stage_queries_f32(idx, w, q_dev, q_dtype, B, st)
+             : stage_queries(idx, w, q_dev, q_dtype, B, st, &qb);
+    if (rc) return rc;
+  }
 
   // B > 128: CTA-pair kernel (256 queries x 256 rows per pair tile); otherwise one CTA per
   // 128-query group with 128-row tiles.
@@ -613,6 +617,9 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
   const int kb_elems = f32 ? 32 : tsv::kBlockK;  // elements per 128-byte k-block row
   p.num_kb = (idx->dim + kb_elems - 1) / kb_elems;
   if (tiled) p.flags |= tsv::kFlagTiled;
+  if (const char* e = getenv("TSV_DIAG"))
+    p.flags |= atoi(e) & (tsv::kFlagDiagNoFilter | tsv::kFlagDiagNoStream |
+                          tsv::kFlagDiagNoQueryLoad);
 
   if (append) {
     const bool lock = nqg > 1 && num_items <= units && !env_flag("TSV_NO_LOCKSTEP");
@@ -725,33 +732,39 @@ int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int
     DeviceGuard g(idx->device);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     Workspace& w = idx->ws[st];
-    int rc = w.seed_s.ensure(static_cast<size_t>(B) * k);
+    int rc = check_dtype(q_dtype);
+    if (!rc && q_dev == nullptr) rc = fail(TSV_ERR_ARGUMENT, "null buffer");
+    if (!rc) rc = w.seed_s.ensure(static_cast<size_t>(B) * k);
     if (!rc) rc = w.seed_i.ensure(static_cast<size_t>(B) * k);
     if (!rc) rc = w.tau0.ensure(static_cast<size_t>(B));
+    if (rc) return rc;
+    // stage (convert / normalise) the queries once for the three passes
+    const void* qb = nullptr;
+    rc = stage_queries(idx, w, q_dev, q_dtype, B, st, &qb);
     if (rc) return rc;
     // Sample pass with 32-entry register lists per corpus range: the k-th best of the union
     // of those lists is still a lower bound of the sample's k-th best (the union holds k
     // distinct rows scoring at least that much) and, with the top rows spread over many
     // ranges, usually equal to it; the k-entry shared-memory lists of the main pass then see
     // few insertions.
-    rc = search_impl(idx, q_dev, q_dtype, B, k, row_beg, row_beg + sample, 0, w.seed_s.ptr,
-                     w.seed_i.ptr, stream, nullptr, tsv::kMaxRegK);
+    rc = search_impl(idx, qb, TSV_BF16, B, k, row_beg, row_beg + sample, 0, w.seed_s.ptr,
+                     w.seed_i.ptr, stream, nullptr, tsv::kMaxRegK, nullptr, false, true);
     if (rc) return rc;
     int e = tsv::launch_seed_floor(w.seed_s.ptr, w.seed_i.ptr, B, k, w.tau0.ptr, st);
     if (e) return cuda_fail(static_cast<cudaError_t>(e), "seed floor");
     g_launches++;
     if (env_flag("TSV_NO_APPEND"))
-      return search_impl(idx, q_dev, q_dtype, B, k, row_beg, row_end, id_offset, scores_dev,
-                         ids_dev, stream, w.tau0.ptr);
+      return search_impl(idx, qb, TSV_BF16, B, k, row_beg, row_end, id_offset, scores_dev,
+                         ids_dev, stream, w.tau0.ptr, 0, nullptr, false, true);
     // Main pass in candidate mode: the register-list pipeline depth (no shared-memory lists),
     // every row above tau0 appended to its query's candidate row, exact top-k selected from
     // those. If any candidate row overflowed, the device-gated list-mode pass recomputes the
     // batch (exact either way; no host round trip decides it).
-    rc = search_impl(idx, q_dev, q_dtype, B, k, row_beg, row_end, id_offset, scores_dev, ids_dev,
-                     stream, w.tau0.ptr, 0, nullptr, true);
+    rc = search_impl(idx, qb, TSV_BF16, B, k, row_beg, row_end, id_offset, scores_dev, ids_dev,
+                     stream, w.tau0.ptr, 0, nullptr, true, true);
     if (rc) return rc;
-    return search_impl(idx, q_dev, q_dtype, B, k, row_beg, row_end, id_offset, scores_dev,
-                       ids_dev, stream, w.tau0.ptr, 0, w.cand_cnt.ptr + B);
+    return search_impl(idx, qb, TSV_BF16, B, k, row_beg, row_end, id_offset, scores_dev,
+                       ids_dev, stream, w.tau0.ptr, 0, w.cand_cnt.ptr + B, false, true);
   }
   return search_impl(idx, q_dev, q_dtype, B, k, row_beg, row_end, id_offset, scores_dev, ids_dev,
                      stream, nullptr);

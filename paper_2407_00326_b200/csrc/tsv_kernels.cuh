@@ -96,6 +96,13 @@ int launch_cand_select(const float* buf_s, const int32_t* buf_i, const int32_t* 
 constexpr int kPairDynMode = 5;
 constexpr int kFlagTiled = 2;
 constexpr int kFlagLockstep = 4;  // static pair kernel: bound drift between range partners
+// Diagnostic flags (TSV_DIAG, pair kernel; results are wrong by design): attribute the step's
+// energy under the power cap. 16: epilogue loads the accumulators but filters nothing;
+// 32: every tile re-reads the range's first corpus tile (L2-resident, no HBM stream).
+constexpr int kFlagDiagNoFilter = 16;
+constexpr int kFlagDiagNoStream = 32;
+// 64: query tiles are loaded for the first corpus tile only (later tiles reuse stale smem).
+constexpr int kFlagDiagNoQueryLoad = 64;
 // Tiled arena layout: row i, element d at ((i/128 * KB + d/64) * 128 + i%128) * 64 + d%64,
 // KB = ceil(dim/64): every [128 rows x 64 elements] k-block tile is one contiguous 16 KB block.
 int launch_seed_floor(const float* s, const int32_t* id, int B, int k, float* floor_out,

@@ -705,13 +705,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
           }
         }
         __syncwarp();
-        const int32_t row0 = static_cast<int32_t>(it.row_begin + t * Pair::kTileRows) + rank * 128;
+        const int64_t tt = (p.flags & kFlagDiagNoStream) ? 0 : t;
+        const int32_t row0 = static_cast<int32_t>(it.row_begin + tt * Pair::kTileRows) + rank * 128;
         for (int kb = 0; kb < p.num_kb; ++kb) {
           ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* st = smem + stage * Pair::kStageBytes;
           const uint32_t fb = ptx::mapa(ptx::smem_u32(&full_bar[stage]), 0);
-          if (leader) ptx::mbar_arrive_expect_tx_warp(&full_bar[stage], 2 * Pair::kStageBytes);
-          ptx::tma_load_2d_pair_warp(st, &tmap_q, fb, kb * kBlockK, it.q_begin + rank * 128, pol_q);
+          const bool skip_a = (p.flags & kFlagDiagNoQueryLoad) && t > 0;
+          if (leader)
+            ptx::mbar_arrive_expect_tx_warp(&full_bar[stage],
+                                            skip_a ? Pair::kStageBytes : 2 * Pair::kStageBytes);
+          if (!skip_a)
+            ptx::tma_load_2d_pair_warp(st, &tmap_q, fb, kb * kBlockK, it.q_begin + rank * 128,
+                                       pol_q);
           if (p.flags & kFlagTiled)
             ptx::tma_load_3d_pair_warp(st + Pair::kHalfBytes, &tmap_c, fb, 0, 0,
                                        (row0 >> 7) * p.num_kb + kb, pol_c);
@@ -812,12 +818,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
         ptx::mbar_wait(&tfull_bar[abuf], aphase);
         ptx::tc_fence_after();
         const uint32_t taddr = lane_addr + abuf * Pair::kAccCols;
+        const bool diag_nofilter = (p.flags & kFlagDiagNoFilter) != 0;
 #pragma unroll 1
         for (int c = 0; c < Pair::kTileRows; c += 64) {
           uint32_t va[32], vb[32];
           ptx::tmem_ld_32x32b_x32(taddr + c, va);
           ptx::tmem_ld_32x32b_x32(taddr + c + 32, vb);
           ptx::tmem_ld_wait();
+          if (diag_nofilter) continue;
           if constexpr (kAppend) {
             scan_chunk_append(va, athr, id0 + c, valid - c, ccnt, cbs, cbi, p.cand_cap);
             scan_chunk_append(vb, athr, id0 + c + 32, valid - c - 32, ccnt, cbs, cbi, p.cand_cap);
