@@ -592,11 +592,25 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
   const int nqg = (B + qg - 1) / qg;
   const int64_t n = row_end - row_beg;
   const int64_t tiles = std::max<int64_t>(1, (n + tile_rows - 1) / tile_rows);
-  // Ranges per query group: one round over all workers when that idles at most ~3% of them,
-  // otherwise two full rounds (every worker busy; the corpus is then streamed twice).
+  // Ranges per query group: one round over all workers when nqg divides them. Otherwise the
+  // pair kernel takes its items in range-major order over whole rounds (nqg * R a multiple of
+  // the worker count, at most 4 rounds): every pair is busy and each range's query groups
+  // still run in the same round, so the corpus is streamed once. Failing that, one round if
+  // it idles at most ~3% of the workers, else two full rounds (corpus streamed twice).
   int R = std::max(1, units / nqg);
-  if (nqg * R < units * 97 / 100 && (2 * units) % nqg == 0) R = 2 * units / nqg;
-  if (const char* e = getenv("TSV_SCAN_RANGES")) R = std::max(1, atoi(e));
+  bool range_major = false;
+  if (pair && nqg > 1 && units % nqg != 0 && !env_flag("TSV_NO_RANGE_MAJOR")) {
+    for (int rounds = 2; rounds <= 4 && !range_major; ++rounds)
+      if ((rounds * units) % nqg == 0 && tiles >= 8 * (rounds * units / nqg)) {
+        R = rounds * units / nqg;
+        range_major = true;
+      }
+  }
+  if (!range_major && nqg * R < units * 97 / 100 && (2 * units) % nqg == 0) R = 2 * units / nqg;
+  if (const char* e = getenv("TSV_SCAN_RANGES")) {
+    R = std::max(1, atoi(e));
+    range_major = false;
+  }
   // at least kMinTilesPerRange tiles per range: tiny scans gain nothing from more workers, and
   // every extra range is one more list for the merge
   R = static_cast<int>(std::min<int64_t>(R, std::max<int64_t>(1, tiles / kMinTilesPerRange)));
@@ -614,6 +628,7 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
   p.row_end = row_end;
   p.tau0 = tau0;
   p.gate = gate;
+  if (range_major) p.flags |= tsv::kFlagRangeMajor;
   const int kb_elems = f32 ? 32 : tsv::kBlockK;  // elements per 128-byte k-block row
   p.num_kb = (idx->dim + kb_elems - 1) / kb_elems;
   if (tiled) p.flags |= tsv::kFlagTiled;
@@ -622,7 +637,8 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
                           tsv::kFlagDiagNoQueryLoad);
 
   if (append) {
-    const bool lock = nqg > 1 && num_items <= units && !env_flag("TSV_NO_LOCKSTEP");
+    const bool lock =
+        nqg > 1 && (num_items <= units || range_major) && !env_flag("TSV_NO_LOCKSTEP");
     const size_t nc = lock ? static_cast<size_t>(num_items) : 0;
     rc = w.cand_s.ensure(static_cast<size_t>(B) * tsv::kCandCap);
     if (!rc) rc = w.cand_i.ensure(static_cast<size_t>(B) * tsv::kCandCap);
@@ -677,7 +693,8 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
     g_launches++;
     return TSV_OK;
   }
-  const bool lock = nqg > 1 && num_items <= units && !env_flag("TSV_NO_LOCKSTEP");
+  const bool lock =
+      nqg > 1 && (num_items <= units || range_major) && !env_flag("TSV_NO_LOCKSTEP");
   const bool floor = R > 1 && !env_flag("TSV_NO_FLOOR");
   if (lock || floor) {  // one zeroed buffer: [progress counters][per-query floors]
     const size_t nc = lock ? static_cast<size_t>(num_items) : 0;

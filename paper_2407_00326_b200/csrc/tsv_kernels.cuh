@@ -96,6 +96,11 @@ int launch_cand_select(const float* buf_s, const int32_t* buf_i, const int32_t* 
 constexpr int kPairDynMode = 5;
 constexpr int kFlagTiled = 2;
 constexpr int kFlagLockstep = 4;  // static pair kernel: bound drift between range partners
+// Implicit grid in range-major order (pair kernel): item i covers corpus range i / nqg for query
+// group i % nqg, so the items of one range are adjacent and, when nqg * R is a multiple of the
+// worker count, all workers stay busy over several rounds while each range is still streamed
+// once (its query groups run in the same round, in lockstep).
+constexpr int kFlagRangeMajor = 8;
 // Diagnostic flags (TSV_DIAG, pair kernel; results are wrong by design): attribute the step's
 // energy under the power cap. 16: epilogue loads the accumulators but filters nothing;
 // 32: every tile re-reads the range's first corpus tile (L2-resident, no HBM stream).

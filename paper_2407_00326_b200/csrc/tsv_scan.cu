@@ -63,8 +63,15 @@ __device__ __forceinline__ void resolve_item(const ScanParams& p, int i, ScanIte
     it = p.items[i];
     return;
   }
-  const int qg = i / p.R;
-  const int r = i - qg * p.R;
+  int qg, r;
+  if (p.flags & kFlagRangeMajor) {
+    const int nqg = (p.B + qg_size - 1) / qg_size;
+    r = i / nqg;
+    qg = i - r * nqg;
+  } else {
+    qg = i / p.R;
+    r = i - qg * p.R;
+  }
   it.q_begin = qg * qg_size;
   it.q_count = min(qg_size, p.B - it.q_begin);
   const int64_t n = p.row_end - p.row_beg;
@@ -685,14 +692,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
     // Range lockstep (flag bit 2): the pairs that stream the same corpus range for different
     // query groups publish their tile progress and none runs more than kLockWindow tiles ahead,
     // so each corpus tile is fetched from HBM once and served to the others from L2.
-    const bool lockstep = (p.flags & kFlagLockstep) && p.items == nullptr && num_items <= npairs;
+    // With range-major items several rounds are allowed: partners are the items of the same
+    // range in the same round (a partner of a later round has not started and must not be
+    // waited for).
+    const bool range_major = (p.flags & kFlagRangeMajor) != 0;
+    const bool lockstep = (p.flags & kFlagLockstep) && p.items == nullptr &&
+                          (num_items <= npairs || range_major);
     volatile int32_t* progress = p.counter;
     for (int i = pair; i < num_items; i += npairs) {
       ScanItem it;
       resolve_item(p, i, it, Pair::kQG, Pair::kTileRows);
       const int64_t ntiles = (it.row_end - it.row_begin + Pair::kTileRows - 1) / Pair::kTileRows;
-      const int my_qg = i / p.R, my_r = i - (i / p.R) * p.R;
-      const int nqg = num_items / p.R;
+      const int nqg = range_major ? (p.B + Pair::kQG - 1) / Pair::kQG : num_items / p.R;
+      const int my_qg = range_major ? i % nqg : i / p.R;
+      const int my_r = range_major ? i / nqg : i - my_qg * p.R;
+      const int round = i / npairs;
       for (int64_t t = 0; t < ntiles; ++t) {
         if (lockstep && leader && lane == 0) {
           const int w = p.lock_window > 0 ? p.lock_window : kLockWindow;
@@ -700,7 +714,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
           if (t >= w) {
             for (int g = 0; g < nqg; ++g) {
               if (g == my_qg) continue;
-              while (progress[g * p.R + my_r] < t - w) __nanosleep(256);
+              const int j = range_major ? my_r * nqg + g : g * p.R + my_r;
+              if (j / npairs != round) continue;
+              while (progress[j] < t - w) __nanosleep(256);
             }
           }
         }

@@ -411,3 +411,21 @@ def test_candidate_overflow_falls_back_exactly(cuda):
     np.testing.assert_array_equal(s1, s2)
     # the tied block: row 1, 3, 5, ... (all equal v; row 7 is v too but odd, so included)
     np.testing.assert_array_equal(i1[0], np.arange(1, 2 * k, 2))
+
+
+@pytest.mark.parametrize("b,k", [(1024, 10), (768, 16), (1024, 32)])
+def test_range_major_rounds_identical(cuda, b, k):
+    """B=1024 (4 query groups) and B=768 (3) do not divide the 74 CTA pairs: the pair kernel
+    then takes range-major items over 2 or 3 rounds with lockstepped range partners. The result
+    must be identical to the one-round layout and match the oracle."""
+    n, dim = 200_000, 256
+    c = orc.make_corpus(n, dim, seed=0)
+    q, _ = orc.make_queries(c, b, seed=1)
+    idx = _index_from(c, cuda)
+    qd = to_dev_bf16(q, cuda)
+    s1, i1 = _search_env(idx, qd, k)
+    s2, i2 = _search_env(idx, qd, k, TSV_NO_RANGE_MAJOR=1)
+    np.testing.assert_array_equal(i1, i2)
+    np.testing.assert_array_equal(s1, s2)
+    sub = np.r_[0:16, b - 16:b]
+    assert_topk(s1[sub], i1[sub], q[sub], c, k, TOL)
