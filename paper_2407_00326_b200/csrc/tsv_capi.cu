@@ -600,11 +600,17 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
   int R = std::max(1, units / nqg);
   bool range_major = false;
   if (pair && nqg > 1 && units % nqg != 0 && !env_flag("TSV_NO_RANGE_MAJOR")) {
-    for (int rounds = 2; rounds <= 4 && !range_major; ++rounds)
-      if ((rounds * units) % nqg == 0 && tiles >= 8 * (rounds * units / nqg)) {
+    // preferred round counts: ~4 rounds measured best at B=1024 (finer items even out the
+    // pairs' finishing times); up to 6 so that 5 query groups also fit
+    static const int kRounds[] = {4, 3, 2, 5, 6};
+    for (int rounds : kRounds) {
+      if (const char* e = getenv("TSV_ROUNDS")) rounds = atoi(e);
+      if (rounds >= 2 && (rounds * units) % nqg == 0 && tiles >= 8 * (rounds * units / nqg)) {
         R = rounds * units / nqg;
         range_major = true;
+        break;
       }
+    }
   }
   if (!range_major && nqg * R < units * 97 / 100 && (2 * units) % nqg == 0) R = 2 * units / nqg;
   if (const char* e = getenv("TSV_SCAN_RANGES")) {
