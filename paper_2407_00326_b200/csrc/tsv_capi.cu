@@ -599,7 +599,8 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
   // it idles at most ~3% of the workers, else two full rounds (corpus streamed twice).
   int R = std::max(1, units / nqg);
   bool range_major = false;
-  if (pair && nqg > 1 && units % nqg != 0 && !env_flag("TSV_NO_RANGE_MAJOR")) {
+  if (pair && nqg > 1 && (units % nqg != 0 || getenv("TSV_ROUNDS")) &&
+      !env_flag("TSV_NO_RANGE_MAJOR")) {
     // preferred round counts: ~4 rounds measured best at B=1024 (finer items even out the
     // pairs' finishing times); up to 6 so that 5 query groups also fit
     static const int kRounds[] = {4, 3, 2, 5, 6};
