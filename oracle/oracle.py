@@ -14,7 +14,10 @@ semantics of those primitives and is pinned by (a) the reference's own structura
 golden e-graph for the path (cardinalities, slices, Aggregate concatenation — see
 tests/golden/make_golden.py) and (b) known-answer vectors (planted neighbours, identity corpus,
 exact ties, duplicate candidates, shard boundaries, k >= N) committed under tests/golden/.
-Score arithmetic itself is "parity unpinned" against the reference (there is none to pin to).
+Score arithmetic itself is "parity unpinned" against the reference (there is none to pin to);
+`pgvector_exact_search` restates the published distance functions of the third-party engine
+the paper's prototype used (pgvector, unversioned in the reference) and the GPU parity tests
+also run the comparator against it.
 
 Semantics restated here:
   * Searching ("Perform vector searching in the database"): per query, the
@@ -210,6 +213,55 @@ def merge(scores: np.ndarray, ids: np.ndarray, k: int):
         i = ids[:, r, :].reshape(-1).astype(np.int64)
         keep = i >= 0
         out_s[r], out_i[r] = pad_topk(s[keep], i[keep], k)
+    return out_s, out_i
+
+
+# ------------------------------------------------------------------ pgvector restatement
+def pgvector_exact_search(q: np.ndarray, c: np.ndarray, k: int, op: str = "<#>",
+                          keep: int = 0) -> tuple[np.ndarray, np.ndarray]:
+    """The original Teola's vector search, restated: PostgreSQL + pgvector,
+    `SELECT id FROM chunks ORDER BY embedding <op> $query LIMIT k` on a table without an ANN
+    index, i.e. an exact sequential scan. pgvector is a third-party dependency of the paper's
+    prototype that the reference neither vendors nor pins (no version anywhere in
+    /root/reference; no call site), so this follows pgvector's published distance functions
+    for the `vector` type (float4 elements), unchanged across its releases:
+      * `<#>` negative inner product: -(sum_i a[i] * b[i]) accumulated in float32, returned as
+        float8 (vector_negative_inner_product / VectorInnerProduct);
+      * `<=>` cosine distance: 1 - dot / sqrt(|a|^2 |b|^2) with dot and the squared norms
+        accumulated in float32, the quotient in float8 and clamped to [-1, 1]
+        (cosine_distance);
+    ascending distance, LIMIT k. PostgreSQL's top-N sort does not define an order among equal
+    distances; `id` breaks them here (ascending), which is the order this repo emits.
+    pgvector compiles the accumulation loop with auto-vectorisation, so its exact float32
+    summation order is build-dependent; this restatement sums sequentially over i.
+
+    Returned in this repo's convention: scores (higher = better: -distance for `<#>`,
+    1 - distance for `<=>`) and ids, [B, k + keep], padded with (-inf, -1)."""
+    qf = np.asarray(q, dtype=np.float32)
+    cf = np.asarray(c, dtype=np.float32)
+    b, n = qf.shape[0], cf.shape[0]
+    dot = np.zeros((b, n), dtype=np.float32)
+    for i in range(qf.shape[1]):  # sequential float32 accumulation, as VectorInnerProduct
+        dot += qf[:, i, None] * cf[None, :, i]
+    if op == "<#>":
+        score = dot.astype(np.float64)
+    elif op == "<=>":
+        na = np.zeros(b, dtype=np.float32)
+        nb = np.zeros(n, dtype=np.float32)
+        for i in range(qf.shape[1]):
+            na += qf[:, i] * qf[:, i]
+            nb += cf[:, i] * cf[:, i]
+        sim = dot.astype(np.float64) / np.sqrt(na.astype(np.float64)[:, None] *
+                                               nb.astype(np.float64)[None, :])
+        score = np.clip(sim, -1.0, 1.0)  # 1 - cosine_distance
+    else:
+        raise ValueError(f"unknown pgvector operator {op!r}")
+    kk = k + keep
+    out_s = np.full((b, kk), -np.inf)
+    out_i = np.full((b, kk), PAD_ID, dtype=np.int64)
+    ids = np.arange(n, dtype=np.int64)
+    for r in range(b):
+        out_s[r], out_i[r] = pad_topk(score[r], ids, kk)
     return out_s, out_i
 
 

@@ -116,9 +116,15 @@ class ShardedSearch:
                 torch.empty((self.world, B, k), dtype=torch.int32, device=device))
         return self._bufs[key]
 
-    def search(self, q: torch.Tensor, k: int):
-        """Global top-k of q over the sharded corpus; identical result on every rank."""
+    def search(self, q: torch.Tensor, k: int,
+               out: tuple[torch.Tensor, torch.Tensor] | None = None):
+        """Global top-k of q over the sharded corpus; identical result on every rank.
+
+        With world == 1 the result is written to `out` when given (otherwise to a buffer
+        reused by the next call); with world > 1 it is a new pair of tensors."""
         s_loc, i_loc, s_all, i_all = self._buffers(q.shape[0], k, q.device)
+        if self.world == 1 and out is not None:
+            s_loc, i_loc = out
         self.search_fn(q, k, id_offset=self.lo, out=(s_loc, i_loc))
         if self.world == 1:
             return s_loc, i_loc

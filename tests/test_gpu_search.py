@@ -429,3 +429,18 @@ def test_range_major_rounds_identical(cuda, b, k):
     np.testing.assert_array_equal(s1, s2)
     sub = np.r_[0:16, b - 16:b]
     assert_topk(s1[sub], i1[sub], q[sub], c, k, TOL)
+
+
+@pytest.mark.parametrize("n,dim,b,k", [(20000, 1024, 256, 10), (5000, 384, 16, 5),
+                                       (300_000, 256, 300, 100)])
+def test_search_matches_pgvector_restatement(cuda, n, dim, b, k):
+    """The original system's search, `ORDER BY embedding <#> q LIMIT k` in PostgreSQL +
+    pgvector (oracle.pgvector_exact_search: float32 sequential accumulation), as the oracle of
+    the comparator: scores within 1e-3 relative, ids exact outside tie bands."""
+    c = orc.make_corpus(n, dim, seed=0)
+    q, _ = orc.make_queries(c, b, seed=1)
+    idx = _index_from(c, cuda)
+    s, i = idx.search(to_dev_bf16(q, cuda), k)
+    sub = np.r_[0:min(b, 24)]
+    pg = orc.pgvector_exact_search(q[sub], c, k, op="<#>", keep=64)
+    assert_topk(from_dev(s)[sub], from_dev(i)[sub], q[sub], c, k, TOL, oracle=pg)

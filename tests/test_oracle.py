@@ -109,3 +109,21 @@ def test_c_oracle_matches_numpy_oracle():
         es, ei = _exp(kat)
         np.testing.assert_array_equal(i, ei)
         np.testing.assert_array_equal(s, es.astype(np.float32))
+
+
+@pytest.mark.parametrize("op", ["<#>", "<=>"])
+def test_pgvector_restatement_agrees_with_oracle(op):
+    """The pgvector restatement (float32 sequential accumulation, ORDER BY distance LIMIT k)
+    and the float64 oracle give the same top-k under the comparator at 1e-5 (fp32 mode's
+    tolerance)."""
+    c = orc.make_corpus(3000, 384, seed=0)
+    q, _ = orc.make_queries(c, 12, seed=1)
+    ps, pi = orc.pgvector_exact_search(q, c, 10, op=op)
+    if op == "<=>":  # cosine of the stored (bf16-rounded, so not exactly unit) rows, in f64
+        q = q / np.linalg.norm(q.astype(np.float64), axis=1, keepdims=True)
+        c = c / np.linalg.norm(c.astype(np.float64), axis=1, keepdims=True)
+    assert not orc.check_topk(ps, pi, q, c, 10, 1e-5)
+    # ties: duplicated rows come back in ascending id order
+    c2 = np.concatenate([c[:50], c[:50]])
+    ps2, pi2 = orc.pgvector_exact_search(c2[:3], c2, 2, op=op)
+    np.testing.assert_array_equal(pi2, [[0, 50], [1, 51], [2, 52]])
