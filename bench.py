@@ -298,10 +298,18 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # BENCH_DIST_BACKEND=gloo (test only): run the N>1 code path with every rank on the GPUs
+    # present (ranks share a GPU when there are fewer GPUs than ranks; NCCL refuses that)
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     _native.load()
 
     B, D, k, N = args.batch, args.dim, args.k, args.rows
@@ -326,7 +334,7 @@ def run_ours(args):
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -337,6 +345,13 @@ def run_ours(args):
     clocks.start()
     for _ in range(args.warmup):
         step(q_dev)
+    # keep the GPU busy (more untimed steps) until every rank's sampler has produced a sample,
+    # at most ~2 s; the decision is collective because a sharded step is
+    t_w = time.time()
+    while max_over_ranks(float(clocks.proc is not None and not clocks.rows
+                               and time.time() - t_w < 2.0)) > 0:
+        step(q_dev)
+        torch.cuda.synchronize(dev)
     barrier()
 
     def device_region(steps):

@@ -1,0 +1,61 @@
+"""bench.py contract on the GPU: one JSON line with the driver's keys, and the N>1 sharded path
+(two ranks sharing this GPU over gloo; the driver's scaling run uses NCCL across GPUs) finds
+every planted neighbour with its global id."""
+
+from __future__ import annotations
+
+import json
+import os
+import socket
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+        "scaling", "vs_baseline", "dtype", "data", "config", "e2e", "roofline", "cpu_baseline",
+        "gpu_launches", "clocks"}
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _last_json(out: str) -> dict:
+    lines = [ln for ln in out.splitlines() if ln.startswith("{")]
+    assert lines, out[-2000:]
+    return json.loads(lines[-1])
+
+
+def test_bench_one_gpu_line(cuda):
+    r = subprocess.run([sys.executable, "bench.py", "--rows", "1000000", "--steps", "8",
+                        "--warmup", "3", "--cpu-seconds", "1"], cwd=ROOT, capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = _last_json(r.stdout)
+    assert KEYS <= set(d)
+    assert d["n_gpus"] == 1 and d["planted_top1"] == 1.0
+    assert d["gpu_launches"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 1024 * 1024 * 2
+    assert d["roofline"]["bound"] in ("tensor", "hbm") and d["roofline"]["frac"] > 0
+    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+
+
+def test_bench_two_ranks_sharded(cuda):
+    env = dict(os.environ, BENCH_DIST_BACKEND="gloo")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port",
+                        str(_port()), "bench.py", "--gpus", "2", "--rows", "1000000",
+                        "--steps", "4", "--warmup", "3"], cwd=ROOT, capture_output=True,
+                       text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = _last_json(r.stdout)
+    assert d["n_gpus"] == 2 and d["config"]["shard_rows"] == 500_000
+    assert d["config"]["exchange"] == "p2p"
+    assert d["planted_top1"] == 1.0  # global ids survive the exchange + merge
