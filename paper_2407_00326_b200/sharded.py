@@ -47,21 +47,43 @@ class PeerExchange:
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.max_b, self.max_k = max_b, max_k
-        h = ctypes.c_void_p()
-        self.check(self.lib.tsv_peer_create(device.index, self.world, self.rank, max_b, max_k,
-                                            ctypes.byref(h)))
-        self._h = h
-        raw = (ctypes.c_ubyte * 64)()
-        n = ctypes.c_int()
-        self.check(self.lib.tsv_peer_handle(h, raw, ctypes.byref(n)))
+        nccl = dist.get_backend(group) == "nccl"
+        self._h = ctypes.c_void_p()
+        # Every rank must take the same exchange path, so failures are agreed collectively:
+        # byte 64 of each rank's published handle flags a local setup failure, and the
+        # result of opening the peers' handles is all-reduced before the buffers are used.
+        err = None
+        raw = (ctypes.c_ubyte * 65)()
+        try:
+            self.check(self.lib.tsv_peer_create(device.index, self.world, self.rank, max_b, max_k,
+                                                ctypes.byref(self._h)))
+            n = ctypes.c_int()
+            self.check(self.lib.tsv_peer_handle(self._h, raw, ctypes.byref(n)))
+        except Exception as exc:  # noqa: BLE001 - reported collectively below
+            err = exc
+            raw[64] = 1
         mine = torch.tensor(list(bytes(raw)), dtype=torch.uint8)
-        if dist.get_backend(group) == "nccl":
+        if nccl:
             mine = mine.to(device)
         got = [torch.empty_like(mine) for _ in range(self.world)]
         dist.all_gather(got, mine, group=group)
+        got = [t.cpu() for t in got]
+        if any(int(t[64]) for t in got):
+            self.close()
+            raise RuntimeError(f"peer buffer setup failed on some rank ({err or 'another rank'})")
         for p, t in enumerate(got):
-            buf = (ctypes.c_ubyte * 64)(*t.cpu().tolist())
-            self.check(self.lib.tsv_peer_open(h, p, buf))
+            buf = (ctypes.c_ubyte * 64)(*t[:64].tolist())
+            try:
+                self.check(self.lib.tsv_peer_open(self._h, p, buf))
+            except Exception as exc:  # noqa: BLE001 - reported collectively below
+                err = exc
+                break
+        flag = torch.tensor([0 if err is None else 1], dtype=torch.int32,
+                            device=device if nccl else "cpu")
+        dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
+        if int(flag.item()) != 0:
+            self.close()
+            raise RuntimeError(f"peer mapping failed on some rank ({err or 'another rank'})")
         dist.barrier(group)
 
     def allgather_merge(self, s_loc: torch.Tensor, i_loc: torch.Tensor, k: int,
