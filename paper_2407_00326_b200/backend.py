@@ -441,15 +441,26 @@ class RetrievalBackend:
             seg = self._local_segment(ctx.query_id, idx[0][1][1], self.replicas.index(rep))
             rows = torch.where(part >= 0, part + seg.row_beg, part).to(torch.int32)
             qv = self.data.question(rep.device, ctx.query_id)
-            jobs.append((task, lo, top_k, seg, qv, rows.reshape(1, -1).contiguous()))
-        start.record(rep.stream)
-        for task, lo, top_k, seg, qv, rows in jobs:
-            s, i = rep.arena.rerank(qv, rows, top_k, stream=rep.stream)
-            i = torch.where(i >= 0, i - seg.row_beg, i).to(torch.int32)
-            self.acc.setdefault((task.ctx.query_id, task.node_id), []).append(
-                (lo, s, i, self._record(rep), self.replicas.index(rep)))
-        n_rows = sum(j[5].shape[1] for j in jobs)
+            jobs.append((task, lo, top_k, seg, qv.reshape(1, -1), rows.reshape(-1)))
+        # One K3 launch for the whole batch: question j scores its own candidate row (padded
+        # with -1, which K3 skips), the best max(top_k) are kept and each job takes its top_k.
+        n_c = max(j[5].shape[0] for j in jobs)
         k_out = max(j[2] for j in jobs)
+        cand = torch.full((len(jobs), n_c), -1, dtype=torch.int32, device=rep.device)
+        for j, job in enumerate(jobs):
+            cand[j, :job[5].shape[0]] = job[5]
+        qs = torch.cat([j[4] for j in jobs]) if len(jobs) > 1 else jobs[0][4]
+        offs = torch.tensor([[j[3].row_beg] for j in jobs], dtype=torch.int32).pin_memory()
+        offs = offs.to(rep.device, non_blocking=True)
+        start.record(rep.stream)
+        s_all, i_all = rep.arena.rerank(qs, cand, k_out, stream=rep.stream)
+        i_all = torch.where(i_all >= 0, i_all - offs, i_all)
+        ready = self._record(rep)
+        r = self.replicas.index(rep)
+        for j, (task, lo, top_k, seg, qv, rows) in enumerate(jobs):
+            self.acc.setdefault((task.ctx.query_id, task.node_id), []).append(
+                (lo, s_all[j:j + 1, :top_k], i_all[j:j + 1, :top_k], ready, r))
+        n_rows = sum(j[5].shape[0] for j in jobs)
         return LaunchRecord("", 0, "rerank", len(jobs), n_rows, k_out, self.dim,
                             bytes=n_rows * (self.dim * 2 + 4) + len(jobs) * (self.dim * 2 + k_out * 8),
                             flops=2 * n_rows * self.dim)
