@@ -544,11 +544,12 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
                        int64_t row_beg, int64_t row_end, int32_t id_offset, float* scores_dev,
                        int32_t* ids_dev, void* stream, const float* tau0, int list_cap = 0,
                        const int32_t* gate = nullptr, bool append = false,
-                       bool staged = false) {
+                       bool staged = false, int sample_div = 0) {
   // list_cap > 0 (sample pass of a seeded search): per-range lists of list_cap < k entries;
   // the merge then returns the best k of the union of those lists.
   // gate != nullptr: every launch is skipped on the device unless *gate != 0.
   // staged: q_dev is already the bf16 (normalised for cosine) matrix the scan reads.
+  // sample_div > 1: every range scans only its first 1/sample_div (seeding sample pass).
   // append (requires tau0): candidate mode — rows above tau0 go to per-query candidate rows and
   // a select kernel writes the top k; a candidate row overflow sets the flag at
   // cand_cnt[B], which the caller passes as the gate of a list-mode fallback pass.
@@ -635,6 +636,7 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
   p.row_end = row_end;
   p.tau0 = tau0;
   p.gate = gate;
+  p.sample_div = sample_div;
   if (range_major) p.flags |= tsv::kFlagRangeMajor;
   const int kb_elems = f32 ? 32 : tsv::kBlockK;  // elements per 128-byte k-block row
   p.num_kb = (idx->dim + kb_elems - 1) / kb_elems;
@@ -743,16 +745,15 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
 int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int64_t row_beg,
                int64_t row_end, int32_t id_offset, float* scores_dev, int32_t* ids_dev,
                void* stream) {
-  // k > 32 keeps shared-memory lists whose cost is the number of admitted candidates. A top-k
-  // over a 1/16 sample of the rows bounds every query's final k-th score from below; seeding
-  // the main scan with it keeps the result exact and skips most insertions.
+  // k > 32: a top-k over a 1/16 sample of the rows bounds every query's final k-th score from
+  // below; the main scan then only has to keep rows above that floor (candidate mode), which
+  // keeps the result exact.
   const int kcap = tsv::scan_kcap_for(k);
   const int64_t n = row_end - row_beg;
   if (idx != nullptr && kcap > tsv::kMaxRegK && idx->storage != TSV_F32 && B > 0 &&
       n >= 64 * 4096 && !env_flag("TSV_NO_SEED")) {
     int frac = 16;
     if (const char* e = getenv("TSV_SEED_FRAC")) frac = std::max(2, atoi(e));
-    const int64_t sample = ((n / frac + 255) / 256) * 256;
     DeviceGuard g(idx->device);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     Workspace& w = idx->ws[st];
@@ -766,13 +767,19 @@ int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int
     const void* qb = nullptr;
     rc = stage_queries(idx, w, q_dev, q_dtype, B, st, &qb);
     if (rc) return rc;
-    // Sample pass with 32-entry register lists per corpus range: the k-th best of the union
-    // of those lists is still a lower bound of the sample's k-th best (the union holds k
-    // distinct rows scoring at least that much) and, with the top rows spread over many
-    // ranges, usually equal to it; the k-entry shared-memory lists of the main pass then see
-    // few insertions.
-    rc = search_impl(idx, qb, TSV_BF16, B, k, row_beg, row_beg + sample, 0, w.seed_s.ptr,
-                     w.seed_i.ptr, stream, nullptr, tsv::kMaxRegK, nullptr, false, true);
+    // Sample pass with 32-entry register lists per corpus range, each range scanning only the
+    // first 1/frac of its tiles (a sample spread over the whole row range, so a corpus stored
+    // in topical order still yields a tight floor): the k-th best of the union of those lists
+    // is a lower bound of the final k-th score (the union holds k distinct rows scoring at
+    // least that much) and, with the top rows spread over many ranges, usually equal to the
+    // sample's k-th best.
+    if (env_flag("TSV_SEED_CONTIG"))  // A/B: the first 1/frac of the rows instead
+      rc = search_impl(idx, qb, TSV_BF16, B, k, row_beg, row_beg + ((n / frac + 255) / 256) * 256,
+                       0, w.seed_s.ptr, w.seed_i.ptr, stream, nullptr, tsv::kMaxRegK, nullptr,
+                       false, true);
+    else
+      rc = search_impl(idx, qb, TSV_BF16, B, k, row_beg, row_end, 0, w.seed_s.ptr, w.seed_i.ptr,
+                       stream, nullptr, tsv::kMaxRegK, nullptr, false, true, frac);
     if (rc) return rc;
     int e = tsv::launch_seed_floor(w.seed_s.ptr, w.seed_i.ptr, B, k, w.tau0.ptr, st);
     if (e) return cuda_fail(static_cast<cudaError_t>(e), "seed floor");

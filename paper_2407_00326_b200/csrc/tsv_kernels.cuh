@@ -81,6 +81,9 @@ struct ScanParams {
   // Device-side gate (nullptr = always run): the kernel returns at once unless *gate != 0. Used
   // for the overflow fallback, so the decision needs no host round trip.
   const int32_t* gate;
+  // Sample pass of a seeded search (> 1): every implicit-grid range scans only its first
+  // ceil(1/sample_div) of its tiles, so the sample is spread over the whole row range.
+  int32_t sample_div;
 };
 
 // List-capacity value selecting candidate (append) mode in launch_scan_topk.

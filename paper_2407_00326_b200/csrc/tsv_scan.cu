@@ -77,7 +77,8 @@ __device__ __forceinline__ void resolve_item(const ScanParams& p, int i, ScanIte
   const int64_t n = p.row_end - p.row_beg;
   const int64_t tiles = (n + tile_rows - 1) / tile_rows;
   const int64_t t0 = tiles * r / p.R;
-  const int64_t t1 = tiles * (r + 1) / p.R;
+  int64_t t1 = tiles * (r + 1) / p.R;
+  if (p.sample_div > 1 && t1 > t0) t1 = t0 + (t1 - t0 + p.sample_div - 1) / p.sample_div;
   it.row_begin = p.row_beg + t0 * tile_rows;
   it.row_end = min(p.row_end, p.row_beg + t1 * tile_rows);
   if (it.row_end < it.row_begin) it.row_end = it.row_begin;

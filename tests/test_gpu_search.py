@@ -444,3 +444,21 @@ def test_search_matches_pgvector_restatement(cuda, n, dim, b, k):
     sub = np.r_[0:min(b, 24)]
     pg = orc.pgvector_exact_search(q[sub], c, k, op="<#>", keep=64)
     assert_topk(from_dev(s)[sub], from_dev(i)[sub], q[sub], c, k, TOL, oracle=pg)
+
+
+def test_seeded_search_on_sorted_corpus(cuda):
+    """A corpus stored in topical order (rows sorted by their score against a direction v,
+    best last) with queries near v: the seeding sample (the first 1/16 of every range) still
+    gives an exact result equal to the unseeded search."""
+    n, dim, b, k = 300_000, 128, 256, 64
+    c = orc.make_corpus(n, dim, seed=3)
+    v = orc.make_corpus(1, dim, seed=9)[0]
+    c = c[np.argsort(c @ v, kind="stable")]
+    q = orc.normalize_rows(v[None, :] + 0.3 * orc.make_corpus(b, dim, seed=4))
+    idx = _index_from(c, cuda)
+    qd = to_dev_bf16(q, cuda)
+    s1, i1 = _search_env(idx, qd, k)
+    s2, i2 = _search_env(idx, qd, k, TSV_NO_SEED=1)
+    np.testing.assert_array_equal(i1, i2)
+    np.testing.assert_array_equal(s1, s2)
+    assert_topk(s1[:8], i1[:8], q[:8], c, k, TOL)
