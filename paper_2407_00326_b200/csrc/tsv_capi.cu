@@ -607,6 +607,7 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
     static const int kRounds[] = {4, 3, 2, 5, 6};
     for (int rounds : kRounds) {
       if (const char* e = getenv("TSV_ROUNDS")) rounds = atoi(e);
+      if (const char* e = getenv("TSV_SAMPLE_ROUNDS"); e && sample_div > 1) rounds = atoi(e);
       if (rounds >= 2 && (rounds * units) % nqg == 0 && tiles >= 8 * (rounds * units / nqg)) {
         R = rounds * units / nqg;
         range_major = true;
