@@ -23,9 +23,20 @@ from .engines import EngineProfile, EngineSet, max_efficient_batch, measured_pro
 from .index import DeviceIndex, normalize_rows
 
 
-def _time(fn, reps: int = 20, warmup: int = 3) -> float:
+def _time(fn, reps: int = 20, warmup: int = 3, min_warm_ms: float = 100.0) -> float:
+    """Mean device ms per call after `warmup` calls and at least `min_warm_ms` of warm-up
+    (a jump in load shifts the power-capped clock for some tens of ms)."""
     for _ in range(warmup):
         fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    spent = 0.0
+    while spent < min_warm_ms:
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        spent += a.elapsed_time(b)
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
