@@ -17,6 +17,15 @@ inline bool first_on_device(std::atomic<uint64_t>& mask) {
   return (mask.fetch_or(bit) & bit) == 0;
 }
 
+// Programmatic dependent launch (PDL): the merge-side kernels are launched with programmatic
+// stream serialisation, so their launch overlaps the tail of the scan before them; they wait
+// for the scan's completion (and memory) in griddepcontrol.wait. The scan CTAs allow the early
+// launch at their start.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_allow_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // Geometry of the fused scan (K1). Queries sit on the UMMA M side (one TMEM lane per query),
 // corpus rows on the N side; K is the embedding dimension, streamed 64 bf16 (one 128 B swizzle
 // row) per k-block.

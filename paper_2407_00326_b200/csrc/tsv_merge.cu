@@ -232,6 +232,7 @@ __global__ void merge_topk_kernel(const float* __restrict__ in_s, const int32_t*
                                   int dedup, const int32_t* __restrict__ gate) {
   extern __shared__ uint64_t keys[];
   __shared__ int count;
+  pdl_wait();
   if (gate != nullptr && *gate == 0) return;
   const int b = blockIdx.x;
   const int n = lists * kin;
@@ -299,6 +300,7 @@ __global__ void cand_select_kernel(const float* __restrict__ buf_s, const int32_
                                    float* __restrict__ out_s, int32_t* __restrict__ out_id,
                                    int32_t* __restrict__ overflow) {
   extern __shared__ uint64_t keys[];
+  pdl_wait();
   const int b = blockIdx.x;
   const int m = cnt[b];
   if (m > cap) {
@@ -599,6 +601,23 @@ __global__ void peer_exchange_merge_kernel(const PeerArgs a) {
   }
 }
 
+// Launch with programmatic stream serialisation (see pdl_wait in tsv_kernels.cuh).
+template <typename... KArgs, typename... Args>
+int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+               Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return static_cast<int>(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+}
+
 }  // namespace
 
 size_t peer_buffer_bytes(int world, int max_b, int max_k) {
@@ -663,9 +682,8 @@ int launch_cand_select(const float* buf_s, const int32_t* buf_i, const int32_t* 
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return static_cast<int>(e);
   }
-  cand_select_kernel<<<B, 256, smem, stream>>>(buf_s, buf_i, cnt, cap, kout, out_s, out_id,
-                                               overflow);
-  return static_cast<int>(cudaGetLastError());
+  return launch_pdl(cand_select_kernel, dim3(B), dim3(256), smem, stream, buf_s, buf_i, cnt, cap,
+                    kout, out_s, out_id, overflow);
 }
 
 int launch_merge_topk(const float* in_s, const int32_t* in_id, int lists, int B, int kin,
@@ -685,9 +703,8 @@ int launch_merge_topk(const float* in_s, const int32_t* in_id, int lists, int B,
     if (e != cudaSuccess) return static_cast<int>(e);
   }
   const int threads = np >= 1024 ? 256 : (np >= 256 ? 128 : 64);
-  merge_topk_kernel<<<B, threads, smem, stream>>>(in_s, in_id, lists, B, kin, list_stride_rows,
-                                                  kout, out_s, out_id, dedup, gate);
-  return static_cast<int>(cudaGetLastError());
+  return launch_pdl(merge_topk_kernel, dim3(B), dim3(threads), smem, stream, in_s, in_id, lists,
+                    B, kin, list_stride_rows, kout, out_s, out_id, dedup, gate);
 }
 
 int launch_rerank(const void* arena, const float* arena_hi, const float* arena_lo, int64_t nrows,

@@ -308,6 +308,7 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
   constexpr bool kSmemList = Cfg::kSmemList;
   constexpr bool kAppend = KCAP == kAppendCap;
   constexpr int kRegK = (kSmemList || kAppend) ? 1 : KCAP;
+  if (threadIdx.x == 0) pdl_allow_dependents();
   if (p.gate != nullptr && *p.gate == 0) return;
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -641,6 +642,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
   constexpr int kStages = PairStages<KCAP>::value;
   constexpr bool kAppend = KCAP == kAppendCap;
   constexpr int kRegK = (kSmemList || kAppend) ? 1 : KCAP;
+  if (threadIdx.x == 0) pdl_allow_dependents();
   if (p.gate != nullptr && *p.gate == 0) return;  // both CTAs of the pair see the same gate
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
