@@ -312,7 +312,7 @@ def test_fp32_mode_rerank(cuda):
 
 
 @pytest.mark.parametrize("n,dim,b,k", [(20000, 768, 256, 10), (4099, 72, 1, 5), (30011, 1024, 300, 50),
-                                       (1000, 384, 1030, 16)])
+                                       (1000, 384, 1030, 16), (300_000, 128, 1024, 100)])
 def test_tiled_layout_identical_to_row_major(cuda, n, dim, b, k):
     """The tiled arena (contiguous 16 KB k-block tiles) feeds the same operands to the tensor
     cores, so results are bit-identical to the row-major arena, and match the oracle."""
@@ -462,3 +462,17 @@ def test_seeded_search_on_sorted_corpus(cuda):
     np.testing.assert_array_equal(i1, i2)
     np.testing.assert_array_equal(s1, s2)
     assert_topk(s1[:8], i1[:8], q[:8], c, k, TOL)
+
+
+@pytest.mark.parametrize("n,dim,b,k", [(200_000, 128, 1024, 128), (50_000, 256, 600, 64),
+                                       (262_144, 64, 1030, 33), (300_007, 200, 130, 100)])
+def test_large_k_paths_match_oracle(cuda, n, dim, b, k):
+    """k > 32 through every path: pair kernel with shared-memory lists and range-major rounds
+    (no seeding below 262,144 rows), B not a multiple of the query group, seeded candidate mode
+    with the single-CTA kernel (B <= 128 per group) and odd row counts / dims."""
+    c = orc.make_corpus(n, dim, seed=5)
+    q, _ = orc.make_queries(c, b, seed=6)
+    idx = _index_from(c, cuda)
+    s, i = idx.search(to_dev_bf16(q, cuda), k)
+    sub = np.r_[0:12, b - 12:b]
+    assert_topk(from_dev(s)[sub], from_dev(i)[sub], q[sub], c, k, TOL)
