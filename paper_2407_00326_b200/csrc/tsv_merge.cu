@@ -341,20 +341,22 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(
 
   const int chunks = dim >> 3;  // 8 bf16 (16 B) per chunk; dim % 8 == 0 enforced by the host
   const int64_t kb_per_row = (dim + 63) >> 6;
-  // Two candidates per warp iteration with independent loads and accumulators (the gather is
-  // latency-bound: one row is only 2 KB at D=1024).
-  for (int c0 = 2 * warp; c0 < C; c0 += 2 * kWarps) {
-    int32_t id[2];
-    bool ok[2];
-    float acc[2] = {0.f, 0.f};
+  // kPer candidates per warp iteration with independent loads and accumulators: the gather is
+  // latency-bound (one row is only 1.5-2 KB), so every lane keeps kPer rows' chunks in flight.
+  constexpr int kPer = 4;
+  for (int c0 = kPer * warp; c0 < C; c0 += kPer * kWarps) {
+    int32_t id[kPer];
+    bool ok[kPer];
+    float acc[kPer];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < kPer; ++u) {
       id[u] = c0 + u < C ? cand[static_cast<int64_t>(b) * C + c0 + u] : -1;
       ok[u] = id[u] >= 0 && id[u] < nrows;  // warp-uniform
+      acc[u] = 0.f;
     }
     if (arena_hi != nullptr) {  // fp32 storage: row = hi + lo, fp32 FMA
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < kPer; ++u) {
         if (!ok[u]) continue;
         const float4* hi = reinterpret_cast<const float4*>(arena_hi + static_cast<int64_t>(id[u]) * dim);
         const float4* lo = reinterpret_cast<const float4*>(arena_lo + static_cast<int64_t>(id[u]) * dim);
@@ -368,9 +370,9 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(
         }
       }
     } else {
-      const uint4* row[2];
+      const uint4* row[kPer];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < kPer; ++u) {
         const int64_t r = ok[u] ? id[u] : 0;
         // tiled layout: 16-byte chunk ch of row r lives in k-block tile (r/128, ch/8)
         row[u] = tiled ? reinterpret_cast<const uint4*>(
@@ -380,12 +382,12 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(
 #pragma unroll 2
       for (int ch = lane; ch < chunks; ch += 32) {
         const int64_t off = tiled ? static_cast<int64_t>(ch >> 3) * 1024 + (ch & 7) : ch;
-        uint4 raw[2];
+        uint4 raw[kPer];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) raw[u] = ok[u] ? __ldg(row[u] + off) : make_uint4(0, 0, 0, 0);
+        for (int u = 0; u < kPer; ++u) raw[u] = ok[u] ? __ldg(row[u] + off) : make_uint4(0, 0, 0, 0);
         const float* qq = qv + ch * 8;
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < kPer; ++u) {
           const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw[u]);
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
@@ -397,7 +399,7 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(
       }
     }
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < kPer; ++u) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
       if (lane == 0 && ok[u]) keys[c0 + u] = make_key(acc[u], id[u]);
