@@ -540,19 +540,28 @@ int tsv_index_scan_time(tsv_index* idx, double* total_ms, int64_t* launches) {
   return TSV_OK;
 }
 
+// Variants of one search pass (the seeded k > 32 search chains several).
+struct PassOpts {
+  const float* tau0 = nullptr;    // per-query admission floor (seeded passes)
+  int list_cap = 0;               // > 0: per-range lists of list_cap < k entries (sample pass;
+                                  // the merge returns the best k of their union)
+  const int32_t* gate = nullptr;  // every launch skipped on the device unless *gate != 0
+  bool append = false;            // candidate mode (needs tau0): rows above tau0 go to
+                                  // per-query candidate rows, a select kernel writes the top
+                                  // k; an overflow sets the flag at cand_cnt[B], which the
+                                  // caller passes as the gate of a list-mode fallback pass
+  bool staged = false;            // q_dev is already the bf16 (normalised) matrix the scan reads
+  int sample_div = 0;             // > 1: every range scans only its first 1/sample_div
+};
+
 static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k,
                        int64_t row_beg, int64_t row_end, int32_t id_offset, float* scores_dev,
-                       int32_t* ids_dev, void* stream, const float* tau0, int list_cap = 0,
-                       const int32_t* gate = nullptr, bool append = false,
-                       bool staged = false, int sample_div = 0) {
-  // list_cap > 0 (sample pass of a seeded search): per-range lists of list_cap < k entries;
-  // the merge then returns the best k of the union of those lists.
-  // gate != nullptr: every launch is skipped on the device unless *gate != 0.
-  // staged: q_dev is already the bf16 (normalised for cosine) matrix the scan reads.
-  // sample_div > 1: every range scans only its first 1/sample_div (seeding sample pass).
-  // append (requires tau0): candidate mode — rows above tau0 go to per-query candidate rows and
-  // a select kernel writes the top k; a candidate row overflow sets the flag at
-  // cand_cnt[B], which the caller passes as the gate of a list-mode fallback pass.
+                       int32_t* ids_dev, void* stream, const PassOpts& o = PassOpts()) {
+  const float* tau0 = o.tau0;
+  const int list_cap = o.list_cap;
+  const int32_t* gate = o.gate;
+  const bool append = o.append, staged = o.staged;
+  const int sample_div = o.sample_div;
   if (idx == nullptr) return fail(TSV_ERR_ARGUMENT, "index is null");
   int rc = check_dtype(q_dtype);
   if (rc) return rc;
@@ -774,32 +783,42 @@ int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int
     // is a lower bound of the final k-th score (the union holds k distinct rows scoring at
     // least that much) and, with the top rows spread over many ranges, usually equal to the
     // sample's k-th best.
-    if (env_flag("TSV_SEED_CONTIG"))  // A/B: the first 1/frac of the rows instead
+    PassOpts sample_pass;
+    sample_pass.list_cap = tsv::kMaxRegK;
+    sample_pass.staged = true;
+    if (env_flag("TSV_SEED_CONTIG")) {  // A/B: the first 1/frac of the rows instead
       rc = search_impl(idx, qb, TSV_BF16, B, k, row_beg, row_beg + ((n / frac + 255) / 256) * 256,
-                       0, w.seed_s.ptr, w.seed_i.ptr, stream, nullptr, tsv::kMaxRegK, nullptr,
-                       false, true);
-    else
+                       0, w.seed_s.ptr, w.seed_i.ptr, stream, sample_pass);
+    } else {
+      sample_pass.sample_div = frac;
       rc = search_impl(idx, qb, TSV_BF16, B, k, row_beg, row_end, 0, w.seed_s.ptr, w.seed_i.ptr,
-                       stream, nullptr, tsv::kMaxRegK, nullptr, false, true, frac);
+                       stream, sample_pass);
+    }
     if (rc) return rc;
     int e = tsv::launch_seed_floor(w.seed_s.ptr, w.seed_i.ptr, B, k, w.tau0.ptr, st);
     if (e) return cuda_fail(static_cast<cudaError_t>(e), "seed floor");
     g_launches++;
+    PassOpts list_pass;  // k-entry shared-memory lists admitting only rows above tau0
+    list_pass.tau0 = w.tau0.ptr;
+    list_pass.staged = true;
     if (env_flag("TSV_NO_APPEND"))
       return search_impl(idx, qb, TSV_BF16, B, k, row_beg, row_end, id_offset, scores_dev,
-                         ids_dev, stream, w.tau0.ptr, 0, nullptr, false, true);
+                         ids_dev, stream, list_pass);
     // Main pass in candidate mode: the register-list pipeline depth (no shared-memory lists),
     // every row above tau0 appended to its query's candidate row, exact top-k selected from
     // those. If any candidate row overflowed, the device-gated list-mode pass recomputes the
     // batch (exact either way; no host round trip decides it).
+    PassOpts cand_pass = list_pass;
+    cand_pass.append = true;
     rc = search_impl(idx, qb, TSV_BF16, B, k, row_beg, row_end, id_offset, scores_dev, ids_dev,
-                     stream, w.tau0.ptr, 0, nullptr, true, true);
+                     stream, cand_pass);
     if (rc) return rc;
+    list_pass.gate = w.cand_cnt.ptr + B;
     return search_impl(idx, qb, TSV_BF16, B, k, row_beg, row_end, id_offset, scores_dev,
-                       ids_dev, stream, w.tau0.ptr, 0, w.cand_cnt.ptr + B, false, true);
+                       ids_dev, stream, list_pass);
   }
   return search_impl(idx, q_dev, q_dtype, B, k, row_beg, row_end, id_offset, scores_dev, ids_dev,
-                     stream, nullptr);
+                     stream);
 }
 
 int tsv_search_segmented(tsv_index* idx, const void* q_dev, int q_dtype, int nseg,
