@@ -484,7 +484,13 @@ def run_ours(args):
         peak_tf_sus /= 6.0
         bytes_alg = n_local * D * 8 + B * D * 4 + B * k * 8
     peak_bw = float(peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"]))
-    t_tc = flops / (peak_tf * 1e12)
+    # The timed kernels run after >= 1 s of continuous load, i.e. at the settled power-capped
+    # clock: the sustained bf16 figure is the denominator for that (MEASURED_PEAKS: "burst for a
+    # kernel timed alone, sustained for a kernel timed inside a long step"); with
+    # --min-warmup-s below 1 the burst figure is used. Both fractions are reported.
+    long_step = args.min_warmup_s >= 1.0
+    peak_tc = peak_tf_sus if long_step else peak_tf
+    t_tc = flops / (peak_tc * 1e12)
     t_bw = bytes_alg / (peak_bw * 1e9)
     traffic = None
     tf = ROOT / "profiles" / "traffic.json"
@@ -496,14 +502,15 @@ def run_ours(args):
         except (ValueError, OSError):
             traffic = None
     if t_tc >= t_bw:
-        roof = {"bound": "tensor", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
-                "frac": achieved_tf / peak_tf, "traffic": traffic,
+        roof = {"bound": "tensor", "achieved": achieved_tf, "peak": peak_tc, "unit": "TFLOP/s",
+                "frac": achieved_tf / peak_tc, "traffic": traffic,
+                "frac_of_burst": achieved_tf / peak_tf,
                 "frac_of_sustained": achieved_tf / peak_tf_sus}
     else:
         roof = {"bound": "hbm", "achieved": achieved_gbs, "peak": peak_bw, "unit": "GB/s",
                 "frac": achieved_gbs / peak_bw, "traffic": traffic}
     # the north star's per-kernel pair: both utilisations, whichever bounds
-    roof.update({"tensor_tflops": achieved_tf, "tensor_frac": achieved_tf / peak_tf,
+    roof.update({"tensor_tflops": achieved_tf, "tensor_frac": achieved_tf / peak_tc,
                  "hbm_gbs": achieved_gbs, "hbm_frac": achieved_gbs / peak_bw,
                  "corpus_bytes_frac_at_peak": achieved_gbs / peak_bw})
     roof.update({"kernel": "scan_topk_pair_kernel / scan_topk_kernel (K1, tcgen05 fused IP + "
@@ -512,7 +519,8 @@ def run_ours(args):
                  "launches_timed": scan_launches,
                  "algorithmic_flops_per_launch": flops,
                  "algorithmic_bytes_per_launch": bytes_alg,
-                 "peak_source": (f"{peak_src} (MEASURED_PEAKS.json burst bf16 / copy GB/s)"
+                 "peak_source": (f"{peak_src} (MEASURED_PEAKS.json "
+                                 f"{'sustained' if long_step else 'burst'} bf16 / copy GB/s)"
                                  if peak_src == "measured" else "fallback (B200_PROFILING.md)")
                  + (" / 6 for fp32 mode (3 tf32 MMAs at half the bf16 rate)"
                     if args.storage == "f32" else "")})
