@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <numeric>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -554,6 +555,17 @@ struct PassOpts {
   int sample_div = 0;             // > 1: every range scans only its first 1/sample_div
 };
 
+// Range lockstep (pairs scanning one corpus range for different query groups stay within a
+// few tiles of each other, so each corpus tile comes from HBM once and from L2 for the rest).
+// Measured: a clear win with up to 4 query groups (B <= 1024), a loss with 8 or 16 (every
+// pair then waits for the slowest of many partners; their drift fits in L2 anyway).
+constexpr int kMaxLockGroups = 4;
+bool lockstep_wanted(int nqg, int num_items, int units, bool range_major) {
+  if (env_flag("TSV_NO_LOCKSTEP")) return false;
+  const bool many = nqg > kMaxLockGroups && !env_flag("TSV_LOCKSTEP_ALL");
+  return nqg > 1 && !many && (num_items <= units || range_major);
+}
+
 static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k,
                        int64_t row_beg, int64_t row_end, int32_t id_offset, float* scores_dev,
                        int32_t* ids_dev, void* stream, const PassOpts& o = PassOpts()) {
@@ -611,17 +623,17 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
   bool range_major = false;
   if (pair && nqg > 1 && (units % nqg != 0 || getenv("TSV_ROUNDS")) &&
       !env_flag("TSV_NO_RANGE_MAJOR")) {
-    // preferred round counts: ~4 rounds measured best at B=1024 (finer items even out the
-    // pairs' finishing times); up to 6 so that 5 query groups also fit
-    static const int kRounds[] = {4, 3, 2, 5, 6};
-    for (int rounds : kRounds) {
-      if (const char* e = getenv("TSV_ROUNDS")) rounds = atoi(e);
-      if (const char* e = getenv("TSV_SAMPLE_ROUNDS"); e && sample_div > 1) rounds = atoi(e);
-      if (rounds >= 2 && (rounds * units) % nqg == 0 && tiles >= 8 * (rounds * units / nqg)) {
-        R = rounds * units / nqg;
-        range_major = true;
-        break;
-      }
+    // Whole rounds need nqg * R to be a multiple of the worker count: rounds must be a
+    // multiple of base = lcm(units, nqg) / units. About 4 rounds measured best at B=1024 (finer
+    // items even out the pairs' finishing times), so take the multiple of base nearest 4.
+    const int base = nqg / std::gcd(units, nqg);
+    int rounds = base * std::max(1, (4 + base / 2) / base);
+    if (const char* e = getenv("TSV_ROUNDS")) rounds = atoi(e);
+    if (const char* e = getenv("TSV_SAMPLE_ROUNDS"); e && sample_div > 1) rounds = atoi(e);
+    if (rounds >= 2 && (static_cast<int64_t>(rounds) * units) % nqg == 0 &&
+        tiles >= 8 * (static_cast<int64_t>(rounds) * units / nqg)) {
+      R = rounds * units / nqg;
+      range_major = true;
     }
   }
   if (!range_major && nqg * R < units * 97 / 100 && (2 * units) % nqg == 0) R = 2 * units / nqg;
@@ -656,8 +668,7 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
                           tsv::kFlagDiagNoQueryLoad);
 
   if (append) {
-    const bool lock =
-        nqg > 1 && (num_items <= units || range_major) && !env_flag("TSV_NO_LOCKSTEP");
+    const bool lock = lockstep_wanted(nqg, num_items, units, range_major);
     const size_t nc = lock ? static_cast<size_t>(num_items) : 0;
     rc = w.cand_s.ensure(static_cast<size_t>(B) * tsv::kCandCap);
     if (!rc) rc = w.cand_i.ensure(static_cast<size_t>(B) * tsv::kCandCap);
@@ -712,8 +723,7 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
     g_launches++;
     return TSV_OK;
   }
-  const bool lock =
-      nqg > 1 && (num_items <= units || range_major) && !env_flag("TSV_NO_LOCKSTEP");
+  const bool lock = lockstep_wanted(nqg, num_items, units, range_major);
   const bool floor = R > 1 && !env_flag("TSV_NO_FLOOR");
   if (lock || floor) {  // one zeroed buffer: [progress counters][per-query floors]
     const size_t nc = lock ? static_cast<size_t>(num_items) : 0;

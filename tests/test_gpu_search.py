@@ -413,11 +413,13 @@ def test_candidate_overflow_falls_back_exactly(cuda):
     np.testing.assert_array_equal(i1[0], np.arange(1, 2 * k, 2))
 
 
-@pytest.mark.parametrize("b,k", [(1024, 10), (768, 16), (1024, 32)])
+@pytest.mark.parametrize("b,k", [(1024, 10), (768, 16), (1024, 32), (2048, 10), (4096, 8),
+                                 (1280, 16)])
 def test_range_major_rounds_identical(cuda, b, k):
-    """B=1024 (4 query groups) and B=768 (3) do not divide the 74 CTA pairs: the pair kernel
-    then takes range-major items over 2 or 3 rounds with lockstepped range partners. The result
-    must be identical to the one-round layout and match the oracle."""
+    """B=1024 (4 query groups), 768 (3), 1280 (5), 2048 (8), 4096 (16) do not divide the 74 CTA
+    pairs: the pair kernel then takes range-major items over 3-8 rounds (lockstepped range
+    partners up to 4 query groups). The result must be identical to the one-round layout and
+    match the oracle."""
     n, dim = 200_000, 256
     c = orc.make_corpus(n, dim, seed=0)
     q, _ = orc.make_queries(c, b, seed=1)
