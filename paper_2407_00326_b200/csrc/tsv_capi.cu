@@ -555,15 +555,17 @@ struct PassOpts {
   int sample_div = 0;             // > 1: every range scans only its first 1/sample_div
 };
 
-// Range lockstep (pairs scanning one corpus range for different query groups stay within a
+// Range lockstep (workers scanning one corpus range for different query groups stay within a
 // few tiles of each other, so each corpus tile comes from HBM once and from L2 for the rest).
-// Measured: a clear win with up to 4 query groups (B <= 1024), a loss with 8 or 16 (every
-// pair then waits for the slowest of many partners; their drift fits in L2 anyway).
+// Measured: with range-major rounds (short items) a clear win up to 4 query groups
+// (B <= 1024) and a loss with 8 or 16 (every pair waits for the slowest of many partners,
+// while their drift over a short item fits in L2 anyway); with one round of long items (the
+// single-CTA fp32 mode, 8 groups of 128) it still wins (91.5-94.1 vs 98-99 ms).
 constexpr int kMaxLockGroups = 4;
 bool lockstep_wanted(int nqg, int num_items, int units, bool range_major) {
   if (env_flag("TSV_NO_LOCKSTEP")) return false;
-  const bool many = nqg > kMaxLockGroups && !env_flag("TSV_LOCKSTEP_ALL");
-  return nqg > 1 && !many && (num_items <= units || range_major);
+  if (range_major && nqg > kMaxLockGroups && !env_flag("TSV_LOCKSTEP_ALL")) return false;
+  return nqg > 1 && (num_items <= units || range_major);
 }
 
 static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k,
