@@ -553,6 +553,7 @@ struct PassOpts {
                                   // caller passes as the gate of a list-mode fallback pass
   bool staged = false;            // q_dev is already the bf16 (normalised) matrix the scan reads
   int sample_div = 0;             // > 1: every range scans only its first 1/sample_div
+  int cand_cap = 0;               // candidate-row capacity (0 = tsv::kCandCap)
 };
 
 // Range lockstep (workers scanning one corpus range for different query groups stay within a
@@ -562,6 +563,9 @@ struct PassOpts {
 // while their drift over a short item fits in L2 anyway); with one round of long items (the
 // single-CTA fp32 mode, 8 groups of 128) it still wins (91.5-94.1 vs 98-99 ms).
 constexpr int kMaxLockGroups = 4;
+// Candidate mode keeps kCandCap (score, id) slots per query (64 KB): beyond this many queries
+// per call the k > 32 search uses shared-memory lists instead.
+constexpr int kMaxCandQueries = 32768;
 bool lockstep_wanted(int nqg, int num_items, int units, bool range_major) {
   if (env_flag("TSV_NO_LOCKSTEP")) return false;
   if (range_major && nqg > kMaxLockGroups && !env_flag("TSV_LOCKSTEP_ALL")) return false;
@@ -576,6 +580,7 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
   const int32_t* gate = o.gate;
   const bool append = o.append, staged = o.staged;
   const int sample_div = o.sample_div;
+  const int cand_cap = o.cand_cap > 0 ? o.cand_cap : tsv::kCandCap;
   if (idx == nullptr) return fail(TSV_ERR_ARGUMENT, "index is null");
   int rc = check_dtype(q_dtype);
   if (rc) return rc;
@@ -672,8 +677,8 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
   if (append) {
     const bool lock = lockstep_wanted(nqg, num_items, units, range_major);
     const size_t nc = lock ? static_cast<size_t>(num_items) : 0;
-    rc = w.cand_s.ensure(static_cast<size_t>(B) * tsv::kCandCap);
-    if (!rc) rc = w.cand_i.ensure(static_cast<size_t>(B) * tsv::kCandCap);
+    rc = w.cand_s.ensure(static_cast<size_t>(B) * cand_cap);
+    if (!rc) rc = w.cand_i.ensure(static_cast<size_t>(B) * cand_cap);
     if (!rc) rc = w.cand_cnt.ensure(static_cast<size_t>(B) + 1);
     if (!rc && lock) rc = w.counter.ensure(nc);
     if (rc) return rc;
@@ -688,11 +693,11 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
     p.out_scores = w.cand_s.ptr;
     p.out_ids = w.cand_i.ptr;
     p.cand_count = w.cand_cnt.ptr;
-    p.cand_cap = tsv::kCandCap;
+    p.cand_cap = cand_cap;
     rc = run_scan(idx, mb, tsv::kAppendCap, qb, B, p, grid, st);
     if (rc) return rc;
-    int e = tsv::launch_cand_select(w.cand_s.ptr, w.cand_i.ptr, w.cand_cnt.ptr, tsv::kCandCap, B,
-                                    k, scores_dev, ids_dev, w.cand_cnt.ptr + B, st);
+    int e = tsv::launch_cand_select(w.cand_s.ptr, w.cand_i.ptr, w.cand_cnt.ptr, cand_cap, B, k,
+                                    scores_dev, ids_dev, w.cand_cnt.ptr + B, st);
     if (e) return cuda_fail(static_cast<cudaError_t>(e), "candidate select launch");
     g_launches++;
     return TSV_OK;
@@ -769,11 +774,13 @@ int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int
                void* stream) {
   // k > 32: a top-k over a 1/16 sample of the rows bounds every query's final k-th score from
   // below; the main scan then only has to keep rows above that floor (candidate mode), which
-  // keeps the result exact.
+  // keeps the result exact. Ranges of at most kCandCap rows skip the sample: every row is a
+  // candidate and no candidate row can overflow. (Shared-memory lists, the fallback, insert
+  // one candidate per warp step and are slow when many rows qualify.)
   const int kcap = tsv::scan_kcap_for(k);
   const int64_t n = row_end - row_beg;
   if (idx != nullptr && kcap > tsv::kMaxRegK && idx->storage != TSV_F32 && B > 0 &&
-      n >= 64 * 4096 && !env_flag("TSV_NO_SEED")) {
+      B <= kMaxCandQueries && n > 0 && !env_flag("TSV_NO_SEED")) {
     int frac = 16;
     if (const char* e = getenv("TSV_SEED_FRAC")) frac = std::max(2, atoi(e));
     DeviceGuard g(idx->device);
@@ -789,6 +796,14 @@ int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int
     const void* qb = nullptr;
     rc = stage_queries(idx, w, q_dev, q_dtype, B, st, &qb);
     if (rc) return rc;
+    if (n <= tsv::kCandCap) {
+      PassOpts all_rows;
+      all_rows.append = true;
+      all_rows.staged = true;
+      all_rows.cand_cap = static_cast<int>((n + 31) & ~int64_t(31));
+      return search_impl(idx, qb, TSV_BF16, B, k, row_beg, row_end, id_offset, scores_dev,
+                         ids_dev, stream, all_rows);
+    }
     // Sample pass with 32-entry register lists per corpus range, each range scanning only the
     // first 1/frac of its tiles (a sample spread over the whole row range, so a corpus stored
     // in topical order still yields a tight floor): the k-th best of the union of those lists

@@ -222,6 +222,14 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                : "memory");
 }
+// Arrive on a (possibly remote) cluster barrier with the default semantics (release at CTA
+// scope). For the TMEM hand-off from the epilogue to the MMA issuer the ordering that matters
+// is tcgen05.ld before the next MMA, which tcgen05.fence::before/after_thread_sync provide; a
+// cluster-scope release would also wait for the warp's outstanding global accesses (the
+// admission-floor load / atomic) at every tile.
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
 __device__ __forceinline__ void tmem_alloc2(uint32_t* smem_dst, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                    smem_u32(smem_dst)),

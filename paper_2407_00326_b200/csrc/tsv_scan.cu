@@ -490,14 +490,17 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
       float s[kRegK];
       int32_t id[kRegK];
       const int t_epi = quad * 32 + lane;  // row of this thread's shared-memory list
-      const float tau_floor = (p.tau0 != nullptr && lq < it.q_count) ? p.tau0[it.q_begin + lq]
-                                                                      : -FLT_MAX;
+      // Padding query rows (lq >= q_count: the last group of a batch that is not a multiple of
+      // the tile) admit nothing, so their lanes never enter the insertion paths that the
+      // real lanes of the warp would otherwise wait for.
+      const float tau_floor = lq >= it.q_count ? INFINITY
+                              : (p.tau0 != nullptr ? p.tau0[it.q_begin + lq] : -FLT_MAX);
       float tau = tau_floor;
       uint32_t* const fslot =
           (p.floor_g != nullptr && lq < it.q_count) ? p.floor_g + it.q_begin + lq : nullptr;
       float fl = tau_floor, published = -FLT_MAX;
       // append mode: admit scores above tau0 (padding query rows admit nothing)
-      const float athr = lq < it.q_count ? tau_floor : INFINITY;
+      const float athr = tau_floor;
       const int64_t qrow = static_cast<int64_t>(it.q_begin) + (lq < it.q_count ? lq : 0);
       int32_t* const ccnt = kAppend ? p.cand_count + qrow : nullptr;
       float* const cbs = kAppend ? p.out_scores + qrow * p.cand_cap : nullptr;
@@ -803,14 +806,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
       float s[kRegK];
       int32_t id[kRegK];
       const int t_epi = quad * 32 + lane;
-      const float tau_floor = (p.tau0 != nullptr && lq < it.q_count) ? p.tau0[it.q_begin + lq]
-                                                                      : -FLT_MAX;
+      // Padding query rows (lq >= q_count: the last group of a batch that is not a multiple of
+      // the tile) admit nothing, so their lanes never enter the insertion paths that the
+      // real lanes of the warp would otherwise wait for.
+      const float tau_floor = lq >= it.q_count ? INFINITY
+                              : (p.tau0 != nullptr ? p.tau0[it.q_begin + lq] : -FLT_MAX);
       float tau = tau_floor;
       uint32_t* const fslot =
           (p.floor_g != nullptr && lq < it.q_count) ? p.floor_g + it.q_begin + lq : nullptr;
       float fl = tau_floor, published = -FLT_MAX;
       // append mode: admit scores above tau0 (padding query rows admit nothing)
-      const float athr = lq < it.q_count ? tau_floor : INFINITY;
+      const float athr = tau_floor;
       const int64_t qrow = static_cast<int64_t>(it.q_begin) + (lq < it.q_count ? lq : 0);
       int32_t* const ccnt = kAppend ? p.cand_count + qrow : nullptr;
       float* const cbs = kAppend ? p.out_scores + qrow * p.cand_cap : nullptr;
@@ -860,7 +866,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
         }
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader0 + abuf * 8);
+        if (lane == 0) ptx::mbar_arrive_remote(tempty_leader0 + abuf * 8);
         if (p.floor_g != nullptr)  // warp-uniform (the smem-list variant syncs the warp)
           share_floor<KCAP, kSmemList>(fslot, fkey, s, id, list_s, list_i, t_epi, fl, tau,
                                        published);
