@@ -267,16 +267,18 @@ def pgvector_exact_search(q: np.ndarray, c: np.ndarray, k: int, op: str = "<#>",
 
 # ------------------------------------------------------------------ comparator
 def check_topk(g_s, g_i, q, c, k: int, tol: float, id_offset: int = 0, local=None,
-               oracle=None) -> list[str]:
+               oracle=None, abs_floor: float = 1e-6) -> list[str]:
     """Tolerance-aware comparison of device top-k against the exact oracle.
 
     For each rank r with oracle (o_s[r], o_id[r]) and band(r) = ids whose exact score is
-    within tol*max(|o_s[r]|, 1e-6) of o_s[r]:
-      1. |g_s[r] - o_s[r]| <= tol*max(|o_s[r]|, 1e-6);
+    within tol*max(|o_s[r]|, abs_floor) of o_s[r]:
+      1. |g_s[r] - o_s[r]| <= tol*max(|o_s[r]|, abs_floor);
       2. g_id[r] == o_id[r] when band(r) == {o_id[r]};
       3. otherwise g_id[r] in band(r);
       4. ids are distinct;
       5. the exact score of g_id[r] matches g_s[r] within tol.
+    abs_floor: scale below which the tolerance is absolute (tol * abs_floor); deep ranks of a
+    small segment score near zero, where a relative bound is meaningless.
     Returns a list of violation strings (empty = pass)."""
     g_s = np.asarray(g_s, dtype=np.float64)
     g_i = np.asarray(g_i, dtype=np.int64)
@@ -299,7 +301,7 @@ def check_topk(g_s, g_i, q, c, k: int, tol: float, id_offset: int = 0, local=Non
                 if gi >= 0:
                     problems.append(f"q{r} rank{j}: expected padding, got id {gi}")
                 continue
-            eps = tol * max(abs(os_), 1e-6)
+            eps = tol * max(abs(os_), abs_floor)
             if not abs(gs - os_) <= eps:
                 problems.append(f"q{r} rank{j}: score {gs} vs oracle {os_}")
             band = o_i[r][(np.abs(o_s[r] - os_) <= eps) & (o_i[r] >= 0)]

@@ -887,6 +887,10 @@ int tsv_search_segmented(tsv_index* idx, const void* q_dev, int q_dtype, int nse
            : stage_queries(idx, w, q_dev, q_dtype, B, st, &qb);
   if (rc) return rc;
 
+  // k > 32 with every segment at most kCandCap rows: candidate mode with every row a candidate
+  // (no lists, no overflow possible), as tsv_search does for small ranges
+  const bool append_all = !f32 && kcap > tsv::kMaxRegK && max_rows <= tsv::kCandCap &&
+                          B <= kMaxCandQueries && !env_flag("TSV_NO_SEED");
   const int mb = (!f32 && max_q > tsv::kBlockM && kcap <= tsv::kMaxRegK) ? 2 : 1;
   const int qg = mb * tsv::kBlockM;
   int units = 0;
@@ -944,6 +948,26 @@ int tsv_search_segmented(tsv_index* idx, const void* q_dev, int q_dtype, int nse
   p.num_kb = (idx->dim + kb_elems - 1) / kb_elems;
   if (tiled) p.flags |= tsv::kFlagTiled;
   const int grid = std::min(p.num_items, idx->num_sms);
+  if (append_all) {
+    const int cap = static_cast<int>((std::max<int64_t>(max_rows, 1) + 31) & ~int64_t(31));
+    rc = w.cand_s.ensure(static_cast<size_t>(B) * cap);
+    if (!rc) rc = w.cand_i.ensure(static_cast<size_t>(B) * cap);
+    if (!rc) rc = w.cand_cnt.ensure(static_cast<size_t>(B) + 1);
+    if (rc) return rc;
+    TSV_CUDA(cudaMemsetAsync(w.cand_cnt.ptr, 0, sizeof(int32_t) * (B + 1), st), "count reset");
+    p.out_k = 0;
+    p.out_scores = w.cand_s.ptr;
+    p.out_ids = w.cand_i.ptr;
+    p.cand_count = w.cand_cnt.ptr;
+    p.cand_cap = cap;
+    rc = run_scan(idx, 1, tsv::kAppendCap, qb, B, p, grid, st);
+    if (rc) return rc;
+    int e = tsv::launch_cand_select(w.cand_s.ptr, w.cand_i.ptr, w.cand_cnt.ptr, cap, B, k,
+                                    scores_dev, ids_dev, w.cand_cnt.ptr + B, st);
+    if (e) return cuda_fail(static_cast<cudaError_t>(e), "candidate select launch");
+    g_launches++;
+    return TSV_OK;
+  }
   if (R > 1 && !env_flag("TSV_NO_FLOOR")) {  // shared admission floors (see ScanParams)
     rc = w.counter.ensure(static_cast<size_t>(B));
     if (rc) return rc;

@@ -478,3 +478,41 @@ def test_large_k_paths_match_oracle(cuda, n, dim, b, k):
     s, i = idx.search(to_dev_bf16(q, cuda), k)
     sub = np.r_[0:12, b - 12:b]
     assert_topk(from_dev(s)[sub], from_dev(i)[sub], q[sub], c, k, TOL)
+
+
+@pytest.mark.parametrize("k", [33, 64, 128])
+def test_segmented_large_k_candidate_mode(cuda, k):
+    """Segmented search with k > 32 and every segment <= 8192 rows runs candidate mode (every
+    row a candidate, exact select); it must equal the shared-memory-list path bit for bit and
+    the oracle, including segments with fewer rows than k (padding)."""
+    import os
+
+    import torch
+
+    sizes = [48, 32, 64, 1, 8000, 700, 129, 256]
+    nq = [1, 3, 1, 2, 16, 4, 1, 130]
+    arena = orc.make_corpus(sum(sizes), 256, seed=12)
+    q = orc.make_corpus(sum(nq), 256, seed=13)
+    row_ranges, q_off, lo = [], [0], 0
+    for sz, m in zip(sizes, nq):
+        row_ranges.append((lo, lo + sz))
+        lo += sz
+        q_off.append(q_off[-1] + m)
+    idx = _index_from(arena, cuda)
+    qd = to_dev_bf16(q, cuda)
+    s1, i1 = idx.search_segmented(qd, q_off, row_ranges, k, local_ids=True)
+    os.environ["TSV_NO_SEED"] = "1"
+    try:
+        s2, i2 = idx.search_segmented(qd, q_off, row_ranges, k, local_ids=True)
+        torch.cuda.synchronize()
+    finally:
+        del os.environ["TSV_NO_SEED"]
+    np.testing.assert_array_equal(from_dev(i1), from_dev(i2))
+    np.testing.assert_array_equal(from_dev(s1), from_dev(s2))
+    gs, gi = from_dev(s1), from_dev(i1)
+    for sidx, (a, b) in enumerate(row_ranges):
+        qa, qb = q_off[sidx], q_off[sidx + 1]
+        # deep ranks of the small segments score ~0: absolute tolerance below 1e-2
+        probs = orc.check_topk(gs[qa:qb], gi[qa:qb], q[qa:qb], arena[a:b], k, TOL,
+                               abs_floor=1e-2)
+        assert not probs, f"segment {sidx}: {probs[:5]}"
