@@ -152,6 +152,9 @@ class ShardedSearch:
             return s_loc, i_loc
         if self.exchange == "p2p":
             if self._peer is None or self._peer.max_b < q.shape[0] or self._peer.max_k < k:
+                if self._peer is not None:  # outgrown: every rank re-creates it (same B, k)
+                    self._peer.close()
+                    self._peer = None
                 try:
                     self._peer = PeerExchange(q.device, q.shape[0], k, self.group)
                 except Exception as exc:  # no peer mapping on this node: use NCCL instead
