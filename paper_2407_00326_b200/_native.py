@@ -15,6 +15,8 @@ from pathlib import Path
 from .errors import STATUS_ERRORS, DeviceError
 
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libtsv.so"
+if os.environ.get("TSV_LIB_PATH"):  # development A/B of two builds of the same ABI
+    LIB_PATH = Path(os.environ["TSV_LIB_PATH"])
 
 TSV_BF16 = 0
 TSV_F32 = 1

@@ -330,6 +330,12 @@ __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&v)
 __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+// Compiler-ordering fence for registers written by an asynchronous tcgen05.ld: every use of v
+// must come after this point (place it right after tmem_ld_wait). Emits no instructions.
+__device__ __forceinline__ void tmem_regs_ready(uint32_t (&v)[32]) {
+#pragma unroll
+  for (int j = 0; j < 32; ++j) asm volatile("" : "+r"(v[j]));
+}
 
 // UMMA shared-memory descriptor for a K-major, 128B-swizzled operand tile whose rows are
 // 128 bytes (64 bf16 / 32 fp32) and whose 8-row core-matrix groups are 1024 B apart.

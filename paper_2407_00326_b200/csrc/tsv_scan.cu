@@ -844,25 +844,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
         ptx::tc_fence_after();
         const uint32_t taddr = lane_addr + abuf * Pair::kAccCols;
         const bool diag_nofilter = (p.flags & kFlagDiagNoFilter) != 0;
+        auto consume = [&](uint32_t (&v)[32], int col) {
+          if (diag_nofilter) return;
+          if constexpr (kAppend)
+            scan_chunk_append(v, athr, id0 + col, valid - col, ccnt, cbs, cbi, p.cand_cap);
+          else if constexpr (kSmemList)
+            scan_chunk_coop<KCAP>(v, list_s, list_i, quad * 32, lane, tau, id0 + col,
+                                  valid - col, fl);
+          else
+            scan_chunk<kRegK>(v, s, id, id0 + col, valid - col, fl);
+        };
+        // Ping-pong over 32-column chunks: the next chunk's tcgen05.ld is in flight while the
+        // current one is filtered, so the TMEM load latency is off the epilogue's critical
+        // path (it bounds the tile rate when D is small and the MMA per tile is short).
+        uint32_t va[32], vb[32];
+        ptx::tmem_ld_32x32b_x32(taddr, va);
+        ptx::tmem_ld_wait();
+        ptx::tmem_regs_ready(va);
 #pragma unroll 1
         for (int c = 0; c < Pair::kTileRows; c += 64) {
-          uint32_t va[32], vb[32];
-          ptx::tmem_ld_32x32b_x32(taddr + c, va);
           ptx::tmem_ld_32x32b_x32(taddr + c + 32, vb);
+          consume(va, c);
           ptx::tmem_ld_wait();
-          if (diag_nofilter) continue;
-          if constexpr (kAppend) {
-            scan_chunk_append(va, athr, id0 + c, valid - c, ccnt, cbs, cbi, p.cand_cap);
-            scan_chunk_append(vb, athr, id0 + c + 32, valid - c - 32, ccnt, cbs, cbi, p.cand_cap);
-          } else if constexpr (kSmemList) {
-            scan_chunk_coop<KCAP>(va, list_s, list_i, quad * 32, lane, tau, id0 + c, valid - c,
-                                  fl);
-            scan_chunk_coop<KCAP>(vb, list_s, list_i, quad * 32, lane, tau, id0 + c + 32,
-                                  valid - c - 32, fl);
-          } else {
-            scan_chunk<kRegK>(va, s, id, id0 + c, valid - c, fl);
-            scan_chunk<kRegK>(vb, s, id, id0 + c + 32, valid - c - 32, fl);
-          }
+          ptx::tmem_regs_ready(vb);
+          if (c + 64 < Pair::kTileRows) ptx::tmem_ld_32x32b_x32(taddr + c + 64, va);
+          consume(vb, c + 32);
+          ptx::tmem_ld_wait();
+          ptx::tmem_regs_ready(va);
         }
         ptx::tc_fence_before();
         __syncwarp();
