@@ -28,6 +28,16 @@ def main():
     s = torch.sort(torch.randn((8, 37, 16), generator=g, device=dev), dim=2, descending=True)[0]
     i = torch.arange(8 * 37 * 16, device=dev, dtype=torch.int32).reshape(8, 37, 16)
     merge_topk(s, i, 10)
+    # k > 32 candidate mode: every row (<= 8192 rows), seeded (sample + candidate pass + gated
+    # fallback), segmented; range-major rounds with and without lockstep (B=1024 / 2048)
+    small = DeviceIndex(256, 6000, metric="cosine", device=0)
+    small.append(torch.randn((6000, 256), generator=g, device=dev))
+    small.search(normalize_rows(torch.randn((50, 256), generator=g, device=dev)), 100)
+    big = DeviceIndex(128, 300_000, metric="cosine", device=0)
+    big.append(torch.randn((300_000, 128), generator=g, device=dev))
+    for B, k in ((1024, 100), (1024, 10), (2048, 10), (200, 64)):
+        big.search(normalize_rows(torch.randn((B, 128), generator=g, device=dev)), k)
+    idx.search_segmented(q, [0, 10, 25, 40], [(0, 48), (48, 3000), (3000, 9000)], 64)
     f32 = DeviceIndex(64, 5000, metric="ip", device=0, storage="f32")
     f32.append(torch.randn((5000, 64), generator=g, device=dev))
     f32.search(torch.randn((20, 64), generator=g, device=dev), 10)
