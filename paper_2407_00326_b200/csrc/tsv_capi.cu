@@ -672,7 +672,7 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
   if (tiled) p.flags |= tsv::kFlagTiled;
   if (const char* e = getenv("TSV_DIAG"))
     p.flags |= atoi(e) & (tsv::kFlagDiagNoFilter | tsv::kFlagDiagNoStream |
-                          tsv::kFlagDiagNoQueryLoad);
+                          tsv::kFlagDiagNoQueryLoad | tsv::kFlagDiagSetupOnly);
 
   if (append) {
     const bool lock = lockstep_wanted(nqg, num_items, units, range_major);

@@ -120,6 +120,8 @@ constexpr int kFlagDiagNoFilter = 16;
 constexpr int kFlagDiagNoStream = 32;
 // 64: query tiles are loaded for the first corpus tile only (later tiles reuse stale smem).
 constexpr int kFlagDiagNoQueryLoad = 64;
+// 128 (single-CTA kernel): set up and tear down only (no items): the launch's fixed cost.
+constexpr int kFlagDiagSetupOnly = 128;
 // Tiled arena layout: row i, element d at ((i/128 * KB + d/64) * 128 + i%128) * 64 + d%64,
 // KB = ceil(dim/64): every [128 rows x 64 elements] k-block tile is one contiguous 16 KB block.
 int launch_seed_floor(const float* s, const int32_t* id, int B, int k, float* floor_out,

@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int num_items = p.num_items;
+  const int num_items = (p.flags & kFlagDiagSetupOnly) ? 0 : p.num_items;
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer

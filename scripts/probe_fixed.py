@@ -1,4 +1,5 @@
-"""Diagnostic: fixed per-launch cost of the scan kernels (ncu --profile-from-start off)."""
+"""Diagnostic: fixed per-launch cost of the scan kernels (ncu --profile-from-start off).
+Set TSV_DIAG=128 for setup/teardown only (single-CTA kernel)."""
 import os
 import sys
 
@@ -8,17 +9,14 @@ sys.path.insert(0, os.getcwd())
 from paper_2407_00326_b200.index import DeviceIndex, normalize_rows  # noqa: E402
 
 dev = torch.device("cuda", 0)
-cases = []
-for n in (256, 25_600, 100_000):
-    idx = DeviceIndex(384, n, metric="cosine", device=0)
-    idx.append(torch.randn((n, 384), device=dev))
-    for b in (16, 256):
-        cases.append((idx, normalize_rows(torch.randn((b, 384), device=dev))))
-for idx, q in cases:
+idx = DeviceIndex(384, 256, metric="ip", device=0)   # one tile: R = 1, no merge; ip: no normalize
+idx.append(normalize_rows(torch.randn((256, 384), device=dev)))
+q = normalize_rows(torch.randn((int(os.environ.get("PROBE_B", "16")), 384), device=dev))
+for _ in range(3):
     idx.search(q, 10)
 torch.cuda.synchronize()
 torch.cuda.profiler.start()
-for idx, q in cases:
+for _ in range(3):
     idx.search(q, 10)
 torch.cuda.synchronize()
 torch.cuda.profiler.stop()
