@@ -1,4 +1,4 @@
-"""Fused peer all-gather + merge (sharded mode over NVLink): two ranks, run here as two
+"""Fused peer all-gather + merge (sharded mode over NVLink): 2 and 4 ranks, run here as
 processes sharing one GPU through CUDA IPC (the same code maps peer GPUs over NVLink on a
 node). The result must equal the unsharded search, over several calls (buffer parities)."""
 
@@ -51,12 +51,12 @@ def _worker(rank, world, port, out):
     dist.destroy_process_group()
 
 
-def test_p2p_exchange_equals_unsharded(cuda):
+@pytest.mark.parametrize("world", [2, 4])
+def test_p2p_exchange_equals_unsharded(cuda, world):
     import torch.multiprocessing as mp
 
     from oracle import oracle as orc
 
-    world = 2
     ctx = mp.get_context("spawn")
     mgr = ctx.Manager()
     out = mgr.dict()
@@ -73,4 +73,5 @@ def test_p2p_exchange_equals_unsharded(cuda):
         for r in range(world):
             s, i = out[r][call]
             assert not orc.check_topk(s, i, q, corpus, 10, 1e-3)
-        np.testing.assert_array_equal(out[0][call][1], out[1][call][1])
+        for r in range(1, world):
+            np.testing.assert_array_equal(out[0][call][1], out[r][call][1])
