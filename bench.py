@@ -305,7 +305,9 @@ def run_ours(args):
     # BENCH_DIST_BACKEND=gloo (test only): run the N>1 code path with every rank on the GPUs
     # present (ranks share a GPU when there are fewer GPUs than ranks; NCCL refuses that)
     backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
-    if backend != "nccl":
+    if backend != "nccl" or local >= torch.cuda.device_count():
+        # gloo test runs share a GPU; a launcher that gives every rank its own
+        # CUDA_VISIBLE_DEVICES shows each process one device
         local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
