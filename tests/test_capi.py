@@ -102,3 +102,40 @@ def test_missing_library_fails_loudly(tmp_path):
             _native.load(tmp_path / "nope.so")
     finally:
         _native._lib = saved
+
+
+def _build_c_example(out_dir):
+    import shutil
+    import subprocess
+
+    root = Path(__file__).resolve().parents[1]
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    cuda = Path("/usr/local/cuda")
+    exe = Path(out_dir) / "tsv_example"
+    lib = root / "paper_2407_00326_b200" / "lib"
+    cmd = [cc, "-O2", "-Wall", "-Werror", "-I", str(root / "include"), "-I", str(cuda / "include"),
+           str(root / "examples" / "tsv_example.c"), "-L", str(lib), "-ltsv",
+           "-L", str(cuda / "lib64"), "-lcudart", f"-Wl,-rpath,{lib}", "-o", str(exe)]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return exe
+
+
+def test_c_example_builds_against_the_abi(tmp_path):
+    """examples/tsv_example.c uses only include/tsv.h + libtsv.so + the CUDA runtime: the C ABI
+    is usable without Python or torch (a cgo / JNI / N-API binding links the same way)."""
+    if not (Path("/usr/local/cuda") / "include" / "cuda_runtime.h").exists():
+        pytest.skip("CUDA headers not present")
+    _build_c_example(tmp_path)
+
+
+@pytest.mark.gpu
+def test_c_example_runs(tmp_path):
+    import subprocess
+
+    exe = _build_c_example(tmp_path)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "64/64 queries found their row first" in r.stdout
