@@ -81,13 +81,18 @@ def test_k_exceeds_rows_pads(cuda):
     assert_topk(s, i, q, c, 8, TOL)
 
 
-def test_row_range_and_id_offset(cuda):
-    c = orc.make_corpus(40000, 512, seed=0)
-    q, _ = orc.make_queries(c, 200, seed=1)
+@pytest.mark.parametrize("n,b,k,lo,hi", [(40000, 200, 10, 12345, 33333),
+                                         (300_000, 1024, 10, 1001, 290_001),
+                                         (300_000, 1024, 100, 77, 299_000)])
+def test_row_range_and_id_offset(cuda, n, b, k, lo, hi):
+    """A row range that starts mid-arena (a shard of a larger corpus) with a global id offset,
+    for the one-round, range-major (B=1024) and seeded candidate (k=100) layouts."""
+    c = orc.make_corpus(n, 256, seed=0)
+    q, _ = orc.make_queries(c[lo:hi], b, seed=1)
     idx = _index_from(c, cuda)
-    lo, hi = 12345, 33333
-    s, i = idx.search(to_dev_bf16(q, cuda), 10, row_range=(lo, hi), id_offset=1_000_000 - lo)
-    assert_topk(s, i, q, c[lo:hi], 10, TOL, id_offset=1_000_000)
+    s, i = idx.search(to_dev_bf16(q, cuda), k, row_range=(lo, hi), id_offset=1_000_000 - lo)
+    sub = np.r_[0:16, b - 16:b]
+    assert_topk(from_dev(s)[sub], from_dev(i)[sub], q[sub], c[lo:hi], k, TOL, id_offset=1_000_000)
 
 
 def test_f32_queries_and_cosine(cuda):
