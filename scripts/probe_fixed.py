@@ -13,10 +13,10 @@ idx = DeviceIndex(384, 256, metric="ip", device=0)   # one tile: R = 1, no merge
 idx.append(normalize_rows(torch.randn((256, 384), device=dev)))
 q = normalize_rows(torch.randn((int(os.environ.get("PROBE_B", "16")), 384), device=dev))
 for _ in range(3):
-    idx.search(q, 10)
+    idx.search(q, int(os.environ.get("PROBE_K", "10")))
 torch.cuda.synchronize()
 torch.cuda.profiler.start()
 for _ in range(3):
-    idx.search(q, 10)
+    idx.search(q, int(os.environ.get("PROBE_K", "10")))
 torch.cuda.synchronize()
 torch.cuda.profiler.stop()
