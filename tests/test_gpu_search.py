@@ -521,3 +521,27 @@ def test_segmented_large_k_candidate_mode(cuda, k):
         probs = orc.check_topk(gs[qa:qb], gi[qa:qb], q[qa:qb], arena[a:b], k, TOL,
                                abs_floor=1e-2)
         assert not probs, f"segment {sidx}: {probs[:5]}"
+
+
+@pytest.mark.parametrize("n,dim,b,k", [(20000, 1024, 24, 10), (8000, 384, 16, 50)])
+def test_fp32_mode_matches_pgvector_cosine(cuda, n, dim, b, k):
+    """fp32 mode against the original engine's own arithmetic: pgvector stores float4 vectors
+    and `ORDER BY embedding <=> q LIMIT k` ranks by cosine distance computed in float32
+    (oracle.pgvector_exact_search). The fp32-mode index (cosine metric, raw fp32 rows in)
+    must agree at the fp32 mode's 1e-5 tolerance; the comparator's exact scores are the
+    float64 cosines of the raw vectors."""
+    import torch
+    from paper_2407_00326_b200.index import DeviceIndex
+
+    rng = np.random.default_rng(33)
+    raw = rng.standard_normal((n, dim)).astype(np.float32)
+    qraw = rng.standard_normal((b, dim)).astype(np.float32)
+    qraw[: b // 2] = raw[rng.integers(0, n, b // 2)] + 0.02 * qraw[: b // 2]
+    idx = DeviceIndex(dim, n, metric="cosine", device=cuda.index, storage="f32")
+    idx.append(torch.from_numpy(raw).to(cuda))
+    s, i = idx.search(torch.from_numpy(qraw).to(cuda), k)
+    pg = orc.pgvector_exact_search(qraw, raw, k, op="<=>", keep=64)
+    cn = raw.astype(np.float64) / np.linalg.norm(raw.astype(np.float64), axis=1, keepdims=True)
+    qn = qraw.astype(np.float64) / np.linalg.norm(qraw.astype(np.float64), axis=1, keepdims=True)
+    probs = orc.check_topk(from_dev(s), from_dev(i), qn, cn, k, 1e-5, oracle=pg)
+    assert not probs, probs[:5]
