@@ -545,3 +545,28 @@ def test_fp32_mode_matches_pgvector_cosine(cuda, n, dim, b, k):
     qn = qraw.astype(np.float64) / np.linalg.norm(qraw.astype(np.float64), axis=1, keepdims=True)
     probs = orc.check_topk(from_dev(s), from_dev(i), qn, cn, k, 1e-5, oracle=pg)
     assert not probs, probs[:5]
+
+
+def test_two_streams_share_an_index(cuda):
+    """Searches issued on two streams against one index keep separate workspaces (partial
+    lists, candidate rows, staged queries): interleaved calls return what sequential calls do."""
+    import torch
+
+    n, dim = 300_000, 128
+    c = orc.make_corpus(n, dim, seed=41)
+    idx = _index_from(c, cuda)
+    qa = to_dev_bf16(orc.make_queries(c, 1024, seed=42)[0], cuda)
+    qb = to_dev_bf16(orc.make_queries(c, 300, seed=43)[0], cuda)
+    ref_a = [from_dev(x) for x in idx.search(qa, 10)]
+    ref_b = [from_dev(x) for x in idx.search(qb, 100)]
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(cuda), torch.cuda.Stream(cuda)
+    outs = []
+    for _ in range(3):
+        outs.append((idx.search(qa, 10, stream=s1), idx.search(qb, 100, stream=s2)))
+    torch.cuda.synchronize()
+    for (a, b) in outs:
+        np.testing.assert_array_equal(from_dev(a[1]), ref_a[1])
+        np.testing.assert_array_equal(from_dev(a[0]), ref_a[0])
+        np.testing.assert_array_equal(from_dev(b[1]), ref_b[1])
+        np.testing.assert_array_equal(from_dev(b[0]), ref_b[0])
