@@ -32,7 +32,7 @@ __device__ __forceinline__ void pdl_allow_dependents() {
 constexpr int kBlockM = 128;   // queries per UMMA tile
 constexpr int kBlockN = 128;   // corpus rows per tile
 constexpr int kBlockK = 64;    // bf16 elements per k-block (128 B rows, SWIZZLE_128B)
-constexpr int kNumNonEpiWarps = 4;  // warp 0 TMA, warp 1 MMA, warp 2 TMEM alloc, warp 3 idle
+constexpr int kNumNonEpiWarps = 4;  // warp 0 TMA, warp 1 MMA, warp 2 TMEM alloc, warp 3 (pair: query TMA)
 
 // One unit of scan work: a block of up to MB*128 consecutive queries against a contiguous
 // corpus row range. Each query of the item produces one sorted partial list of KCAP

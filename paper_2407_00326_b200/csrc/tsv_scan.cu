@@ -627,12 +627,20 @@ struct Pair {
   static constexpr int kSmemBytes = kStages * kStageBytes + 256 + 1024;
 };
 
+// Operand rings of the pair kernel: the query operand (A, L2-resident) and the corpus operand
+// (B, streamed from HBM) have separate rings of 16 KB half-stages, each fed by its own producer
+// warp, so the corpus ring runs kB k-blocks ahead independently of the short-latency query ring.
 template <int KCAP>
 struct PairStages {
-  static constexpr int value =
-      KCAP > kRegListMax ? (227 * 1024 - 2048 - 128 * KCAP * 8) / Pair::kStageBytes : Pair::kStages;
-  static constexpr int smem =
-      value * Pair::kStageBytes + (KCAP > kRegListMax ? 128 * KCAP * 8 : 0) + 256 + 1024;
+  static constexpr int kListBytes = KCAP > kRegListMax ? 128 * KCAP * 8 : 0;
+  static constexpr int kBarBytes = 512;
+  static constexpr int kHalves = (227 * 1024 - 1024 - kBarBytes - kListBytes) / Pair::kHalfBytes;
+  static constexpr int kA = kHalves >= 12 ? 4 : kHalves / 2;  // query k-blocks in flight
+  static constexpr int kB = kHalves - kA;                      // corpus k-blocks in flight
+  static constexpr int value = kHalves;
+  static constexpr int smem = kHalves * Pair::kHalfBytes + kListBytes + kBarBytes + 1024;
+  static_assert(kA >= 2 && kB >= 2, "pair kernel: not enough shared memory for the rings");
+  static_assert(2 * (kA + kB) * 8 + 4 * 8 + 16 <= kBarBytes, "pair kernel: barrier area");
 };
 
 template <int KCAP>
@@ -641,8 +649,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
                           const __grid_constant__ CUtensorMap tmap_c, const ScanParams p) {
   // k > 32: warp-cooperative lists in shared memory (128 query rows x KCAP), fewer stages
   constexpr bool kSmemList = KCAP > kRegListMax;
-  constexpr int kListBytes = kSmemList ? 128 * KCAP * 8 : 0;
-  constexpr int kStages = PairStages<KCAP>::value;
+  using St = PairStages<KCAP>;
+  constexpr int kListBytes = St::kListBytes;
+  constexpr int kA = St::kA, kB = St::kB;
   constexpr bool kAppend = KCAP == kAppendCap;
   constexpr int kRegK = (kSmemList || kAppend) ? 1 : KCAP;
   if (threadIdx.x == 0) pdl_allow_dependents();
@@ -650,12 +659,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  float* list_s = reinterpret_cast<float*>(smem + kStages * Pair::kStageBytes);
+  uint8_t* ring_a = smem;                                  // kA x [128 query rows x 64]
+  uint8_t* ring_b = smem + kA * Pair::kHalfBytes;          // kB x [128 corpus rows x 64]
+  float* list_s = reinterpret_cast<float*>(smem + St::kHalves * Pair::kHalfBytes);
   int32_t* list_i = reinterpret_cast<int32_t*>(list_s + (kSmemList ? 128 * KCAP : 0));
-  uint64_t* full_bar =
-      reinterpret_cast<uint64_t*>(smem + kStages * Pair::kStageBytes + kListBytes);
-  uint64_t* empty_bar = full_bar + kStages;
-  uint64_t* tfull_bar = empty_bar + kStages;
+  uint64_t* fullA = reinterpret_cast<uint64_t*>(smem + St::kHalves * Pair::kHalfBytes + kListBytes);
+  uint64_t* emptyA = fullA + kA;
+  uint64_t* fullB = emptyA + kA;
+  uint64_t* emptyB = fullB + kB;
+  uint64_t* tfull_bar = emptyB + kB;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
 
@@ -669,9 +681,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&tmap_q);
     ptx::tma_prefetch_desc(&tmap_c);
-    for (int s = 0; s < kStages; ++s) {
-      ptx::mbar_init(&full_bar[s], 1);
-      ptx::mbar_init(&empty_bar[s], 1);
+    for (int s = 0; s < kA; ++s) {
+      ptx::mbar_init(&fullA[s], 1);
+      ptx::mbar_init(&emptyA[s], 1);
+    }
+    for (int s = 0; s < kB; ++s) {
+      ptx::mbar_init(&fullB[s], 1);
+      ptx::mbar_init(&emptyB[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tfull_bar[b], 1);
@@ -689,9 +705,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
   const int num_items = p.num_items;
 
-  if (warp == 0) {
-    // ---- TMA producer (both CTAs): own halves of A and B, completion on the leader's barrier
+  if (warp == 3) {
+    // ---- query producer (both CTAs): own half of A per k-block, completion on the leader
     const uint64_t pol_q = ptx::policy_evict_last();
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int i = pair; i < num_items; i += npairs) {
+      ScanItem it;
+      resolve_item(p, i, it, Pair::kQG, Pair::kTileRows);
+      const int64_t ntiles = (it.row_end - it.row_begin + Pair::kTileRows - 1) / Pair::kTileRows;
+      for (int64_t t = 0; t < ntiles; ++t) {
+        const bool skip_a = (p.flags & kFlagDiagNoQueryLoad) && t > 0;
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          ptx::mbar_wait(&emptyA[stage], phase ^ 1);
+          const uint32_t fb = ptx::mapa(ptx::smem_u32(&fullA[stage]), 0);
+          if (leader) ptx::mbar_arrive_expect_tx_warp(&fullA[stage], skip_a ? 0 : 2 * Pair::kHalfBytes);
+          if (!skip_a)
+            ptx::tma_load_2d_pair_warp(ring_a + stage * Pair::kHalfBytes, &tmap_q, fb, kb * kBlockK,
+                                       it.q_begin + rank * 128, pol_q);
+          if (++stage == kA) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 0) {
+    // ---- corpus producer (both CTAs): own half of B per k-block, completion on the leader
     const uint64_t pol_c = ptx::policy_evict_normal();
     int stage = 0;
     uint32_t phase = 0;
@@ -730,23 +770,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
         const int64_t tt = (p.flags & kFlagDiagNoStream) ? 0 : t;
         const int32_t row0 = static_cast<int32_t>(it.row_begin + tt * Pair::kTileRows) + rank * 128;
         for (int kb = 0; kb < p.num_kb; ++kb) {
-          ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
-          uint8_t* st = smem + stage * Pair::kStageBytes;
-          const uint32_t fb = ptx::mapa(ptx::smem_u32(&full_bar[stage]), 0);
-          const bool skip_a = (p.flags & kFlagDiagNoQueryLoad) && t > 0;
-          if (leader)
-            ptx::mbar_arrive_expect_tx_warp(&full_bar[stage],
-                                            skip_a ? Pair::kStageBytes : 2 * Pair::kStageBytes);
-          if (!skip_a)
-            ptx::tma_load_2d_pair_warp(st, &tmap_q, fb, kb * kBlockK, it.q_begin + rank * 128,
-                                       pol_q);
+          ptx::mbar_wait(&emptyB[stage], phase ^ 1);
+          uint8_t* st = ring_b + stage * Pair::kHalfBytes;
+          const uint32_t fb = ptx::mapa(ptx::smem_u32(&fullB[stage]), 0);
+          if (leader) ptx::mbar_arrive_expect_tx_warp(&fullB[stage], 2 * Pair::kHalfBytes);
           if (p.flags & kFlagTiled)
-            ptx::tma_load_3d_pair_warp(st + Pair::kHalfBytes, &tmap_c, fb, 0, 0,
-                                       (row0 >> 7) * p.num_kb + kb, pol_c);
+            ptx::tma_load_3d_pair_warp(st, &tmap_c, fb, 0, 0, (row0 >> 7) * p.num_kb + kb, pol_c);
           else
-            ptx::tma_load_2d_pair_warp(st + Pair::kHalfBytes, &tmap_c, fb, kb * kBlockK, row0,
-                                       pol_c);
-          if (++stage == kStages) {
+            ptx::tma_load_2d_pair_warp(st, &tmap_c, fb, kb * kBlockK, row0, pol_c);
+          if (++stage == kB) {
             stage = 0;
             phase ^= 1;
           }
@@ -758,9 +790,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
     // ---- MMA issuer (leader CTA only)
     if (leader) {
       constexpr uint32_t idesc = ptx::idesc_bf16_f32(256, 256);
-      const uint64_t desc0 = ptx::umma_desc_sw128(ptx::smem_u32(smem));
-      int stage = 0;
-      uint32_t phase = 0;
+      const uint64_t descA0 = ptx::umma_desc_sw128(ptx::smem_u32(ring_a));
+      const uint64_t descB0 = ptx::umma_desc_sw128(ptx::smem_u32(ring_b));
+      int sa = 0, sb = 0;
+      uint32_t pa = 0, pb = 0;
       int abuf = 0;
       uint32_t aphase = 0;
       for (int i = pair; i < num_items; i += npairs) {
@@ -772,18 +805,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
           ptx::tc_fence_after();
           const uint32_t d0 = tmem_base + abuf * Pair::kAccCols;
           for (int kb = 0; kb < p.num_kb; ++kb) {
-            ptx::mbar_wait(&full_bar[stage], phase);
+            ptx::mbar_wait(&fullA[sa], pa);
+            ptx::mbar_wait(&fullB[sb], pb);
             ptx::tc_fence_after();
-            const uint64_t sdesc = desc0 + static_cast<uint64_t>((stage * Pair::kStageBytes) >> 4);
+            const uint64_t adesc = descA0 + static_cast<uint64_t>((sa * Pair::kHalfBytes) >> 4);
+            const uint64_t bdesc = descB0 + static_cast<uint64_t>((sb * Pair::kHalfBytes) >> 4);
 #pragma unroll
             for (int k = 0; k < kBlockK / 16; ++k)
-              ptx::mma2_f16_ss_warp(d0, sdesc + 2 * k,
-                                    sdesc + static_cast<uint64_t>(Pair::kHalfBytes >> 4) + 2 * k,
-                                    idesc, (kb | k) != 0 ? 1u : 0u);
-            ptx::mma2_commit_mc_warp(&empty_bar[stage], 0x3);
-            if (++stage == kStages) {
-              stage = 0;
-              phase ^= 1;
+              ptx::mma2_f16_ss_warp(d0, adesc + 2 * k, bdesc + 2 * k, idesc,
+                                    (kb | k) != 0 ? 1u : 0u);
+            ptx::mma2_commit_mc_warp(&emptyA[sa], 0x3);
+            ptx::mma2_commit_mc_warp(&emptyB[sb], 0x3);
+            if (++sa == kA) {
+              sa = 0;
+              pa ^= 1;
+            }
+            if (++sb == kB) {
+              sb = 0;
+              pb ^= 1;
             }
           }
           ptx::mma2_commit_mc_warp(&tfull_bar[abuf], 0x3);
