@@ -637,7 +637,6 @@ struct PairStages {
   static constexpr int kHalves = (227 * 1024 - 1024 - kBarBytes - kListBytes) / Pair::kHalfBytes;
   static constexpr int kA = kHalves >= 12 ? 4 : kHalves / 2;  // query k-blocks in flight
   static constexpr int kB = kHalves - kA;                      // corpus k-blocks in flight
-  static constexpr int value = kHalves;
   static constexpr int smem = kHalves * Pair::kHalfBytes + kListBytes + kBarBytes + 1024;
   static_assert(kA >= 2 && kB >= 2, "pair kernel: not enough shared memory for the rings");
   static_assert(2 * (kA + kB) * 8 + 4 * 8 + 16 <= kBarBytes, "pair kernel: barrier area");
