@@ -47,17 +47,19 @@ def test_bench_one_gpu_line(cuda):
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_bench_ranks_sharded(cuda, world):
+@pytest.mark.parametrize("world,exchange", [(2, "p2p"), (4, "p2p"), (2, "nccl")])
+def test_bench_ranks_sharded(cuda, world, exchange):
+    """p2p: fused peer exchange + merge kernel; nccl: the collective all-gather + K4 merge path
+    (run over gloo here, since the ranks share one GPU)."""
     env = dict(os.environ, BENCH_DIST_BACKEND="gloo")
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                         "--nproc-per-node", str(world), "--master-addr", "127.0.0.1",
                         "--master-port", str(_port()), "bench.py", "--gpus", str(world),
                         "--rows", "1000000", "--steps", "4", "--warmup", "3",
-                        "--min-warmup-s", "0"], cwd=ROOT, capture_output=True,
-                       text=True, timeout=300, env=env)
+                        "--min-warmup-s", "0", "--exchange", exchange], cwd=ROOT,
+                       capture_output=True, text=True, timeout=300, env=env)
     assert r.returncode == 0, r.stderr[-2000:]
     d = _last_json(r.stdout)
     assert d["n_gpus"] == world and d["config"]["shard_rows"] == 1_000_000 // world
-    assert d["config"]["exchange"] == "p2p"
+    assert d["config"]["exchange"] == exchange
     assert d["planted_top1"] == 1.0  # global ids survive the exchange + merge
