@@ -29,6 +29,7 @@ CASES = [
     ("K1 single-CTA B=16", "10M x 1024, B=16, k=10 (HBM-bound)"),
     ("K2 segmented", "16 queries x own 48-row segment, k=32 (C5)"),
     ("K3 rerank", "256 questions x 200 candidates x 768 -> 10 (C3)"),
+    ("K1f fp32 mode", "1M x 1024 fp32 (3xTF32), B=1024, k=10"),
 ]
 
 
@@ -53,6 +54,9 @@ def run():
     q3 = normalize_rows(torch.randn((256, 768), device=dev))
     cand = torch.randint(0, 1 << 20, (256, 200), dtype=torch.int32, device=dev)
     seg_q = normalize_rows(torch.randn((16, D), device=dev))
+    f32 = DeviceIndex(D, 1 << 20, metric="cosine", device=0, storage="f32")
+    f32.append(torch.randn((1 << 20, D), device=dev))
+    qf = torch.randn((1024, D), device=dev)
 
     def one_pass():
         normalize_rows(raw)
@@ -62,6 +66,7 @@ def run():
         seg_idx.search_segmented(seg_q, list(range(17)), [(48 * s, 48 * s + 48) for s in range(16)],
                                  32)
         c3.rerank(q3, cand, 10)
+        f32.search(qf, 10)
         torch.cuda.synchronize()
 
     one_pass()
