@@ -570,3 +570,24 @@ def test_two_streams_share_an_index(cuda):
         np.testing.assert_array_equal(from_dev(a[0]), ref_a[0])
         np.testing.assert_array_equal(from_dev(b[1]), ref_b[1])
         np.testing.assert_array_equal(from_dev(b[0]), ref_b[0])
+
+
+def test_view_index_matches_arena_and_rejects_append(cuda):
+    """DeviceIndex.view wraps an existing bf16 matrix without copying: same results as an arena
+    holding the same rows (including the k > 32 path), and appends are refused."""
+    from paper_2407_00326_b200.errors import TeolaError
+    from paper_2407_00326_b200.index import DeviceIndex
+
+    c = orc.make_corpus(300_000, 128, seed=51)
+    q, _ = orc.make_queries(c, 300, seed=52)
+    rows = to_dev_bf16(c, cuda)
+    view = DeviceIndex.view(rows)
+    arena = _index_from(c, cuda)
+    qd = to_dev_bf16(q, cuda)
+    for k in (10, 64):
+        s1, i1 = _search_env(view, qd, k)
+        s2, i2 = _search_env(arena, qd, k)
+        np.testing.assert_array_equal(i1, i2)
+        np.testing.assert_array_equal(s1, s2)
+    with pytest.raises(TeolaError):
+        view.append(rows[:10])
