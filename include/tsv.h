@@ -97,7 +97,7 @@ TSV_API int tsv_index_scan_time(tsv_index* idx, double* total_ms, int64_t* launc
  * "search" (engines.py:21, graph.py:47-59). q_dev: [B, dim] (bf16 or f32). Emitted id =
  * arena row + id_offset. Outputs scores/ids [B, k]. k <= 128. k <= 32 keeps the top-k lists in
  * registers (CTA-pair kernel for B > 128). Larger k on >= 262,144 rows runs a sample pass
- * (1/16 of every range) for a per-query floor, then a candidate pass appending every row
+ * (1/32 of every range; 1/16 for k > 100) for a per-query floor, then a candidate pass appending every row
  * above the floor plus an exact select, with a device-gated shared-memory-list pass if a
  * candidate row overflows; smaller scans use the shared-memory lists directly. Exact in all
  * cases. ---- */

@@ -772,7 +772,7 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
 int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int64_t row_beg,
                int64_t row_end, int32_t id_offset, float* scores_dev, int32_t* ids_dev,
                void* stream) {
-  // k > 32: a top-k over a 1/16 sample of the rows bounds every query's final k-th score from
+  // k > 32: a top-k over a 1/32 (k > 100: 1/16) sample of the rows bounds every query's final k-th score from
   // below; the main scan then only has to keep rows above that floor (candidate mode), which
   // keeps the result exact. Ranges of at most kCandCap rows skip the sample: every row is a
   // candidate and no candidate row can overflow. (Shared-memory lists, the fallback, insert
@@ -781,10 +781,10 @@ int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int
   const int64_t n = row_end - row_beg;
   if (idx != nullptr && kcap > tsv::kMaxRegK && idx->storage != TSV_F32 && B > 0 &&
       B <= kMaxCandQueries && n > 0 && !env_flag("TSV_NO_SEED")) {
-    // Sample fraction: ~frac * k rows then clear the floor, so 1/32 for k <= 64 (<= ~2k
-    // candidates per query) and 1/16 above (<= ~2k at k = 128) keeps the candidate rows well
-    // inside kCandCap. 10M x 1024, k=64: 16.6-17.3 -> 16.1-16.2 ms at 1/32.
-    int frac = kcap <= 64 ? 32 : 16;
+    // Sample fraction: about frac * k rows then clear the floor, so 1/32 up to k = 100 (<= ~3.2k
+    // candidates per query, 2.5x inside kCandCap) and 1/16 above (~2k at k = 128). 10M x 1024:
+    // k=64 16.6-17.3 -> 16.1-16.2 ms, k=100 17.0-17.1 -> 16.6-16.7 ms at 1/32.
+    int frac = k <= 100 ? 32 : 16;
     if (const char* e = getenv("TSV_SEED_FRAC")) frac = std::max(2, atoi(e));
     DeviceGuard g(idx->device);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
