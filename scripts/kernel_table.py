@@ -23,7 +23,7 @@ CASES = [
     ("K5 normalize", "ingest 1M x 1024 fp32 rows -> L2-normalised bf16"),
     ("K1 pair k=10", "10M x 1024, B=1024, k=10 (bench config)"),
     ("K4 range merge", "74..296 ranges x 10 -> 10, B=1024"),
-    ("K1 sample + K4 + seed floor", "k=100 seeding pass (1/16 of every range)"),
+    ("K1 sample + K4 + seed floor", "k=100 seeding pass (1/32 of every range)"),
     ("K1c candidate", "10M x 1024, B=1024, k=100 main pass"),
     ("cand select", "B=1024 candidate rows -> top 100"),
     ("K1 single-CTA B=16", "10M x 1024, B=16, k=10 (HBM-bound)"),
