@@ -125,7 +125,7 @@ struct DevBuf {
 };
 
 struct Workspace {
-  DevBuf<int32_t> counter;     // dynamic-unit scheduler counter
+  DevBuf<int32_t> counter;     // lockstep progress counters + shared admission floors
   DevBuf<uint16_t> qbuf;       // bf16 staged queries
   DevBuf<float> qhi, qlo;      // fp32-mode query planes
   DevBuf<float> seed_s, tau0;  // threshold seeding for k > 32
@@ -699,34 +699,6 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
     int e = tsv::launch_cand_select(w.cand_s.ptr, w.cand_i.ptr, w.cand_cnt.ptr, cand_cap, B, k,
                                     scores_dev, ids_dev, w.cand_cnt.ptr + B, st);
     if (e) return cuda_fail(static_cast<cudaError_t>(e), "candidate select launch");
-    g_launches++;
-    return TSV_OK;
-  }
-  if (pair && nqg <= 64 && kcap <= tsv::kMaxRegK && env_flag("TSV_DYN")) {
-    // Dynamic-unit pair kernel (experimental, opt-in): every pair keeps one list per query;
-    // K4 merges the pairs. Streams the corpus from HBM once for any B, but is slower than the
-    // static range kernel today ("dynamic units").
-    const int npairs = idx->num_sms / 2;
-    const int stride = (kcap + 3) & ~3;
-    rc = w.counter.ensure(1);
-    if (rc) return rc;
-    rc = w.part_s.ensure(static_cast<size_t>(npairs) * B * stride);
-    if (rc) return rc;
-    rc = w.part_i.ensure(static_cast<size_t>(npairs) * B * stride);
-    if (rc) return rc;
-    TSV_CUDA(cudaMemsetAsync(w.counter.ptr, 0, sizeof(int32_t), st), "counter reset");
-    p.counter = w.counter.ptr;
-    p.flags = env_flag("TSV_DYN_CTA_WAITS") ? 1 : 0;
-    p.chunk = 1;
-    if (const char* e = getenv("TSV_DYN_CHUNK")) p.chunk = std::max(1, atoi(e));
-    p.out_k = stride;
-    p.out_scores = w.part_s.ptr;
-    p.out_ids = w.part_i.ptr;
-    rc = run_scan(idx, tsv::kPairDynMode, kcap, qb, B, p, 2 * npairs, st);
-    if (rc) return rc;
-    int e = tsv::launch_merge_topk(w.part_s.ptr, w.part_i.ptr, npairs, B, stride, B, k,
-                                   scores_dev, ids_dev, st);
-    if (e) return cuda_fail(static_cast<cudaError_t>(e), "merge launch");
     g_launches++;
     return TSV_OK;
   }

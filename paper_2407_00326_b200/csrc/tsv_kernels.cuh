@@ -60,12 +60,9 @@ struct ScanParams {
   int32_t out_k;      // entries written per partial row (<= KCAP)
   float* out_scores;  // [rows][out_k]
   int32_t* out_ids;
-  // dynamic-unit pair kernel: work counter (zeroed before the launch); partial / state lists
-  // are rows pair * B + query with out_k (a multiple of 4) entries each
+  // lockstep progress counters, one per item (zeroed before the launch)
   int32_t* counter;
-  int32_t flags;  // bit 0: CTA-scope (not cluster-scope) unit/accumulator barrier waits
-                  // bit 1: corpus map is the tiled layout (3-D: 64 x 128 x tiles*kblocks)
-  int32_t chunk;  // corpus tiles per dynamic unit
+  int32_t flags;  // kFlag* bits below
   // Optional per-query admission floor (k > 32 lists): a lower bound of the query's final k-th
   // score (from a sample pass); candidates at or below it can never be in the result.
   const float* tau0;
@@ -104,8 +101,6 @@ int launch_cand_select(const float* buf_s, const int32_t* buf_i, const int32_t* 
                        int B, int kout, float* out_s, int32_t* out_id, int32_t* overflow,
                        cudaStream_t stream);
 
-// `mb` argument selecting the dynamic-unit CTA-pair kernel (see tsv_scan.cu).
-constexpr int kPairDynMode = 5;
 constexpr int kFlagTiled = 2;
 constexpr int kFlagLockstep = 4;  // static pair kernel: bound drift between range partners
 // Implicit grid in range-major order (pair kernel): item i covers corpus range i / nqg for query

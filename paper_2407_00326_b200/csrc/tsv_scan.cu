@@ -618,13 +618,10 @@ struct Pair {
   static constexpr int kTileRows = 256;                 // corpus rows per pair tile (N)
   static constexpr int kQG = 256;                       // queries per pair (M)
   static constexpr int kHalfBytes = 128 * kBlockK * 2;  // 16 KB: one CTA's half of A or B
-  static constexpr int kStageBytes = 2 * kHalfBytes;    // A half + B half per CTA
-  static constexpr int kStages = 7;  // 7 x 32 KB: measured ~2% over 6 (latency hiding)
   static constexpr int kAccCols = 256;
   static constexpr int kTmemCols = 512;                 // 2 accumulator buffers
   static constexpr int kEpiWarps = 4;
   static constexpr int kThreads = (kNumNonEpiWarps + kEpiWarps) * 32;
-  static constexpr int kSmemBytes = kStages * kStageBytes + 256 + 1024;
 };
 
 // Operand rings of the pair kernel: the query operand (A, L2-resident) and the corpus operand
@@ -950,330 +947,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
   }
 }
 
-// ---------------------------------------------------------------------------------------------
-// Dynamic-unit CTA-pair kernel. Work units are (corpus tile of 256 rows, query group of 256)
-// numbered tile-major: u = tile * nqg + qg. Pairs take units from a global counter, so the
-// nqg units of one corpus tile run on different pairs at nearly the same time and the tile is
-// read from HBM once and served from L2 to the others; every pair stays busy until the corpus
-// is exhausted (no static range imbalance). Because a pair may visit any query group, each
-// (pair, query) top-k list lives in global memory (L2-resident, one row per pair per query)
-// between units: loaded into registers when the pair starts a unit of that group and stored
-// back when it ends. Those rows are the partial lists K4 merges (lists = pairs).
-//
-// Unit hand-off inside the pair: the leader's producer warp claims a unit and publishes it in
-// a 4-slot ring in both CTAs' shared memory (st.shared::cluster + remote mbarrier arrive);
-// the peer producer, the MMA warp and both CTAs' epilogues consume it from their local ring.
-constexpr int kUnitSlots = 4;
-
-__device__ __forceinline__ int64_t min_i64(int64_t a, int64_t b) { return a < b ? a : b; }
-
-__device__ __forceinline__ void st_cluster_u32(uint32_t cluster_addr, int32_t v) {
-  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
-}
-
-template <int KCAP>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
-    scan_topk_dyn_kernel(const __grid_constant__ CUtensorMap tmap_q,
-                         const __grid_constant__ CUtensorMap tmap_c, const ScanParams p) {
-  constexpr int kStages = Pair::kStages;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * Pair::kStageBytes);
-  uint64_t* empty_bar = full_bar + kStages;
-  uint64_t* tfull_bar = empty_bar + kStages;
-  uint64_t* tempty_bar = tfull_bar + 2;
-  uint64_t* ufull_bar = tempty_bar + 2;
-  uint64_t* uempty_bar = ufull_bar + kUnitSlots;
-  int32_t* unit_ring = reinterpret_cast<int32_t*>(uempty_bar + kUnitSlots);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(unit_ring + kUnitSlots);
-
-  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
-  const int lane = threadIdx.x & 31;
-  const uint32_t rank = ptx::cluster_ctarank();
-  const bool leader = rank == 0;
-  const int pair = blockIdx.x >> 1;
-  const int nqg = (p.B + Pair::kQG - 1) / Pair::kQG;
-  const int64_t nrows = p.row_end - p.row_beg;
-  const int64_t ntiles = (nrows + Pair::kTileRows - 1) / Pair::kTileRows;
-  const int chunk = p.chunk > 0 ? p.chunk : 1;
-  const int64_t nchunks = (ntiles + chunk - 1) / chunk;
-  const int64_t nunits = nchunks * nqg;
-
-  if (warp == 0 && lane == 0) {
-    ptx::tma_prefetch_desc(&tmap_q);
-    ptx::tma_prefetch_desc(&tmap_c);
-    for (int s = 0; s < kStages; ++s) {
-      ptx::mbar_init(&full_bar[s], 1);
-      ptx::mbar_init(&empty_bar[s], 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      ptx::mbar_init(&tfull_bar[b], 1);
-      ptx::mbar_init(&tempty_bar[b], 2 * Pair::kEpiWarps);
-    }
-    for (int s = 0; s < kUnitSlots; ++s) {
-      ptx::mbar_init(&ufull_bar[s], 1);
-      // leader's MMA warp + 4 epilogue warps per CTA + the peer's producer
-      ptx::mbar_init(&uempty_bar[s], 1 + 2 * Pair::kEpiWarps + 1);
-    }
-    ptx::fence_mbar_init();
-  }
-  if (warp == 2) {
-    ptx::tmem_alloc2(tmem_slot, Pair::kTmemCols);
-    ptx::tmem_relinquish2();
-  }
-  ptx::tc_fence_before();
-  ptx::cluster_sync();
-  ptx::tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-  const uint32_t uempty_leader = ptx::mapa(ptx::smem_u32(&uempty_bar[0]), 0);
-  const bool cta_waits = (p.flags & 1) != 0;
-  auto xwait = [&](uint64_t* bar, uint32_t parity) {
-    if (cta_waits)
-      ptx::mbar_wait(bar, parity);
-    else
-      ptx::mbar_wait_cluster(bar, parity);
-  };
-
-  if (warp == 0) {
-    // ---- producer: the leader claims units and publishes them; both CTAs load their halves
-    const uint64_t pol_q = ptx::policy_evict_last();
-    const uint64_t pol_c = ptx::policy_evict_normal();
-    const uint32_t ring_peer = ptx::mapa(ptx::smem_u32(unit_ring), 1);
-    const uint32_t ufull_peer = ptx::mapa(ptx::smem_u32(ufull_bar), 1);
-    int stage = 0, uslot = 0;
-    uint32_t phase = 0, uphase = 0;
-    // The leader claims one unit ahead, so the atomic's round trip overlaps the TMA issue of
-    // the current unit instead of sitting between units.
-    int32_t next_claim = 0;
-    if (leader && lane == 0) next_claim = atomicAdd(p.counter, 1);
-    while (true) {
-      int32_t u;
-      if (leader) {
-        xwait(&uempty_bar[uslot], uphase ^ 1);
-        int32_t claimed = __shfl_sync(0xffffffffu, next_claim, 0);
-        if (lane == 0 && claimed < nunits) next_claim = atomicAdd(p.counter, 1);
-        u = claimed < nunits ? claimed : -1;
-        if (lane == 0) {
-          unit_ring[uslot] = u;
-          st_cluster_u32(ring_peer + uslot * 4, u);
-          ptx::mbar_arrive(&ufull_bar[uslot]);
-          ptx::mbar_arrive_cluster(ufull_peer + uslot * 8);
-        }
-        __syncwarp();
-      } else {
-        xwait(&ufull_bar[uslot], uphase);
-        u = unit_ring[uslot];
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive_cluster(uempty_leader + uslot * 8);
-      }
-      if (++uslot == kUnitSlots) {
-        uslot = 0;
-        uphase ^= 1;
-      }
-      if (u < 0) break;
-      const int qg = u % nqg;
-      const int64_t t_end = min_i64(ntiles, (u / nqg + 1) * chunk);
-      const int32_t q0 = qg * Pair::kQG + rank * 128;
-      for (int64_t tile = (u / nqg) * chunk; tile < t_end; ++tile) {
-      const int32_t row0 = static_cast<int32_t>(p.row_beg + tile * Pair::kTileRows) + rank * 128;
-      for (int kb = 0; kb < p.num_kb; ++kb) {
-        ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
-        uint8_t* st = smem + stage * Pair::kStageBytes;
-        const uint32_t fb = ptx::mapa(ptx::smem_u32(&full_bar[stage]), 0);
-        if (leader) ptx::mbar_arrive_expect_tx_warp(&full_bar[stage], 2 * Pair::kStageBytes);
-        ptx::tma_load_2d_pair_warp(st, &tmap_q, fb, kb * kBlockK, q0, pol_q);
-        if (p.flags & kFlagTiled)
-          ptx::tma_load_3d_pair_warp(st + Pair::kHalfBytes, &tmap_c, fb, 0, 0,
-                                     (row0 >> 7) * p.num_kb + kb, pol_c);
-        else
-          ptx::tma_load_2d_pair_warp(st + Pair::kHalfBytes, &tmap_c, fb, kb * kBlockK, row0, pol_c);
-        if (++stage == kStages) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
-      }
-    }
-  } else if (warp == 1) {
-    // ---- MMA issuer (leader only)
-    if (leader) {
-      constexpr uint32_t idesc = ptx::idesc_bf16_f32(256, 256);
-      const uint64_t desc0 = ptx::umma_desc_sw128(ptx::smem_u32(smem));
-      int stage = 0, abuf = 0, uslot = 0;
-      uint32_t phase = 0, aphase = 0, uphase = 0;
-      while (true) {
-        xwait(&ufull_bar[uslot], uphase);
-        const int32_t u = unit_ring[uslot];
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&uempty_bar[uslot]);
-        if (++uslot == kUnitSlots) {
-          uslot = 0;
-          uphase ^= 1;
-        }
-        if (u < 0) break;
-        const int64_t t_end = min_i64(ntiles, (u / nqg + 1) * chunk);
-        for (int64_t tile = (u / nqg) * chunk; tile < t_end; ++tile) {
-        xwait(&tempty_bar[abuf], aphase ^ 1);
-        ptx::tc_fence_after();
-        const uint32_t d0 = tmem_base + abuf * Pair::kAccCols;
-        for (int kb = 0; kb < p.num_kb; ++kb) {
-          ptx::mbar_wait(&full_bar[stage], phase);
-          ptx::tc_fence_after();
-          const uint64_t sdesc = desc0 + static_cast<uint64_t>((stage * Pair::kStageBytes) >> 4);
-#pragma unroll
-          for (int k = 0; k < kBlockK / 16; ++k)
-            ptx::mma2_f16_ss_warp(d0, sdesc + 2 * k,
-                                  sdesc + static_cast<uint64_t>(Pair::kHalfBytes >> 4) + 2 * k,
-                                  idesc, (kb | k) != 0 ? 1u : 0u);
-          ptx::mma2_commit_mc_warp(&empty_bar[stage], 0x3);
-          if (++stage == kStages) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-        ptx::mma2_commit_mc_warp(&tfull_bar[abuf], 0x3);
-        abuf ^= 1;
-        if (abuf == 0) aphase ^= 1;
-        }
-      }
-    }
-  } else if (warp >= kNumNonEpiWarps) {
-    // ---- epilogue (both CTAs): one query per thread, list swapped in/out per unit
-    const int quad = warp & 3;
-    const int lq = static_cast<int>(rank) * 128 + quad * 32 + lane;
-    const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
-    const uint32_t tempty_leader0 = ptx::mapa(ptx::smem_u32(&tempty_bar[0]), 0);
-    const int stride = p.out_k;  // >= KCAP, multiple of 4
-    float* const sbase = p.out_scores + static_cast<int64_t>(pair) * p.B * stride;
-    int32_t* const ibase = p.out_ids + static_cast<int64_t>(pair) * p.B * stride;
-    uint64_t touched = 0;
-    int cur_qg = -1;
-    float s[KCAP];
-    int32_t id[KCAP];
-    int abuf = 0, uslot = 0;
-    uint32_t aphase = 0, uphase = 0;
-
-    auto store_list = [&](int qg) {
-      const int q = qg * Pair::kQG + lq;
-      if (q < p.B) {
-        float* os = sbase + static_cast<int64_t>(q) * stride;
-        int32_t* oi = ibase + static_cast<int64_t>(q) * stride;
-#pragma unroll
-        for (int j = 0; j < KCAP; ++j) {
-          os[j] = s[j];
-          oi[j] = id[j];
-        }
-      }
-    };
-
-    while (true) {
-      xwait(&ufull_bar[uslot], uphase);
-      const int32_t u = unit_ring[uslot];
-      const int cur_slot = uslot;
-      if (++uslot == kUnitSlots) {
-        uslot = 0;
-        uphase ^= 1;
-      }
-      if (u < 0) break;
-      const int qg = u % nqg;
-      if (qg != cur_qg) {
-        if (cur_qg >= 0) store_list(cur_qg);
-        const int q = qg * Pair::kQG + lq;
-        if (((touched >> qg) & 1ull) && q < p.B) {
-          const float* ls = sbase + static_cast<int64_t>(q) * stride;
-          const int32_t* li = ibase + static_cast<int64_t>(q) * stride;
-#pragma unroll
-          for (int j = 0; j < KCAP; ++j) {
-            s[j] = ls[j];
-            id[j] = li[j];
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < KCAP; ++j) {
-            s[j] = -FLT_MAX;
-            id[j] = -1;
-          }
-        }
-        touched |= 1ull << qg;
-        cur_qg = qg;
-      }
-      const int64_t t_end = min_i64(ntiles, (u / nqg + 1) * chunk);
-      for (int64_t tile = (u / nqg) * chunk; tile < t_end; ++tile) {
-      const int64_t row0 = p.row_beg + tile * Pair::kTileRows;
-      const int valid = static_cast<int>(
-          p.row_end - row0 < Pair::kTileRows ? p.row_end - row0 : Pair::kTileRows);
-      const int32_t id0 = static_cast<int32_t>(row0) + p.id_offset;
-      ptx::mbar_wait(&tfull_bar[abuf], aphase);
-      ptx::tc_fence_after();
-      const uint32_t taddr = lane_addr + abuf * Pair::kAccCols;
-#pragma unroll 1
-      for (int c = 0; c < Pair::kTileRows; c += 64) {
-        uint32_t va[32], vb[32];
-        ptx::tmem_ld_32x32b_x32(taddr + c, va);
-        ptx::tmem_ld_32x32b_x32(taddr + c + 32, vb);
-        ptx::tmem_ld_wait();
-        scan_chunk<KCAP>(va, s, id, id0 + c, valid - c, -FLT_MAX);
-        scan_chunk<KCAP>(vb, s, id, id0 + c + 32, valid - c - 32, -FLT_MAX);
-      }
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader0 + abuf * 8);
-      abuf ^= 1;
-      if (abuf == 0) aphase ^= 1;
-      }
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_cluster(uempty_leader + cur_slot * 8);
-    }
-    if (cur_qg >= 0) store_list(cur_qg);
-    // lists of this pair: sort order (score desc, id asc) is kept by list_insert; padding
-    // entries become (-inf, -1); groups this pair never visited are all padding
-    for (int qg = 0; qg < nqg; ++qg) {
-      const int q = qg * Pair::kQG + lq;
-      if (q >= p.B) continue;
-      float* os = sbase + static_cast<int64_t>(q) * stride;
-      int32_t* oi = ibase + static_cast<int64_t>(q) * stride;
-      const bool seen = (touched >> qg) & 1ull;
-      for (int j = 0; j < stride; ++j) {
-        const int32_t v = (seen && j < KCAP) ? oi[j] : -1;
-        oi[j] = v;
-        os[j] = v < 0 ? -INFINITY : os[j];
-      }
-    }
-  }
-
-  ptx::tc_fence_before();
-  ptx::cluster_sync();
-  if (warp == 2) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc2(tmem_base, Pair::kTmemCols);
-  }
-}
-
-template <int KCAP>
-int launch_dyn_impl(const CUtensorMap& tq, const CUtensorMap& tc, const ScanParams& p, int grid,
-                    cudaStream_t stream) {
-  auto kern = scan_topk_dyn_kernel<KCAP>;
-  constexpr int smem = Pair::kSmemBytes + 256;
-  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (err != cudaSuccess) return static_cast<int>(err);
-  kern<<<grid, Pair::kThreads, smem, stream>>>(tq, tc, p);
-  return static_cast<int>(cudaGetLastError());
-}
-
-int dispatch_dyn(int kcap, const CUtensorMap& tq, const CUtensorMap& tc, const ScanParams& p,
-                 int grid, cudaStream_t stream) {
-  switch (kcap) {
-    case 1: return launch_dyn_impl<1>(tq, tc, p, grid, stream);
-    case 4: return launch_dyn_impl<4>(tq, tc, p, grid, stream);
-    case 8: return launch_dyn_impl<8>(tq, tc, p, grid, stream);
-    case 10: return launch_dyn_impl<10>(tq, tc, p, grid, stream);
-    case 16: return launch_dyn_impl<16>(tq, tc, p, grid, stream);
-    case 32: return launch_dyn_impl<32>(tq, tc, p, grid, stream);
-    default: return static_cast<int>(cudaErrorInvalidValue);
-  }
-}
-
 template <int KCAP>
 int launch_pair_impl(const CUtensorMap& tq, const CUtensorMap& tc, const ScanParams& p, int grid,
                      cudaStream_t stream) {
@@ -1380,7 +1053,6 @@ int launch_scan_topk(int mb, int kcap, const CUtensorMap& tmap_q, const CUtensor
   if (mb == 2) return dispatch_kcap<2>(kcap, tmap_q, tmap_c, p, grid, stream);
   if (mb == 1) return dispatch_kcap<1>(kcap, tmap_q, tmap_c, p, grid, stream);
   if (mb == kPairMode) return dispatch_pair(kcap, tmap_q, tmap_c, p, grid, stream);
-  if (mb == kPairDynMode) return dispatch_dyn(kcap, tmap_q, tmap_c, p, grid, stream);
   return static_cast<int>(cudaErrorInvalidValue);
 }
 
