@@ -77,8 +77,8 @@ class ClockSampler:
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
-        self.index = index
+    def __init__(self, index):
+        self.index = index  # CUDA ordinal, or the GPU UUID (robust to CUDA_VISIBLE_DEVICES)
         self.rows: list[list[str]] = []
         self.first = 0  # rows before this index were sampled before the timed region
         self.proc = None
@@ -382,7 +382,11 @@ def run_ours(args):
     # The clock sampler starts before the warm-up, so the timed blocks follow the warm-up with
     # no idle gap (an idle pause would hand the first block burst clocks); only samples taken
     # inside the timed region are reported.
-    clocks = ClockSampler(local)
+    try:  # nvidia-smi numbers GPUs physically; the UUID names this process's device exactly
+        smi_id = "GPU-" + str(torch.cuda.get_device_properties(dev).uuid)
+    except Exception:  # noqa: BLE001
+        smi_id = local
+    clocks = ClockSampler(smi_id)
     clocks.start()
     for _ in range(args.warmup):
         step(q_dev)
