@@ -4,8 +4,9 @@
 Workload (BASELINE.json metric, config C4 at k=10): B=1024 queries per step against a
 10,000,000 x 1024 bf16 corpus (cosine = inner product over L2-normalised rows), top-10 per
 query. With --gpus N the corpus is sharded N ways (strong scaling: total work fixed); each
-rank runs the fused scan + top-k (K1) and the range merge (K4) on its shard, the per-rank
-top-k lists are all-gathered over NCCL and merged again (K4). One step = one batch of B
+rank runs the fused scan + top-k (K1) and the range merge (K4) on its shard, and the per-rank
+top-k lists are exchanged and merged by one kernel that pushes them into the peers' buffers
+over NVLink (K6; --exchange nccl: NCCL all-gather + K4 instead). One step = one batch of B
 queries through that path.
 
 value : queries/s with queries already resident in HBM (device time, max over ranks).
