@@ -221,6 +221,7 @@ int check_dtype(int dt) {
 
 constexpr int kMergeCap = 16384;  // candidates per query the merge kernel sorts in smem
 constexpr int kMinTilesPerRange = 1;
+constexpr int64_t kWideMinRows = 1 << 19;  // scans shorter than this keep 128-row tiles (TSV_WIDE=0/1 forces)
 
 bool env_flag(const char* name) {
   const char* v = getenv(name);
@@ -280,7 +281,7 @@ int run_scan(tsv_index* idx, int mb, int kcap, const void* qb, int64_t B, tsv::S
   // One query group of fewer than 128 queries: load only its rows (TMA out-of-bounds fill of
   // the rest of a 128-row box costs as much as real rows and halves the HBM-bound scan rate).
   // (Segmented searches set a_rows from their largest query group before the call.)
-  if (p.a_rows == 0 && mb == 1 && p.items == nullptr && B < tsv::kBlockM &&
+  if (p.a_rows == 0 && (mb == 1 || mb == tsv::kWideMode) && p.items == nullptr && B < tsv::kBlockM &&
       !getenv("TSV_FULL_QBOX"))
     p.a_rows = static_cast<int>((B + 7) & ~7);
   if (getenv("TSV_FULL_QBOX")) p.a_rows = 0;
@@ -614,12 +615,19 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
   // B > 128: CTA-pair kernel (256 queries x 256 rows per pair tile); otherwise one CTA per
   // 128-query group with 128-row tiles.
   const bool pair = !f32 && B > tsv::kBlockM && !env_flag("TSV_NO_PAIR");
-  const int mb = pair ? tsv::kPairMode : 1;
+  const int64_t n = row_end - row_beg;
+  // 96 < B <= 128 on long scans with register lists: 256-row corpus tiles (M=128 x N=256 MMAs;
+  // the query operand is re-read from L2 once per 256 corpus rows instead of 128). ~3% at
+  // 10M x 1024, B=128, where the scan runs at the power cap; even at B <= 96 and in
+  // candidate mode, so those keep 128-row tiles.
+  bool wide = !pair && !f32 && B > 96 && n >= kWideMinRows && kcap <= tsv::kMaxRegK && !append;
+  if (const char* e = getenv("TSV_WIDE")) wide = !pair && !f32 && atoi(e) != 0 &&
+                                                 (kcap <= tsv::kMaxRegK || append);
+  const int mb = pair ? tsv::kPairMode : (wide ? tsv::kWideMode : 1);
   const int qg = pair ? tsv::kPairQG : tsv::kBlockM;
-  const int tile_rows = pair ? tsv::kPairTileRows : tsv::kBlockN;
+  const int tile_rows = pair ? tsv::kPairTileRows : (wide ? tsv::kWideTileRows : tsv::kBlockN);
   const int units = pair ? idx->num_sms / 2 : idx->num_sms;  // concurrent workers
   const int nqg = (B + qg - 1) / qg;
-  const int64_t n = row_end - row_beg;
   const int64_t tiles = std::max<int64_t>(1, (n + tile_rows - 1) / tile_rows);
   // Ranges per query group: one round over all workers when nqg divides them. Otherwise the
   // pair kernel takes its items in range-major order over whole rounds (nqg * R a multiple of

@@ -135,6 +135,10 @@ int launch_scatter_tiled(const void* src, int src_is_f32, int64_t n, int dim, in
 constexpr int kPairMode = 4;
 constexpr int kPairQG = 256;
 constexpr int kPairTileRows = 256;
+// `mb` selecting the single-CTA kernel with 256-row corpus tiles (M=128 x N=256 per MMA; k <= 32
+// or candidate append; 128 queries per group).
+constexpr int kWideMode = 5;
+constexpr int kWideTileRows = 256;
 
 // Host-side launchers (return cudaError_t as int).
 int launch_scan_topk(int mb, int kcap, const CUtensorMap& tmap_q, const CUtensorMap& tmap_c,

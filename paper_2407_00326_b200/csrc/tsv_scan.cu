@@ -31,22 +31,26 @@ constexpr int kRegListMax = 32;
 
 // TF32 = fp32 mode (K1f): operands are fp32 (hi, lo) splits, 32 elements per 128-byte k-block
 // row, three kind::tf32 MMAs per k-step (hi*hi + hi*lo + lo*hi).
-template <int MB, int KCAP = 1, bool TF32 = false>
+// NB = 2 (wide tile): M=128 queries x N=256 corpus rows per MMA, for 64 < B <= 128 on long
+// scans: the query operand is re-read from L2 once per 256 corpus rows instead of per 128.
+template <int MB, int KCAP = 1, bool TF32 = false, int NB = 1>
 struct ScanCfg {
+  static constexpr int kTileN = NB * kBlockN;                      // corpus rows per tile
   static constexpr bool kSmemList = KCAP > kRegListMax;
   static constexpr int kParts = TF32 ? 2 : 1;                      // hi (+ lo) planes
   static constexpr int kABytes = kBlockM * 128;                    // 16 KB per plane tile
-  static constexpr int kBBytes = kBlockN * 128;                    // 16 KB per plane tile
+  static constexpr int kBBytes = kTileN * 128;                     // 16 (32) KB per plane tile
   static constexpr int kStageBytes = kParts * (MB * kABytes + kBBytes);
   static constexpr int kListBytes = kSmemList ? kBlockM * KCAP * 8 : 0;
   static constexpr int kStages =
-      (kSmemList || TF32) ? (227 * 1024 - 2048 - kListBytes) / kStageBytes : (MB == 2 ? 4 : 7);
+      (kSmemList || TF32 || NB > 1) ? (227 * 1024 - 2048 - kListBytes) / kStageBytes
+                                    : (MB == 2 ? 4 : 7);
   // fp32 mode keeps three accumulators per tile (hi*hi of even k-blocks, of odd k-blocks, and
   // the small hi*lo + lo*hi terms): the tensor core accumulates with truncation, so fewer
   // additions per accumulator keep the sum within 1e-5; they are added (round-to-nearest) in
   // the epilogue. That needs 384 columns, so fp32 mode runs single-buffered.
   static constexpr int kAccBufs = TF32 ? 1 : 2;
-  static constexpr int kAccCols = TF32 ? 3 * kBlockN : MB * kBlockN;  // per accumulator buffer
+  static constexpr int kAccCols = TF32 ? 3 * kBlockN : MB * kTileN;  // per accumulator buffer
   static constexpr int kTmemCols = TF32 ? 512 : 2 * kAccCols;
   static constexpr int kEpiWarps = MB * 4;
   static constexpr int kThreads = (kNumNonEpiWarps + kEpiWarps) * 32;
@@ -54,6 +58,7 @@ struct ScanCfg {
   static constexpr int kSmemBytes = kStages * kStageBytes + kListBytes + kBarBytes + 1024;
   static_assert(!kSmemList || MB == 1, "shared-memory lists need one query tile per CTA");
   static_assert(!TF32 || MB == 1, "fp32 mode uses one query tile per CTA");
+  static_assert(NB == 1 || (MB == 1 && !TF32 && !kSmemList), "wide tiles: one query tile, bf16");
   static_assert(kStages >= 2, "not enough shared memory for the pipeline");
 };
 
@@ -295,13 +300,14 @@ __device__ __forceinline__ void share_floor(uint32_t* fslot, uint32_t fkey, cons
   }
 }
 
-template <int MB, int KCAP, bool TF32>
-__global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
+template <int MB, int KCAP, bool TF32, int NB>
+__global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32, NB>::kThreads, 1)
     scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_q,
                      const __grid_constant__ CUtensorMap tmap_c,
                      const __grid_constant__ CUtensorMap tmap_q_lo,
                      const __grid_constant__ CUtensorMap tmap_c_lo, const ScanParams p) {
-  using Cfg = ScanCfg<MB, KCAP, TF32>;
+  using Cfg = ScanCfg<MB, KCAP, TF32, NB>;
+  constexpr int kTileN = Cfg::kTileN;
   constexpr int kElemsPerKb = TF32 ? 32 : kBlockK;  // elements per 128-byte k-block row
   constexpr int kStages = Cfg::kStages;
   constexpr int kQG = MB * kBlockM;
@@ -368,8 +374,8 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
                                   : static_cast<uint32_t>(Cfg::kStageBytes);
     for (int i = blockIdx.x; i < num_items; i += gridDim.x) {
       ScanItem it;
-      resolve_item(p, i, it, kQG);
-      const int64_t ntiles = (it.row_end - it.row_begin + kBlockN - 1) / kBlockN;
+      resolve_item(p, i, it, kQG, kTileN);
+      const int64_t ntiles = (it.row_end - it.row_begin + kTileN - 1) / kTileN;
       const int my_qg = p.R > 0 ? i / p.R : 0, my_r = p.R > 0 ? i - my_qg * p.R : 0;
       const int nqg = p.R > 0 ? num_items / p.R : 1;
       for (int64_t t = 0; t < ntiles; ++t) {
@@ -382,7 +388,7 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
           }
         }
         __syncwarp();
-        const int32_t row0 = static_cast<int32_t>(it.row_begin + t * kBlockN);
+        const int32_t row0 = static_cast<int32_t>(it.row_begin + t * kTileN);
         for (int kb = 0; kb < p.num_kb; ++kb) {
           ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* st = smem + stage * Cfg::kStageBytes;
@@ -391,12 +397,16 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
           for (int mb = 0; mb < MB; ++mb)
             ptx::tma_load_2d_warp(st + mb * Cfg::kABytes, &tmap_q, &full_bar[stage],
                                   kb * kElemsPerKb, it.q_begin + mb * kBlockM, pol_q);
-          if (p.flags & kFlagTiled)  // row0 is a multiple of 128 in the tiled layout
-            ptx::tma_load_3d_warp(st + MB * Cfg::kABytes, &tmap_c, &full_bar[stage], 0, 0,
-                                  (row0 >> 7) * p.num_kb + kb, pol_c);
-          else
-            ptx::tma_load_2d_warp(st + MB * Cfg::kABytes, &tmap_c, &full_bar[stage],
-                                  kb * kElemsPerKb, row0, pol_c);
+#pragma unroll
+          for (int h = 0; h < NB; ++h) {  // 128-row corpus boxes, stacked along N
+            uint8_t* dst = st + MB * Cfg::kABytes + h * (kBlockN * 128);
+            if (p.flags & kFlagTiled)  // row0 is a multiple of 128 in the tiled layout
+              ptx::tma_load_3d_warp(dst, &tmap_c, &full_bar[stage], 0, 0,
+                                    ((row0 >> 7) + h) * p.num_kb + kb, pol_c);
+            else
+              ptx::tma_load_2d_warp(dst, &tmap_c, &full_bar[stage], kb * kElemsPerKb,
+                                    row0 + h * kBlockN, pol_c);
+          }
           if constexpr (TF32) {  // lo planes follow the hi planes in the stage
             uint8_t* lo = st + MB * Cfg::kABytes + Cfg::kBBytes;
             ptx::tma_load_2d_warp(lo, &tmap_q_lo, &full_bar[stage], kb * kElemsPerKb,
@@ -415,7 +425,7 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     // Warp-uniform loop; descriptors are built from the smem base plus compile-time offsets.
-    constexpr uint32_t idesc = ptx::idesc_bf16_f32(kBlockM, kBlockN);
+    constexpr uint32_t idesc = ptx::idesc_bf16_f32(kBlockM, kTileN);
     constexpr uint32_t idesc_tf32 = ptx::idesc_tf32_f32(kBlockM, kBlockN);
     const uint64_t desc0 = ptx::umma_desc_sw128(ptx::smem_u32(smem));
     int stage = 0;
@@ -424,8 +434,8 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
     uint32_t aphase = 0;
     for (int i = blockIdx.x; i < num_items; i += gridDim.x) {
       ScanItem it;
-      resolve_item(p, i, it, kQG);
-      const int64_t ntiles = (it.row_end - it.row_begin + kBlockN - 1) / kBlockN;
+      resolve_item(p, i, it, kQG, kTileN);
+      const int64_t ntiles = (it.row_end - it.row_begin + kTileN - 1) / kTileN;
       for (int64_t t = 0; t < ntiles; ++t) {
         ptx::mbar_wait(&tempty_bar[abuf], aphase ^ 1);
         ptx::tc_fence_after();
@@ -455,7 +465,7 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
           for (int k = 0; k < kBlockK / 16; ++k) {
 #pragma unroll
             for (int mb = 0; mb < MB; ++mb) {
-              ptx::mma_f16_ss_warp(d0 + mb * kBlockN,
+              ptx::mma_f16_ss_warp(d0 + mb * kTileN,
                                    sdesc + static_cast<uint64_t>((mb * Cfg::kABytes) >> 4) + 2 * k,
                                    sdesc + static_cast<uint64_t>((MB * Cfg::kABytes) >> 4) + 2 * k,
                                    idesc, (kb | k) != 0 ? 1u : 0u);
@@ -481,12 +491,12 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
     const int quad = warp & 3;          // TMEM lane quadrant this warp may access
     const int mb = e >> 2;              // which query tile of the group
     const int lq = mb * kBlockM + quad * 32 + lane;  // local query index within the item
-    const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + mb * kBlockN;
+    const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + mb * kTileN;
     int abuf = 0;
     uint32_t aphase = 0;
     for (int i = blockIdx.x; i < num_items; i += gridDim.x) {
       ScanItem it;
-      resolve_item(p, i, it, kQG);
+      resolve_item(p, i, it, kQG, kTileN);
       float s[kRegK];
       int32_t id[kRegK];
       const int t_epi = quad * 32 + lane;  // row of this thread's shared-memory list
@@ -517,10 +527,10 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
         }
         __syncwarp();
       }
-      const int64_t ntiles = (it.row_end - it.row_begin + kBlockN - 1) / kBlockN;
+      const int64_t ntiles = (it.row_end - it.row_begin + kTileN - 1) / kTileN;
       for (int64_t t = 0; t < ntiles; ++t) {
-        const int64_t row0 = it.row_begin + t * kBlockN;
-        const int valid = static_cast<int>(it.row_end - row0 < kBlockN ? it.row_end - row0 : kBlockN);
+        const int64_t row0 = it.row_begin + t * kTileN;
+        const int valid = static_cast<int>(it.row_end - row0 < kTileN ? it.row_end - row0 : kTileN);
         const int32_t id0 = static_cast<int32_t>(row0) + it.id_offset;
         const uint32_t fkey = fslot != nullptr ? floor_load(fslot) : 0u;  // used after this tile
         ptx::mbar_wait(&tfull_bar[abuf], aphase);
@@ -548,7 +558,7 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32>::kThreads, 1)
           }
         } else {
 #pragma unroll 1
-        for (int c = 0; c < kBlockN; c += 64) {
+        for (int c = 0; c < kTileN; c += 64) {
           uint32_t va[32], vb[32];
           ptx::tmem_ld_32x32b_x32(taddr + c, va);
           ptx::tmem_ld_32x32b_x32(taddr + c + 32, vb);
@@ -961,12 +971,12 @@ int launch_pair_impl(const CUtensorMap& tq, const CUtensorMap& tc, const ScanPar
   return static_cast<int>(cudaGetLastError());
 }
 
-template <int MB, int KCAP, bool TF32 = false>
+template <int MB, int KCAP, bool TF32 = false, int NB = 1>
 int launch_impl(const CUtensorMap& tq, const CUtensorMap& tc, const ScanParams& p, int grid,
                 cudaStream_t stream, const CUtensorMap* tq_lo = nullptr,
                 const CUtensorMap* tc_lo = nullptr) {
-  using Cfg = ScanCfg<MB, KCAP, TF32>;
-  auto kern = scan_topk_kernel<MB, KCAP, TF32>;
+  using Cfg = ScanCfg<MB, KCAP, TF32, NB>;
+  auto kern = scan_topk_kernel<MB, KCAP, TF32, NB>;
   static std::atomic<uint64_t> configured{0};  // per instantiation and device
   if (first_on_device(configured)) {
     cudaError_t err =
@@ -997,6 +1007,20 @@ int dispatch_kcap(int kcap, const CUtensorMap& tq, const CUtensorMap& tc, const 
     case 128:
       if constexpr (MB == 1) return launch_impl<1, 128>(tq, tc, p, grid, stream);
       return static_cast<int>(cudaErrorInvalidValue);
+    default: return static_cast<int>(cudaErrorInvalidValue);
+  }
+}
+
+int dispatch_wide(int kcap, const CUtensorMap& tq, const CUtensorMap& tc, const ScanParams& p,
+                  int grid, cudaStream_t stream) {
+  switch (kcap) {
+    case kAppendCap: return launch_impl<1, kAppendCap, false, 2>(tq, tc, p, grid, stream);
+    case 1: return launch_impl<1, 1, false, 2>(tq, tc, p, grid, stream);
+    case 4: return launch_impl<1, 4, false, 2>(tq, tc, p, grid, stream);
+    case 8: return launch_impl<1, 8, false, 2>(tq, tc, p, grid, stream);
+    case 10: return launch_impl<1, 10, false, 2>(tq, tc, p, grid, stream);
+    case 16: return launch_impl<1, 16, false, 2>(tq, tc, p, grid, stream);
+    case 32: return launch_impl<1, 32, false, 2>(tq, tc, p, grid, stream);
     default: return static_cast<int>(cudaErrorInvalidValue);
   }
 }
@@ -1050,6 +1074,7 @@ int launch_scan_topk_tf32(int kcap, const CUtensorMap& tmap_q, const CUtensorMap
 int launch_scan_topk(int mb, int kcap, const CUtensorMap& tmap_q, const CUtensorMap& tmap_c,
                      const ScanParams& p, int grid, cudaStream_t stream) {
   if (grid <= 0) return 0;
+  if (mb == kWideMode) return dispatch_wide(kcap, tmap_q, tmap_c, p, grid, stream);
   if (mb == 2) return dispatch_kcap<2>(kcap, tmap_q, tmap_c, p, grid, stream);
   if (mb == 1) return dispatch_kcap<1>(kcap, tmap_q, tmap_c, p, grid, stream);
   if (mb == kPairMode) return dispatch_pair(kcap, tmap_q, tmap_c, p, grid, stream);

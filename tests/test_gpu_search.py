@@ -357,7 +357,7 @@ def test_tiled_segmented_requires_aligned_segments(cuda):
         tl.search_segmented(to_dev_bf16(q, cuda), [0, 3], [(5, 300)], 7)
 
 
-def _search_env(idx, qd, k, **env):
+def _search_env(idx, qd, k, row_range=None, **env):
     import os
 
     import torch
@@ -365,7 +365,7 @@ def _search_env(idx, qd, k, **env):
     old = {key: os.environ.get(key) for key in env}
     os.environ.update({key: str(v) for key, v in env.items()})
     try:
-        s, i = idx.search(qd, k)
+        s, i = idx.search(qd, k) if row_range is None else idx.search(qd, k, row_range=row_range)
         torch.cuda.synchronize()
     finally:
         for key, v in old.items():
@@ -591,3 +591,21 @@ def test_view_index_matches_arena_and_rejects_append(cuda):
         np.testing.assert_array_equal(s1, s2)
     with pytest.raises(TeolaError):
         view.append(rows[:10])
+
+
+@pytest.mark.parametrize("n,dim,b,k,lo", [(600_000, 128, 128, 10, 0), (524_416, 256, 100, 32, 0),
+                                          (40_000, 768, 128, 16, 1000), (1003, 64, 120, 4, 5)])
+def test_wide_tiles_identical(cuda, n, dim, b, k, lo):
+    """96 < B <= 128 on long scans uses 256-row corpus tiles (M=128 x N=256 MMAs); TSV_WIDE=1
+    forces them on short scans too (ragged last tile, odd row ranges). Results must equal the
+    128-row tiles' bit for bit and match the oracle."""
+    c = orc.make_corpus(n, dim, seed=0)
+    q, _ = orc.make_queries(c, b, seed=1)
+    idx = _index_from(c, cuda)
+    qd = to_dev_bf16(q, cuda)
+    s1, i1 = _search_env(idx, qd, k, row_range=(lo, n), TSV_WIDE=1)
+    s2, i2 = _search_env(idx, qd, k, row_range=(lo, n), TSV_WIDE=0)
+    np.testing.assert_array_equal(i1, i2)
+    np.testing.assert_array_equal(s1, s2)
+    sub = np.r_[0:8, b - 8:b]
+    assert_topk(s1[sub], i1[sub], q[sub], c[lo:], k, TOL, id_offset=lo)
