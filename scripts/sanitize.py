@@ -3,6 +3,7 @@
 
     compute-sanitizer --tool memcheck python scripts/sanitize.py
 """
+import os
 import sys
 from pathlib import Path
 
@@ -21,6 +22,10 @@ def main():
     for B, k in ((1, 5), (100, 10), (300, 10), (64, 100)):
         q = normalize_rows(torch.randn((B, 256), generator=g, device=dev))
         idx.search(q, k)
+    os.environ["TSV_WIDE"] = "1"  # 256-row corpus tiles (single-CTA kernel, 96 < B <= 128)
+    idx.search(normalize_rows(torch.randn((120, 256), generator=g, device=dev)), 16,
+               row_range=(77, 40_000))
+    del os.environ["TSV_WIDE"]
     q = normalize_rows(torch.randn((40, 256), generator=g, device=dev))
     idx.search_segmented(q, [0, 10, 25, 40], [(0, 48), (48, 3000), (3000, 40_000)], 8)
     cand = torch.randint(0, 40_000, (4, 200), generator=g, device=dev, dtype=torch.int32)
