@@ -171,6 +171,32 @@ def test_rerank_fewer_distinct_than_k_pads(cuda):
     assert gi[1, 2] == -1 and set(gi[1, :2].tolist()) == {1, 2}
 
 
+@pytest.mark.parametrize("n,dim,b,c,k", [(5000, 768, 64, 200, 10), (3000, 1024, 16, 32, 3),
+                                         (2000, 64, 5, 7, 7), (4000, 4096, 3, 50, 10),
+                                         (1000, 384, 300, 33, 5)])
+def test_rerank_shapes_match_oracle(cuda, n, dim, b, c, k):
+    """K3 over candidate counts below, at and above one gather iteration (40 rows per block),
+    dims below and above 1024 (the unrolled chunk loop), invalid ids and duplicates."""
+    import torch
+
+    rng = np.random.default_rng(3)
+    arena = orc.make_corpus(n, dim, seed=0)
+    qs = orc.make_corpus(b, dim, seed=7)
+    cand = rng.integers(0, n, size=(b, c)).astype(np.int32)
+    cand[::3, 0] = -1
+    cand[::4, c - 1] = n + 5
+    if c > 4:
+        cand[:, 2] = cand[:, 1]
+    idx = _index_from(arena, cuda)
+    s, i = idx.rerank(to_dev_bf16(qs, cuda), torch.from_numpy(cand).to(cuda), k)
+    exp_s, exp_i = orc.rerank(qs, arena, cand, k)
+    np.testing.assert_allclose(from_dev(s), exp_s, rtol=TOL, atol=1e-6)
+    gi = from_dev(i)
+    for r in range(b):
+        got = [x for x in gi[r].tolist() if x >= 0]
+        assert len(got) == len(set(got))
+
+
 def test_merge_matches_oracle(cuda):
     import torch
     from paper_2407_00326_b200.index import merge_topk
