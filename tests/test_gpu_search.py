@@ -635,3 +635,63 @@ def test_wide_tiles_identical(cuda, n, dim, b, k, lo):
     np.testing.assert_array_equal(s1, s2)
     sub = np.r_[0:8, b - 8:b]
     assert_topk(s1[sub], i1[sub], q[sub], c[lo:], k, TOL, id_offset=lo)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("k", [10, 100])
+def test_headline_full_size_exact(cuda, k):
+    """The bench configuration at full size (10M x 1024 bf16, B=1024; k=10 and C4's k=100):
+    every query's list sorted with distinct ids, planted rows found first, every returned score
+    equal to an fp32 re-scoring of its row, and 64 queries (32 planted, 32 fresh) identical to
+    an exact fp32 torch search over all 10M rows (same scores within 2e-5; same ids wherever
+    neighbouring exact scores differ by more than that)."""
+    import torch
+
+    from paper_2407_00326_b200.index import DeviceIndex, normalize_rows
+
+    n, dim, b = 10_000_000, 1024, 1024
+    g = torch.Generator(device=cuda).manual_seed(0)
+    idx = DeviceIndex(dim, n, metric="cosine", device=cuda.index)
+    for a in range(0, n, 1 << 20):
+        idx.append(torch.randn((min(1 << 20, n - a), dim), generator=g, device=cuda))
+    rows = idx.data()
+    planted = torch.randint(0, n, (b // 2,), generator=g, device=cuda)
+    q = torch.empty((b, dim), dtype=torch.bfloat16, device=cuda)
+    q[: b // 2] = rows[planted]
+    q[b // 2:] = normalize_rows(torch.randn((b // 2, dim), generator=g, device=cuda))
+    s, i = idx.search(q, k)
+    torch.cuda.synchronize()
+    assert bool((s[:, 1:] <= s[:, :-1]).all())
+    srt = torch.sort(i, dim=1).values
+    assert bool((srt[:, 1:] != srt[:, :-1]).all())
+    top1_ok = (i[: b // 2, 0] == planted.to(torch.int32)) | (s[: b // 2, 0] == s[: b // 2, 1])
+    assert bool(top1_ok.all())
+    resc = torch.einsum("bd,bkd->bk", q.float(), rows[i.long()].float())
+    assert float((resc - s).abs().max()) < 2e-5
+
+    sub = torch.cat([torch.arange(0, 32), torch.arange(b - 32, b)]).to(cuda)
+    qs = q[sub].float()
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        best_s, best_i = None, None
+        for a in range(0, n, 1 << 20):
+            sc = qs @ rows[a: a + (1 << 20)].float().T
+            ts, ti = torch.topk(sc, k, dim=1)
+            ti = ti + a
+            if best_s is None:
+                best_s, best_i = ts, ti
+            else:
+                cs, ci = torch.cat([best_s, ts], 1), torch.cat([best_i, ti], 1)
+                best_s, o = torch.topk(cs, k, dim=1)
+                best_i = torch.gather(ci, 1, o)
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    gs, gi = s[sub], i[sub].long()
+    assert float((gs - best_s).abs().max()) < 2e-5
+    gap_prev = torch.cat([torch.full_like(best_s[:, :1], float("inf")),
+                          best_s[:, :-1] - best_s[:, 1:]], 1)
+    gap_next = torch.cat([best_s[:, :-1] - best_s[:, 1:],
+                          torch.full_like(best_s[:, :1], float("inf"))], 1)
+    sep = (gap_prev > 2e-5) & (gap_next > 2e-5)
+    assert bool((gi[sep] == best_i[sep]).all())
