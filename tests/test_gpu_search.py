@@ -695,3 +695,22 @@ def test_headline_full_size_exact(cuda, k):
                           torch.full_like(best_s[:, :1], float("inf"))], 1)
     sep = (gap_prev > 2e-5) & (gap_next > 2e-5)
     assert bool((gi[sep] == best_i[sep]).all())
+
+
+@pytest.mark.parametrize("n,lo", [(600_000, 0), (70_001, 256), (3000, 128)])
+def test_wide_tiles_on_tiled_arena(cuda, n, lo):
+    """256-row corpus tiles over the tiled arena (two 128-row k-block tiles per step, the
+    second one past the end for a ragged last tile) equal the row-major 128-row-tile result."""
+    from paper_2407_00326_b200.index import DeviceIndex
+
+    dim, b, k = 256, 120, 10
+    c = orc.make_corpus(n, dim, seed=0)
+    q, _ = orc.make_queries(c, b, seed=1)
+    rm = _index_from(c, cuda)
+    tl = DeviceIndex(dim, n, device=cuda.index, storage="bf16_tiled")
+    tl.append(to_dev_bf16(c, cuda))
+    qd = to_dev_bf16(q, cuda)
+    s1, i1 = _search_env(tl, qd, k, row_range=(lo, n), TSV_WIDE=1)
+    s2, i2 = _search_env(rm, qd, k, row_range=(lo, n), TSV_WIDE=0)
+    np.testing.assert_array_equal(i1, i2)
+    np.testing.assert_array_equal(s1, s2)
