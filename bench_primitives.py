@@ -156,10 +156,15 @@ def c3(args, dev, peaks, threads):
     ms_s = dev_time(search, args.reps)
     ms_r = dev_time(rerank, args.reps)
     ms_both = dev_time(lambda: (search(), rerank()), args.reps)
+    from paper_2407_00326_b200.launcher import CapturedRetrieval
+
+    chain = CapturedRetrieval(idx, Bq, E, k_s, k_r)
+    ms_graph = dev_time(lambda: chain.run(qx, qq), args.reps)
     cpu_ms, m = cpu_search_ms(qx, idx.data(), k_s, 50_000, threads)
     return {"config": "C3 primitive: 256 questions x 4 queries x top-50 over 1M x 768, "
                       "Aggregate 200 -> rerank 200 -> 10 (dedup)",
             "search_ms": ms_s, "rerank_ms": ms_r, "device_ms": ms_both,
+            "device_ms_cuda_graph": ms_graph,
             "questions_per_s": Bq / (ms_both * 1e-3),
             "search_roofline": roof(2.0 * Bq * E * N * D, N * D * 2, ms_s, peaks),
             "rerank_roofline": roof(2.0 * Bq * C * D, Bq * C * D * 2, ms_r, peaks),

@@ -203,15 +203,19 @@ class DeviceIndex:
         return scores, ids
 
     def rerank(self, q: torch.Tensor, cand_ids: torch.Tensor, k: int,
-               stream: torch.cuda.Stream | None = None):
+               stream: torch.cuda.Stream | None = None,
+               out: tuple[torch.Tensor, torch.Tensor] | None = None):
         """Score cand_ids[b, :] (arena rows) against q[b]; dedup ids; keep the best k."""
         self._check_queries(q)
         _require_cuda(cand_ids, "cand_ids")
         if cand_ids.dtype != torch.int32 or cand_ids.dim() != 2 or cand_ids.shape[0] != q.shape[0]:
             raise ConfigParse("cand_ids must be int32 [B, C]")
         B, C = cand_ids.shape
-        scores = torch.empty((B, k), dtype=torch.float32, device=self.device)
-        ids = torch.empty((B, k), dtype=torch.int32, device=self.device)
+        if out is None:
+            scores = torch.empty((B, k), dtype=torch.float32, device=self.device)
+            ids = torch.empty((B, k), dtype=torch.int32, device=self.device)
+        else:
+            scores, ids = out
         nat.check(nat.load().tsv_rerank(self._h, q.data_ptr(), _dtype_code(q), B,
                                         cand_ids.data_ptr(), C, int(k), scores.data_ptr(),
                                         ids.data_ptr(), _stream_handle(stream, self.device)))

@@ -156,3 +156,51 @@ class CapturedSearch:
         self.q.copy_(q)
         self.graph.replay()
         return self.scores, self.ids
+
+
+class CapturedRetrieval:
+    """The advanced-RAG retrieval chain captured in one CUDA graph: Searching
+    over `questions * expansions` expanded queries (top-k_search each), the Aggregate join of a
+    question's expansions (a view: candidates in slice order, optimizer.py:620-661) and
+    Reranking of those candidates against the question (dedup, top-k_rerank;
+    optimizer.py:199-218). One graph replay replaces the chain's 6-8 kernel launches (k > 32
+    search: sample pass, merges, candidate pass, select, gated fallback; K3) and their host
+    issue cost.
+
+    run(qx, qq) copies the expanded queries [questions * expansions, dim] and the questions
+    [questions, dim] into the captured buffers and replays; returns the reranked (scores, ids)
+    buffers (valid until the next call). The graph owns a private stream, so its per-stream
+    workspace in the index is not shared with other callers."""
+
+    def __init__(self, index, questions: int, expansions: int, k_search: int, k_rerank: int,
+                 dtype=torch.bfloat16, warmup: int = 2):
+        self.index = index
+        dev = index.device
+        self.questions, self.expansions = questions, expansions
+        self.k_search, self.k_rerank = k_search, k_rerank
+        self.qx = torch.zeros((questions * expansions, index.dim), dtype=dtype, device=dev)
+        self.qq = torch.zeros((questions, index.dim), dtype=dtype, device=dev)
+        self.s_s = torch.empty((questions * expansions, k_search), dtype=torch.float32, device=dev)
+        self.s_i = torch.empty((questions * expansions, k_search), dtype=torch.int32, device=dev)
+        self.r_s = torch.empty((questions, k_rerank), dtype=torch.float32, device=dev)
+        self.r_i = torch.empty((questions, k_rerank), dtype=torch.int32, device=dev)
+        stream = torch.cuda.Stream(dev)
+        with torch.cuda.stream(stream):
+            for _ in range(warmup):  # grows the per-stream workspace before capture
+                self._run(stream)
+        stream.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=stream, capture_error_mode="thread_local"):
+            self._run(torch.cuda.current_stream(dev))
+
+    def _run(self, stream):
+        self.index.search(self.qx, self.k_search, stream=stream, out=(self.s_s, self.s_i))
+        cand = self.s_i.view(self.questions, self.expansions * self.k_search)  # Aggregate
+        self.index.rerank(self.qq, cand, self.k_rerank, stream=stream, out=(self.r_s, self.r_i))
+
+    def run(self, qx: torch.Tensor, qq: torch.Tensor):
+        self.qx.copy_(qx)
+        self.qq.copy_(qq)
+        self.graph.replay()
+        return self.r_s, self.r_i
+

@@ -58,3 +58,33 @@ def test_captured_search_replays_exactly(cuda):
         torch.cuda.synchronize()
         np.testing.assert_array_equal(from_dev(i), from_dev(ei))
         np.testing.assert_array_equal(from_dev(s), from_dev(es))
+
+
+@pytest.mark.parametrize("metric,k_search,n", [("cosine", 50, 300_000), ("ip", 10, 40_000)])
+def test_captured_retrieval_chain_replays_exactly(cuda, metric, k_search, n):
+    """Search (k=50: sample pass + candidate mode; k=10: register lists) -> Aggregate -> rerank
+    captured in one CUDA graph equals the same primitives called one by one, and the reranked
+    lists match the oracle on the aggregated candidates."""
+    import torch
+    from paper_2407_00326_b200.index import DeviceIndex
+    from paper_2407_00326_b200.launcher import CapturedRetrieval
+
+    dim, nq, e, k_r = 256, 24, 4, 10
+    c = orc.make_corpus(n, dim, seed=0)
+    idx = DeviceIndex(dim, n, metric=metric, device=cuda.index)
+    idx.append(to_dev_bf16(c, cuda))
+    cap = CapturedRetrieval(idx, nq, e, k_search, k_r)
+    for seed in (1, 2):
+        qx, _ = orc.make_queries(c, nq * e, seed=seed)
+        qq, _ = orc.make_queries(c, nq, seed=seed + 10)
+        qxd, qqd = to_dev_bf16(qx, cuda), to_dev_bf16(qq, cuda)
+        rs, ri = cap.run(qxd, qqd)
+        ss, si = idx.search(qxd, k_search)
+        es, ei = idx.rerank(qqd, si.view(nq, e * k_search), k_r)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(from_dev(ri), from_dev(ei))
+        np.testing.assert_array_equal(from_dev(rs), from_dev(es))
+        if metric == "ip":  # (cosine re-normalises the stored rows)
+            cand = from_dev(si).reshape(nq, e * k_search)
+            exp_s, _ = orc.rerank(qq, c, cand, k_r)
+            np.testing.assert_allclose(from_dev(rs), exp_s, rtol=1e-3, atol=1e-6)
