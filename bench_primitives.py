@@ -211,9 +211,15 @@ def c5(args, dev, peaks, threads):
     search()
     ms_s = dev_time(search, args.reps)
     ms_r = dev_time(rerank, args.reps)
+    ms_both = dev_time(lambda: (search(), rerank()), args.reps)
+    from paper_2407_00326_b200.launcher import CapturedContextual
+
+    chain = CapturedContextual(idx, offs, ranges, k, k_r)
+    ms_graph = dev_time(lambda: chain.run(q), args.reps)
     return {"config": "C5 primitive: 16 queries, each top-32 over its own 48-row segment "
                       "(one segmented launch), rerank 32 -> 3",
-            "search_ms": ms_s, "rerank_ms": ms_r,
+            "search_ms": ms_s, "rerank_ms": ms_r, "chain_ms": ms_both,
+            "chain_ms_cuda_graph": ms_graph,
             "note": "launch / latency bound (98 KB per segment)",
             "simulated_reference_ms": {"search": simulated("vdb-search0", nq),
                                        "rerank": simulated("rerank0", 32)}}

@@ -147,12 +147,22 @@ struct Workspace {
     cudaEvent_t done = nullptr;
   } pinned[kPinnedSlots];
   int pinned_next = 0;
+  // Item tables uploaded by CUDA graphs captured on this stream: the captured memcpy node
+  // reads its host source at every replay, so each capture takes a region of this pinned pool
+  // (allocated by the first segmented search outside capture; pinned allocation is not
+  // permitted while a stream captures) and keeps it for the workspace's lifetime.
+  static constexpr size_t kCapturePoolBytes = 1 << 20;
+  uint8_t* capture_pool = nullptr;
+  size_t capture_used = 0;
   void release() {
     for (auto& s : pinned) {
       if (s.ptr) cudaFreeHost(s.ptr);
       if (s.done) cudaEventDestroy(s.done);
       s = Pinned{};
     }
+    if (capture_pool) cudaFreeHost(capture_pool);
+    capture_pool = nullptr;
+    capture_used = 0;
     counter.release();
     qbuf.release();
     qhi.release();
@@ -905,6 +915,26 @@ int tsv_search_segmented(tsv_index* idx, const void* q_dev, int q_dtype, int nse
   }
   rc = w.items.ensure(hi.size());
   if (rc) return rc;
+  cudaStreamCaptureStatus capturing = cudaStreamCaptureStatusNone;
+  TSV_CUDA(cudaStreamIsCapturing(st, &capturing), "cudaStreamIsCapturing");
+  if (capturing != cudaStreamCaptureStatusNone) {
+    // Inside a CUDA-graph capture the upload becomes a memcpy node that reads its host source
+    // at every replay: give it a region of the capture pool that is never reused.
+    const size_t bytes = (hi.size() * sizeof(tsv::ScanItem) + 255) & ~size_t(255);
+    if (w.capture_pool == nullptr || w.capture_used + bytes > Workspace::kCapturePoolBytes)
+      return fail(TSV_ERR_CAPACITY,
+                  "segmented search under graph capture: run it once on this stream outside "
+                  "the capture first (pinned pool %s)",
+                  w.capture_pool == nullptr ? "not allocated" : "exhausted");
+    uint8_t* hp = w.capture_pool + w.capture_used;
+    w.capture_used += bytes;
+    std::memcpy(hp, hi.data(), hi.size() * sizeof(tsv::ScanItem));
+    TSV_CUDA(cudaMemcpyAsync(w.items.ptr, hp, hi.size() * sizeof(tsv::ScanItem),
+                             cudaMemcpyHostToDevice, st),
+             "items upload (graph capture)");
+  } else {
+  if (w.capture_pool == nullptr)
+    TSV_CUDA(cudaMallocHost(&w.capture_pool, Workspace::kCapturePoolBytes), "cudaMallocHost");
   Workspace::Pinned& slot = w.pinned[w.pinned_next];
   w.pinned_next = (w.pinned_next + 1) % Workspace::kPinnedSlots;
   if (slot.done == nullptr)
@@ -922,6 +952,7 @@ int tsv_search_segmented(tsv_index* idx, const void* q_dev, int q_dtype, int nse
                            cudaMemcpyHostToDevice, st),
            "items upload");
   TSV_CUDA(cudaEventRecord(slot.done, st), "cudaEventRecord");
+  }
   tsv::ScanParams p{};
   p.items = w.items.ptr;
   p.num_items = static_cast<int>(hi.size());

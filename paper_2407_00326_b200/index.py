@@ -181,7 +181,8 @@ class DeviceIndex:
 
     def search_segmented(self, q: torch.Tensor, q_offsets: Sequence[int],
                          row_ranges: Sequence[tuple[int, int]], k: int, local_ids: bool = True,
-                         stream: torch.cuda.Stream | None = None):
+                         stream: torch.cuda.Stream | None = None,
+                         out: tuple[torch.Tensor, torch.Tensor] | None = None):
         """Queries q[q_offsets[s]:q_offsets[s+1]] search only arena rows row_ranges[s]."""
         self._check_queries(q)
         nseg = len(row_ranges)
@@ -193,8 +194,11 @@ class DeviceIndex:
         rb = (ctypes.c_int64 * nseg)(*[int(a) for a, _ in row_ranges])
         re = (ctypes.c_int64 * nseg)(*[int(b) for _, b in row_ranges])
         B = q.shape[0]
-        scores = torch.empty((B, k), dtype=torch.float32, device=self.device)
-        ids = torch.empty((B, k), dtype=torch.int32, device=self.device)
+        if out is None:
+            scores = torch.empty((B, k), dtype=torch.float32, device=self.device)
+            ids = torch.empty((B, k), dtype=torch.int32, device=self.device)
+        else:
+            scores, ids = out
         nat.check(nat.load().tsv_search_segmented(
             self._h, q.data_ptr(), _dtype_code(q), nseg, ctypes.cast(qo, ctypes.c_void_p),
             ctypes.cast(rb, ctypes.c_void_p), ctypes.cast(re, ctypes.c_void_p), int(k),

@@ -204,3 +204,46 @@ class CapturedRetrieval:
         self.graph.replay()
         return self.r_s, self.r_i
 
+
+class CapturedContextual:
+    """The contextual-retrieval chain captured in one CUDA graph: each query
+    searches its own per-query index segment (segmented Searching, top-k_search; the
+    per-query indexes of workloads.py:95-97 built by each query's Ingestion) and its hits are
+    reranked against it (Reranking, dedup, top-k_rerank). Segment layout is fixed at capture
+    (the item list the graph uploads lives in a pinned buffer owned by the index).
+
+    run(q) copies the queries into the captured buffer and replays; returns the reranked
+    (scores, ids) buffers, ids being arena rows (valid until the next call)."""
+
+    def __init__(self, index, q_offsets, row_ranges, k_search: int, k_rerank: int,
+                 dtype=torch.bfloat16, warmup: int = 2):
+        self.index = index
+        dev = index.device
+        b = int(q_offsets[-1])
+        self.q_offsets, self.row_ranges = list(q_offsets), list(row_ranges)
+        self.k_search, self.k_rerank = k_search, k_rerank
+        self.q = torch.zeros((b, index.dim), dtype=dtype, device=dev)
+        self.s_s = torch.empty((b, k_search), dtype=torch.float32, device=dev)
+        self.s_i = torch.empty((b, k_search), dtype=torch.int32, device=dev)
+        self.r_s = torch.empty((b, k_rerank), dtype=torch.float32, device=dev)
+        self.r_i = torch.empty((b, k_rerank), dtype=torch.int32, device=dev)
+        stream = torch.cuda.Stream(dev)
+        with torch.cuda.stream(stream):
+            for _ in range(warmup):  # grows the per-stream workspace before capture
+                self._run(stream)
+        stream.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=stream, capture_error_mode="thread_local"):
+            self._run(torch.cuda.current_stream(dev))
+
+    def _run(self, stream):
+        self.index.search_segmented(self.q, self.q_offsets, self.row_ranges, self.k_search,
+                                    local_ids=False, stream=stream, out=(self.s_s, self.s_i))
+        self.index.rerank(self.q, self.s_i, self.k_rerank, stream=stream,
+                          out=(self.r_s, self.r_i))
+
+    def run(self, q: torch.Tensor):
+        self.q.copy_(q)
+        self.graph.replay()
+        return self.r_s, self.r_i
+

@@ -88,3 +88,34 @@ def test_captured_retrieval_chain_replays_exactly(cuda, metric, k_search, n):
             cand = from_dev(si).reshape(nq, e * k_search)
             exp_s, _ = orc.rerank(qq, c, cand, k_r)
             np.testing.assert_allclose(from_dev(rs), exp_s, rtol=1e-3, atol=1e-6)
+
+
+def test_captured_contextual_chain_replays_exactly(cuda):
+    """Segmented search (each query over its own 48-row segment, top-32, arena-row ids) ->
+    rerank 32 -> 3 captured in one CUDA graph equals the primitives called one by one, for
+    several query batches replayed through the same graph; an uncaptured segmented search in
+    between (which reuses the rotating pinned upload slots) does not disturb the graph."""
+    import torch
+    from paper_2407_00326_b200.index import DeviceIndex
+    from paper_2407_00326_b200.launcher import CapturedContextual
+
+    nq, seg, dim, k, k_r = 16, 48, 1024, 32, 3
+    c = orc.make_corpus(nq * seg, dim, seed=0)
+    idx = DeviceIndex(dim, nq * seg, device=cuda.index)
+    idx.append(to_dev_bf16(c, cuda))
+    offs = list(range(nq + 1))
+    ranges = [(i * seg, (i + 1) * seg) for i in range(nq)]
+    cap = CapturedContextual(idx, offs, ranges, k, k_r)
+    for seed in (1, 2, 3):
+        q, _ = orc.make_queries(c, nq, seed=seed)
+        qd = to_dev_bf16(q, cuda)
+        idx.search_segmented(qd, [0, nq], [(0, nq * seg)], 8)  # other item lists in between
+        rs, ri = cap.run(qd)
+        ss, si = idx.search_segmented(qd, offs, ranges, k, local_ids=False)
+        es, ei = idx.rerank(qd, si, k_r)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(from_dev(ri), from_dev(ei))
+        np.testing.assert_array_equal(from_dev(rs), from_dev(es))
+        gi = from_dev(ri)
+        for r in range(nq):
+            assert ((gi[r] >= r * seg) & (gi[r] < (r + 1) * seg)).all()
