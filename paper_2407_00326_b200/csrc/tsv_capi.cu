@@ -231,6 +231,7 @@ int check_dtype(int dt) {
 
 constexpr int kMergeCap = 16384;  // candidates per query the merge kernel sorts in smem
 constexpr int kMinTilesPerRange = 1;
+constexpr int64_t kMinSampleTiles = 8;  // tiles per sample-pass item (TSV_SAMPLE_MIN_TILES)
 constexpr int64_t kWideMinRows = 1 << 19;  // scans shorter than this keep 128-row tiles (TSV_WIDE=0/1 forces)
 
 bool env_flag(const char* name) {
@@ -669,6 +670,15 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
   // at least kMinTilesPerRange tiles per range: tiny scans gain nothing from more workers, and
   // every extra range is one more list for the merge
   R = static_cast<int>(std::min<int64_t>(R, std::max<int64_t>(1, tiles / kMinTilesPerRange)));
+  // A sample pass reads 1/sample_div of every range: keep >= kMinSampleTiles tiles per item,
+  // or per-item pipeline fill and first-tile insertions dominate it (1M rows at B=1024 would
+  // otherwise run 296 two-tile items).
+  if (sample_div > 1) {
+    int64_t min_tiles = kMinSampleTiles;
+    if (const char* e = getenv("TSV_SAMPLE_MIN_TILES")) min_tiles = std::max(1, atoi(e));
+    R = static_cast<int>(std::min<int64_t>(R, std::max<int64_t>(1, tiles / (sample_div * min_tiles))));
+    if (nqg * R > units && nqg * R < 2 * units) R = std::max(1, units / nqg);  // one round
+  }
   if (!append) R = std::min(R, kMergeCap / kcap);  // the range merge holds R * kcap per query
   const int num_items = nqg * R;
   const int grid = pair ? 2 * std::min(num_items, units) : std::min(num_items, units);
