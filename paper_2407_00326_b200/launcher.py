@@ -30,6 +30,7 @@ import time
 import torch
 
 from .engines import EngineSet
+from .errors import ConfigParse
 from .runtime import BatchRecord, RuntimeOptions, Simulator
 
 
@@ -123,6 +124,13 @@ def run_streamed(engines: EngineSet, graphs_with_arrivals, backend,
     return rt, rt.run()
 
 
+def _same_shape(t: torch.Tensor, captured: torch.Tensor, name: str) -> None:
+    """Replays take exactly the captured shapes (copy_ would broadcast a mismatch silently)."""
+    if tuple(t.shape) != tuple(captured.shape):
+        raise ConfigParse(f"{name}: shape {tuple(t.shape)} differs from the captured "
+                          f"{tuple(captured.shape)}")
+
+
 class CapturedSearch:
     """A fixed-shape search captured in a CUDA graph.
 
@@ -153,6 +161,7 @@ class CapturedSearch:
                           stream=stream, out=(self.scores, self.ids))
 
     def search(self, q: torch.Tensor):
+        _same_shape(q, self.q, "queries")
         self.q.copy_(q)
         self.graph.replay()
         return self.scores, self.ids
@@ -199,6 +208,8 @@ class CapturedRetrieval:
         self.index.rerank(self.qq, cand, self.k_rerank, stream=stream, out=(self.r_s, self.r_i))
 
     def run(self, qx: torch.Tensor, qq: torch.Tensor):
+        _same_shape(qx, self.qx, "expanded queries")
+        _same_shape(qq, self.qq, "questions")
         self.qx.copy_(qx)
         self.qq.copy_(qq)
         self.graph.replay()
@@ -243,6 +254,7 @@ class CapturedContextual:
                           out=(self.r_s, self.r_i))
 
     def run(self, q: torch.Tensor):
+        _same_shape(q, self.q, "queries")
         self.q.copy_(q)
         self.graph.replay()
         return self.r_s, self.r_i

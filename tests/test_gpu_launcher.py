@@ -119,3 +119,16 @@ def test_captured_contextual_chain_replays_exactly(cuda):
         gi = from_dev(ri)
         for r in range(nq):
             assert ((gi[r] >= r * seg) & (gi[r] < (r + 1) * seg)).all()
+
+
+def test_captured_replay_rejects_other_shapes(cuda):
+    from paper_2407_00326_b200.errors import ConfigParse
+    from paper_2407_00326_b200.index import DeviceIndex
+    from paper_2407_00326_b200.launcher import CapturedSearch
+
+    c = orc.make_corpus(5000, 128, seed=0)
+    idx = DeviceIndex(128, 5000, device=cuda.index)
+    idx.append(to_dev_bf16(c, cuda))
+    cap = CapturedSearch(idx, batch=16, k=5)
+    with pytest.raises(ConfigParse):
+        cap.search(to_dev_bf16(c[:1], cuda))  # would broadcast into the 16-row buffer
