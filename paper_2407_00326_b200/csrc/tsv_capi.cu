@@ -600,7 +600,7 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
   if (k <= 0) return fail(TSV_ERR_CONFIG, "k must be >= 1");
   if (tsv::scan_kcap_for(k) == 0)
     return fail(TSV_ERR_CONFIG, "k=%d exceeds the supported maximum (128)", k);
-  const int kcap = list_cap > 0 ? tsv::scan_kcap_for(list_cap) : tsv::scan_kcap_for(k);
+  int kcap = list_cap > 0 ? tsv::scan_kcap_for(list_cap) : tsv::scan_kcap_for(k);
   if (q_dev == nullptr || scores_dev == nullptr || ids_dev == nullptr)
     return fail(TSV_ERR_ARGUMENT, "null buffer");
   if (row_beg < 0 || row_end > idx->rows || row_beg > row_end)
@@ -680,6 +680,12 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
     if (nqg * R > units && nqg * R < 2 * units) R = std::max(1, units / nqg);  // one round
   }
   if (!append) R = std::min(R, kMergeCap / kcap);  // the range merge holds R * kcap per query
+  // Sample pass: 16-entry lists when the ranges' lists still hold >= 2k entries. The floor is
+  // the k-th best of their union (exact whenever no range holds more than 16 of the sample's
+  // top k); shorter lists halve the first-tile insertion chains of the short sample items.
+  if (sample_div > 1 && kcap == tsv::kMaxRegK && static_cast<int64_t>(R) * 16 >= 2 * k &&
+      !env_flag("TSV_SAMPLE_LIST32"))
+    kcap = 16;
   const int num_items = nqg * R;
   const int grid = pair ? 2 * std::min(num_items, units) : std::min(num_items, units);
 
