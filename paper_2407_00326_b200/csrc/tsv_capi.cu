@@ -670,13 +670,20 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
   // at least kMinTilesPerRange tiles per range: tiny scans gain nothing from more workers, and
   // every extra range is one more list for the merge
   R = static_cast<int>(std::min<int64_t>(R, std::max<int64_t>(1, tiles / kMinTilesPerRange)));
-  // A sample pass reads 1/sample_div of every range: keep >= kMinSampleTiles tiles per item,
-  // or per-item pipeline fill and first-tile insertions dominate it (1M rows at B=1024 would
-  // otherwise run 296 two-tile items).
+  // A sample pass reads 1/sample_div of every range: keep >= kMinSampleTiles tiles per item
+  // where that still fills a round, or per-item pipeline fill and first-tile insertions
+  // dominate it (1M rows at B=1024 would otherwise run 4 rounds of 296 two-tile items).
+  // The floor is the k-th best of the ranges' lists together, so keep >= 2k list entries.
   if (sample_div > 1) {
+    const int r0 = R;
     int64_t min_tiles = kMinSampleTiles;
     if (const char* e = getenv("TSV_SAMPLE_MIN_TILES")) min_tiles = std::max(1, atoi(e));
-    R = static_cast<int>(std::min<int64_t>(R, std::max<int64_t>(1, tiles / (sample_div * min_tiles))));
+    // (never below one round of items: with few workers busy the sample costs more than the
+    // per-item overhead it saves, e.g. 300K x 4096 or 100K-row scans)
+    const int64_t one_round = (units + nqg - 1) / nqg;
+    R = static_cast<int>(std::min<int64_t>(
+        R, std::max<int64_t>(one_round, tiles / (sample_div * min_tiles))));
+    R = std::max(R, std::min(r0, (2 * k + kcap - 1) / kcap));
     if (nqg * R > units && nqg * R < 2 * units) R = std::max(1, units / nqg);  // one round
   }
   if (!append) R = std::min(R, kMergeCap / kcap);  // the range merge holds R * kcap per query
