@@ -96,11 +96,12 @@ TSV_API int tsv_index_scan_time(tsv_index* idx, double* total_ms, int64_t* launc
  * Replaces the PHASE_GENERAL latency lookup of runtime.py:653-655 for engine category
  * "search" (engines.py:21, graph.py:47-59). q_dev: [B, dim] (bf16 or f32). Emitted id =
  * arena row + id_offset. Outputs scores/ids [B, k]. k <= 128. k <= 32 keeps the top-k lists in
- * registers (CTA-pair kernel for B > 128). Larger k on >= 262,144 rows runs a sample pass
- * (1/32 of every range; 1/16 for k > 100) for a per-query floor, then a candidate pass appending every row
- * above the floor plus an exact select, with a device-gated shared-memory-list pass if a
- * candidate row overflows; smaller scans use the shared-memory lists directly. Exact in all
- * cases. ---- */
+ * registers (CTA-pair kernel for B > 128; 256-row corpus tiles for 96 < B <= 128 on long
+ * scans). Larger k (B <= 32768): scans of <= 8192 rows append every row as a candidate and
+ * select exactly; longer scans run a sample pass (1/32 of every range; 1/16 for k > 100) for a
+ * per-query floor, then a candidate pass appending every row above the floor plus an exact
+ * select, with a device-gated shared-memory-list pass if a candidate row overflows. Exact in
+ * all cases. ---- */
 TSV_API int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int64_t row_beg,
                int64_t row_end, int32_t id_offset, float* scores_dev, int32_t* ids_dev,
                void* stream);
