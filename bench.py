@@ -59,7 +59,83 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--exchange", choices=("p2p", "nccl"), default="p2p",
                     help="N>1: fused peer all-gather + merge over NVLink, or NCCL all-gather + K4")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="start the ranks, agree on the shard plan and print it (no kernels); "
+                         "checks the N-rank launch without a GPU")
     return ap.parse_args()
+
+
+# ---------------------------------------------------------------------- N-rank launch
+def _free_port() -> int:
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn_ranks(args) -> int:
+    """`bench.py --gpus N` (N > 1) started without a launcher: re-run this script under
+    torch.distributed.run with N ranks on this node (one GPU per rank), forwarding the
+    arguments; rank 0's JSON line is this process's output. A box with fewer than N GPUs is
+    refused up front (NCCL cannot put two ranks on one GPU) unless BENCH_DIST_BACKEND=gloo."""
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    if backend == "nccl" and args.impl == "ours" and not args.dry_run:
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs on this node, found "
+                  f"{have} (NCCL runs one rank per GPU)", file=sys.stderr, flush=True)
+            return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           "--nproc-per-node", str(args.gpus), "--master-addr", "127.0.0.1",
+           "--master-port", str(_free_port()), str(Path(__file__).resolve()), *sys.argv[1:]]
+    env = dict(os.environ, BENCH_SPAWNED="1", OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    print(f"bench.py: starting {args.gpus} ranks: {' '.join(cmd[1:6])} ...", file=sys.stderr,
+          flush=True)
+    return subprocess.run(cmd, env=env, cwd=str(ROOT)).returncode
+
+
+def dist_env() -> tuple[int, int, int]:
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def check_world(args, world: int) -> None:
+    """Every line is measured on exactly --gpus ranks: a mismatch is an error, never a line."""
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but the launcher started {world} "
+                         f"rank(s); refusing to report a {world}-rank measurement as "
+                         f"{args.gpus}")
+
+
+def run_dry(args) -> int:
+    """The N-rank plan without kernels: ranks join the process group, each reports its shard,
+    rank 0 prints the agreed plan (world size as the process group sees it)."""
+    import torch.distributed as dist
+
+    from paper_2407_00326_b200.sharded import shard_range
+
+    rank, world, _ = dist_env()
+    check_world(args, world)
+    group_world = 1
+    shards = [shard_range(args.rows, 0, 1)]
+    if world > 1:
+        dist.init_process_group(os.environ.get("BENCH_DIST_BACKEND", "nccl"))
+        group_world = dist.get_world_size()
+        got = [None] * group_world
+        dist.all_gather_object(got, (rank, *shard_range(args.rows, rank, world)))
+        shards = [(lo, hi) for _, lo, hi in sorted(got)]
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "world_size_from_group": group_world,
+                          "spawned": os.environ.get("BENCH_SPAWNED") == "1",
+                          "shards": shards, "config": _config(args, shards[0][1] - shards[0][0])}),
+              flush=True)
+    return 0
 
 
 def load_peaks():
@@ -335,9 +411,11 @@ def run_ours(args):
     from paper_2407_00326_b200.index import DeviceIndex, normalize_rows
     from paper_2407_00326_b200.sharded import ShardedSearch, shard_range
 
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    rank, world, local = dist_env()
+    check_world(args, world)
+    # NCCL's own log stays on (to a file per rank, so stdout keeps exactly one JSON line)
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_FILE", f"/tmp/bench_nccl.{os.getpid()}.log")
     # BENCH_DIST_BACKEND=gloo (test only): run the N>1 code path with every rank on the GPUs
     # present (ranks share a GPU when there are fewer GPUs than ranks; NCCL refuses that)
     backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
@@ -353,6 +431,14 @@ def run_ours(args):
         else:
             dist.init_process_group(backend)
     _native.load()
+    group_world = dist.get_world_size() if world > 1 else 1
+    check_world(args, group_world)
+    # every rank's device (distinct physical GPUs under NCCL), gathered for the JSON line
+    me = f"{torch.cuda.get_device_name(dev)} {torch.cuda.get_device_properties(dev).uuid}"
+    device_names = [me]
+    if world > 1:
+        device_names = [None] * world
+        dist.all_gather_object(device_names, me)
 
     B, D, k, N = args.batch, args.dim, args.k, args.rows
     lo, hi = shard_range(N, rank, world)
@@ -594,6 +680,10 @@ def run_ours(args):
             "metric": "vector-search queries/s (10Mx1024 corpus, k=10)",
             "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "warmup_extra_steps": warm_extra,
+            "world": {"ranks": world, "process_group": group_world, "backend": backend if world > 1 else None,
+                      "spawned_by_bench": os.environ.get("BENCH_SPAWNED") == "1",
+                      "devices": device_names,
+                      "nccl_log": os.environ.get("NCCL_DEBUG_FILE") if world > 1 else None},
             "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None,
             "dtype": "f32 (3xTF32)" if args.storage == "f32" else "bf16",
@@ -627,6 +717,12 @@ def run_ours(args):
 
 def main():
     args = parse_args()
+    if args.gpus < 1:
+        raise SystemExit("bench.py: --gpus must be >= 1")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
+    if args.dry_run:
+        return run_dry(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

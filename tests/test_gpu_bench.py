@@ -63,3 +63,18 @@ def test_bench_ranks_sharded(cuda, world, exchange):
     assert d["n_gpus"] == world and d["config"]["shard_rows"] == 1_000_000 // world
     assert d["config"]["exchange"] == exchange
     assert d["planted_top1"] == 1.0  # global ids survive the exchange + merge
+
+
+def test_bench_spawns_its_own_ranks(cuda):
+    """`bench.py --gpus 2` with no launcher starts 2 ranks itself and reports them (ranks share
+    this GPU over gloo; on an 8-GPU node the same command runs one NCCL rank per GPU)."""
+    env = dict(os.environ, BENCH_DIST_BACKEND="gloo")
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--rows", "1000000",
+                        "--steps", "4", "--warmup", "3", "--min-warmup-s", "0"], cwd=ROOT,
+                       capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = _last_json(r.stdout)
+    assert d["n_gpus"] == 2 and d["world"]["process_group"] == 2
+    assert d["world"]["spawned_by_bench"] and d["config"]["shard_rows"] == 500_000
+    assert d["planted_top1"] == 1.0
