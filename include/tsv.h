@@ -131,7 +131,9 @@ TSV_API int tsv_merge_topk(const float* in_scores, const int32_t* in_ids, int li
  * cross-shard merge (replaces ncclAllGather + tsv_merge_topk). One process per GPU; each
  * rank creates a symmetric buffer, exports its IPC handle, opens every peer's handle (handles
  * travel over any side channel, e.g. torch.distributed), then calls allgather_merge with the
- * same B, k on every rank. Ranks push their lists into peers' memory and merge on arrival. ---- */
+ * same call sequence on every rank (B <= max_b and k <= max_k may vary from call to call). Ranks
+ * push their lists into peers' memory, stamp each (source, query) slot with the call's epoch
+ * and merge on arrival. ---- */
 typedef struct tsv_peer_group tsv_peer_group;
 TSV_API int tsv_peer_create(int device, int world, int rank, int max_b, int max_k,
                             tsv_peer_group** out);
@@ -140,6 +142,13 @@ TSV_API int tsv_peer_open(tsv_peer_group* g, int peer, const void* handle);
 TSV_API int tsv_peer_allgather_merge(tsv_peer_group* g, const float* local_scores,
                                      const int32_t* local_ids, int B, int k, float* out_scores,
                                      int32_t* out_ids, void* stream);
+/* A wait longer than the timeout (default 60 s; TSV_PEER_TIMEOUT_MS) aborts: every rank's
+ * kernel ends with padded outputs, the group is marked dead and the next call (or
+ * tsv_peer_status after a stream sync) returns TSV_ERR_DEVICE. */
+TSV_API int tsv_peer_set_timeout_ms(tsv_peer_group* g, int64_t ms);
+/* *aborted = 1 (and TSV_ERR_DEVICE) once an exchange of this group gave up waiting. Reads a
+ * host-mapped word; synchronise the stream of the last call first. */
+TSV_API int tsv_peer_status(tsv_peer_group* g, int* aborted);
 TSV_API int tsv_peer_destroy(tsv_peer_group* g);
 
 /* ---- K5: L2-normalise (normalize != 0) and cast rows to bf16. ---- */

@@ -60,6 +60,8 @@ SIGNATURES = {
     "tsv_peer_handle": (c_int, [c_vp, c_vp, ctypes.POINTER(c_int)]),
     "tsv_peer_open": (c_int, [c_vp, c_int, c_vp]),
     "tsv_peer_allgather_merge": (c_int, [c_vp, c_vp, c_vp, c_int, c_int, c_vp, c_vp, c_vp]),
+    "tsv_peer_set_timeout_ms": (c_int, [c_vp, c_i64]),
+    "tsv_peer_status": (c_int, [c_vp, ctypes.POINTER(c_int)]),
     "tsv_peer_destroy": (c_int, [c_vp]),
 }
 

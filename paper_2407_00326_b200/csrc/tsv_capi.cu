@@ -1096,7 +1096,10 @@ struct tsv_peer_group {
   std::vector<bool> opened;     // peers mapped through IPC (closed on destroy)
   void** d_peers = nullptr;     // device copy of `peers`
   bool dirty = true;
-  int epoch = 0;
+  uint32_t epoch = 0;
+  uint64_t timeout_ns = 60ull * 1000 * 1000 * 1000;  // a wait longer than this aborts the group
+  uint32_t* err_host = nullptr;  // host-mapped error word written by the kernel (1 = aborted)
+  uint32_t* err_dev = nullptr;
 };
 
 extern "C" {
@@ -1116,13 +1119,23 @@ int tsv_peer_create(int device, int world, int rank, int max_b, int max_k, tsv_p
   pg->max_b = max_b;
   pg->max_k = max_k;
   cudaDeviceGetAttribute(&pg->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (const char* t = getenv("TSV_PEER_TIMEOUT_MS"))
+    pg->timeout_ns = static_cast<uint64_t>(std::max(1L, atol(t))) * 1000000ull;
   const size_t bytes = tsv::peer_buffer_bytes(world, max_b, max_k);
   cudaError_t e = cudaMalloc(&pg->buf, bytes);
   if (e == cudaSuccess) e = cudaMemset(pg->buf, 0, bytes);
   if (e == cudaSuccess) e = cudaMalloc(&pg->d_peers, sizeof(void*) * world);
+  if (e == cudaSuccess)
+    e = cudaHostAlloc(reinterpret_cast<void**>(&pg->err_host), sizeof(uint32_t), cudaHostAllocMapped);
+  if (e == cudaSuccess) {
+    *pg->err_host = 0;
+    e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&pg->err_dev), pg->err_host, 0);
+  }
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     if (pg->buf) cudaFree(pg->buf);
+    if (pg->d_peers) cudaFree(pg->d_peers);
+    if (pg->err_host) cudaFreeHost(pg->err_host);
     delete pg;
     return cuda_fail(e, "peer buffer");
   }
@@ -1164,6 +1177,10 @@ int tsv_peer_allgather_merge(tsv_peer_group* pg, const float* local_s, const int
   if (B <= 0 || k <= 0) return fail(TSV_ERR_CAPACITY, "empty exchange");
   if (B > pg->max_b || k > pg->max_k) return fail(TSV_ERR_CAPACITY, "exchange exceeds buffer");
   if (!local_s || !local_i || !out_s || !out_i) return fail(TSV_ERR_ARGUMENT, "null buffer");
+  if (*reinterpret_cast<volatile uint32_t*>(pg->err_host) != 0)
+    return fail(TSV_ERR_DEVICE, "peer exchange aborted: a peer did not deliver within %llu ms "
+                "(dead rank or mismatched call sequence); recreate the group",
+                (unsigned long long)(pg->timeout_ns / 1000000ull));
   for (int r = 0; r < pg->world; ++r)
     if (pg->peers[r] == nullptr) return fail(TSV_ERR_CONFIG, "peer %d not opened", r);
   DeviceGuard g(pg->device);
@@ -1177,10 +1194,26 @@ int tsv_peer_allgather_merge(tsv_peer_group* pg, const float* local_s, const int
   }
   pg->epoch++;
   int e = tsv::launch_peer_exchange_merge(pg->d_peers, pg->rank, pg->world, B, k, pg->max_b,
-                                          pg->max_k, pg->epoch, local_s, local_i, out_s, out_i,
-                                          pg->num_sms, st);
+                                          pg->max_k, pg->epoch, pg->timeout_ns, local_s, local_i,
+                                          out_s, out_i, pg->err_dev, pg->num_sms, st);
   if (e) return cuda_fail(static_cast<cudaError_t>(e), "peer exchange launch");
   g_launches++;
+  return TSV_OK;
+}
+
+int tsv_peer_set_timeout_ms(tsv_peer_group* pg, int64_t ms) {
+  if (pg == nullptr) return fail(TSV_ERR_ARGUMENT, "peer group is null");
+  if (ms <= 0) return fail(TSV_ERR_CONFIG, "timeout must be positive");
+  pg->timeout_ns = static_cast<uint64_t>(ms) * 1000000ull;
+  return TSV_OK;
+}
+
+int tsv_peer_status(tsv_peer_group* pg, int* aborted) {
+  if (pg == nullptr || aborted == nullptr) return fail(TSV_ERR_ARGUMENT, "null argument");
+  *aborted = *reinterpret_cast<volatile uint32_t*>(pg->err_host) != 0;
+  if (*aborted)
+    return fail(TSV_ERR_DEVICE, "peer exchange aborted: a peer did not deliver within %llu ms",
+                (unsigned long long)(pg->timeout_ns / 1000000ull));
   return TSV_OK;
 }
 
@@ -1190,6 +1223,7 @@ int tsv_peer_destroy(tsv_peer_group* pg) {
   cudaDeviceSynchronize();
   for (int r = 0; r < pg->world; ++r)
     if (pg->opened[r]) cudaIpcCloseMemHandle(pg->peers[r]);
+  if (pg->err_host) cudaFreeHost(pg->err_host);
   if (pg->d_peers) cudaFree(pg->d_peers);
   if (pg->buf) cudaFree(pg->buf);
   delete pg;

@@ -123,9 +123,10 @@ int launch_seed_floor(const float* s, const int32_t* id, int B, int k, float* fl
                       cudaStream_t stream);
 size_t peer_buffer_bytes(int world, int max_b, int max_k);
 int launch_peer_exchange_merge(void* const* peers_dev, int rank, int world, int B, int k,
-                               int max_b, int max_k, int epoch, const float* local_s,
-                               const int32_t* local_i, float* out_s, int32_t* out_i,
-                               int num_sms, cudaStream_t stream);
+                               int max_b, int max_k, uint32_t epoch, uint64_t timeout_ns,
+                               const float* local_s, const int32_t* local_i, float* out_s,
+                               int32_t* out_i, uint32_t* err_word, int num_sms,
+                               cudaStream_t stream);
 int launch_scatter_tiled(const void* src, int src_is_f32, int64_t n, int dim, int do_normalize,
                          void* arena, int64_t first_row, cudaStream_t stream);
 

@@ -523,40 +523,71 @@ __global__ void seed_floor_kernel(const float* __restrict__ s, const int32_t* __
 
 // ---------------------------------------------------------------------------------------------
 // Peer exchange fused with the cross-shard merge (sharded mode over NVLink / NVSwitch).
-// Every rank owns a symmetric buffer: flags[max_b] (cumulative arrival counters), then
-// recv_s / recv_i [2 parities][world][max_b][max_k]. A call (epoch e, parity e & 1):
+// Every rank owns a symmetric buffer:
+//   header   word 0: abort flag (any rank that gave up waiting sets it in every buffer)
+//   stamps   [world][max_b] u32: stamps[src][b] = epoch of the last call in which rank src
+//            delivered query b's list into this buffer
+//   recv_s / recv_i [2 parities][world][max_b][max_k]
+// A call (epoch e, parity e & 1):
 //   phase 1  each CTA pushes its queries' local top-k into slot [parity][rank][b] of every
 //            peer's buffer (stores through mapped peer memory), fences at system scope and
-//            bumps the peer's flags[b];
-//   phase 2  each CTA waits until its own flags[b] reach e * world (all ranks delivered),
-//            then merges the world lists of query b and writes the global top-k.
-// Every CTA sends everything before it waits and the grid is at most one CTA per SM, so no
-// CTA can wait on data that a non-resident CTA still has to send.
+//            writes stamp e into the peer's stamps[rank][b] (release);
+//   phase 2  each CTA waits until stamps[src][b] >= e for every src (acquire), then merges the
+//            world lists of query b and writes the global top-k.
+// Stamps are per (source, query slot), so calls with different batch sizes interleave freely:
+// a slot left untouched by a smaller batch is simply older, and the next call that covers it
+// waits for that call's own stamp. A rank can be at most one call ahead of another (its next
+// call waits for this call's stamps of every peer), so the two parities never alias.
+// Every CTA sends everything before it waits and the grid is at most one CTA per SM, so no CTA
+// waits on data that a non-resident CTA still has to send. A wait longer than timeout_ns (a
+// peer that never arrives: dead rank, mismatched call sequence) aborts: the waiting CTA writes
+// padding for its queries, raises the abort flag in every rank's buffer (their waits end at
+// once) and in the caller-visible error word, and the host reports DeviceError.
 struct PeerArgs {
   void* const* peers;  // device array: base of each rank's symmetric buffer
   int rank, world, B, k, max_b, max_k, parity;
-  uint32_t expected;
+  uint32_t epoch;
+  uint64_t timeout_ns;
   const float* local_s;
   const int32_t* local_i;
   float* out_s;
   int32_t* out_i;
+  uint32_t* err;  // host-mapped error word (1 = aborted)
 };
+
+constexpr size_t kPeerHeaderBytes = 256;
 
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t global_timer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__host__ __device__ __forceinline__ size_t peer_stamp_bytes(int world, int max_b) {
+  return ((static_cast<size_t>(world) * max_b * 4 + 255) / 256) * 256;
+}
 
 __global__ void peer_exchange_merge_kernel(const PeerArgs a) {
   extern __shared__ uint64_t keys[];
-  const size_t flags_bytes = ((static_cast<size_t>(a.max_b) * 4 + 255) / 256) * 256;
+  __shared__ int aborted;
+  const size_t data_off = kPeerHeaderBytes + peer_stamp_bytes(a.world, a.max_b);
   const size_t plane = static_cast<size_t>(a.world) * a.max_b * a.max_k;  // entries per parity
+  auto stamps = [&](void* base) {
+    return reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(base) + kPeerHeaderBytes);
+  };
   auto recv_s = [&](void* base) {
-    return reinterpret_cast<float*>(static_cast<uint8_t*>(base) + flags_bytes);
+    return reinterpret_cast<float*>(static_cast<uint8_t*>(base) + data_off);
   };
   auto recv_i = [&](void* base) {
-    return reinterpret_cast<int32_t*>(static_cast<uint8_t*>(base) + flags_bytes + 2 * plane * 4);
+    return reinterpret_cast<int32_t*>(static_cast<uint8_t*>(base) + data_off + 2 * plane * 4);
   };
   // phase 1: push
   for (int b = blockIdx.x; b < a.B; b += gridDim.x) {
@@ -572,19 +603,44 @@ __global__ void peer_exchange_merge_kernel(const PeerArgs a) {
     if (threadIdx.x == 0) {
       __threadfence_system();
       for (int p = 0; p < a.world; ++p)
-        atomicAdd_system(reinterpret_cast<uint32_t*>(a.peers[p]) + b, 1u);
+        st_release_sys(stamps(a.peers[p]) + static_cast<size_t>(a.rank) * a.max_b + b, a.epoch);
     }
   }
   // phase 2: wait for every rank's contribution, merge
   void* own = a.peers[a.rank];
-  const uint32_t* flags = reinterpret_cast<const uint32_t*>(own);
+  uint32_t* abort_word = static_cast<uint32_t*>(own);
+  const uint32_t* st = stamps(own);
   const int n = a.world * a.k;
   const int np = pow2_ceil(n);
+  const uint64_t t0 = global_timer_ns();
   for (int b = blockIdx.x; b < a.B; b += gridDim.x) {
-    if (threadIdx.x == 0) {
-      while (ld_acquire_sys(flags + b) < a.expected) __nanosleep(128);
+    if (threadIdx.x == 0) aborted = 0;
+    __syncthreads();
+    if (threadIdx.x < a.world) {  // one waiting thread per source rank
+      const uint32_t* w = st + static_cast<size_t>(threadIdx.x) * a.max_b + b;
+      // (signed distance: stamps are a wrapping u32 epoch counter)
+      while (static_cast<int32_t>(ld_acquire_sys(w) - a.epoch) < 0) {
+        if (ld_acquire_sys(abort_word) != 0 || global_timer_ns() - t0 > a.timeout_ns) {
+          aborted = 1;
+          break;
+        }
+        __nanosleep(256);
+      }
     }
     __syncthreads();
+    if (aborted) {
+      if (threadIdx.x == 0) {
+        for (int p = 0; p < a.world; ++p) st_release_sys(static_cast<uint32_t*>(a.peers[p]), 1u);
+        *reinterpret_cast<volatile uint32_t*>(a.err) = 1u;
+        __threadfence_system();
+      }
+      for (int j = threadIdx.x; j < a.k; j += blockDim.x) {
+        a.out_s[static_cast<int64_t>(b) * a.k + j] = -INFINITY;
+        a.out_i[static_cast<int64_t>(b) * a.k + j] = -1;
+      }
+      __syncthreads();
+      continue;
+    }
     for (int i = threadIdx.x; i < np; i += blockDim.x) {
       uint64_t key = pad_key();
       if (i < n) {
@@ -626,17 +682,17 @@ int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaS
 }  // namespace
 
 size_t peer_buffer_bytes(int world, int max_b, int max_k) {
-  const size_t flags_bytes = ((static_cast<size_t>(max_b) * 4 + 255) / 256) * 256;
-  return flags_bytes + 2 * 2 * static_cast<size_t>(world) * max_b * max_k * 4;
+  return kPeerHeaderBytes + peer_stamp_bytes(world, max_b) +
+         2 * 2 * static_cast<size_t>(world) * max_b * max_k * 4;
 }
 
 int launch_peer_exchange_merge(void* const* peers_dev, int rank, int world, int B, int k,
-                               int max_b, int max_k, int epoch, const float* local_s,
-                               const int32_t* local_i, float* out_s, int32_t* out_i,
-                               int num_sms, cudaStream_t stream) {
-  PeerArgs a{peers_dev, rank, world, B, k, max_b, max_k, epoch & 1,
-             static_cast<uint32_t>(epoch) * static_cast<uint32_t>(world), local_s, local_i,
-             out_s, out_i};
+                               int max_b, int max_k, uint32_t epoch, uint64_t timeout_ns,
+                               const float* local_s, const int32_t* local_i, float* out_s,
+                               int32_t* out_i, uint32_t* err_word, int num_sms,
+                               cudaStream_t stream) {
+  PeerArgs a{peers_dev, rank, world, B, k, max_b, max_k, static_cast<int>(epoch & 1u), epoch,
+             timeout_ns, local_s, local_i, out_s, out_i, err_word};
   int np = 1;
   while (np < world * k) np <<= 1;
   const int grid = B < num_sms ? B : num_sms;

@@ -86,6 +86,16 @@ class PeerExchange:
             raise RuntimeError(f"peer mapping failed on some rank ({err or 'another rank'})")
         dist.barrier(group)
 
+    def set_timeout_ms(self, ms: int) -> None:
+        """Longest wait for a peer's lists before the exchange aborts (DeviceError)."""
+        self.check(self.lib.tsv_peer_set_timeout_ms(self._h, int(ms)))
+
+    def status(self) -> None:
+        """Raise DeviceError if an exchange of this group gave up waiting for a peer
+        (synchronise the stream of the last call first)."""
+        flag = ctypes.c_int()
+        self.check(self.lib.tsv_peer_status(self._h, ctypes.byref(flag)))
+
     def allgather_merge(self, s_loc: torch.Tensor, i_loc: torch.Tensor, k: int,
                         stream: torch.cuda.Stream | None = None):
         B = s_loc.shape[0]

@@ -1,7 +1,8 @@
 """End-to-end: the reference's e-graphs run through the mirrored Simulator with the B200
 RetrievalBackend bound at `_execute` (runtime.py:625-656). Checks (1) the trace stays
 byte-identical to the reference's in timing="profile" mode, (2) every Searching stage /
-Reranking output matches the CPU oracle on the data the device actually holds, (3)
+Reranking output matches the CPU oracle on the data the device actually holds (D=1024, the
+bge-large embedding width of BASELINE C3 / C5), (3)
 timing="measured" reports real device durations."""
 
 from __future__ import annotations
@@ -26,13 +27,13 @@ def _fixture():
     return traces, prof
 
 
-def _run(case, prof, timing="profile", devices=None):
+def _run(case, prof, timing="profile", devices=None, dim=1024):
     from paper_2407_00326_b200 import engines as E, runtime as R
     from paper_2407_00326_b200.backend import RetrievalBackend
     from paper_2407_00326_b200.graph import parse_graph
 
     es = E.EngineSet.from_dict(prof)
-    backend = RetrievalBackend(dim=256, devices=devices, arena_rows=1 << 16, timing=timing)
+    backend = RetrievalBackend(dim=dim, devices=devices, arena_rows=1 << 16, timing=timing)
     subs = [(parse_graph(g), a, b) for g, a, b in case["graphs"]]
     sim, trace = R.run_queries(es, subs, R.RuntimeOptions(scheduler=case["scheduler"]),
                                backend=backend)

@@ -11,6 +11,9 @@ import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
+# (query seed, batch): smaller batches leave the upper query slots of the group untouched; the
+# next full batch must not wait for them (cumulative per-slot counters hung here)
+CALLS = [(1, 64), (2, 32), (3, 64), (4, 16), (5, 64)]
 
 
 def _free_port():
@@ -40,8 +43,8 @@ def _worker(rank, world, port, out):
     idx.append(to_dev_bf16(corpus[lo:hi], dev))
     ss = ShardedSearch(idx, n, rank=rank, world=world, exchange="p2p")
     results = []
-    for seed in (1, 2, 3):
-        q, _ = orc.make_queries(corpus, 64, seed=seed)
+    for seed, b in CALLS:  # varying batch sizes reuse the group created for the first (64)
+        q, _ = orc.make_queries(corpus, b, seed=seed)
         s, i = ss.search(to_dev_bf16(q, dev), k)
         torch.cuda.synchronize()
         results.append((from_dev(s).copy(), from_dev(i).copy()))
@@ -68,10 +71,68 @@ def test_p2p_exchange_equals_unsharded(cuda, world):
         p.join(timeout=240)
         assert p.exitcode == 0
     corpus = orc.make_corpus(20000, 256, seed=0)
-    for call, seed in enumerate((1, 2, 3)):
-        q, _ = orc.make_queries(corpus, 64, seed=seed)
+    for call, (seed, b) in enumerate(CALLS):
+        q, _ = orc.make_queries(corpus, b, seed=seed)
         for r in range(world):
             s, i = out[r][call]
             assert not orc.check_topk(s, i, q, corpus, 10, 1e-3)
         for r in range(1, world):
             np.testing.assert_array_equal(out[0][call][1], out[r][call][1])
+
+
+def _silent_peer_worker(rank, world, port, out):
+    """Rank 1 never calls the exchange: rank 0's call must abort after its timeout and report
+    DeviceError, not hang."""
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2407_00326_b200.errors import DeviceError
+    from paper_2407_00326_b200.sharded import PeerExchange
+
+    dev = torch.device("cuda", 0)
+    pe = PeerExchange(dev, 64, 10)
+    if rank == 0:
+        import time
+
+        pe.set_timeout_ms(500)
+        s = torch.zeros((64, 10), dtype=torch.float32, device=dev)
+        i = torch.arange(640, dtype=torch.int32, device=dev).view(64, 10)
+        t = time.time()
+        o_s, o_i = pe.allgather_merge(s, i, 10)
+        torch.cuda.synchronize()
+        out["elapsed"] = time.time() - t
+        out["padded"] = bool((o_i == -1).all().item())
+        try:
+            pe.status()
+            out["status"] = "ok"
+        except DeviceError as exc:
+            out["status"] = f"DeviceError: {exc}"
+        try:
+            pe.allgather_merge(s, i, 10)
+            out["next"] = "ok"
+        except DeviceError:
+            out["next"] = "DeviceError"
+    dist.barrier()
+    pe.close()
+    dist.destroy_process_group()
+
+
+def test_p2p_missing_peer_times_out(cuda):
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    mgr = ctx.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_silent_peer_worker, args=(r, 2, port, out)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert out["elapsed"] < 30
+    assert out["padded"]
+    assert out["status"].startswith("DeviceError")
+    assert out["next"] == "DeviceError"

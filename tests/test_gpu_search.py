@@ -642,9 +642,9 @@ def test_wide_tiles_identical(cuda, n, dim, b, k, lo):
 def test_headline_full_size_exact(cuda, k):
     """The bench configuration at full size (10M x 1024 bf16, B=1024; k=10 and C4's k=100):
     every query's list sorted with distinct ids, planted rows found first, every returned score
-    equal to an fp32 re-scoring of its row, and 64 queries (32 planted, 32 fresh) identical to
-    an exact fp32 torch search over all 10M rows (same scores within 2e-5; same ids wherever
-    neighbouring exact scores differ by more than that)."""
+    equal to an fp32 re-scoring of its row, and 64 queries (32 planted, 32 fresh) checked
+    against the CPU oracle (the C restatement, fp64 accumulation, over all 10M rows): ids
+    bit-exact wherever the oracle's score gap exceeds the 1e-3 tolerance, scores within it."""
     import torch
 
     from paper_2407_00326_b200.index import DeviceIndex, normalize_rows
@@ -669,32 +669,34 @@ def test_headline_full_size_exact(cuda, k):
     resc = torch.einsum("bd,bkd->bk", q.float(), rows[i.long()].float())
     assert float((resc - s).abs().max()) < 2e-5
 
+    # 64 queries (32 planted, 32 fresh) against the CPU oracle: the C restatement in fp64 over
+    # the host copy of all 10M rows (1M-row chunks, per-chunk top-(k+16) with global ids,
+    # merged), then the comparator of SURVEY.md §7.1 at the bf16 tolerance.
+    from oracle import c_oracle
+
     sub = torch.cat([torch.arange(0, 32), torch.arange(b - 32, b)]).to(cuda)
-    qs = q[sub].float()
-    prev = torch.backends.cuda.matmul.allow_tf32
-    torch.backends.cuda.matmul.allow_tf32 = False
-    try:
-        best_s, best_i = None, None
-        for a in range(0, n, 1 << 20):
-            sc = qs @ rows[a: a + (1 << 20)].float().T
-            ts, ti = torch.topk(sc, k, dim=1)
-            ti = ti + a
-            if best_s is None:
-                best_s, best_i = ts, ti
-            else:
-                cs, ci = torch.cat([best_s, ts], 1), torch.cat([best_i, ti], 1)
-                best_s, o = torch.topk(cs, k, dim=1)
-                best_i = torch.gather(ci, 1, o)
-    finally:
-        torch.backends.cuda.matmul.allow_tf32 = prev
-    gs, gi = s[sub], i[sub].long()
-    assert float((gs - best_s).abs().max()) < 2e-5
-    gap_prev = torch.cat([torch.full_like(best_s[:, :1], float("inf")),
-                          best_s[:, :-1] - best_s[:, 1:]], 1)
-    gap_next = torch.cat([best_s[:, :-1] - best_s[:, 1:],
-                          torch.full_like(best_s[:, :1], float("inf"))], 1)
-    sep = (gap_prev > 2e-5) & (gap_next > 2e-5)
-    assert bool((gi[sep] == best_i[sep]).all())
+    q_bits = q[sub].view(torch.int16).cpu().numpy().view(np.uint16)
+    keep = k + 16
+    parts_s, parts_i = [], []
+    for a in range(0, n, 1 << 20):
+        chunk = rows[a: a + (1 << 20)].view(torch.int16).cpu().numpy().view(np.uint16)
+        cs, ci = c_oracle.search(q_bits, chunk, keep, use_double=True, id_offset=a)
+        parts_s.append(cs)
+        parts_i.append(ci)
+    o_s, o_i = orc.merge(np.stack(parts_s), np.stack(parts_i), keep)
+
+    class _HostRows:  # rows of the device corpus fetched on demand for exact re-scoring
+        shape = (n, dim)
+
+        def __getitem__(self, r):
+            return from_dev(rows[int(r)])
+
+    qs = from_dev(q[sub])
+    probs = orc.check_topk(from_dev(s[sub]), from_dev(i[sub]), qs, _HostRows(), k, TOL,
+                           oracle=(o_s, o_i))
+    assert not probs, probs[:10]
+    planted_sub = planted[:32].cpu().numpy()
+    assert (o_i[:32, 0] == planted_sub).all()  # the oracle finds the planted rows too
 
 
 @pytest.mark.parametrize("n,lo", [(600_000, 0), (70_001, 256), (3000, 128)])
