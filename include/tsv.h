@@ -151,6 +151,23 @@ TSV_API int tsv_peer_set_timeout_ms(tsv_peer_group* g, int64_t ms);
 TSV_API int tsv_peer_status(tsv_peer_group* g, int* aborted);
 TSV_API int tsv_peer_destroy(tsv_peer_group* g);
 
+/* ---- Corpus-sharded search inside one process (several devices, or one device twice):
+ * shard g is an index on its own device holding global rows [id_offsets[g], ...). A search
+ * copies the queries (on device `root`, caller's stream) to every shard's device, runs K1 on
+ * each shard on the shard's own stream with global ids, writes the per-shard [B, k] lists
+ * straight into a gather buffer on the root over NVLink (peer access; staged copies where
+ * peers cannot map each other) and merges them there (K4) on the caller's stream. Buffers are
+ * sized at create time for B <= max_b, k <= max_k: the call allocates nothing.
+ * Replaces the reference executor's single "search" engine call (runtime.py:625-656 ->
+ * engines.py:105-109) for a corpus too large for one GPU; SURVEY.md §8(b) `tsv_sharded_search`.
+ * The shard indexes must outlive the handle. ---- */
+typedef struct tsv_sharded tsv_sharded;
+TSV_API int tsv_sharded_create(tsv_index* const* shards, const int64_t* id_offsets, int nshards,
+                               int root, int max_b, int max_k, tsv_sharded** out);
+TSV_API int tsv_sharded_search(tsv_sharded* sh, const void* q_dev, int q_dtype, int B, int k,
+                               float* scores_dev, int32_t* ids_dev, void* stream);
+TSV_API int tsv_sharded_destroy(tsv_sharded* sh);
+
 /* ---- K5: L2-normalise (normalize != 0) and cast rows to bf16. ---- */
 TSV_API int tsv_normalize_rows(const void* src_dev, int src_dtype, int64_t n, int dim, int normalize,
                        void* dst_bf16_dev, void* stream);

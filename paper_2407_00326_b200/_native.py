@@ -63,6 +63,9 @@ SIGNATURES = {
     "tsv_peer_set_timeout_ms": (c_int, [c_vp, c_i64]),
     "tsv_peer_status": (c_int, [c_vp, ctypes.POINTER(c_int)]),
     "tsv_peer_destroy": (c_int, [c_vp]),
+    "tsv_sharded_create": (c_int, [c_vp, c_vp, c_int, c_int, c_int, c_int, ctypes.POINTER(c_vp)]),
+    "tsv_sharded_search": (c_int, [c_vp, c_vp, c_int, c_int, c_int, c_vp, c_vp, c_vp]),
+    "tsv_sharded_destroy": (c_int, [c_vp]),
 }
 
 _lib = None

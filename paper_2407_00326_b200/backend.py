@@ -156,7 +156,10 @@ class RetrievalBackend:
     def __init__(self, dim: int, devices: list[int] | None = None, arena_rows: int = 1 << 20,
                  engines=("vdb-search0", "rerank0"), timing: str = TIMING_PROFILE,
                  data: SyntheticData | None = None, metric: str = "cosine",
-                 global_index: DeviceIndex | None = None):
+                 global_index=None):
+        """global_index: the resident corpus searched by Searching nodes that have no per-query
+        index input — a DeviceIndex, or a ShardedIndex spanning several devices (shards
+        searched concurrently, merged on its root device)."""
         if timing not in (TIMING_PROFILE, TIMING_MEASURED):
             raise ConfigParse(f"unknown timing mode {timing!r}")
         _native.load()
@@ -406,6 +409,9 @@ class RetrievalBackend:
             raise ConfigParse(f"per_query_top_k={kmax} exceeds the fused kernel's limit (128)")
         start.record(rep.stream)
         if use_global:
+            if self.global_index.device != rep.device:
+                raise ConfigParse(f"the global corpus is searched from {self.global_index.device}; "
+                                  f"bind the search engine's replicas there (got {rep.device})")
             scores, ids = self.global_index.search(q, kmax, stream=rep.stream)
         else:
             scores, ids = rep.arena.search_segmented(q, q_off, ranges, kmax, local_ids=True,

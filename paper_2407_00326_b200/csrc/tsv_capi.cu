@@ -1230,6 +1230,185 @@ int tsv_peer_destroy(tsv_peer_group* pg) {
   return TSV_OK;
 }
 
+}  // extern "C"
+
+// ---- corpus-sharded search within one process (single process, several devices) ----
+struct tsv_sharded {
+  struct Shard {
+    tsv_index* idx = nullptr;
+    int64_t id_offset = 0;
+    cudaStream_t stream = nullptr;  // the shard's own stream on its device
+    cudaEvent_t done = nullptr;     // shard's part of a call finished (root waits on it)
+    cudaEvent_t go = nullptr;       // recorded on the root stream: queries ready
+    void* q = nullptr;              // query copy on the shard's device (root's own otherwise)
+    float* part_s = nullptr;        // shard-local top-k, copied to root when not peer-writable
+    int32_t* part_i = nullptr;
+    bool direct = false;            // the shard writes straight into root memory (peer access)
+  };
+  std::vector<Shard> shards;
+  int root = 0, dim = 0, max_b = 0, max_k = 0;
+  float* gather_s = nullptr;  // [G][max_b][max_k] on root (slot stride B*k per call)
+  int32_t* gather_i = nullptr;
+};
+
+extern "C" {
+
+int tsv_sharded_create(tsv_index* const* shards, const int64_t* id_offsets, int nshards, int root,
+                       int max_b, int max_k, tsv_sharded** out) {
+  if (out == nullptr || shards == nullptr || id_offsets == nullptr)
+    return fail(TSV_ERR_ARGUMENT, "null argument");
+  *out = nullptr;
+  if (nshards < 1 || nshards > 64) return fail(TSV_ERR_CONFIG, "bad shard count %d", nshards);
+  if (max_b <= 0 || max_k <= 0 || max_k > tsv::kMaxK)
+    return fail(TSV_ERR_CAPACITY, "bad max_b/max_k %d/%d", max_b, max_k);
+  if (static_cast<int64_t>(nshards) * max_k > kMergeCap)
+    return fail(TSV_ERR_CAPACITY, "%d shards x k=%d exceed the merge capacity", nshards, max_k);
+  int ndev = 0;
+  TSV_CUDA(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+  if (root < 0 || root >= ndev) return fail(TSV_ERR_CONFIG, "bad root device %d", root);
+  for (int g = 0; g < nshards; ++g) {
+    if (shards[g] == nullptr) return fail(TSV_ERR_ARGUMENT, "shard %d is null", g);
+    if (shards[g]->dim != shards[0]->dim || shards[g]->metric != shards[0]->metric ||
+        shards[g]->storage != shards[0]->storage)
+      return fail(TSV_ERR_CONFIG, "shard %d differs in dim / metric / storage", g);
+  }
+  auto* sh = new tsv_sharded();
+  sh->root = root;
+  sh->dim = shards[0]->dim;
+  sh->max_b = max_b;
+  sh->max_k = max_k;
+  auto cleanup = [&](int rc) {
+    tsv_sharded_destroy(sh);
+    return rc;
+  };
+  sh->shards.resize(nshards);
+  {
+    DeviceGuard g(root);
+    const size_t n = static_cast<size_t>(nshards) * max_b * max_k;
+    cudaError_t e = cudaMalloc(&sh->gather_s, n * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc(&sh->gather_i, n * sizeof(int32_t));
+    if (e != cudaSuccess) return cleanup(cuda_fail(e, "gather buffer"));
+  }
+  for (int g = 0; g < nshards; ++g) {
+    auto& s = sh->shards[g];
+    s.idx = shards[g];
+    s.id_offset = id_offsets[g];
+    const int dev = s.idx->device;
+    DeviceGuard guard(dev);
+    cudaError_t e = cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cleanup(cuda_fail(e, "shard stream"));
+    {
+      DeviceGuard rg(root);
+      e = cudaEventCreateWithFlags(&s.go, cudaEventDisableTiming);
+      if (e != cudaSuccess) return cleanup(cuda_fail(e, "shard event"));
+    }
+    if (dev != root) {
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, dev, root);
+      if (can) {
+        e = cudaDeviceEnablePeerAccess(root, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) {
+          cudaGetLastError();
+          e = cudaSuccess;
+        }
+        s.direct = e == cudaSuccess;
+        if (e != cudaSuccess) cudaGetLastError();
+      }
+      // queries arrive as bf16 or f32: room for the wider one
+      e = cudaMalloc(&s.q, static_cast<size_t>(max_b) * sh->dim * 4);
+      if (e == cudaSuccess && !s.direct) {
+        e = cudaMalloc(&s.part_s, static_cast<size_t>(max_b) * max_k * sizeof(float));
+        if (e == cudaSuccess) e = cudaMalloc(&s.part_i, static_cast<size_t>(max_b) * max_k * sizeof(int32_t));
+      }
+      if (e != cudaSuccess) return cleanup(cuda_fail(e, "shard buffers"));
+    } else {
+      s.direct = true;
+    }
+  }
+  *out = sh;
+  return TSV_OK;
+}
+
+int tsv_sharded_search(tsv_sharded* sh, const void* q_dev, int q_dtype, int B, int k,
+                       float* scores_dev, int32_t* ids_dev, void* stream) {
+  if (sh == nullptr) return fail(TSV_ERR_ARGUMENT, "sharded index is null");
+  int rc = check_dtype(q_dtype);
+  if (rc) return rc;
+  if (B <= 0) return fail(TSV_ERR_CAPACITY, "empty batch");
+  if (k <= 0) return fail(TSV_ERR_CONFIG, "k must be >= 1");
+  if (B > sh->max_b || k > sh->max_k)
+    return fail(TSV_ERR_CAPACITY, "B=%d / k=%d exceed the sharded index's %d / %d", B, k,
+                sh->max_b, sh->max_k);
+  if (q_dev == nullptr || scores_dev == nullptr || ids_dev == nullptr)
+    return fail(TSV_ERR_ARGUMENT, "null buffer");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int G = static_cast<int>(sh->shards.size());
+  const size_t qbytes = static_cast<size_t>(B) * sh->dim * (q_dtype == TSV_F32 ? 4 : 2);
+  const size_t plane = static_cast<size_t>(B) * k;
+  // 1. every shard stream waits for the caller's queries (stream order on the root)
+  {
+    DeviceGuard g(sh->root);
+    for (auto& s : sh->shards) TSV_CUDA(cudaEventRecord(s.go, st), "cudaEventRecord");
+  }
+  // 2. per shard: queries to its device, fused scan + top-k with global ids, results to root
+  for (int gi = 0; gi < G; ++gi) {
+    auto& s = sh->shards[gi];
+    DeviceGuard g(s.idx->device);
+    TSV_CUDA(cudaStreamWaitEvent(s.stream, s.go, 0), "cudaStreamWaitEvent");
+    const void* q = q_dev;
+    if (s.idx->device != sh->root) {
+      TSV_CUDA(cudaMemcpyPeerAsync(s.q, s.idx->device, q_dev, sh->root, qbytes, s.stream),
+               "query copy to shard");
+      q = s.q;
+    }
+    float* os = s.direct ? sh->gather_s + gi * plane : s.part_s;
+    int32_t* oi = s.direct ? sh->gather_i + gi * plane : s.part_i;
+    rc = tsv_search(s.idx, q, q_dtype, B, k, 0, s.idx->rows,
+                    static_cast<int32_t>(s.id_offset), os, oi, s.stream);
+    if (rc) return rc;
+    if (!s.direct) {
+      TSV_CUDA(cudaMemcpyPeerAsync(sh->gather_s + gi * plane, sh->root, s.part_s, s.idx->device,
+                                   plane * sizeof(float), s.stream), "result copy to root");
+      TSV_CUDA(cudaMemcpyPeerAsync(sh->gather_i + gi * plane, sh->root, s.part_i, s.idx->device,
+                                   plane * sizeof(int32_t), s.stream), "result copy to root");
+    }
+    TSV_CUDA(cudaEventRecord(s.done, s.stream), "cudaEventRecord");
+  }
+  // 3. the caller's stream waits for every shard, then merges G x k -> k (K4)
+  DeviceGuard g(sh->root);
+  for (auto& s : sh->shards) TSV_CUDA(cudaStreamWaitEvent(st, s.done, 0), "cudaStreamWaitEvent");
+  int e = tsv::launch_merge_topk(sh->gather_s, sh->gather_i, G, B, k, B, k, scores_dev, ids_dev,
+                                 st);
+  if (e) return cuda_fail(static_cast<cudaError_t>(e), "merge launch");
+  g_launches++;
+  return TSV_OK;
+}
+
+int tsv_sharded_destroy(tsv_sharded* sh) {
+  if (sh == nullptr) return TSV_OK;
+  for (auto& s : sh->shards) {
+    if (s.idx == nullptr) continue;
+    DeviceGuard g(s.idx->device);
+    if (s.stream) {
+      cudaStreamSynchronize(s.stream);
+      cudaStreamDestroy(s.stream);
+    }
+    if (s.done) cudaEventDestroy(s.done);
+    if (s.go) cudaEventDestroy(s.go);
+    if (s.q) cudaFree(s.q);
+    if (s.part_s) cudaFree(s.part_s);
+    if (s.part_i) cudaFree(s.part_i);
+  }
+  {
+    DeviceGuard g(sh->root);
+    if (sh->gather_s) cudaFree(sh->gather_s);
+    if (sh->gather_i) cudaFree(sh->gather_i);
+  }
+  delete sh;
+  return TSV_OK;
+}
+
 int tsv_normalize_rows(const void* src_dev, int src_dtype, int64_t n, int dim, int normalize,
                        void* dst_bf16_dev, void* stream) {
   int rc = check_dtype(src_dtype);

@@ -25,6 +25,36 @@ namespace {
 
 constexpr int kLockWindow = 2;  // 256-row tiles a worker may run ahead of its range partners
 
+// Range lockstep is a cache optimisation, never a correctness requirement: the launch is not
+// cooperative, so a partner CTA may not be resident (another kernel holds SMs: concurrent
+// scans on two streams, MPS, green contexts). A wait that sees no progress for kLockSpinNs
+// gives up and the waiter runs the rest of its item unlocked (it keeps publishing its own
+// progress for partners that do wait). Co-resident partners are never more than a tile or two
+// (~15-30 us at D=1024) behind, so the bound only fires when a partner cannot run.
+constexpr uint64_t kLockSpinNs = 200 * 1000;
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Wait until *progress >= target; false when it stalled for kLockSpinNs (partner not running).
+__device__ __forceinline__ bool lock_wait(volatile int32_t* progress, int64_t target) {
+  if (*progress >= target) return true;
+  int32_t seen = *progress;
+  uint64_t t0 = global_ns();
+  while (true) {
+    __nanosleep(256);
+    const int32_t now = *progress;
+    if (now >= target) return true;
+    if (now != seen) {  // partner moving: restart the stall clock
+      seen = now;
+      t0 = global_ns();
+    } else if (global_ns() - t0 > kLockSpinNs) {
+      return false;
+    }
+  }
+}
+
 // Lists of more than kRegListMax entries live in shared memory (one column per query thread,
 // entry j of thread t at [j * 128 + t], so lock-step accesses are bank-conflict free).
 constexpr int kRegListMax = 32;
@@ -378,13 +408,14 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32, NB>::kThreads, 1)
       const int64_t ntiles = (it.row_end - it.row_begin + kTileN - 1) / kTileN;
       const int my_qg = p.R > 0 ? i / p.R : 0, my_r = p.R > 0 ? i - my_qg * p.R : 0;
       const int nqg = p.R > 0 ? num_items / p.R : 1;
+      bool lock_live = lockstep;  // cleared when a partner is not progressing (see below)
       for (int64_t t = 0; t < ntiles; ++t) {
         if (lockstep && lane == 0) {
           if ((t & 3) == 0) progress[i] = static_cast<int32_t>(t);
-          if (t >= 2 * kLockWindow) {
-            for (int g = 0; g < nqg; ++g)
+          if (lock_live && t >= 2 * kLockWindow) {
+            for (int g = 0; g < nqg && lock_live; ++g)
               if (g != my_qg)
-                while (progress[g * p.R + my_r] < t - 2 * kLockWindow) __nanosleep(256);
+                lock_live = lock_wait(progress + g * p.R + my_r, t - 2 * kLockWindow);
           }
         }
         __syncwarp();
@@ -759,16 +790,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
       const int my_qg = range_major ? i % nqg : i / p.R;
       const int my_r = range_major ? i / nqg : i - my_qg * p.R;
       const int round = i / npairs;
+      bool lock_live = lockstep;  // cleared when a partner is not progressing (see below)
       for (int64_t t = 0; t < ntiles; ++t) {
         if (lockstep && leader && lane == 0) {
           const int w = p.lock_window > 0 ? p.lock_window : kLockWindow;
           if ((t & 1) == 0) progress[i] = static_cast<int32_t>(t);
-          if (t >= w) {
-            for (int g = 0; g < nqg; ++g) {
+          if (lock_live && t >= w) {
+            for (int g = 0; g < nqg && lock_live; ++g) {
               if (g == my_qg) continue;
               const int j = range_major ? my_r * nqg + g : g * p.R + my_r;
               if (j / npairs != round) continue;
-              while (progress[j] < t - w) __nanosleep(256);
+              lock_live = lock_wait(progress + j, t - w);
             }
           }
         }

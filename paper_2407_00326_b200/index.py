@@ -32,6 +32,23 @@ def _require_cuda(t: torch.Tensor, name: str) -> None:
         raise ConfigParse(f"{name} must be contiguous")
 
 
+def _check_out(out, B: int, k: int, device: torch.device) -> None:
+    """Caller-provided result buffers: contiguous float32 scores / int32 ids [B, k] on the
+    index's device (the kernels write B * k entries through raw pointers)."""
+    if not isinstance(out, (tuple, list)) or len(out) != 2:
+        raise ConfigParse("out must be a (scores, ids) pair")
+    s, i = out
+    for t, name, dt in ((s, "out scores", torch.float32), (i, "out ids", torch.int32)):
+        if not isinstance(t, torch.Tensor) or t.dtype != dt:
+            raise ConfigParse(f"{name} must be a {dt} tensor")
+        if tuple(t.shape) != (B, k):
+            raise ConfigParse(f"{name} must have shape {(B, k)}, got {tuple(t.shape)}")
+        if not t.is_cuda or t.device != device:
+            raise DeviceError(f"{name} must be on {device}")
+        if not t.is_contiguous():
+            raise ConfigParse(f"{name} must be contiguous")
+
+
 def _stream_handle(stream: torch.cuda.Stream | None, device: torch.device) -> int:
     s = stream if stream is not None else torch.cuda.current_stream(device)
     return s.cuda_stream
@@ -157,6 +174,8 @@ class DeviceIndex:
     # -- primitives ----------------------------------------------------------
     def _check_queries(self, q: torch.Tensor) -> None:
         _require_cuda(q, "queries")
+        if q.device != self.device:
+            raise DeviceError(f"queries are on {q.device}, the index on {self.device}")
         if q.dim() != 2 or q.shape[1] != self.dim:
             raise ConfigParse(f"queries must be [B, {self.dim}]")
         if q.shape[0] == 0:
@@ -173,6 +192,7 @@ class DeviceIndex:
             scores = torch.empty((B, k), dtype=torch.float32, device=self.device)
             ids = torch.empty((B, k), dtype=torch.int32, device=self.device)
         else:
+            _check_out(out, B, int(k), self.device)
             scores, ids = out
         nat.check(nat.load().tsv_search(self._h, q.data_ptr(), _dtype_code(q), B, int(k), int(lo),
                                         int(hi), int(id_offset), scores.data_ptr(), ids.data_ptr(),
@@ -198,6 +218,7 @@ class DeviceIndex:
             scores = torch.empty((B, k), dtype=torch.float32, device=self.device)
             ids = torch.empty((B, k), dtype=torch.int32, device=self.device)
         else:
+            _check_out(out, B, int(k), self.device)
             scores, ids = out
         nat.check(nat.load().tsv_search_segmented(
             self._h, q.data_ptr(), _dtype_code(q), nseg, ctypes.cast(qo, ctypes.c_void_p),
@@ -214,11 +235,14 @@ class DeviceIndex:
         _require_cuda(cand_ids, "cand_ids")
         if cand_ids.dtype != torch.int32 or cand_ids.dim() != 2 or cand_ids.shape[0] != q.shape[0]:
             raise ConfigParse("cand_ids must be int32 [B, C]")
+        if cand_ids.device != self.device:
+            raise DeviceError(f"cand_ids are on {cand_ids.device}, the index on {self.device}")
         B, C = cand_ids.shape
         if out is None:
             scores = torch.empty((B, k), dtype=torch.float32, device=self.device)
             ids = torch.empty((B, k), dtype=torch.int32, device=self.device)
         else:
+            _check_out(out, B, int(k), self.device)
             scores, ids = out
         nat.check(nat.load().tsv_rerank(self._h, q.data_ptr(), _dtype_code(q), B,
                                         cand_ids.data_ptr(), C, int(k), scores.data_ptr(),

@@ -183,3 +183,80 @@ class ShardedSearch:
     def exchange_bytes(self, B: int, k: int) -> int:
         """Bytes each rank receives per step in the all-gather."""
         return (self.world - 1) * B * k * 8
+
+
+class ShardedIndex:
+    """A corpus split over several devices inside ONE process (tsv_sharded_* in the C ABI).
+
+    Shard g is a DeviceIndex on its own device holding the global rows [offsets[g],
+    offsets[g] + rows_g). `search` runs the fused scan + top-k (K1) on every shard on the
+    shard's own stream with global ids, gathers the per-shard lists on the root device over
+    NVLink (peer writes) and merges them there (K4), stream-ordered on the caller's stream:
+    the same result as one index holding every row. This is the single-process counterpart of
+    `ShardedSearch` (one process per GPU), so the single-process executor (`Simulator._execute`,
+    reference runtime.py:625-656) can serve a corpus larger than one GPU.
+    One device may hold several shards (the shards then run concurrently on its SMs)."""
+
+    def __init__(self, shards, root: int | None = None, max_batch: int = 4096, max_k: int = 128,
+                 id_offsets=None):
+        from . import _native as nat
+        from .errors import ConfigParse
+
+        if not shards:
+            raise ConfigParse("a sharded index needs at least one shard")
+        self.lib = nat.load()
+        self._check = nat.check
+        self.shards = list(shards)
+        self.dim = self.shards[0].dim
+        self.metric = self.shards[0].metric
+        if id_offsets is None:
+            id_offsets, acc = [], 0
+            for s in self.shards:
+                id_offsets.append(acc)
+                acc += s.rows
+        self.offsets = [int(x) for x in id_offsets]
+        self.device = torch.device("cuda", self.shards[0].device.index if root is None else root)
+        self.max_batch, self.max_k = int(max_batch), int(max_k)
+        hs = (ctypes.c_void_p * len(self.shards))(*[s._h.value for s in self.shards])
+        offs = (ctypes.c_int64 * len(self.shards))(*self.offsets)
+        self._h = ctypes.c_void_p()
+        self._check(self.lib.tsv_sharded_create(hs, offs, len(self.shards), self.device.index,
+                                                self.max_batch, self.max_k,
+                                                ctypes.byref(self._h)))
+
+    @property
+    def rows(self) -> int:
+        return sum(s.rows for s in self.shards)
+
+    def search(self, q: torch.Tensor, k: int, stream: torch.cuda.Stream | None = None,
+               out: tuple[torch.Tensor, torch.Tensor] | None = None):
+        """Global top-k of q ([B, dim] bf16 / f32 on the root device) over every shard."""
+        from .errors import CapacityExceeded, ConfigParse, DeviceError
+        from .index import _check_out, _dtype_code
+
+        if not q.is_cuda or q.device != self.device:
+            raise DeviceError(f"queries must be on the root device {self.device}")
+        if q.dim() != 2 or q.shape[1] != self.dim or not q.is_contiguous():
+            raise ConfigParse(f"queries must be a contiguous [B, {self.dim}] matrix")
+        if q.shape[0] == 0:
+            raise CapacityExceeded("empty batch")
+        B = q.shape[0]
+        if out is None:
+            out = (torch.empty((B, k), dtype=torch.float32, device=self.device),
+                   torch.empty((B, k), dtype=torch.int32, device=self.device))
+        _check_out(out, B, k, self.device)
+        st = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        self._check(self.lib.tsv_sharded_search(self._h, q.data_ptr(), _dtype_code(q), B, int(k),
+                                                out[0].data_ptr(), out[1].data_ptr(), st))
+        return out
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self.lib.tsv_sharded_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
