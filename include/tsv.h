@@ -119,6 +119,13 @@ TSV_API int tsv_search_segmented(tsv_index* idx, const void* q_dev, int q_dtype,
  * candidate arena rows cand_ids_dev[b, :] (id < 0 ignored), drop duplicate ids, keep k. ---- */
 TSV_API int tsv_rerank(tsv_index* idx, const void* q_dev, int q_dtype, int B, const int32_t* cand_ids_dev,
                int C, int k, float* scores_dev, int32_t* ids_dev, void* stream);
+/* K3 over per-query indexes: question b's candidate ids are rows of its own index segment,
+ * i.e. arena row = row_offsets_dev[b] + id (device int32 [B]); the returned ids stay
+ * segment-local, as the Searching stages that produced the candidates emitted them. A batch of
+ * Reranking requests from different queries is one launch. */
+TSV_API int tsv_rerank_segmented(tsv_index* idx, const void* q_dev, int q_dtype, int B,
+                                 const int32_t* cand_ids_dev, int C, const int32_t* row_offsets_dev,
+                                 int k, float* scores_dev, int32_t* ids_dev, void* stream);
 
 /* ---- K4: merge `lists` sorted lists per query. Input layout [lists][B][kin]; output [B][kout].
  * This is the Aggregate join of split Searching stages (optimizer.py:620-661,

@@ -1035,8 +1035,9 @@ int tsv_search_segmented(tsv_index* idx, const void* q_dev, int q_dtype, int nse
   return TSV_OK;
 }
 
-int tsv_rerank(tsv_index* idx, const void* q_dev, int q_dtype, int B, const int32_t* cand_ids_dev,
-               int C, int k, float* scores_dev, int32_t* ids_dev, void* stream) {
+static int rerank_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B,
+                       const int32_t* cand_ids_dev, int C, const int32_t* row_offsets_dev, int k,
+                       float* scores_dev, int32_t* ids_dev, void* stream) {
   if (idx == nullptr) return fail(TSV_ERR_ARGUMENT, "index is null");
   int rc = check_dtype(q_dtype);
   if (rc) return rc;
@@ -1064,14 +1065,36 @@ int tsv_rerank(tsv_index* idx, const void* q_dev, int q_dtype, int B, const int3
     if (rc) return rc;
     q_f32 = 0;
   }
-  int e = tsv::launch_rerank(f32 ? nullptr : idx->arena,
-                             f32 ? static_cast<const float*>(idx->arena) : nullptr,
-                             f32 ? idx->arena_lo : nullptr, idx->rows, idx->dim, q, q_lo, q_f32,
-                             B, cand_ids_dev, C, k, scores_dev, ids_dev, st,
-                             idx->storage == TSV_BF16_TILED);
+  const bool tiled = idx->storage == TSV_BF16_TILED;
+  int e;
+  // (rows up to 4 KB: two ring slots per warp fit next to the question vector)
+  if (!f32 && idx->dim <= 2048 && !env_flag("TSV_RERANK_LDG")) {
+    // bf16 arenas: gather pipelined through per-warp shared-memory rings (cp.async)
+    e = tsv::launch_rerank_ring(idx->arena, idx->rows, idx->dim, q, q_f32, B, cand_ids_dev, C, k,
+                                row_offsets_dev, scores_dev, ids_dev, st, tiled);
+  } else {
+    e = tsv::launch_rerank(f32 ? nullptr : idx->arena,
+                           f32 ? static_cast<const float*>(idx->arena) : nullptr,
+                           f32 ? idx->arena_lo : nullptr, idx->rows, idx->dim, q, q_lo, q_f32, B,
+                           cand_ids_dev, C, k, scores_dev, ids_dev, st, tiled, row_offsets_dev);
+  }
   if (e) return cuda_fail(static_cast<cudaError_t>(e), "rerank launch");
   g_launches++;
   return TSV_OK;
+}
+
+int tsv_rerank(tsv_index* idx, const void* q_dev, int q_dtype, int B, const int32_t* cand_ids_dev,
+               int C, int k, float* scores_dev, int32_t* ids_dev, void* stream) {
+  return rerank_impl(idx, q_dev, q_dtype, B, cand_ids_dev, C, nullptr, k, scores_dev, ids_dev,
+                     stream);
+}
+
+int tsv_rerank_segmented(tsv_index* idx, const void* q_dev, int q_dtype, int B,
+                         const int32_t* cand_ids_dev, int C, const int32_t* row_offsets_dev, int k,
+                         float* scores_dev, int32_t* ids_dev, void* stream) {
+  if (row_offsets_dev == nullptr) return fail(TSV_ERR_ARGUMENT, "row_offsets_dev is null");
+  return rerank_impl(idx, q_dev, q_dtype, B, cand_ids_dev, C, row_offsets_dev, k, scores_dev,
+                     ids_dev, stream);
 }
 
 int tsv_merge_topk(const float* in_scores, const int32_t* in_ids, int lists, int B, int kin,

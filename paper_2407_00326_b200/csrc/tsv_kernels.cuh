@@ -163,7 +163,13 @@ int launch_merge_topk(const float* in_s, const int32_t* in_id, int lists, int B,
 int launch_rerank(const void* arena, const float* arena_hi, const float* arena_lo, int64_t nrows,
                   int dim, const void* q, const float* q_lo, int q_is_f32, int B,
                   const int32_t* cand, int C, int k, float* out_s, int32_t* out_id,
-                  cudaStream_t stream, int tiled = 0);
+                  cudaStream_t stream, int tiled = 0, const int32_t* offs = nullptr);
+
+// K3 over a bf16 arena with the gather pipelined through shared memory (cp.async rings);
+// offs (optional, device [B]): candidate ids of question b are relative to arena row offs[b].
+int launch_rerank_ring(const void* arena, int64_t nrows, int dim, const void* q, int q_is_f32,
+                       int B, const int32_t* cand, int C, int k, const int32_t* offs,
+                       float* out_s, int32_t* out_id, cudaStream_t stream, int tiled);
 
 int launch_normalize(const void* src, int src_is_f32, int64_t n, int dim, int do_normalize,
                      void* dst_bf16, cudaStream_t stream);

@@ -322,7 +322,8 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(
     const __nv_bfloat16* __restrict__ arena, const float* __restrict__ arena_hi,
     const float* __restrict__ arena_lo, int64_t nrows, int dim, const void* __restrict__ q,
     const float* __restrict__ q_lo, int q_is_f32, const int32_t* __restrict__ cand, int C, int k,
-    float* __restrict__ out_s, int32_t* __restrict__ out_id, int tiled) {
+    float* __restrict__ out_s, int32_t* __restrict__ out_id, int tiled,
+    const int32_t* __restrict__ offs) {
   extern __shared__ uint8_t sm[];
   float* qv = reinterpret_cast<float*>(sm);                       // dim floats
   uint64_t* keys = reinterpret_cast<uint64_t*>(sm + ((dim * 4 + 15) & ~15));
@@ -334,6 +335,7 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(
 
   // the question vector and the candidate ids are staged once, so the gather loop below waits
   // on one memory round trip per batch of rows instead of two
+  const int64_t base = offs != nullptr ? __ldg(offs + b) : 0;  // per-question segment start
   for (int c = threadIdx.x; c < C; c += kThreads) ids[c] = __ldg(cand + static_cast<int64_t>(b) * C + c);
   for (int d = threadIdx.x; d < dim; d += kThreads) {
     const int64_t o = static_cast<int64_t>(b) * dim + d;
@@ -354,15 +356,15 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
       id[u] = c0 + u < C ? ids[c0 + u] : -1;
-      ok[u] = id[u] >= 0 && id[u] < nrows;  // warp-uniform
+      ok[u] = id[u] >= 0 && base + id[u] < nrows;  // warp-uniform
       acc[u] = 0.f;
     }
     if (arena_hi != nullptr) {  // fp32 storage: row = hi + lo, fp32 FMA
 #pragma unroll
       for (int u = 0; u < kPer; ++u) {
         if (!ok[u]) continue;
-        const float4* hi = reinterpret_cast<const float4*>(arena_hi + static_cast<int64_t>(id[u]) * dim);
-        const float4* lo = reinterpret_cast<const float4*>(arena_lo + static_cast<int64_t>(id[u]) * dim);
+        const float4* hi = reinterpret_cast<const float4*>(arena_hi + (base + id[u]) * dim);
+        const float4* lo = reinterpret_cast<const float4*>(arena_lo + (base + id[u]) * dim);
         for (int ch = lane; ch < (dim >> 2); ch += 32) {
           const float4 h = __ldg(hi + ch), l = __ldg(lo + ch);
           const float* qq = qv + ch * 4;
@@ -376,7 +378,7 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(
       const uint4* row[kPer];
 #pragma unroll
       for (int u = 0; u < kPer; ++u) {
-        const int64_t r = ok[u] ? id[u] : 0;
+        const int64_t r = ok[u] ? base + id[u] : 0;
         // tiled layout: 16-byte chunk ch of row r lives in k-block tile (r/128, ch/8)
         row[u] = tiled ? reinterpret_cast<const uint4*>(
                              arena + ((r >> 7) * kb_per_row * 128 + (r & 127)) * 64)
@@ -413,6 +415,126 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(
   if (threadIdx.x == 0) {
     int w = 0;
     int32_t last = -2;
+    for (int i = 0; i < np && w < k; ++i) {
+      const int32_t id = key_id(keys[i]);
+      if (id < 0) break;
+      if (id == last) continue;
+      last = id;
+      out_s[static_cast<int64_t>(b) * k + w] = key_score(keys[i]);
+      out_id[static_cast<int64_t>(b) * k + w] = id;
+      ++w;
+    }
+    for (; w < k; ++w) {
+      out_s[static_cast<int64_t>(b) * k + w] = -INFINITY;
+      out_id[static_cast<int64_t>(b) * k + w] = -1;
+    }
+  }
+}
+
+// K3, bf16 arenas: the same computation as rerank_kernel with the gather pipelined through
+// shared memory. Each warp owns a ring of `slots` row buffers and walks its candidates
+// (c = warp, warp + kWarps, ...): it keeps `slots` rows in flight with cp.async (16-byte
+// LDGSTS per lane, no registers held) and scores the oldest as soon as it lands, then refills
+// that slot. A warp therefore never idles between a round trip and the next: the memory
+// system sees ~slots rows per warp continuously instead of bursts of 2 rows per round trip
+// (the register-gather kernel's 5 dependent rounds for C = 200).
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int kWarps, int kSlots>
+__global__ void __launch_bounds__(kWarps * 32) rerank_ring_kernel(
+    const __nv_bfloat16* __restrict__ arena, int64_t nrows, int dim, const void* __restrict__ q,
+    int q_is_f32, const int32_t* __restrict__ cand, int C, int k, const int32_t* __restrict__ offs,
+    float* __restrict__ out_s, int32_t* __restrict__ out_id, int tiled) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int row_bytes = dim * 2;
+  uint8_t* ring = sm;                                                   // [kWarps][kSlots][row]
+  float* qv = reinterpret_cast<float*>(sm + static_cast<size_t>(kWarps) * kSlots * row_bytes);
+  uint64_t* keys = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(qv) + ((dim * 4 + 15) & ~15));
+  const int np = pow2_ceil(C);
+  int32_t* ids = reinterpret_cast<int32_t*>(keys + np);                 // arena rows
+  const int b = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t base = offs != nullptr ? __ldg(offs + b) : 0;  // per-question segment start
+  for (int c = threadIdx.x; c < C; c += kWarps * 32) {
+    const int32_t id = __ldg(cand + static_cast<int64_t>(b) * C + c);
+    ids[c] = id;
+  }
+  for (int i = threadIdx.x; i < np; i += kWarps * 32) keys[i] = pad_key();
+  __syncthreads();
+
+  const int chunks = dim >> 3;  // 16-byte chunks per row
+  const int64_t kb_per_row = (dim + 63) >> 6;
+  uint8_t* my_ring = ring + static_cast<size_t>(warp) * kSlots * row_bytes;
+  auto row_ptr = [&](int64_t r) -> const uint4* {
+    return tiled ? reinterpret_cast<const uint4*>(arena + ((r >> 7) * kb_per_row * 128 + (r & 127)) * 64)
+                 : reinterpret_cast<const uint4*>(arena + r * dim);
+  };
+  auto valid = [&](int c) {
+    if (c >= C) return false;
+    const int32_t id = ids[c];
+    return id >= 0 && base + id < nrows;
+  };
+  auto issue = [&](int c, int slot) {  // whole warp; always commits one group
+    if (valid(c)) {
+      const uint4* src = row_ptr(base + ids[c]);
+      uint4* dst = reinterpret_cast<uint4*>(my_ring + static_cast<size_t>(slot) * row_bytes);
+      for (int ch = lane; ch < chunks; ch += 32) {
+        const int64_t off = tiled ? static_cast<int64_t>(ch >> 3) * 1024 + (ch & 7) : ch;
+        cp_async16(dst + ch, src + off);
+      }
+    }
+    cp_async_commit();
+  };
+  // my candidates: c = warp + j * kWarps
+#pragma unroll
+  for (int s = 0; s < kSlots; ++s) issue(warp + s * kWarps, s);
+  // the question vector (fp32) while the first rows are in flight
+  for (int d = threadIdx.x; d < dim; d += kWarps * 32) {
+    const int64_t o = static_cast<int64_t>(b) * dim + d;
+    qv[d] = q_is_f32 ? reinterpret_cast<const float*>(q)[o]
+                     : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(q)[o]);
+  }
+  __syncthreads();
+  int slot = 0;
+  for (int c = warp; c < C; c += kWarps) {
+    cp_async_wait<kSlots - 1>();  // the oldest group (candidate c) has landed
+    __syncwarp();
+    float acc = 0.f;
+    if (valid(c)) {
+      const uint4* row = reinterpret_cast<const uint4*>(my_ring + static_cast<size_t>(slot) * row_bytes);
+      for (int ch = lane; ch < chunks; ch += 32) {
+        const uint4 raw = row[ch];
+        const float* qq = qv + ch * 8;
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const float2 f = __bfloat1622float2(h[t]);
+          acc = fmaf(f.x, qq[2 * t], acc);
+          acc = fmaf(f.y, qq[2 * t + 1], acc);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) keys[c] = make_key(acc, ids[c]);
+    }
+    __syncwarp();  // every lane done reading the slot before it is refilled
+    issue(c + kSlots * kWarps, slot);
+    if (++slot == kSlots) slot = 0;
+  }
+  cp_async_wait<0>();
+  bitonic_sort_desc_fast(keys, np);
+  // Dedup: duplicates of one id carry identical scores, so they are adjacent after the sort.
+  if (threadIdx.x == 0) {
+    int w = 0;
+    int32_t last = INT32_MIN;
     for (int i = 0; i < np && w < k; ++i) {
       const int32_t id = key_id(keys[i]);
       if (id < 0) break;
@@ -772,7 +894,7 @@ template <int kThreads, int kPer, int kUnroll>
 int launch_rerank_v(const void* arena, const float* arena_hi, const float* arena_lo, int64_t nrows,
                     int dim, const void* q, const float* q_lo, int q_is_f32, int B,
                     const int32_t* cand, int C, int k, float* out_s, int32_t* out_id,
-                    cudaStream_t stream, int tiled, size_t smem) {
+                    cudaStream_t stream, int tiled, size_t smem, const int32_t* offs) {
   auto kern = rerank_kernel<kThreads, kPer, kUnroll>;
   static std::atomic<uint64_t> configured{0};
   if (smem > 48 * 1024 && first_on_device(configured)) {
@@ -781,14 +903,14 @@ int launch_rerank_v(const void* arena, const float* arena_hi, const float* arena
   }
   kern<<<B, kThreads, smem, stream>>>(reinterpret_cast<const __nv_bfloat16*>(arena), arena_hi,
                                       arena_lo, nrows, dim, q, q_lo, q_is_f32, cand, C, k, out_s,
-                                      out_id, tiled);
+                                      out_id, tiled, offs);
   return static_cast<int>(cudaGetLastError());
 }
 
 int launch_rerank(const void* arena, const float* arena_hi, const float* arena_lo, int64_t nrows,
                   int dim, const void* q, const float* q_lo, int q_is_f32, int B,
                   const int32_t* cand, int C, int k, float* out_s, int32_t* out_id,
-                  cudaStream_t stream, int tiled) {
+                  cudaStream_t stream, int tiled, const int32_t* offs) {
   if (B <= 0) return 0;
   int np = 1;
   while (np < C) np <<= 1;
@@ -799,7 +921,51 @@ int launch_rerank(const void* arena, const float* arena_hi, const float* arena_l
   // flight at once for dim <= 1024), two blocks per SM: C=200 takes 5 iterations. Measured at
   // C3 (256 x 200 x 768, rows from HBM): 24.8 us vs 32.6 with 16 warps x 4 rows, unroll 2.
   return launch_rerank_v<640, 2, 4>(arena, arena_hi, arena_lo, nrows, dim, q, q_lo, q_is_f32, B,
-                                    cand, C, k, out_s, out_id, stream, tiled, smem);
+                                    cand, C, k, out_s, out_id, stream, tiled, smem, offs);
+}
+
+template <int kWarps, int kSlots>
+int launch_rerank_ring_v(const void* arena, int64_t nrows, int dim, const void* q, int q_is_f32,
+                         int B, const int32_t* cand, int C, int k, const int32_t* offs,
+                         float* out_s, int32_t* out_id, cudaStream_t stream, int tiled) {
+  int np = 1;
+  while (np < C) np <<= 1;
+  const size_t smem = static_cast<size_t>(kWarps) * kSlots * dim * 2 +
+                      ((static_cast<size_t>(dim) * 4 + 15) & ~size_t(15)) + np * sizeof(uint64_t) +
+                      static_cast<size_t>(C) * sizeof(int32_t);
+  if (smem > 220 * 1024) return static_cast<int>(cudaErrorInvalidValue);
+  auto kern = rerank_ring_kernel<kWarps, kSlots>;
+  static std::atomic<uint64_t> configured{0};
+  if (smem > 48 * 1024 && first_on_device(configured)) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    if (e != cudaSuccess) return static_cast<int>(e);
+  }
+  kern<<<B, kWarps * 32, smem, stream>>>(reinterpret_cast<const __nv_bfloat16*>(arena), nrows, dim,
+                                         q, q_is_f32, cand, C, k, offs, out_s, out_id, tiled);
+  return static_cast<int>(cudaGetLastError());
+}
+
+// Pipelined gather (bf16 arenas). Ring depth per warp from the row size: ~96 KB of rows in
+// flight per block (two blocks per SM up to dim 1024).
+int launch_rerank_ring(const void* arena, int64_t nrows, int dim, const void* q, int q_is_f32,
+                       int B, const int32_t* cand, int C, int k, const int32_t* offs,
+                       float* out_s, int32_t* out_id, cudaStream_t stream, int tiled) {
+  if (B <= 0) return 0;
+  int slots = 4;
+  if (const char* e = getenv("TSV_RERANK_SLOTS")) slots = atoi(e);
+  const int row_bytes = dim * 2;
+  if (!getenv("TSV_RERANK_SLOTS")) {
+    slots = (96 * 1024) / (16 * row_bytes);
+    slots = slots >= 8 ? 8 : (slots >= 4 ? 4 : 2);
+  }
+  if (16 * 2 * row_bytes > 200 * 1024) return static_cast<int>(cudaErrorInvalidValue);
+  switch (slots) {
+    case 2: return launch_rerank_ring_v<16, 2>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream, tiled);
+    case 8: return launch_rerank_ring_v<16, 8>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream, tiled);
+    case 6: return launch_rerank_ring_v<16, 6>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream, tiled);
+    case 3: return launch_rerank_ring_v<16, 3>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream, tiled);
+    default: return launch_rerank_ring_v<16, 4>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream, tiled);
+  }
 }
 
 int launch_normalize(const void* src, int src_is_f32, int64_t n, int dim, int do_normalize,

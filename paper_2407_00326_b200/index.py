@@ -229,8 +229,11 @@ class DeviceIndex:
 
     def rerank(self, q: torch.Tensor, cand_ids: torch.Tensor, k: int,
                stream: torch.cuda.Stream | None = None,
-               out: tuple[torch.Tensor, torch.Tensor] | None = None):
-        """Score cand_ids[b, :] (arena rows) against q[b]; dedup ids; keep the best k."""
+               out: tuple[torch.Tensor, torch.Tensor] | None = None,
+               row_offsets: torch.Tensor | None = None):
+        """Score cand_ids[b, :] (arena rows) against q[b]; dedup ids; keep the best k.
+        row_offsets (int32 [B] on the device): the candidates of question b are rows of its
+        own index segment starting at arena row row_offsets[b]; ids stay segment-local."""
         self._check_queries(q)
         _require_cuda(cand_ids, "cand_ids")
         if cand_ids.dtype != torch.int32 or cand_ids.dim() != 2 or cand_ids.shape[0] != q.shape[0]:
@@ -244,6 +247,16 @@ class DeviceIndex:
         else:
             _check_out(out, B, int(k), self.device)
             scores, ids = out
+        if row_offsets is not None:
+            _require_cuda(row_offsets, "row_offsets")
+            if (row_offsets.dtype != torch.int32 or row_offsets.numel() != B
+                    or row_offsets.device != self.device):
+                raise ConfigParse(f"row_offsets must be int32 [{B}] on {self.device}")
+            nat.check(nat.load().tsv_rerank_segmented(
+                self._h, q.data_ptr(), _dtype_code(q), B, cand_ids.data_ptr(), C,
+                row_offsets.data_ptr(), int(k), scores.data_ptr(), ids.data_ptr(),
+                _stream_handle(stream, self.device)))
+            return scores, ids
         nat.check(nat.load().tsv_rerank(self._h, q.data_ptr(), _dtype_code(q), B,
                                         cand_ids.data_ptr(), C, int(k), scores.data_ptr(),
                                         ids.data_ptr(), _stream_handle(stream, self.device)))

@@ -197,6 +197,79 @@ def test_rerank_shapes_match_oracle(cuda, n, dim, b, c, k):
         assert len(got) == len(set(got))
 
 
+@pytest.mark.parametrize("dim,c,k,slots", [(768, 200, 10, None), (1024, 32, 3, None),
+                                            (384, 57, 5, 2), (256, 300, 12, 8), (2048, 40, 4, None),
+                                            (64, 3, 3, 3)])
+def test_rerank_ring_equals_register_gather(cuda, dim, c, k, slots):
+    """The pipelined K3 (cp.async rings, bf16 arenas) against the register-gather K3
+    (TSV_RERANK_LDG=1): same chunk order, same reduction tree, so bit-identical scores and ids;
+    ring depths 2-8, candidate counts below / above one ring's worth, invalid ids, duplicates."""
+    import os
+
+    import torch
+
+    rng = np.random.default_rng(dim + c)
+    n, b = 4000, 70
+    arena = orc.make_corpus(n, dim, seed=2)
+    qs = orc.make_corpus(b, dim, seed=3)
+    cand = rng.integers(0, n, size=(b, c)).astype(np.int32)
+    cand[::3, 0] = -1
+    cand[::4, c - 1] = n + 5
+    if c > 4:
+        cand[:, 2] = cand[:, 1]
+    idx = _index_from(arena, cuda)
+    qd, cd = to_dev_bf16(qs, cuda), torch.from_numpy(cand).to(cuda)
+    env = {"TSV_RERANK_SLOTS": str(slots)} if slots else {}
+    old = {key: os.environ.get(key) for key in ("TSV_RERANK_SLOTS", "TSV_RERANK_LDG")}
+    try:
+        os.environ.update(env)
+        s1, i1 = idx.rerank(qd, cd, k)
+        os.environ["TSV_RERANK_LDG"] = "1"
+        s2, i2 = idx.rerank(qd, cd, k)
+        torch.cuda.synchronize()
+    finally:
+        for key, v in old.items():
+            if v is None:
+                os.environ.pop(key, None)
+            else:
+                os.environ[key] = v
+    np.testing.assert_array_equal(from_dev(i1), from_dev(i2))
+    np.testing.assert_array_equal(from_dev(s1), from_dev(s2))
+    exp_s, _ = orc.rerank(qs, arena, cand, k)
+    np.testing.assert_allclose(from_dev(s1), exp_s, rtol=TOL, atol=1e-6)
+
+
+@pytest.mark.parametrize("storage", ["bf16", "bf16_tiled", "f32"])
+def test_rerank_segmented_offsets(cuda, storage):
+    """Reranking a batch of questions from different queries in one launch: question b's
+    candidate ids are local to its own index segment (arena row = row_offsets[b] + id) and the
+    returned ids stay local, as the Searching stages emitted them (tsv_rerank_segmented)."""
+    import torch
+
+    from paper_2407_00326_b200.index import DeviceIndex
+
+    rng = np.random.default_rng(9)
+    dim, k = 256, 5
+    sizes = [48, 64, 33, 128, 40]
+    starts = np.cumsum([0] + sizes)[:-1]
+    arena = orc.make_corpus(int(sum(sizes)), dim, seed=4)
+    qs = orc.make_corpus(len(sizes), dim, seed=5)
+    c = 32
+    cand = np.stack([rng.integers(0, sz, size=c) for sz in sizes]).astype(np.int32)
+    cand[1, 3] = -1
+    cand[2, 5] = cand[2, 4]
+    idx = DeviceIndex(dim, len(arena), device=cuda.index, storage=storage)
+    idx.append(torch.from_numpy(arena).to(cuda) if storage == "f32" else to_dev_bf16(arena, cuda))
+    offs = torch.tensor(starts, dtype=torch.int32, device=cuda)
+    qd = torch.from_numpy(qs).to(cuda) if storage == "f32" else to_dev_bf16(qs, cuda)
+    s, i = idx.rerank(qd, torch.from_numpy(cand).to(cuda), k, row_offsets=offs)
+    torch.cuda.synchronize()
+    for b, (a, sz) in enumerate(zip(starts, sizes)):
+        es, ei = orc.rerank(qs[b:b + 1], arena[a:a + sz], cand[b:b + 1], k)
+        np.testing.assert_allclose(from_dev(s)[b:b + 1], es, rtol=TOL, atol=1e-6)
+        assert set(from_dev(i)[b].tolist()) <= set(cand[b].tolist())
+
+
 def test_merge_matches_oracle(cuda):
     import torch
     from paper_2407_00326_b200.index import merge_topk
