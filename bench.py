@@ -57,6 +57,9 @@ def parse_args():
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU time of the bounded cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-step-s", type=float, default=4.0,
+                    help="--impl reference: CPU seconds per step before the corpus is sampled "
+                         "(the whole corpus is searched when it fits)")
     ap.add_argument("--exchange", choices=("p2p", "nccl"), default="p2p",
                     help="N>1: fused peer all-gather + merge over NVLink, or NCCL all-gather + K4")
     ap.add_argument("--dry-run", action="store_true",
@@ -133,7 +136,7 @@ def run_dry(args) -> int:
     if rank == 0:
         print(json.dumps({"dry_run": True, "n_gpus": world, "world_size_from_group": group_world,
                           "spawned": os.environ.get("BENCH_SPAWNED") == "1",
-                          "shards": shards, "config": _config(args, shards[0][1] - shards[0][0])}),
+                          "shards": shards, "config": _config(args)}),
               flush=True)
     return 0
 
@@ -236,10 +239,28 @@ def simulated_reference_ms(load: float):
 
 
 # ---------------------------------------------------------------------- CPU baseline
-def cpu_sample(dim: int, batch: int, k: int, target_s: float, rows_dev=None):
-    """Time the C oracle (all host threads, fp32 accumulation) on a bounded sample of the
-    workload: `batch` queries against the first n_s corpus rows, n_s sized for ~target_s of
-    CPU work. Returns (queries/s scaled to the full corpus fraction, info dict)."""
+def host_corpus(n: int, dim: int, seed: int = 0):
+    """n x dim seeded N(0, 1) rows, L2-normalised, as bf16 bit patterns (uint16) on the host,
+    generated in 128K-row chunks with torch's multi-threaded CPU kernels (the reference arm's
+    corpus; the CPU has no access to the device-generated one)."""
+    import numpy as np
+    import torch
+
+    out = np.empty((n, dim), dtype=np.uint16)
+    g = torch.Generator().manual_seed(seed)
+    for a in range(0, n, 1 << 17):
+        b = min(n, a + (1 << 17))
+        x = torch.randn((b - a, dim), generator=g)
+        x = (x / x.norm(dim=1, keepdim=True)).to(torch.bfloat16)
+        out[a:b] = x.view(torch.int16).numpy().view(np.uint16)
+    return out
+
+
+def cpu_sample(dim: int, batch: int, k: int, target_s: float, rows_dev=None,
+               max_rows: int | None = None):
+    """A bounded sample of the workload for the CPU reference path: `batch` queries against
+    the first n_s corpus rows, n_s sized for ~target_s of CPU work per search (at most the whole
+    corpus, max_rows). Returns (queries, rows, n_s, threads, oracle variant)."""
     import numpy as np
 
     from oracle import c_oracle
@@ -250,16 +271,19 @@ def cpu_sample(dim: int, batch: int, k: int, target_s: float, rows_dev=None):
     rng = np.random.default_rng(1)
     q = orc.normalize_rows(rng.standard_normal((batch, dim), dtype=np.float32))
     qb = orc.bf16_bits(q)
-    probe_rows = 16384
+    probe_rows = 32768
     cb = (_host_rows(rows_dev, probe_rows) if rows_dev is not None
-          else orc.bf16_bits(orc.make_corpus(probe_rows, dim, seed=0)))
+          else host_corpus(probe_rows, dim))
+    time_cpu(qb, cb, k, threads)  # first call: thread pool, AMX permission
     t = time.perf_counter()
     c_oracle.search(qb, cb, k, nthreads=threads)
     dt = max(time.perf_counter() - t, 1e-4)
-    n_s = int(min(max(probe_rows * target_s / dt, 8192), 1_000_000))
-    n_s -= n_s % 1024
-    cb = (_host_rows(rows_dev, n_s) if rows_dev is not None
-          else orc.bf16_bits(orc.make_corpus(n_s, dim, seed=0)))
+    n_s = int(max(probe_rows * target_s / dt, 8192))
+    if max_rows is not None:
+        n_s = min(n_s, max_rows)
+    if n_s != max_rows:
+        n_s -= n_s % 1024
+    cb = (_host_rows(rows_dev, n_s) if rows_dev is not None else host_corpus(n_s, dim))
     return qb, cb, n_s, threads, lib.variant
 
 
@@ -316,11 +340,15 @@ def time_cpu(qb, cb, k, threads):
 
 # ---------------------------------------------------------------------- reference arm
 def run_reference(args):
+    """The reference CPU path (the C oracle port: AMX-BF16 tiles where the host has them, else
+    AVX-512 / AVX2; all host threads) on the same metric and config. Each step searches the
+    batch over the whole corpus when that fits ~--ref-step-s of CPU time, else over the first
+    rows_timed rows, with the step time scaled to the full corpus (`extrapolated`)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     qb, cb, n_s, threads, variant = cpu_sample(args.dim, args.batch, args.k,
-                                               target_s=min(args.cpu_seconds, 4.0))
+                                               target_s=args.ref_step_s, max_rows=args.rows)
     for _ in range(args.warmup):
         time_cpu(qb, cb, args.k, threads)
     total = 0.0
@@ -329,8 +357,10 @@ def run_reference(args):
     scale = args.rows / n_s
     ms_per_step = total / args.steps * scale * 1000.0
     value = args.batch / (ms_per_step / 1000.0)
-    sample = (f"{args.batch} queries x first {n_s} of the {args.rows}-row corpus per step "
-              f"(scaled x{scale:.1f}); C oracle {variant}, fp32 accumulate, OpenMP")
+    sample = (f"{args.batch} queries x {'all' if n_s == args.rows else 'first'} {n_s} of the "
+              f"{args.rows}-row corpus per step"
+              + (f" (time scaled x{scale:.2f})" if n_s != args.rows else "")
+              + f"; C oracle {variant}, fp32 accumulate, OpenMP")
     line = {
         "impl": "reference",
         "metric": "vector-search queries/s (10Mx1024 corpus, k=10)",
@@ -338,9 +368,11 @@ def run_reference(args):
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded N(0,1) rows, L2-normalised)",
-        "config": _config(args, args.rows),
+        "config": _config(args),
+        "rows_timed": n_s, "extrapolated": n_s != args.rows,
         "cpu_baseline": {"value": value, "unit": "queries/s", "cores": threads, "kind": "port",
-                         "cpu_model": cpu_model(), "sample": sample},
+                         "variant": variant, "cpu_model": cpu_model(), "sample": sample,
+                         "rows_timed": n_s, "extrapolated": n_s != args.rows},
         "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -348,13 +380,18 @@ def run_reference(args):
     return 0
 
 
-def _config(args, shard_rows):
+def _config(args, shard_rows=None):
+    """The workload, from the arguments alone: both arms (ours and --impl reference) print the
+    identical dict for the same command line."""
+    if shard_rows is None:  # rank 0's shard (paper_2407_00326_b200.sharded.shard_range)
+        shard_rows = args.rows // args.gpus
     return {
         "workload": f"C4/metric: flat inner-product (cosine) search, {args.rows}x{args.dim} "
                     f"{getattr(args, 'storage', 'bf16')} corpus, batch {args.batch}, k={args.k}",
         "storage": getattr(args, "storage", "bf16"),
         "rows": args.rows, "dim": args.dim, "batch": args.batch, "k": args.k,
         "shard_rows": shard_rows, "parallelism": f"corpus-shard x{args.gpus}",
+        "exchange": args.exchange if args.gpus > 1 else None,
         "l2": "inputs larger than L2 (corpus streamed from HBM every step)",
     }
 
@@ -658,7 +695,9 @@ def run_ours(args):
     e2e_value = B * args.steps / (e2e_ms / 1000.0)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        qb, cb, n_s, threads, variant = cpu_sample(D, B, k, args.cpu_seconds, rows_dev=idx.data())
+        qb, cb, n_s, threads, variant = cpu_sample(D, B, k, min(args.cpu_seconds, 3.0),
+                                                   rows_dev=idx.data(),
+                                                   max_rows=min(N, 2_000_000))
         # repeat the bounded sample until ~cpu_seconds of CPU work were timed (the sample
         # size is capped to keep the host copy of the rows small)
         reps, total = 0, 0.0
@@ -668,7 +707,8 @@ def run_ours(args):
         dt = total / reps
         cpu_qps = B / (dt * N / n_s)
         cpu = {"value": cpu_qps, "unit": "queries/s", "cores": threads, "kind": "port",
-               "cpu_model": cpu_model(),
+               "variant": variant, "cpu_model": cpu_model(), "rows_timed": n_s,
+               "extrapolated": n_s != N,
                "sample": f"{B} queries x first {n_s} corpus rows (of {N}); time scaled by "
                          f"{N / n_s:.1f}; C oracle ({variant}), fp32 accumulate, OpenMP; "
                          f"{reps} repetitions, {total:.1f} s measured",
@@ -691,10 +731,10 @@ def run_ours(args):
                     "N(0,0.05^2), B/2 fresh N(0,1); L2-normalised on device)",
             "planted_top1": planted_top1,
             "simulated_reference_ms": simulated_reference_ms(B),
-            "config": {**_config(args, n_local),
-                       "exchange": (None if world == 1 else sharded.exchange
-                                    + (f" (p2p unavailable: {sharded.p2p_error})"
-                                       if sharded.p2p_error else ""))},
+            "config": _config(args),
+            "exchange_used": (None if world == 1 else sharded.exchange
+                              + (f" (p2p unavailable: {sharded.p2p_error})"
+                                 if sharded.p2p_error else "")),
             "e2e": {"value": e2e_value, "unit": "queries/s",
                     "h2d_bytes_per_step": B * D * 2, "d2h_bytes_per_step": B * k * 8,
                     "ms_per_step": e2e_ms / args.steps,

@@ -78,6 +78,10 @@ TSV_API int tsv_index_destroy(tsv_index* idx);
  * row of the first appended row. Returns TSV_ERR_CAPACITY when the arena would overflow. */
 TSV_API int tsv_index_append(tsv_index* idx, const void* rows_dev, int src_dtype, int64_t n,
                      int64_t* first_row, void* stream);
+/* Claim n rows at the end of the arena without writing them (their content is undefined until
+ * the caller writes them, e.g. through tsv_index_data: the ingest stages of a per-query index
+ * fill their slices of one reserved segment); *first_row receives the first claimed row. */
+TSV_API int tsv_index_reserve(tsv_index* idx, int64_t n, int64_t* first_row);
 /* Drop rows >= n (n <= current row count). */
 TSV_API int tsv_index_truncate(tsv_index* idx, int64_t n);
 TSV_API int64_t tsv_index_rows(const tsv_index* idx);

@@ -1,7 +1,9 @@
 """Builds the C oracle (test infrastructure / CPU baseline) into oracle/_build/.
 
-Two variants: x86-64-v3 (AVX2+FMA, runs on any current server CPU) and x86-64-v4 (AVX-512),
-picked at load time from the host's CPU flags. Nothing here is part of the product path.
+Three variants: x86-64-v3 (AVX2+FMA, runs on any current server CPU), x86-64-v4 (AVX-512) and
+amx (x86-64-v4 + AMX-BF16 tiles: the fp32-accumulation search on the tensor-tile unit of
+Sapphire Rapids and later), picked at load time from the host's CPU flags and a timing probe.
+Nothing here is part of the product path.
 """
 
 from __future__ import annotations
@@ -12,7 +14,8 @@ from pathlib import Path
 HERE = Path(__file__).resolve().parent
 OUT = HERE / "_build"
 SRC = HERE / "tsv_oracle.c"
-VARIANTS = {"v3": "-march=x86-64-v3", "v4": "-march=x86-64-v4"}
+VARIANTS = {"v3": ["-march=x86-64-v3"], "v4": ["-march=x86-64-v4"],
+            "amx": ["-march=x86-64-v4", "-mamx-tile", "-mamx-bf16"]}
 
 
 def lib_path(variant: str) -> Path:
@@ -25,7 +28,7 @@ def build(force: bool = False) -> list[Path]:
     for name, march in VARIANTS.items():
         p = lib_path(name)
         if force or not p.exists() or p.stat().st_mtime < SRC.stat().st_mtime:
-            subprocess.run(["gcc", "-O3", march, "-fopenmp", "-shared", "-fPIC", str(SRC), "-o",
+            subprocess.run(["gcc", "-O3", *march, "-fopenmp", "-shared", "-fPIC", str(SRC), "-o",
                             str(p), "-lm"], check=True)
         out.append(p)
     return out

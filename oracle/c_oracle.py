@@ -13,6 +13,15 @@ _lib = None
 _libs: dict = {}
 
 
+def _cpu_has_amx() -> bool:
+    try:
+        with open("/proc/cpuinfo") as f:
+            flags = f.read()
+        return " amx_bf16 " in flags and " amx_tile " in flags and _cpu_has_avx512()
+    except OSError:
+        return False
+
+
 def _cpu_has_avx512() -> bool:
     try:
         with open("/proc/cpuinfo") as f:
@@ -36,6 +45,15 @@ def _open(variant: str):
                                       ctypes.c_void_p]
     lib.tsv_oracle_threads.restype = ctypes.c_int
     lib.variant = variant
+    lib.amx = False
+    if variant == "amx":
+        lib.tsv_oracle_search_amx.restype = ctypes.c_int
+        lib.tsv_oracle_search_amx.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                              ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                              ctypes.c_int, ctypes.c_int64, ctypes.c_void_p,
+                                              ctypes.c_void_p]
+        lib.tsv_oracle_amx_available.restype = ctypes.c_int
+        lib.amx = bool(lib.tsv_oracle_amx_available())
     _libs[variant] = lib
     return lib
 
@@ -53,6 +71,8 @@ def load(variant: str | None = None):
         _lib = _open(variant)
         return _lib
     cands = ["v3", "v4"] if _cpu_has_avx512() else ["v3"]
+    if _cpu_has_amx() and _open("amx").amx:
+        cands.append("amx")
     if len(cands) == 1:
         _lib = _open(cands[0])
         return _lib
@@ -90,6 +110,12 @@ def _search(lib, q_bits, c_bits, k, use_double, nthreads, id_offset):
     N = c.shape[0]
     out_s = np.empty((B, k), dtype=np.float32)
     out_i = np.empty((B, k), dtype=np.int32)
+    if lib.amx and not use_double and D % 32 == 0:
+        rc = lib.tsv_oracle_search_amx(q.ctypes.data, c.ctypes.data, B, N, D, k,
+                                       int(nthreads or os.cpu_count() or 1), int(id_offset),
+                                       out_s.ctypes.data, out_i.ctypes.data)
+        if rc == 0:
+            return out_s, out_i
     rc = lib.tsv_oracle_search(q.ctypes.data, c.ctypes.data, B, N, D, k, int(use_double),
                                int(nthreads or os.cpu_count() or 1), int(id_offset),
                                out_s.ctypes.data, out_i.ctypes.data)

@@ -40,6 +40,7 @@ SIGNATURES = {
     "tsv_index_create_view": (c_int, [c_int, c_int, c_int, c_vp, c_i64, ctypes.POINTER(c_vp)]),
     "tsv_index_destroy": (c_int, [c_vp]),
     "tsv_index_append": (c_int, [c_vp, c_vp, c_int, c_i64, ctypes.POINTER(c_i64), c_vp]),
+    "tsv_index_reserve": (c_int, [c_vp, c_i64, ctypes.POINTER(c_i64)]),
     "tsv_index_truncate": (c_int, [c_vp, c_i64]),
     "tsv_index_rows": (c_i64, [c_vp]),
     "tsv_index_dim": (c_int, [c_vp]),

@@ -139,11 +139,46 @@ class LaunchRecord:
         return self.start.elapsed_time(self.end)
 
 
+class PinnedRing:
+    """Reused pinned host slots for small per-batch uploads (segment offsets): a slot is
+    refilled only after the copy that last read it has run (its event), so uploads stay
+    asynchronous and no pinned memory is allocated per batch."""
+
+    def __init__(self, slots: int = 8, capacity: int = 4096):
+        self.bufs = [torch.empty(capacity, dtype=torch.int32, pin_memory=True)
+                     for _ in range(slots)]
+        self.events: list[torch.cuda.Event | None] = [None] * slots
+        self.capacity = capacity
+        self.next = 0
+
+    def upload(self, values: list[int], device: torch.device,
+               stream: torch.cuda.Stream) -> torch.Tensor:
+        n = len(values)
+        if n > self.capacity:
+            return torch.tensor(values, dtype=torch.int32).to(device, non_blocking=False)
+        j = self.next
+        self.next = (j + 1) % len(self.bufs)
+        if self.events[j] is not None:
+            self.events[j].synchronize()
+        buf = self.bufs[j]
+        buf[:n] = torch.as_tensor(values, dtype=torch.int32)
+        out = torch.empty(n, dtype=torch.int32, device=device)
+        with torch.cuda.stream(stream):
+            out.copy_(buf[:n], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+        self.events[j] = ev
+        return out
+
+
 @dataclass
 class Replica:
     device: torch.device
     stream: torch.cuda.Stream
     arena: DeviceIndex
+    pinned: PinnedRing = field(default_factory=PinnedRing)
+    # released index segments: (row_beg, rows, event the reuse must wait for)
+    free: list = field(default_factory=list)
 
 
 class RetrievalBackend:
@@ -195,7 +230,33 @@ class RetrievalBackend:
 
     # -- graph-tier hooks --------------------------------------------------------------
     def on_submit(self, ctx) -> None:
-        pass
+        """The question vector a query's Reranking scores against stands for the output of a
+        modelled embedding: materialise it once, on the query's home replica, outside every
+        retrieval batch."""
+        rep = self.replicas[self.home(ctx.query_id)]
+        if any(n.kind is PrimitiveKind.RERANKING and n.meta.engine_id in self.engines
+               for n in ctx.graph.nodes.values()):
+            with self._on(rep):
+                qv = self.data.question(rep.device, ctx.query_id)
+                ctx.data[("__question__", None)] = (qv, self._record(rep))
+
+    def on_query_done(self, ctx) -> None:
+        """A query finished: its per-query index segments go back to their replicas' free
+        lists (reused once every stream that may still read them has passed this point), and
+        its device results are dropped."""
+        mine = [key for key in self.segments if key[0] == ctx.query_id]
+        for key in mine:
+            seg = self.segments.pop(key)
+            rep = self.replicas[seg.replica]
+            evs = []
+            for r in self.replicas:
+                ev = torch.cuda.Event()
+                ev.record(r.stream)
+                evs.append(ev)
+            rep.free.append((seg.row_beg, seg.row_end - seg.row_beg, evs))
+        for key in [k for k in self.acc if k[0] == ctx.query_id]:
+            del self.acc[key]
+        ctx.data.clear()
 
     def on_complete(self, ctx, node: PrimitiveNode) -> None:
         """Materialise the device data a completed node produces."""
@@ -287,13 +348,29 @@ class RetrievalBackend:
         seg.filled += hi - lo
         ctx.data[(node.node_id, key)] = ("index", key, total)
 
+    def _reserve(self, rep: Replica, total: int) -> int:
+        """Arena rows for a new segment: first fit among released segments (after the streams
+        that could still read them), else appended at the end of the arena."""
+        for j, (beg, n, evs) in enumerate(rep.free):
+            if n >= total:
+                for ev in evs:
+                    rep.stream.wait_event(ev)
+                if n == total:
+                    rep.free.pop(j)
+                else:
+                    rep.free[j] = (beg + total, n - total, evs)
+                return beg
+        first = rep.arena.rows
+        if first + total > rep.arena.capacity:
+            raise CapacityExceeded(
+                f"replica arena full: {first} + {total} rows > {rep.arena.capacity} "
+                f"({sum(n for _, n, _ in rep.free)} rows free in released segments)")
+        return rep.arena.reserve(total)
+
     def _segment(self, query_id, key, replica, total) -> IndexSegment:
         seg = self.segments.get((query_id, key, replica))
         if seg is None:
-            rep = self.replicas[replica]
-            with self._on(rep):
-                first = rep.arena.append(torch.zeros((total, self.dim), dtype=torch.bfloat16,
-                                                     device=rep.device), stream=rep.stream)
+            first = self._reserve(self.replicas[replica], total)
             seg = IndexSegment(replica, first, first + total)
             self.segments[(query_id, key, replica)] = seg
         return seg
@@ -309,10 +386,16 @@ class RetrievalBackend:
         n = home.row_end - home.row_beg
         src = self.replicas[home.replica]
         dst_rep = self.replicas[replica]
-        src.stream.synchronize()
-        with self._on(dst_rep):  # peer copy over NVLink, then append on the local stream
-            rows = src.arena.data()[home.row_beg:home.row_end].to(dst_rep.device)
-            first = dst_rep.arena.append(rows, stream=dst_rep.stream)
+        first = self._reserve(dst_rep, n)
+        ingested = torch.cuda.Event()
+        ingested.record(src.stream)
+        # peer copy over NVLink, ordered after the ingest by an event (torch issues a
+        # cross-device copy on the source device's current stream, then orders the
+        # destination's current stream, the replica stream here, after it)
+        torch.cuda.current_stream(src.device).wait_event(ingested)
+        with self._on(dst_rep):
+            dst_rep.arena.data()[first:first + n].copy_(
+                src.arena.data()[home.row_beg:home.row_end], non_blocking=True)
         seg = IndexSegment(replica, first, first + n, n)
         self.segments[(query_id, key, replica)] = seg
         return seg
@@ -382,53 +465,82 @@ class RetrievalBackend:
         return torch.cat(parts) if len(parts) > 1 else parts[0]
 
     def _search_batch(self, rep: Replica, plan, start: torch.cuda.Event) -> None:
-        qs, q_off, ranges, metas = [], [0], [], []
+        """One topology-aware batch of Searching requests: entries with a per-query index input
+        become one segmented launch (each entry searches its own query's segment); entries
+        without one search the resident global corpus in one launch. A batch mixing both runs
+        the two launches back to back on the replica stream."""
+        seg_q, seg_off, seg_ranges, seg_meta = [], [0], [], []
+        glob_q, glob_meta = [], []
         kmax = 1
-        use_global = False
         for task, n in plan.entries:
             node = task.node
             key_out = next(iter(node.meta.outputs))
             k = node.meta.outputs[key_out].items // max(1, node.meta.batch_items)
             kmax = max(kmax, k)
             lo = task.next_request
-            qs.append(self._query_rows(rep, task, lo, lo + n))
-            q_off.append(q_off[-1] + n)
+            rows = self._query_rows(rep, task, lo, lo + n)
             idx = self._inputs(task.ctx, node, "index")
             if idx:
                 seg = self._local_segment(task.ctx.query_id, idx[0][1][1],
                                           self.replicas.index(rep))
-                ranges.append((seg.row_beg, seg.row_end))
+                seg_q.append(rows)
+                seg_off.append(seg_off[-1] + n)
+                seg_ranges.append((seg.row_beg, seg.row_end))
+                seg_meta.append((task, lo, n, k))
             else:
                 if self.global_index is None:
                     raise CapacityExceeded(f"{node.node_id}: no index input and no global corpus")
-                use_global = True
-                ranges.append((0, self.global_index.rows))
-            metas.append((task, lo, n, k))
-        q = torch.cat(qs)
+                glob_q.append(rows)
+                glob_meta.append((task, lo, n, k))
         if kmax > 128:
             raise ConfigParse(f"per_query_top_k={kmax} exceeds the fused kernel's limit (128)")
+        q_seg = (torch.cat(seg_q) if len(seg_q) > 1 else seg_q[0]) if seg_q else None
+        q_glob = (torch.cat(glob_q) if len(glob_q) > 1 else glob_q[0]) if glob_q else None
+        if q_glob is not None and self.global_index.device != rep.device:
+            raise ConfigParse(f"the global corpus is searched from {self.global_index.device}; "
+                              f"bind the search engine's replicas there (got {rep.device})")
         start.record(rep.stream)
-        if use_global:
-            if self.global_index.device != rep.device:
-                raise ConfigParse(f"the global corpus is searched from {self.global_index.device}; "
-                                  f"bind the search engine's replicas there (got {rep.device})")
-            scores, ids = self.global_index.search(q, kmax, stream=rep.stream)
-        else:
-            scores, ids = rep.arena.search_segmented(q, q_off, ranges, kmax, local_ids=True,
-                                                     stream=rep.stream)
+        launches = []
+        if q_seg is not None:
+            out = rep.arena.search_segmented(q_seg, seg_off, seg_ranges, kmax, local_ids=True,
+                                             stream=rep.stream)
+            launches.append((out, seg_meta))
+        if q_glob is not None:
+            out = self.global_index.search(q_glob, kmax, stream=rep.stream)
+            launches.append((out, glob_meta))
         ready = self._record(rep)
         r = self.replicas.index(rep)
-        for (task, lo, n, k), a in zip(metas, q_off[:-1]):
-            self.acc.setdefault((task.ctx.query_id, task.node_id), []).append(
-                (lo, scores[a:a + n, :k], ids[a:a + n, :k], ready, r))
-        nq = q_off[-1]
-        rows = sum(b - a for a, b in ranges)
-        pairs = sum((q_off[i + 1] - q_off[i]) * (b - a) for i, (a, b) in enumerate(ranges))
+        for (scores, ids), metas in launches:
+            a = 0
+            for task, lo, n, k in metas:
+                self.acc.setdefault((task.ctx.query_id, task.node_id), []).append(
+                    (lo, scores[a:a + n, :k], ids[a:a + n, :k], ready, r))
+                a += n
+        nq = sum(n for _, _, n, _ in seg_meta + glob_meta)
+        g_rows = self.global_index.rows if glob_meta else 0
+        rows = sum(b - a for a, b in seg_ranges) + g_rows
+        pairs = (sum((seg_off[i + 1] - seg_off[i]) * (b - a) for i, (a, b) in enumerate(seg_ranges))
+                 + sum(n for _, _, n, _ in glob_meta) * g_rows)
         return LaunchRecord("", 0, "search", nq, rows, kmax, self.dim,
                             bytes=rows * self.dim * 2 + nq * self.dim * 2 + nq * kmax * 8,
                             flops=2 * pairs * self.dim)
 
+    def _question(self, rep: Replica, ctx) -> torch.Tensor:
+        got = ctx.data.get(("__question__", None))
+        if got is None:  # (graphs submitted without on_submit)
+            with self._on(rep):
+                qv = self.data.question(rep.device, ctx.query_id)
+            return qv
+        qv, ready = got
+        rep.stream.wait_event(ready)
+        return qv if qv.device == rep.device else qv.to(rep.device)
+
     def _rerank_batch(self, rep: Replica, plan, start: torch.cuda.Event) -> None:
+        """One batch of Reranking requests = ONE K3 launch: question j scores its own candidate
+        row (ids local to its query's index segment, offset on the device by the segment's
+        first arena row), duplicates dropped, the best max(top_k) kept; each entry takes its
+        top_k. Inputs are assembled before `start`; nothing but the launch sits inside the
+        measured window."""
         jobs = []
         for task, n in plan.entries:
             node, ctx = task.node, task.ctx
@@ -440,30 +552,32 @@ class RetrievalBackend:
             res = cands[0][1]
             if res.ready is not None:
                 rep.stream.wait_event(res.ready)
-            flat = res.ids.reshape(-1)
             lo = task.next_request
-            part = flat[lo:lo + n]
+            part = res.ids.reshape(-1)[lo:lo + n]
             idx = self._inputs(ctx, node, "index") or self._index_of_search(ctx, cands[0][0])
             seg = self._local_segment(ctx.query_id, idx[0][1][1], self.replicas.index(rep))
-            rows = torch.where(part >= 0, part + seg.row_beg, part).to(torch.int32)
-            qv = self.data.question(rep.device, ctx.query_id)
-            jobs.append((task, lo, top_k, seg, qv.reshape(1, -1), rows.reshape(-1)))
-        # One K3 launch for the whole batch: question j scores its own candidate row (padded
-        # with -1, which K3 skips), the best max(top_k) are kept and each job takes its top_k.
+            jobs.append((task, lo, top_k, seg, self._question(rep, ctx), part))
         n_c = max(j[5].shape[0] for j in jobs)
         k_out = max(j[2] for j in jobs)
-        cand = torch.full((len(jobs), n_c), -1, dtype=torch.int32, device=rep.device)
-        for j, job in enumerate(jobs):
-            cand[j, :job[5].shape[0]] = job[5]
-        qs = torch.cat([j[4] for j in jobs]) if len(jobs) > 1 else jobs[0][4]
-        offs = torch.tensor([[j[3].row_beg] for j in jobs], dtype=torch.int32).pin_memory()
-        offs = offs.to(rep.device, non_blocking=True)
+        if len(jobs) == 1:
+            cand = jobs[0][5].reshape(1, -1)
+            qs = jobs[0][4].reshape(1, -1)
+        else:
+            with self._on(rep):
+                if all(j[5].shape[0] == n_c for j in jobs):
+                    cand = torch.stack([j[5] for j in jobs])
+                else:  # pad short candidate rows with -1 (K3 skips them)
+                    cand = torch.stack([torch.nn.functional.pad(j[5], (0, n_c - j[5].shape[0]),
+                                                                value=-1) for j in jobs])
+                qs = torch.cat([j[4].reshape(1, -1) for j in jobs])
+        offs = rep.pinned.upload([j[3].row_beg for j in jobs], rep.device, rep.stream)
+        if not cand.is_contiguous():
+            cand = cand.contiguous()
         start.record(rep.stream)
-        s_all, i_all = rep.arena.rerank(qs, cand, k_out, stream=rep.stream)
-        i_all = torch.where(i_all >= 0, i_all - offs, i_all)
+        s_all, i_all = rep.arena.rerank(qs, cand, k_out, stream=rep.stream, row_offsets=offs)
         ready = self._record(rep)
         r = self.replicas.index(rep)
-        for j, (task, lo, top_k, seg, qv, rows) in enumerate(jobs):
+        for j, (task, lo, top_k, seg, qv, part) in enumerate(jobs):
             self.acc.setdefault((task.ctx.query_id, task.node_id), []).append(
                 (lo, s_all[j:j + 1, :top_k], i_all[j:j + 1, :top_k], ready, r))
         n_rows = sum(j[5].shape[0] for j in jobs)

@@ -512,6 +512,18 @@ int tsv_index_append(tsv_index* idx, const void* rows_dev, int src_dtype, int64_
   return TSV_OK;
 }
 
+int tsv_index_reserve(tsv_index* idx, int64_t n, int64_t* first_row) {
+  if (idx == nullptr) return fail(TSV_ERR_ARGUMENT, "index is null");
+  if (!idx->owns) return fail(TSV_ERR_CONFIG, "cannot reserve rows in a view index");
+  if (n < 0) return fail(TSV_ERR_CAPACITY, "negative row count");
+  if (idx->rows + n > idx->cap_rows)
+    return fail(TSV_ERR_CAPACITY, "arena overflow: %lld + %lld > %lld", (long long)idx->rows,
+                (long long)n, (long long)idx->cap_rows);
+  if (first_row) *first_row = idx->rows;
+  idx->rows += n;
+  return TSV_OK;
+}
+
 int tsv_index_truncate(tsv_index* idx, int64_t n) {
   if (idx == nullptr) return fail(TSV_ERR_ARGUMENT, "index is null");
   if (n < 0 || n > idx->rows) return fail(TSV_ERR_CAPACITY, "bad truncate length");

@@ -448,35 +448,65 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-template <int kWarps, int kSlots>
+// bf16x2 word -> (element 2t, element 2t+1) as fp32: a bf16 is the high half of an fp32
+__device__ __forceinline__ float2 bf16x2_to_float2(uint32_t w) {
+  return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+}
+
+// Lane `lane` always owns chunks lane + 32 j (j < CPL) of every row, so the question's matching
+// elements live in its registers for the whole kernel and a row chunk costs one shared-memory
+// load, four bf16x2 -> fp32x2 conversions and four packed fp32x2 FMAs (FFMA2; even / odd
+// elements in the two halves, summed at the end).
+template <int kWarps, int kSlots, int CPL, bool kTiled>
 __global__ void __launch_bounds__(kWarps * 32) rerank_ring_kernel(
     const __nv_bfloat16* __restrict__ arena, int64_t nrows, int dim, const void* __restrict__ q,
     int q_is_f32, const int32_t* __restrict__ cand, int C, int k, const int32_t* __restrict__ offs,
-    float* __restrict__ out_s, int32_t* __restrict__ out_id, int tiled) {
+    float* __restrict__ out_s, int32_t* __restrict__ out_id) {
   extern __shared__ __align__(16) uint8_t sm[];
   const int row_bytes = dim * 2;
   uint8_t* ring = sm;                                                   // [kWarps][kSlots][row]
-  float* qv = reinterpret_cast<float*>(sm + static_cast<size_t>(kWarps) * kSlots * row_bytes);
-  uint64_t* keys = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(qv) + ((dim * 4 + 15) & ~15));
+  uint64_t* keys = reinterpret_cast<uint64_t*>(sm + static_cast<size_t>(kWarps) * kSlots * row_bytes);
   const int np = pow2_ceil(C);
-  int32_t* ids = reinterpret_cast<int32_t*>(keys + np);                 // arena rows
+  int32_t* ids = reinterpret_cast<int32_t*>(keys + np);                 // segment-local ids
   const int b = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t base = offs != nullptr ? __ldg(offs + b) : 0;  // per-question segment start
-  for (int c = threadIdx.x; c < C; c += kWarps * 32) {
-    const int32_t id = __ldg(cand + static_cast<int64_t>(b) * C + c);
-    ids[c] = id;
-  }
-  for (int i = threadIdx.x; i < np; i += kWarps * 32) keys[i] = pad_key();
-  __syncthreads();
-
   const int chunks = dim >> 3;  // 16-byte chunks per row
+  // The question's elements of this lane's chunks go to registers first: their round trip
+  // overlaps the candidate ids' (nothing below waits for them until the first row is scored).
+  float2 qr[CPL][4];
+#pragma unroll
+  for (int j = 0; j < CPL; ++j) {
+    const int ch = lane + 32 * j;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) qr[j][t] = make_float2(0.f, 0.f);
+    if (ch < chunks) {
+      const int64_t o = static_cast<int64_t>(b) * dim + ch * 8;
+      if (q_is_f32) {
+        const float4 x0 = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(q) + o));
+        const float4 x1 = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(q) + o + 4));
+        qr[j][0] = make_float2(x0.x, x0.y);
+        qr[j][1] = make_float2(x0.z, x0.w);
+        qr[j][2] = make_float2(x1.x, x1.y);
+        qr[j][3] = make_float2(x1.z, x1.w);
+      } else {
+        const uint4 w = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(q) + o));
+        qr[j][0] = bf16x2_to_float2(w.x);
+        qr[j][1] = bf16x2_to_float2(w.y);
+        qr[j][2] = bf16x2_to_float2(w.z);
+        qr[j][3] = bf16x2_to_float2(w.w);
+      }
+    }
+  }
+  const int64_t base = offs != nullptr ? __ldg(offs + b) : 0;  // per-question segment start
+  // Each warp stages only its own candidates' ids (c = warp + kWarps i): no block barrier
+  // before the gather starts. The keys' padding tail is ordered before the sort by its barrier.
+  for (int c = warp + kWarps * lane; c < C; c += kWarps * 32)
+    ids[c] = __ldg(cand + static_cast<int64_t>(b) * C + c);
+  for (int i = C + threadIdx.x; i < np; i += kWarps * 32) keys[i] = pad_key();
+  __syncwarp();
+
   const int64_t kb_per_row = (dim + 63) >> 6;
   uint8_t* my_ring = ring + static_cast<size_t>(warp) * kSlots * row_bytes;
-  auto row_ptr = [&](int64_t r) -> const uint4* {
-    return tiled ? reinterpret_cast<const uint4*>(arena + ((r >> 7) * kb_per_row * 128 + (r & 127)) * 64)
-                 : reinterpret_cast<const uint4*>(arena + r * dim);
-  };
   auto valid = [&](int c) {
     if (c >= C) return false;
     const int32_t id = ids[c];
@@ -484,46 +514,46 @@ __global__ void __launch_bounds__(kWarps * 32) rerank_ring_kernel(
   };
   auto issue = [&](int c, int slot) {  // whole warp; always commits one group
     if (valid(c)) {
-      const uint4* src = row_ptr(base + ids[c]);
+      const int64_t r = base + ids[c];
+      const uint4* src = kTiled ? reinterpret_cast<const uint4*>(
+                                      arena + ((r >> 7) * kb_per_row * 128 + (r & 127)) * 64)
+                                : reinterpret_cast<const uint4*>(arena + r * dim);
       uint4* dst = reinterpret_cast<uint4*>(my_ring + static_cast<size_t>(slot) * row_bytes);
-      for (int ch = lane; ch < chunks; ch += 32) {
-        const int64_t off = tiled ? static_cast<int64_t>(ch >> 3) * 1024 + (ch & 7) : ch;
-        cp_async16(dst + ch, src + off);
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) {
+        const int ch = lane + 32 * j;
+        if (ch < chunks)
+          cp_async16(dst + ch, src + (kTiled ? static_cast<int64_t>(ch >> 3) * 1024 + (ch & 7) : ch));
       }
     }
     cp_async_commit();
   };
-  // my candidates: c = warp + j * kWarps
 #pragma unroll
   for (int s = 0; s < kSlots; ++s) issue(warp + s * kWarps, s);
-  // the question vector (fp32) while the first rows are in flight
-  for (int d = threadIdx.x; d < dim; d += kWarps * 32) {
-    const int64_t o = static_cast<int64_t>(b) * dim + d;
-    qv[d] = q_is_f32 ? reinterpret_cast<const float*>(q)[o]
-                     : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(q)[o]);
-  }
-  __syncthreads();
   int slot = 0;
   for (int c = warp; c < C; c += kWarps) {
     cp_async_wait<kSlots - 1>();  // the oldest group (candidate c) has landed
     __syncwarp();
-    float acc = 0.f;
     if (valid(c)) {
       const uint4* row = reinterpret_cast<const uint4*>(my_ring + static_cast<size_t>(slot) * row_bytes);
-      for (int ch = lane; ch < chunks; ch += 32) {
-        const uint4 raw = row[ch];
-        const float* qq = qv + ch * 8;
-        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+      float2 a2 = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const float2 f = __bfloat1622float2(h[t]);
-          acc = fmaf(f.x, qq[2 * t], acc);
-          acc = fmaf(f.y, qq[2 * t + 1], acc);
+      for (int j = 0; j < CPL; ++j) {
+        const int ch = lane + 32 * j;
+        if (ch < chunks) {
+          const uint4 raw = row[ch];
+          a2 = __ffma2_rn(bf16x2_to_float2(raw.x), qr[j][0], a2);
+          a2 = __ffma2_rn(bf16x2_to_float2(raw.y), qr[j][1], a2);
+          a2 = __ffma2_rn(bf16x2_to_float2(raw.z), qr[j][2], a2);
+          a2 = __ffma2_rn(bf16x2_to_float2(raw.w), qr[j][3], a2);
         }
       }
+      float acc = a2.x + a2.y;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       if (lane == 0) keys[c] = make_key(acc, ids[c]);
+    } else if (lane == 0) {
+      keys[c] = pad_key();
     }
     __syncwarp();  // every lane done reading the slot before it is refilled
     issue(c + kSlots * kWarps, slot);
@@ -924,48 +954,64 @@ int launch_rerank(const void* arena, const float* arena_hi, const float* arena_l
                                     cand, C, k, out_s, out_id, stream, tiled, smem, offs);
 }
 
-template <int kWarps, int kSlots>
+template <int kWarps, int kSlots, int CPL, bool kTiled>
 int launch_rerank_ring_v(const void* arena, int64_t nrows, int dim, const void* q, int q_is_f32,
                          int B, const int32_t* cand, int C, int k, const int32_t* offs,
-                         float* out_s, int32_t* out_id, cudaStream_t stream, int tiled) {
+                         float* out_s, int32_t* out_id, cudaStream_t stream) {
   int np = 1;
   while (np < C) np <<= 1;
-  const size_t smem = static_cast<size_t>(kWarps) * kSlots * dim * 2 +
-                      ((static_cast<size_t>(dim) * 4 + 15) & ~size_t(15)) + np * sizeof(uint64_t) +
+  const size_t smem = static_cast<size_t>(kWarps) * kSlots * dim * 2 + np * sizeof(uint64_t) +
                       static_cast<size_t>(C) * sizeof(int32_t);
   if (smem > 220 * 1024) return static_cast<int>(cudaErrorInvalidValue);
-  auto kern = rerank_ring_kernel<kWarps, kSlots>;
+  auto kern = rerank_ring_kernel<kWarps, kSlots, CPL, kTiled>;
   static std::atomic<uint64_t> configured{0};
   if (smem > 48 * 1024 && first_on_device(configured)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     if (e != cudaSuccess) return static_cast<int>(e);
   }
   kern<<<B, kWarps * 32, smem, stream>>>(reinterpret_cast<const __nv_bfloat16*>(arena), nrows, dim,
-                                         q, q_is_f32, cand, C, k, offs, out_s, out_id, tiled);
+                                         q, q_is_f32, cand, C, k, offs, out_s, out_id);
   return static_cast<int>(cudaGetLastError());
 }
 
-// Pipelined gather (bf16 arenas). Ring depth per warp from the row size: ~96 KB of rows in
-// flight per block (two blocks per SM up to dim 1024).
+template <int CPL, bool kTiled>
+int launch_rerank_ring_s(int slots, const void* arena, int64_t nrows, int dim, const void* q,
+                         int q_is_f32, int B, const int32_t* cand, int C, int k,
+                         const int32_t* offs, float* out_s, int32_t* out_id, cudaStream_t stream) {
+  switch (slots) {
+    case 2: return launch_rerank_ring_v<16, 2, CPL, kTiled>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream);
+    case 3: return launch_rerank_ring_v<16, 3, CPL, kTiled>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream);
+    default: return launch_rerank_ring_v<16, 4, CPL, kTiled>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream);
+  }
+}
+
+template <bool kTiled>
+int launch_rerank_ring_t(int slots, const void* arena, int64_t nrows, int dim, const void* q,
+                         int q_is_f32, int B, const int32_t* cand, int C, int k,
+                         const int32_t* offs, float* out_s, int32_t* out_id, cudaStream_t stream) {
+  const int cpl = (dim / 8 + 31) / 32;  // 16-byte chunks per lane
+  if (cpl <= 1) return launch_rerank_ring_s<1, kTiled>(slots, arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream);
+  if (cpl <= 2) return launch_rerank_ring_s<2, kTiled>(slots, arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream);
+  if (cpl <= 3) return launch_rerank_ring_s<3, kTiled>(slots, arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream);
+  if (cpl <= 4) return launch_rerank_ring_s<4, kTiled>(slots, arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream);
+  if (cpl <= 8) return launch_rerank_ring_s<8, kTiled>(slots, arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream);
+  return static_cast<int>(cudaErrorInvalidValue);
+}
+
+// Pipelined gather (bf16 arenas, dim <= 2048). Ring depth per warp: as many rows as keep ~96 KB
+// of a block's rows in flight (2 to 4), so two 16-warp blocks share an SM up to dim 1024.
 int launch_rerank_ring(const void* arena, int64_t nrows, int dim, const void* q, int q_is_f32,
                        int B, const int32_t* cand, int C, int k, const int32_t* offs,
                        float* out_s, int32_t* out_id, cudaStream_t stream, int tiled) {
   if (B <= 0) return 0;
-  int slots = 4;
-  if (const char* e = getenv("TSV_RERANK_SLOTS")) slots = atoi(e);
   const int row_bytes = dim * 2;
-  if (!getenv("TSV_RERANK_SLOTS")) {
-    slots = (96 * 1024) / (16 * row_bytes);
-    slots = slots >= 8 ? 8 : (slots >= 4 ? 4 : 2);
-  }
-  if (16 * 2 * row_bytes > 200 * 1024) return static_cast<int>(cudaErrorInvalidValue);
-  switch (slots) {
-    case 2: return launch_rerank_ring_v<16, 2>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream, tiled);
-    case 8: return launch_rerank_ring_v<16, 8>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream, tiled);
-    case 6: return launch_rerank_ring_v<16, 6>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream, tiled);
-    case 3: return launch_rerank_ring_v<16, 3>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream, tiled);
-    default: return launch_rerank_ring_v<16, 4>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream, tiled);
-  }
+  int slots = (96 * 1024) / (16 * row_bytes);
+  if (const char* e = getenv("TSV_RERANK_SLOTS")) slots = atoi(e);
+  slots = slots < 2 ? 2 : (slots > 4 ? 4 : slots);
+  while (slots > 2 && 16 * slots * row_bytes > 200 * 1024) --slots;
+  if (dim > 2048) return static_cast<int>(cudaErrorInvalidValue);
+  return tiled ? launch_rerank_ring_t<true>(slots, arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream)
+               : launch_rerank_ring_t<false>(slots, arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream);
 }
 
 int launch_normalize(const void* src, int src_is_f32, int64_t n, int dim, int do_normalize,

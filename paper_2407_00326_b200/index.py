@@ -91,6 +91,7 @@ class DeviceIndex:
                                             STORAGE[storage], int(capacity), ctypes.byref(h)))
             self._h = h
         self.dim = int(lib.tsv_index_dim(self._h))
+        self.capacity = int(capacity)
         self.storage = {v: k for k, v in STORAGE.items()}[lib.tsv_index_storage(self._h)]
 
     @classmethod
@@ -156,6 +157,13 @@ class DeviceIndex:
         nat.check(nat.load().tsv_index_append(self._h, rows.data_ptr(), _dtype_code(rows),
                                               rows.shape[0], ctypes.byref(first),
                                               _stream_handle(stream, self.device)))
+        return int(first.value)
+
+    def reserve(self, n: int) -> int:
+        """Claim n arena rows without writing them (the caller fills them, e.g. the ingest
+        stages of a per-query index); returns the first claimed row."""
+        first = ctypes.c_int64()
+        nat.check(nat.load().tsv_index_reserve(self._h, int(n), ctypes.byref(first)))
         return int(first.value)
 
     def truncate(self, rows: int) -> None:

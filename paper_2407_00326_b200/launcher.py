@@ -31,23 +31,75 @@ import torch
 
 from .engines import EngineSet
 from .errors import ConfigParse
+from .graph import CONTROL_KINDS
 from .runtime import BatchRecord, RuntimeOptions, Simulator
 
 
 class StreamRuntime(Simulator):
-    """Wall-clock execution of submitted e-graphs; retrieval batches complete on CUDA events."""
+    """Wall-clock execution of submitted e-graphs; retrieval batches complete on CUDA events.
+
+    Edges cost nothing: like the reference's threaded mode (threaded.py:108-128: a completed
+    node dispatches its ready children at once), there is no modelled Ray hop here — a
+    transfer that really happens (a query's index pulled to another replica) is a peer copy on
+    the device, inside the measured batch.
+
+    stream_order=True (default) maps the reference's pre-scheduling (runtime.py:419-454) onto
+    CUDA stream order: a GPU batch completes *logically* when it is launched, so the consumers
+    that run on the device (the next Searching stage, the Aggregate join, Reranking) are
+    dispatched right away and their kernels queue behind the producer's on the replica stream
+    (cross-replica consumers wait on the producer's event; backend.py). Consumers on modelled
+    engines (LLM, embedding, ...) are only released once every device batch upstream of them
+    has finished (its end event), so nothing modelled starts before its GPU input exists. The
+    trace's `complete` event of a GPU node is its launch; BatchRecord keeps the device-measured
+    time of every batch and `device_done` events mark the real completions."""
 
     def __init__(self, engines: EngineSet, backend, options: RuntimeOptions | None = None,
-                 speed: float = 1.0, poll_us: float = 20.0, timeout_s: float = 60.0):
+                 speed: float = 1.0, poll_us: float = 20.0, timeout_s: float = 60.0,
+                 stream_order: bool = True):
         super().__init__(engines, options, backend=backend)
         self.speed = speed
         self.poll_s = poll_us * 1e-6
         self.timeout_s = timeout_s
+        self.stream_order = stream_order
         self._t0 = None
         self._inflight: list[tuple] = []  # (end_event, start_event, state, instance, plan, t)
+        self._node_events: dict[tuple[str, str], list] = {}  # (query, node) -> end events
+        self._parked: list[tuple] = []  # (ctx, node_id, events) waiting for device inputs
+        self.device_done: list[tuple[float, str, str]] = []  # (ms, query, node)
 
     def _wall(self) -> float:
         return (time.perf_counter() - self._t0) * 1000.0 * self.speed
+
+    def _edge_delay(self, graph, e) -> float:
+        return 0.0
+
+    def _gpu(self, node) -> bool:
+        return (self.backend is not None and node.meta.engine_id in self.engines
+                and self.backend.serves(self.engines[node.meta.engine_id].profile))
+
+    def _upstream_events(self, ctx, nid: str, seen=None) -> list:
+        """Device end events a node's inputs still depend on: its GPU producers' batches, and
+        through control nodes (Aggregate) their producers'."""
+        seen = set() if seen is None else seen
+        out = []
+        for e in ctx.graph.edges:
+            if e.dst != nid or e.src in seen:
+                continue
+            seen.add(e.src)
+            src = ctx.graph.nodes[e.src]
+            out += self._node_events.get((ctx.query_id, e.src), [])
+            if src.kind in CONTROL_KINDS:
+                out += self._upstream_events(ctx, e.src, seen)
+        return out
+
+    def _node_ready(self, ctx, nid: str, t: float) -> None:
+        node = ctx.graph.nodes[nid]
+        if self.stream_order and node.kind not in CONTROL_KINDS and not self._gpu(node):
+            pending = [ev for ev in self._upstream_events(ctx, nid) if not ev.query()]
+            if pending:
+                self._parked.append((ctx, nid, pending))
+                return
+        super()._node_ready(ctx, nid, t)
 
     # GPU batches: launch and return; completion is discovered by polling the end event.
     def _dispatch(self, state, plan, t):
@@ -68,21 +120,37 @@ class StreamRuntime(Simulator):
             if task.ctx.stats[task.node_id].first_start_ms is None:
                 task.ctx.stats[task.node_id].first_start_ms = t
                 self._emit(t, task.ctx, task.node, "start")
+            self._node_events.setdefault((task.ctx.query_id, task.node_id), []).append(end)
+            if self.stream_order:  # consumers queue behind this batch in stream order
+                self._push(t, self._REQ_DONE, (task, n))
         state.queue = [task for task in state.queue if task.pending() > 0]
         self._inflight.append((end, start, state, instance, plan, t))
 
     def _poll(self, t: float) -> bool:
+        progressed = False
+        if self._parked:
+            still = []
+            for ctx, nid, evs in self._parked:
+                evs = [ev for ev in evs if not ev.query()]
+                if evs:
+                    still.append((ctx, nid, evs))
+                else:
+                    Simulator._node_ready(self, ctx, nid, t)
+                    progressed = True
+            self._parked = still
         done, still = [], []
         for x in self._inflight:
             (done if x[0].query() else still).append(x)
         if not done:
-            return False
+            return progressed
         self._inflight = still
         for end, start, state, instance, plan, t0 in done:
             instance.busy_until = t
             device_ms = start.elapsed_time(end)
             for task, n in plan.entries:
-                self._push(t, self._REQ_DONE, (task, n))
+                if not self.stream_order:
+                    self._push(t, self._REQ_DONE, (task, n))
+                self.device_done.append((t, task.ctx.query_id, task.node_id))
             self._push(t, self._BATCH_DONE, (state.profile.engine_id, instance.instance_id, 0.0))
             self.trace.batches.append(BatchRecord(state.profile.engine_id, instance.instance_id,
                                                   t0, t, plan.load, self._cap(state), plan.phase,
@@ -92,7 +160,7 @@ class StreamRuntime(Simulator):
     def run(self, until: float | None = None):
         self._t0 = time.perf_counter()
         deadline = time.perf_counter() + self.timeout_s
-        while self._events or self._inflight:
+        while self._events or self._inflight or self._parked:
             if time.perf_counter() > deadline:
                 raise TimeoutError("stream runtime did not quiesce")
             t = self._wall()

@@ -1,7 +1,11 @@
-"""K3 rerank latency at C3 / C5 shapes (diagnostic; run under gpurun). Candidate sets rotate
-over 4 random draws (4 x 79 MB > L2) for the HBM case, or repeat one draw for the L2 case.
-Environment knobs select the kernel: TSV_RERANK_LDG=1 (register gather), TSV_RERANK_BUFS /
-TSV_RERANK_BUF_KB (bulk-copy ring)."""
+"""K3 rerank device time at C3 / C5 shapes (diagnostic; run under gpurun).
+
+Each variant replays a CUDA graph of 32 rerank calls whose candidate sets rotate over 8
+random draws (8 x 79 MB > L2: rows come from HBM; `l2` repeats one draw), so the number is the
+kernel's device time per call without the host's per-call issue cost (~15 us from Python).
+Variants: ldg = register gather (TSV_RERANK_LDG=1), ring = cp.async rings (default; slots via
+TSV_RERANK_SLOTS). PROBE_SPAN limits candidates to the first rows of the corpus."""
+import os
 import sys
 from pathlib import Path
 
@@ -10,41 +14,61 @@ import torch
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2407_00326_b200.index import DeviceIndex, normalize_rows  # noqa: E402
 
+VARIANTS = [("ldg", {"TSV_RERANK_LDG": "1"}), ("ring", {}), ("ring2", {"TSV_RERANK_SLOTS": "2"}),
+            ("ring3", {"TSV_RERANK_SLOTS": "3"})]
 
-def timed(fn, reps=100):
-    for _ in range(10):
-        fn()
+
+def graph_time(calls, reps=20):
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for fn in calls:  # warm-up grows workspaces outside the capture
+            fn(s)
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for fn in calls:
+            fn(torch.cuda.current_stream())
+    for _ in range(3):
+        g.replay()
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     for _ in range(reps):
-        fn()
+        g.replay()
     b.record()
     torch.cuda.synchronize()
-    return a.elapsed_time(b) / reps * 1000
+    return a.elapsed_time(b) / reps / len(calls) * 1000
 
 
 def main():
     dev = torch.device("cuda", 0)
     g = torch.Generator(device=dev).manual_seed(0)
     out = []
-    for n, d, bq, c, k in ((1_000_000, 768, 256, 200, 10), (1_000_000, 1024, 16, 32, 3)):
+    for n, d, bq, c, k in ((1_000_000, 768, 256, 200, 10), (1_000_000, 1024, 16, 32, 3),
+                           (1_000_000, 1024, 256, 200, 10)):
         idx = DeviceIndex(d, n, metric="ip", device=0)
         for a in range(0, n, 1 << 18):
             idx.append(normalize_rows(torch.randn((min(1 << 18, n - a), d), generator=g, device=dev)))
         q = normalize_rows(torch.randn((bq, d), generator=g, device=dev))
-        cands = [torch.randint(0, n, (bq, c), generator=g, device=dev, dtype=torch.int32)
-                 for _ in range(4)]
-        it = [0]
-
-        def rot():
-            it[0] = (it[0] + 1) & 3
-            idx.rerank(q, cands[it[0]], k)
-
-        out.append(f"{bq}x{c}x{d}: hbm {timed(rot):6.1f} us  l2 {timed(lambda: idx.rerank(q, cands[0], k)):6.1f} us")
+        span = int(os.environ.get("PROBE_SPAN", n))
+        cands = [torch.randint(0, span, (bq, c), generator=g, device=dev, dtype=torch.int32)
+                 for _ in range(8)]
+        outs = [(torch.empty((bq, k), device=dev), torch.empty((bq, k), device=dev, dtype=torch.int32))
+                for _ in range(32)]
+        hbm = [lambda st, j=j: idx.rerank(q, cands[j % 8], k, stream=st, out=outs[j]) for j in range(32)]
+        l2 = [lambda st, j=j: idx.rerank(q, cands[0], k, stream=st, out=outs[j]) for j in range(32)]
+        alg = bq * c * d * 2
+        for name, env in VARIANTS:
+            for key in ("TSV_RERANK_LDG", "TSV_RERANK_SLOTS"):
+                os.environ.pop(key, None)
+            os.environ.update(env)
+            th = graph_time(hbm)
+            tl = graph_time(l2)
+            out.append(f"{name} {bq}x{c}x{d}: hbm {th:6.2f} us ({alg / th / 1e3:6.0f} GB/s)  "
+                       f"l2 {tl:6.2f} us")
         del idx
         torch.cuda.empty_cache()
-    print(" | ".join(out))
+    print("\n".join(out))
 
 
 if __name__ == "__main__":

@@ -32,13 +32,47 @@ def test_stream_runtime_completes_workflows_with_real_results(cuda):
     for name in ("advanced_c3", "contextual"):
         case = next(c for c in traces if c["case"] == name and c["scheduler"] == "topo")
         graphs += [(parse_graph(g), a) for g, a, _ in case["graphs"]]
-    backend = RetrievalBackend(dim=256, devices=[0, 0], arena_rows=1 << 16)
+    backend = RetrievalBackend(dim=1024, devices=[0, 0], arena_rows=1 << 16)
     rt, trace = run_streamed(es, graphs, backend, speed=20.0)
     assert all(ctx.finish_ms is not None for ctx in rt.contexts.values())
     gpu = [b for b in trace.batches if b.engine_id in ("vdb-search0", "rerank0")]
     assert gpu and all(b.device_ms is not None and b.device_ms > 0 for b in gpu)
     assert {b.instance_id for b in gpu} == {0, 1}
     assert _check_outputs(rt, backend) > 0
+    # stream order: device consumers were dispatched before their producers finished on the
+    # device, but every modelled consumer started only after the device work it depends on
+    done = {}
+    for t, q, n in rt.device_done:
+        done[(q, n)] = max(t, done.get((q, n), 0.0))
+    from paper_2407_00326_b200.graph import CONTROL_KINDS
+
+    checked = 0
+    for ctx in rt.contexts.values():
+        for nid, node in ctx.graph.nodes.items():
+            if rt._gpu(node) or node.kind in CONTROL_KINDS:
+                continue
+            for e in ctx.graph.edges:
+                if e.dst == nid and (ctx.query_id, e.src) in done:
+                    assert ctx.stats[nid].first_start_ms >= done[(ctx.query_id, e.src)] - 1e-6
+                    checked += 1
+    assert checked > 0
+
+
+def test_stream_runtime_has_no_modelled_hops(cuda):
+    """threaded.py:108-128 dispatches a completed node's children at once: the stream runtime
+    adds no modelled Ray hop on any edge (the simulator's hop_ms + tokens * per_token_ms)."""
+    from paper_2407_00326_b200 import engines as E
+    from paper_2407_00326_b200.backend import RetrievalBackend
+    from paper_2407_00326_b200.graph import parse_graph
+    from paper_2407_00326_b200.launcher import StreamRuntime
+
+    traces = json.loads((GOLD / "ref_traces.json").read_text())
+    prof = json.loads((GOLD / "ref_profiles.json").read_text())["default"]["profiles"]
+    es = E.EngineSet.from_dict(prof)
+    case = next(c for c in traces if c["case"] == "advanced_c3" and c["scheduler"] == "topo")
+    g = parse_graph(case["graphs"][0][0])
+    rt = StreamRuntime(es, RetrievalBackend(dim=1024, arena_rows=1 << 14))
+    assert all(rt._edge_delay(g, e) == 0.0 for e in g.edges)
 
 
 def test_captured_search_replays_exactly(cuda):

@@ -198,12 +198,13 @@ def test_rerank_shapes_match_oracle(cuda, n, dim, b, c, k):
 
 
 @pytest.mark.parametrize("dim,c,k,slots", [(768, 200, 10, None), (1024, 32, 3, None),
-                                            (384, 57, 5, 2), (256, 300, 12, 8), (2048, 40, 4, None),
-                                            (64, 3, 3, 3)])
+                                            (384, 57, 5, 2), (256, 300, 12, 4), (2048, 40, 4, None),
+                                            (64, 3, 3, 3), (520, 77, 6, None)])
 def test_rerank_ring_equals_register_gather(cuda, dim, c, k, slots):
-    """The pipelined K3 (cp.async rings, bf16 arenas) against the register-gather K3
-    (TSV_RERANK_LDG=1): same chunk order, same reduction tree, so bit-identical scores and ids;
-    ring depths 2-8, candidate counts below / above one ring's worth, invalid ids, duplicates."""
+    """The pipelined K3 (cp.async rings, question in registers, packed fp32x2 FMAs; bf16
+    arenas) against the register-gather K3 (TSV_RERANK_LDG=1) and the oracle: scores equal up to
+    the summation order (even / odd halves), ids equal wherever neighbouring scores differ;
+    ring depths 2-4, candidate counts below / above one ring's worth, invalid ids, duplicates."""
     import os
 
     import torch
@@ -233,10 +234,13 @@ def test_rerank_ring_equals_register_gather(cuda, dim, c, k, slots):
                 os.environ.pop(key, None)
             else:
                 os.environ[key] = v
-    np.testing.assert_array_equal(from_dev(i1), from_dev(i2))
-    np.testing.assert_array_equal(from_dev(s1), from_dev(s2))
+    g1, g2 = from_dev(s1), from_dev(s2)
+    np.testing.assert_allclose(g1, g2, rtol=2e-6, atol=1e-7)
+    sep = np.abs(np.diff(g2, axis=1, prepend=np.inf)) > 1e-5
+    sep &= np.abs(np.diff(g2, axis=1, append=-np.inf)) > 1e-5
+    assert (from_dev(i1)[sep] == from_dev(i2)[sep]).all()
     exp_s, _ = orc.rerank(qs, arena, cand, k)
-    np.testing.assert_allclose(from_dev(s1), exp_s, rtol=TOL, atol=1e-6)
+    np.testing.assert_allclose(g1, exp_s, rtol=TOL, atol=1e-6)
 
 
 @pytest.mark.parametrize("storage", ["bf16", "bf16_tiled", "f32"])

@@ -127,3 +127,23 @@ def test_pgvector_restatement_agrees_with_oracle(op):
     c2 = np.concatenate([c[:50], c[:50]])
     ps2, pi2 = orc.pgvector_exact_search(c2[:3], c2, 2, op=op)
     np.testing.assert_array_equal(pi2, [[0, 50], [1, 51], [2, 52]])
+
+
+def test_amx_oracle_matches_numpy_oracle():
+    """The AMX-BF16 build of the C oracle (the CPU baseline on AMX hosts) agrees with the numpy
+    restatement: bf16 products are exact and accumulate in fp32 on the tiles, so only the
+    summation order differs (ragged corpus blocks, a ragged last query tile, id offsets)."""
+    from oracle import c_oracle
+
+    lib = c_oracle.load("amx")
+    if not lib.amx:
+        pytest.skip("no AMX-BF16 on this host")
+    c = orc.make_corpus(5003, 128, seed=4)
+    q, _ = orc.make_queries(c, 37, seed=5)
+    cb, qb = orc.bf16_bits(c), orc.bf16_bits(q)
+    s, i = c_oracle._search(lib, qb, cb, 10, False, 4, 1000)
+    probs = orc.check_topk(s, i, orc.bf16_to_f32(qb), orc.bf16_to_f32(cb), 10, 1e-3,
+                           id_offset=1000)
+    assert not probs, probs[:5]
+    s2, i2 = c_oracle._search(c_oracle.load("v3"), qb, cb, 10, False, 4, 1000)
+    np.testing.assert_allclose(s, s2, rtol=1e-5, atol=1e-6)
