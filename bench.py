@@ -643,11 +643,21 @@ def run_ours(args):
     achieved_gbs = bytes_alg / (avg_scan_ms / 1000.0) / 1e9
     peak_tf = float(peaks.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"]))
     peak_tf_sus = float(peaks.get("bf16_tflops_sustained", FALLBACK_PEAKS["bf16_tflops_sustained"]))
+    f32_peak_src = None
     if args.storage == "f32":
-        # fp32 mode: 3 tf32 MMAs per product; tf32 dense rate is half the bf16 rate, so the
-        # algorithmic-fp32-flop ceiling is bf16 / 6 (no measured tf32 peak in MEASURED_PEAKS)
-        peak_tf /= 6.0
-        peak_tf_sus /= 6.0
+        # fp32 mode: 3 tf32 MMAs per product, so the algorithmic-fp32-flop ceiling is the
+        # measured cuBLAS TF32 peak / 3 (scripts/tf32_peak.py -> profiles/tf32_peak.json);
+        # without that file, the nominal tf32 = bf16 / 2 relation (bf16 / 6)
+        tp = ROOT / "profiles" / "tf32_peak.json"
+        if tp.exists():
+            tj = json.loads(tp.read_text())
+            peak_tf = float(tj["fp32_mode_ceiling_tflops"])
+            peak_tf_sus = float(tj["fp32_mode_ceiling_tflops_sustained"])
+            f32_peak_src = "measured cuBLAS TF32 GEMM / 3 (profiles/tf32_peak.json)"
+        else:
+            peak_tf /= 6.0
+            peak_tf_sus /= 6.0
+            f32_peak_src = "bf16 / 6 (no measured tf32 peak)"
         bytes_alg = n_local * D * 8 + B * D * 4 + B * k * 8
     peak_bw = float(peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"]))
     # The timed kernels run after >= 1 s of continuous load, i.e. at the settled power-capped
@@ -688,8 +698,7 @@ def run_ours(args):
                  "peak_source": (f"{peak_src} (MEASURED_PEAKS.json "
                                  f"{'sustained' if long_step else 'burst'} bf16 / copy GB/s)"
                                  if peak_src == "measured" else "fallback (B200_PROFILING.md)")
-                 + (" / 6 for fp32 mode (3 tf32 MMAs at half the bf16 rate)"
-                    if args.storage == "f32" else "")})
+                 + (f"; fp32 mode: {f32_peak_src}" if args.storage == "f32" else "")})
 
     value = B * args.steps / (dev_ms / 1000.0)
     e2e_value = B * args.steps / (e2e_ms / 1000.0)

@@ -191,10 +191,13 @@ class RetrievalBackend:
     def __init__(self, dim: int, devices: list[int] | None = None, arena_rows: int = 1 << 20,
                  engines=("vdb-search0", "rerank0"), timing: str = TIMING_PROFILE,
                  data: SyntheticData | None = None, metric: str = "cosine",
-                 global_index=None):
+                 global_index=None, release_segments: bool = True):
         """global_index: the resident corpus searched by Searching nodes that have no per-query
         index input — a DeviceIndex, or a ShardedIndex spanning several devices (shards
-        searched concurrently, merged on its root device)."""
+        searched concurrently, merged on its root device).
+        release_segments: a finished query's index segments return to the arena's free list
+        and its device results are dropped (False keeps them for inspection, e.g. tests)."""
+        self.release_segments = release_segments
         if timing not in (TIMING_PROFILE, TIMING_MEASURED):
             raise ConfigParse(f"unknown timing mode {timing!r}")
         _native.load()
@@ -244,6 +247,8 @@ class RetrievalBackend:
         """A query finished: its per-query index segments go back to their replicas' free
         lists (reused once every stream that may still read them has passed this point), and
         its device results are dropped."""
+        if not self.release_segments:
+            return
         mine = [key for key in self.segments if key[0] == ctx.query_id]
         for key in mine:
             seg = self.segments.pop(key)

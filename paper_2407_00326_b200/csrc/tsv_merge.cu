@@ -581,6 +581,147 @@ __global__ void __launch_bounds__(kWarps * 32) rerank_ring_kernel(
   }
 }
 
+// K3 for the common rerank shapes (C <= 32 * kWarps candidates, k <= 32): the gather and
+// scoring of rerank_ring_kernel, with the per-row bookkeeping moved out of the loop and the
+// block-wide sort replaced by per-warp top-k lists.
+//  * each warp owns candidates c = warp + kWarps j (j < 32): lane j holds candidate j's id,
+//    validity (one ballot) and row address, so a row's issue is two shuffles and CPL cp.async;
+//  * after the butterfly reduction every lane holds the row's score; the warp keeps a sorted
+//    top-k list in registers (lane r = rank r) and inserts with one ballot + one shuffle when
+//    the key beats the list's k-th (a key already in the list is a duplicate candidate id:
+//    same row, same score);
+//  * warp 0 merges the kWarps lists with k rounds of a warp-wide max, dropping every copy of
+//    the chosen key (duplicates across warps).
+template <int kWarps, int kSlots, int CPL, bool kTiled>
+__global__ void __launch_bounds__(kWarps * 32) rerank_lists_kernel(
+    const __nv_bfloat16* __restrict__ arena, int64_t nrows, int dim, const void* __restrict__ q,
+    int q_is_f32, const int32_t* __restrict__ cand, int C, int k, const int32_t* __restrict__ offs,
+    float* __restrict__ out_s, int32_t* __restrict__ out_id) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int row_bytes = dim * 2;
+  uint8_t* ring = sm;                                                   // [kWarps][kSlots][row]
+  uint64_t* lists = reinterpret_cast<uint64_t*>(sm + static_cast<size_t>(kWarps) * kSlots * row_bytes);
+  const int b = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int chunks = dim >> 3;
+  float2 qr[CPL][4];
+#pragma unroll
+  for (int j = 0; j < CPL; ++j) {
+    const int ch = lane + 32 * j;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) qr[j][t] = make_float2(0.f, 0.f);
+    if (ch < chunks) {
+      const int64_t o = static_cast<int64_t>(b) * dim + ch * 8;
+      if (q_is_f32) {
+        const float4 x0 = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(q) + o));
+        const float4 x1 = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(q) + o + 4));
+        qr[j][0] = make_float2(x0.x, x0.y);
+        qr[j][1] = make_float2(x0.z, x0.w);
+        qr[j][2] = make_float2(x1.x, x1.y);
+        qr[j][3] = make_float2(x1.z, x1.w);
+      } else {
+        const uint4 w = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(q) + o));
+        qr[j][0] = bf16x2_to_float2(w.x);
+        qr[j][1] = bf16x2_to_float2(w.y);
+        qr[j][2] = bf16x2_to_float2(w.z);
+        qr[j][3] = bf16x2_to_float2(w.w);
+      }
+    }
+  }
+  const int64_t base = offs != nullptr ? __ldg(offs + b) : 0;  // per-question segment start
+  const int nrow = warp < C ? (C - warp + kWarps - 1) / kWarps : 0;  // <= 32
+  const int32_t my_id = lane < nrow ? __ldg(cand + static_cast<int64_t>(b) * C + warp + kWarps * lane) : -1;
+  const bool my_ok = my_id >= 0 && base + my_id < nrows;
+  const uint32_t okmask = __ballot_sync(0xffffffffu, my_ok);
+  const int64_t r = my_ok ? base + my_id : 0;
+  const int64_t kb_per_row = (dim + 63) >> 6;
+  const uint4* my_src = kTiled ? reinterpret_cast<const uint4*>(arena + ((r >> 7) * kb_per_row * 128 + (r & 127)) * 64)
+                               : reinterpret_cast<const uint4*>(arena + r * dim);
+  uint8_t* my_ring = ring + static_cast<size_t>(warp) * kSlots * row_bytes;
+  auto issue = [&](int j, int slot) {  // whole warp; always commits one group
+    const uint4* src = reinterpret_cast<const uint4*>(
+        __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(my_src), j & 31));
+    if (j < nrow && ((okmask >> j) & 1u)) {
+      uint4* dst = reinterpret_cast<uint4*>(my_ring + static_cast<size_t>(slot) * row_bytes);
+#pragma unroll
+      for (int jj = 0; jj < CPL; ++jj) {
+        const int ch = lane + 32 * jj;
+        if (ch < chunks)
+          cp_async16(dst + ch, src + (kTiled ? static_cast<int64_t>(ch >> 3) * 1024 + (ch & 7) : ch));
+      }
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int s_ = 0; s_ < kSlots; ++s_) issue(s_, s_);
+  uint64_t lk = pad_key();   // this warp's top-k list, rank = lane
+  uint64_t thr = pad_key();  // its k-th key
+  int slot = 0;
+  for (int j = 0; j < nrow; ++j) {
+    cp_async_wait<kSlots - 1>();  // the oldest group (row j) has landed
+    __syncwarp();
+    if ((okmask >> j) & 1u) {
+      const uint4* row = reinterpret_cast<const uint4*>(my_ring + static_cast<size_t>(slot) * row_bytes);
+      float2 a2 = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int jj = 0; jj < CPL; ++jj) {
+        const int ch = lane + 32 * jj;
+        if (ch < chunks) {
+          const uint4 raw = row[ch];
+          a2 = __ffma2_rn(bf16x2_to_float2(raw.x), qr[jj][0], a2);
+          a2 = __ffma2_rn(bf16x2_to_float2(raw.y), qr[jj][1], a2);
+          a2 = __ffma2_rn(bf16x2_to_float2(raw.z), qr[jj][2], a2);
+          a2 = __ffma2_rn(bf16x2_to_float2(raw.w), qr[jj][3], a2);
+        }
+      }
+      float acc = a2.x + a2.y;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      const uint64_t key = make_key(acc, __shfl_sync(0xffffffffu, my_id, j));
+      if (key > thr && !__any_sync(0xffffffffu, lk == key)) {
+        const int pos = __popc(__ballot_sync(0xffffffffu, lk > key));
+        const uint64_t up = __shfl_up_sync(0xffffffffu, lk, 1);
+        if (lane == pos) lk = key;
+        else if (lane > pos) lk = up;
+        thr = __shfl_sync(0xffffffffu, lk, k - 1);
+      }
+    }
+    __syncwarp();  // every lane done reading the slot before it is refilled
+    issue(j + kSlots, slot);
+    if (++slot == kSlots) slot = 0;
+  }
+  cp_async_wait<0>();
+  if (lane < k) lists[warp * k + lane] = lk;
+  __syncthreads();
+  if (warp != 0) return;
+  constexpr int kPer = kWarps;  // kWarps * k <= kWarps * 32 keys, kWarps per lane
+  uint64_t mine[kPer];
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const int e = lane + 32 * i;
+    mine[i] = e < kWarps * k ? lists[e] : pad_key();
+  }
+  const uint64_t pad = pad_key();
+  for (int rk = 0; rk < k; ++rk) {
+    uint64_t m = mine[0];
+#pragma unroll
+    for (int i = 1; i < kPer; ++i) m = mine[i] > m ? mine[i] : m;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t other = __shfl_xor_sync(0xffffffffu, m, o);
+      m = other > m ? other : m;
+    }
+    if (lane == 0) {
+      const int32_t id = m == pad ? -1 : key_id(m);
+      out_s[static_cast<int64_t>(b) * k + rk] = id < 0 ? -INFINITY : key_score(m);
+      out_id[static_cast<int64_t>(b) * k + rk] = id;
+    }
+#pragma unroll
+    for (int i = 0; i < kPer; ++i)
+      if (mine[i] == m) mine[i] = pad;  // every copy of this id (duplicate candidates)
+  }
+}
+
 // One warp per row: optional L2 normalisation (fp32 math) and cast to bf16.
 __global__ void normalize_kernel(const void* __restrict__ src, int src_is_f32, int64_t n, int dim,
                                  int do_normalize, __nv_bfloat16* __restrict__ dst) {
@@ -974,10 +1115,47 @@ int launch_rerank_ring_v(const void* arena, int64_t nrows, int dim, const void* 
   return static_cast<int>(cudaGetLastError());
 }
 
+template <int kWarps, int kSlots, int CPL, bool kTiled>
+int launch_rerank_lists_v(const void* arena, int64_t nrows, int dim, const void* q, int q_is_f32,
+                          int B, const int32_t* cand, int C, int k, const int32_t* offs,
+                          float* out_s, int32_t* out_id, cudaStream_t stream) {
+  const size_t smem = static_cast<size_t>(kWarps) * kSlots * dim * 2 +
+                      static_cast<size_t>(kWarps) * 32 * sizeof(uint64_t);
+  if (smem > 220 * 1024) return static_cast<int>(cudaErrorInvalidValue);
+  auto kern = rerank_lists_kernel<kWarps, kSlots, CPL, kTiled>;
+  static std::atomic<uint64_t> configured{0};
+  if (smem > 48 * 1024 && first_on_device(configured)) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    if (e != cudaSuccess) return static_cast<int>(e);
+  }
+  kern<<<B, kWarps * 32, smem, stream>>>(reinterpret_cast<const __nv_bfloat16*>(arena), nrows, dim,
+                                         q, q_is_f32, cand, C, k, offs, out_s, out_id);
+  return static_cast<int>(cudaGetLastError());
+}
+
 template <int CPL, bool kTiled>
 int launch_rerank_ring_s(int slots, const void* arena, int64_t nrows, int dim, const void* q,
                          int q_is_f32, int B, const int32_t* cand, int C, int k,
                          const int32_t* offs, float* out_s, int32_t* out_id, cudaStream_t stream) {
+  // (A/B knob: TSV_RERANK_WARPS=8/32 warps per block for the lists kernel, dim 512-1024)
+  if constexpr ((CPL == 3 || CPL == 4) && !kTiled) {
+    const char* w = getenv("TSV_RERANK_WARPS");
+    const int nw = w ? atoi(w) : 16;
+    if (nw == 8 && C <= 8 * 32 && k <= 32)
+      return slots == 2 ? launch_rerank_lists_v<8, 2, CPL, kTiled>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream)
+                        : launch_rerank_lists_v<8, 4, CPL, kTiled>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream);
+    if (nw == 32 && C <= 32 * 32 && k <= 32)
+      return slots == 2 ? launch_rerank_lists_v<32, 2, CPL, kTiled>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream)
+                        : launch_rerank_lists_v<32, 4, CPL, kTiled>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream);
+  }
+  // C <= 512 candidates and k <= 32: per-warp lists (no block-wide sort)
+  if (C <= 16 * 32 && k <= 32 && !getenv("TSV_RERANK_SORT")) {
+    switch (slots) {
+      case 2: return launch_rerank_lists_v<16, 2, CPL, kTiled>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream);
+      case 3: return launch_rerank_lists_v<16, 3, CPL, kTiled>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream);
+      default: return launch_rerank_lists_v<16, 4, CPL, kTiled>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream);
+    }
+  }
   switch (slots) {
     case 2: return launch_rerank_ring_v<16, 2, CPL, kTiled>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream);
     case 3: return launch_rerank_ring_v<16, 3, CPL, kTiled>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream);

@@ -15,7 +15,12 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2407_00326_b200.index import DeviceIndex, normalize_rows  # noqa: E402
 
 VARIANTS = [("ldg", {"TSV_RERANK_LDG": "1"}), ("ring", {}), ("ring2", {"TSV_RERANK_SLOTS": "2"}),
-            ("ring3", {"TSV_RERANK_SLOTS": "3"})]
+            ("ring3", {"TSV_RERANK_SLOTS": "3"}),
+            ("w8s2", {"TSV_RERANK_WARPS": "8", "TSV_RERANK_SLOTS": "2"}),
+            ("w8s4", {"TSV_RERANK_WARPS": "8", "TSV_RERANK_SLOTS": "4"}),
+            ("w32s2", {"TSV_RERANK_WARPS": "32", "TSV_RERANK_SLOTS": "2"}),
+            ("w32s4", {"TSV_RERANK_WARPS": "32", "TSV_RERANK_SLOTS": "4"})]
+KNOBS = ("TSV_RERANK_LDG", "TSV_RERANK_SLOTS", "TSV_RERANK_WARPS")
 
 
 def graph_time(calls, reps=20):
@@ -59,16 +64,19 @@ def main():
         l2 = [lambda st, j=j: idx.rerank(q, cands[0], k, stream=st, out=outs[j]) for j in range(32)]
         alg = bq * c * d * 2
         for name, env in VARIANTS:
-            for key in ("TSV_RERANK_LDG", "TSV_RERANK_SLOTS"):
+            for key in KNOBS:
                 os.environ.pop(key, None)
             os.environ.update(env)
-            th = graph_time(hbm)
-            tl = graph_time(l2)
-            out.append(f"{name} {bq}x{c}x{d}: hbm {th:6.2f} us ({alg / th / 1e3:6.0f} GB/s)  "
-                       f"l2 {tl:6.2f} us")
+            try:
+                th = graph_time(hbm)
+                tl = graph_time(l2)
+            except Exception as exc:  # noqa: BLE001 - a variant that does not fit this shape
+                print(f"{name} {bq}x{c}x{d}: n/a ({exc})", flush=True)
+                continue
+            print(f"{name} {bq}x{c}x{d}: hbm {th:6.2f} us ({alg / th / 1e3:6.0f} GB/s)  "
+                  f"l2 {tl:6.2f} us", flush=True)
         del idx
         torch.cuda.empty_cache()
-    print("\n".join(out))
 
 
 if __name__ == "__main__":

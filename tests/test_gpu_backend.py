@@ -33,7 +33,8 @@ def _run(case, prof, timing="profile", devices=None, dim=1024):
     from paper_2407_00326_b200.graph import parse_graph
 
     es = E.EngineSet.from_dict(prof)
-    backend = RetrievalBackend(dim=dim, devices=devices, arena_rows=1 << 16, timing=timing)
+    backend = RetrievalBackend(dim=dim, devices=devices, arena_rows=1 << 16, timing=timing,
+                               release_segments=False)
     subs = [(parse_graph(g), a, b) for g, a, b in case["graphs"]]
     sim, trace = R.run_queries(es, subs, R.RuntimeOptions(scheduler=case["scheduler"]),
                                backend=backend)
@@ -149,3 +150,31 @@ def test_measured_profile_gives_gpu_true_beff(cuda):
     assert max_efficient_batch(s) >= 16
     r, _ = measure_rerank_profile(rows=20_000, dim=256, candidates=(8, 32, 128))
     assert r.category == "rerank" and len(r.latency_table) == 3
+
+
+def test_released_segments_are_reused(cuda):
+    """A finished query's per-query index segments go back to the replica's free list and are
+    reused by later queries, so a long run does not grow the arena without bound:
+    six advanced-RAG queries, each arriving after the previous one finished, run in an arena
+    with room for little more than one query's index."""
+    from paper_2407_00326_b200 import engines as E, runtime as R
+    from paper_2407_00326_b200.backend import RetrievalBackend
+    from paper_2407_00326_b200.graph import parse_graph
+
+    traces, prof = _fixture()
+    case = next(c for c in traces if c["case"] == "advanced_c3" and c["scheduler"] == "topo")
+    subs = []
+    for j in range(6):
+        g = parse_graph(case["graphs"][0][0])
+        g.query_id = f"seq-{j}"
+        for n in g.nodes.values():
+            n.meta.query_id = g.query_id
+        subs.append((g, 3000.0 * j, 0.0))
+    need = sum(max(p.items for p in n.meta.outputs.values())
+               for n in subs[0][0].nodes.values() if n.kind.value == "Ingestion")
+    es = E.EngineSet.from_dict(prof)
+    backend = RetrievalBackend(dim=256, arena_rows=need + 16)
+    sim, trace = R.run_queries(es, subs, R.RuntimeOptions(scheduler="topo"), backend=backend)
+    assert all(c.finish_ms is not None for c in sim.contexts.values())
+    assert backend.replicas[0].arena.rows <= need + 16 < 6 * need
+    assert not backend.segments  # every query's segments were released

@@ -32,7 +32,8 @@ def test_stream_runtime_completes_workflows_with_real_results(cuda):
     for name in ("advanced_c3", "contextual"):
         case = next(c for c in traces if c["case"] == name and c["scheduler"] == "topo")
         graphs += [(parse_graph(g), a) for g, a, _ in case["graphs"]]
-    backend = RetrievalBackend(dim=1024, devices=[0, 0], arena_rows=1 << 16)
+    backend = RetrievalBackend(dim=1024, devices=[0, 0], arena_rows=1 << 16,
+                               release_segments=False)
     rt, trace = run_streamed(es, graphs, backend, speed=20.0)
     assert all(ctx.finish_ms is not None for ctx in rt.contexts.values())
     gpu = [b for b in trace.batches if b.engine_id in ("vdb-search0", "rerank0")]

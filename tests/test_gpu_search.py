@@ -199,12 +199,16 @@ def test_rerank_shapes_match_oracle(cuda, n, dim, b, c, k):
 
 @pytest.mark.parametrize("dim,c,k,slots", [(768, 200, 10, None), (1024, 32, 3, None),
                                             (384, 57, 5, 2), (256, 300, 12, 4), (2048, 40, 4, None),
-                                            (64, 3, 3, 3), (520, 77, 6, None)])
+                                            (64, 3, 3, 3), (520, 77, 6, None),
+                                            (768, 200, 10, "sort"), (256, 600, 10, None),
+                                            (512, 100, 40, None), (1024, 512, 32, None)])
 def test_rerank_ring_equals_register_gather(cuda, dim, c, k, slots):
     """The pipelined K3 (cp.async rings, question in registers, packed fp32x2 FMAs; bf16
-    arenas) against the register-gather K3 (TSV_RERANK_LDG=1) and the oracle: scores equal up to
-    the summation order (even / odd halves), ids equal wherever neighbouring scores differ;
-    ring depths 2-4, candidate counts below / above one ring's worth, invalid ids, duplicates."""
+    arenas; per-warp top-k lists for C <= 512, k <= 32, else the block sort, forced by
+    TSV_RERANK_SORT) against the register-gather K3 (TSV_RERANK_LDG=1) and the oracle: scores
+    equal up to the summation order (even / odd halves), ids equal wherever neighbouring scores
+    differ; ring depths 2-4, candidate counts below / above one ring's worth and the lists
+    path's limits, invalid ids, duplicates."""
     import os
 
     import torch
@@ -220,8 +224,10 @@ def test_rerank_ring_equals_register_gather(cuda, dim, c, k, slots):
         cand[:, 2] = cand[:, 1]
     idx = _index_from(arena, cuda)
     qd, cd = to_dev_bf16(qs, cuda), torch.from_numpy(cand).to(cuda)
-    env = {"TSV_RERANK_SLOTS": str(slots)} if slots else {}
-    old = {key: os.environ.get(key) for key in ("TSV_RERANK_SLOTS", "TSV_RERANK_LDG")}
+    env = ({"TSV_RERANK_SORT": "1"} if slots == "sort"
+           else {"TSV_RERANK_SLOTS": str(slots)} if slots else {})
+    old = {key: os.environ.get(key) for key in ("TSV_RERANK_SLOTS", "TSV_RERANK_LDG",
+                                                "TSV_RERANK_SORT")}
     try:
         os.environ.update(env)
         s1, i1 = idx.rerank(qd, cd, k)
