@@ -179,6 +179,14 @@ TSV_API int tsv_sharded_search(tsv_sharded* sh, const void* q_dev, int q_dtype, 
                                float* scores_dev, int32_t* ids_dev, void* stream);
 TSV_API int tsv_sharded_destroy(tsv_sharded* sh);
 
+/* ---- A private (non-blocking) stream of the caller's own, outside any framework's stream
+ * pool: scratch space is kept per (index, stream), so a stream that captures a CUDA graph of
+ * searches must never be handed to another caller (the graph keeps the scratch addresses;
+ * once a stream captured, its scratch is pinned and a call needing more fails with
+ * TSV_ERR_CAPACITY instead of moving it). ---- */
+TSV_API int tsv_stream_create(int device, void** out);
+TSV_API int tsv_stream_destroy(void* stream);
+
 /* ---- K5: L2-normalise (normalize != 0) and cast rows to bf16. ---- */
 TSV_API int tsv_normalize_rows(const void* src_dev, int src_dtype, int64_t n, int dim, int normalize,
                        void* dst_bf16_dev, void* stream);

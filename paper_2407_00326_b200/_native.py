@@ -69,6 +69,8 @@ SIGNATURES = {
     "tsv_sharded_create": (c_int, [c_vp, c_vp, c_int, c_int, c_int, c_int, ctypes.POINTER(c_vp)]),
     "tsv_sharded_search": (c_int, [c_vp, c_vp, c_int, c_int, c_int, c_vp, c_vp, c_vp]),
     "tsv_sharded_destroy": (c_int, [c_vp]),
+    "tsv_stream_create": (c_int, [c_int, ctypes.POINTER(c_vp)]),
+    "tsv_stream_destroy": (c_int, [c_vp]),
 }
 
 _lib = None
@@ -108,3 +110,29 @@ def check(status: int) -> None:
 
 def launch_count() -> int:
     return int(load().tsv_launch_count())
+
+
+class PrivateStream:
+    """A CUDA stream created by the library (not drawn from torch's round-robin stream pool),
+    wrapped as a torch ExternalStream. Captured graphs own one each: a pooled stream could be
+    handed to another caller whose searches would then share (and grow) the scratch space the
+    graph replays."""
+
+    def __init__(self, device: int):
+        h = c_vp()
+        check(load().tsv_stream_create(int(device), ctypes.byref(h)))
+        self.handle = h
+        import torch
+
+        self.stream = torch.cuda.ExternalStream(h.value, device=torch.device("cuda", device))
+
+    def close(self) -> None:
+        if self.handle is not None and self.handle.value:
+            load().tsv_stream_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -103,17 +103,37 @@ int encode_tiled_map(CUtensorMap* map, const void* base, int64_t cap_rows, int d
   return TSV_OK;
 }
 
+// Per-(index, stream) scratch owner: the stream the buffers are used on, and whether a CUDA
+// graph captured on that stream has baked their addresses in (then they may not move).
+struct WsState {
+  cudaStream_t stream = nullptr;
+  bool captured = false;
+};
+
+// Workspace buffer that grows on demand. Growth is stream-ordered (cudaFreeAsync /
+// cudaMallocAsync on the workspace's stream): no device-wide synchronisation inside a search
+// call, and the old buffer is released only after the work queued before it. Once a graph was
+// captured on the stream, growth is refused instead (the graph would keep the old address).
 template <typename T>
 struct DevBuf {
   T* ptr = nullptr;
   size_t cap = 0;  // elements
+  const WsState* ws = nullptr;
   int ensure(size_t n) {
     if (n <= cap) return TSV_OK;
-    if (ptr) cudaFree(ptr);
+    cudaStream_t st = ws ? ws->stream : nullptr;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if ((ws && ws->captured) || cs != cudaStreamCaptureStatusNone)
+      return fail(TSV_ERR_CAPACITY,
+                  "workspace would grow from %zu to %zu elements on a stream with a captured "
+                  "CUDA graph; run the largest shape on it before capturing", cap, n);
+    if (ptr) cudaFreeAsync(ptr, st);
     ptr = nullptr;
     cap = 0;
-    cudaError_t e = cudaMalloc(&ptr, std::max<size_t>(n, 1) * sizeof(T));
-    if (e != cudaSuccess) return cuda_fail(e, "workspace cudaMalloc");
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ptr),
+                                    std::max<size_t>(n, 1) * sizeof(T), st);
+    if (e != cudaSuccess) return cuda_fail(e, "workspace cudaMallocAsync");
     cap = n;
     return TSV_OK;
   }
@@ -125,6 +145,7 @@ struct DevBuf {
 };
 
 struct Workspace {
+  WsState state;
   DevBuf<int32_t> counter;     // lockstep progress counters + shared admission floors
   DevBuf<uint16_t> qbuf;       // bf16 staged queries
   DevBuf<float> qhi, qlo;      // fp32-mode query planes
@@ -136,6 +157,8 @@ struct Workspace {
   DevBuf<int32_t> cand_i;
   DevBuf<int32_t> cand_cnt;    // [B] candidate counts, then the overflow flag
   DevBuf<tsv::ScanItem> items;
+  DevBuf<uint64_t> rr_keys;     // K3 split mode: per-block top-k keys
+  DevBuf<int32_t> rr_arrive;    // K3 split mode: per-question arrival counters (kept zero)
   std::vector<tsv::ScanItem> host_items;
   // Pinned staging for the item table so its upload is a true async copy. A ring of slots,
   // each with an event marking when its upload drained: the host only waits when it laps a
@@ -154,6 +177,15 @@ struct Workspace {
   static constexpr size_t kCapturePoolBytes = 1 << 20;
   uint8_t* capture_pool = nullptr;
   size_t capture_used = 0;
+  void bind(cudaStream_t st) {  // first use on stream st
+    state.stream = st;
+    for (auto* b : {&counter, &seed_i, &part_i, &cand_i, &cand_cnt}) b->ws = &state;
+    for (auto* b : {&qhi, &qlo, &seed_s, &tau0, &part_s, &cand_s}) b->ws = &state;
+    qbuf.ws = &state;
+    items.ws = &state;
+    rr_keys.ws = &state;
+    rr_arrive.ws = &state;
+  }
   void release() {
     for (auto& s : pinned) {
       if (s.ptr) cudaFreeHost(s.ptr);
@@ -176,6 +208,8 @@ struct Workspace {
     cand_i.release();
     cand_cnt.release();
     items.release();
+    rr_keys.release();
+    rr_arrive.release();
   }
 };
 
@@ -217,6 +251,20 @@ struct DeviceGuard {
     if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
   }
 };
+
+// The (index, stream) workspace; a call issued while the stream captures a CUDA graph pins
+// the workspace's buffers for good (see DevBuf).
+Workspace& ws_for(tsv_index* idx, cudaStream_t st) {
+  auto it = idx->ws.find(st);
+  if (it == idx->ws.end()) {
+    it = idx->ws.emplace(st, Workspace()).first;
+    it->second.bind(st);
+  }
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
+    it->second.state.captured = true;
+  return it->second;
+}
 
 int check_dim(int dim) {
   if (dim <= 0 || dim % 8 != 0 || dim > 16384)
@@ -620,7 +668,7 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
                 (long long)row_beg, (long long)row_end, (long long)idx->rows);
   DeviceGuard g(idx->device);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  Workspace& w = idx->ws[st];
+  Workspace& w = ws_for(idx, st);
   const bool f32 = idx->storage == TSV_F32;
   const bool tiled = idx->storage == TSV_BF16_TILED;
   if (tiled && row_beg % 128 != 0)
@@ -813,7 +861,7 @@ int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int
     if (const char* e = getenv("TSV_SEED_FRAC")) frac = std::max(2, atoi(e));
     DeviceGuard g(idx->device);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    Workspace& w = idx->ws[st];
+    Workspace& w = ws_for(idx, st);
     int rc = check_dtype(q_dtype);
     if (!rc && q_dev == nullptr) rc = fail(TSV_ERR_ARGUMENT, "null buffer");
     if (!rc) rc = w.seed_s.ensure(static_cast<size_t>(B) * k);
@@ -902,7 +950,7 @@ int tsv_search_segmented(tsv_index* idx, const void* q_dev, int q_dtype, int nse
   }
   DeviceGuard g(idx->device);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  Workspace& w = idx->ws[st];
+  Workspace& w = ws_for(idx, st);
   const bool f32 = idx->storage == TSV_F32;
   const bool tiled = idx->storage == TSV_BF16_TILED;
   for (int s_ = 0; tiled && s_ < nseg; ++s_)
@@ -1065,14 +1113,14 @@ static int rerank_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B,
   int q_f32 = q_dtype == TSV_F32;
   const bool f32 = idx->storage == TSV_F32;
   if (f32) {  // exact fp32 question (hi + lo) against the hi + lo rows
-    Workspace& w = idx->ws[st];
+    Workspace& w = ws_for(idx, st);
     rc = stage_queries_f32(idx, w, q_dev, q_dtype, B, st);
     if (rc) return rc;
     q = w.qhi.ptr;
     q_lo = w.qlo.ptr;
     q_f32 = 1;
   } else if (idx->metric == TSV_METRIC_COSINE) {
-    Workspace& w = idx->ws[st];
+    Workspace& w = ws_for(idx, st);
     rc = stage_queries(idx, w, q_dev, q_dtype, B, st, &q);
     if (rc) return rc;
     q_f32 = 0;
@@ -1082,8 +1130,25 @@ static int rerank_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B,
   // (rows up to 4 KB: two ring slots per warp fit next to the question vector)
   if (!f32 && idx->dim <= 2048 && !env_flag("TSV_RERANK_LDG")) {
     // bf16 arenas: gather pipelined through per-warp shared-memory rings (cp.async)
+    const int splits = tsv::rerank_lists_splits(B, C, k, idx->dim, idx->num_sms);
+    uint64_t* part_keys = nullptr;
+    int32_t* arrivals = nullptr;
+    if (splits > 1) {
+      Workspace& w = ws_for(idx, st);
+      rc = w.rr_keys.ensure(static_cast<size_t>(B) * splits * k);
+      if (rc) return rc;
+      const size_t had = w.rr_arrive.cap;
+      rc = w.rr_arrive.ensure(static_cast<size_t>(B));
+      if (rc) return rc;
+      if (w.rr_arrive.cap != had)
+        TSV_CUDA(cudaMemsetAsync(w.rr_arrive.ptr, 0, w.rr_arrive.cap * sizeof(int32_t), st),
+                 "arrivals reset");
+      part_keys = w.rr_keys.ptr;
+      arrivals = w.rr_arrive.ptr;
+    }
     e = tsv::launch_rerank_ring(idx->arena, idx->rows, idx->dim, q, q_f32, B, cand_ids_dev, C, k,
-                                row_offsets_dev, scores_dev, ids_dev, st, tiled);
+                                row_offsets_dev, scores_dev, ids_dev, st, tiled, splits,
+                                part_keys, arrivals);
   } else {
     e = tsv::launch_rerank(f32 ? nullptr : idx->arena,
                            f32 ? static_cast<const float*>(idx->arena) : nullptr,
@@ -1441,6 +1506,23 @@ int tsv_sharded_destroy(tsv_sharded* sh) {
     if (sh->gather_i) cudaFree(sh->gather_i);
   }
   delete sh;
+  return TSV_OK;
+}
+
+int tsv_stream_create(int device, void** out) {
+  if (out == nullptr) return fail(TSV_ERR_ARGUMENT, "out is null");
+  *out = nullptr;
+  DeviceGuard g(device);
+  cudaStream_t st = nullptr;
+  TSV_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+  *out = st;
+  return TSV_OK;
+}
+
+int tsv_stream_destroy(void* stream) {
+  if (stream == nullptr) return TSV_OK;
+  TSV_CUDA(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)), "cudaStreamSynchronize");
+  TSV_CUDA(cudaStreamDestroy(reinterpret_cast<cudaStream_t>(stream)), "cudaStreamDestroy");
   return TSV_OK;
 }
 

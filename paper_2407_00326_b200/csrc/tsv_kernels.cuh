@@ -167,9 +167,13 @@ int launch_rerank(const void* arena, const float* arena_hi, const float* arena_l
 
 // K3 over a bf16 arena with the gather pipelined through shared memory (cp.async rings);
 // offs (optional, device [B]): candidate ids of question b are relative to arena row offs[b].
+// splits > 1 (k <= 32): question b's candidates spread over `splits` blocks; part_keys
+// [B * splits * k] and arrivals [B] (zeroed once; the kernel leaves them zero) are scratch.
 int launch_rerank_ring(const void* arena, int64_t nrows, int dim, const void* q, int q_is_f32,
                        int B, const int32_t* cand, int C, int k, const int32_t* offs,
-                       float* out_s, int32_t* out_id, cudaStream_t stream, int tiled);
+                       float* out_s, int32_t* out_id, cudaStream_t stream, int tiled,
+                       int splits, uint64_t* part_keys, int32_t* arrivals);
+int rerank_lists_splits(int B, int C, int k, int dim, int num_sms);
 
 int launch_normalize(const void* src, int src_is_f32, int64_t n, int dim, int do_normalize,
                      void* dst_bf16, cudaStream_t stream);

@@ -11,7 +11,9 @@
 #include "tsv_kernels.cuh"
 
 #include <cuda_bf16.h>
+#include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 
 namespace tsv {
 namespace {
@@ -592,16 +594,56 @@ __global__ void __launch_bounds__(kWarps * 32) rerank_ring_kernel(
 //    same row, same score);
 //  * warp 0 merges the kWarps lists with k rounds of a warp-wide max, dropping every copy of
 //    the chosen key (duplicates across warps).
+// k rounds of a warp-wide max over the keys in `mine` (pad-filled): round r yields the r-th key
+// (score desc, id asc) and drops every copy of it (duplicate candidate ids). Lane 0 writes the
+// result to out_key (as keys) or to out_s / out_id. Whole warp.
+template <int kPer>
+__device__ __forceinline__ void warp_topk_rounds(uint64_t (&mine)[kPer], int k, uint64_t* out_key,
+                                                 float* out_s, int32_t* out_id) {
+  const uint64_t pad = pad_key();
+  const int lane = threadIdx.x & 31;
+  for (int rk = 0; rk < k; ++rk) {
+    uint64_t m = mine[0];
+#pragma unroll
+    for (int i = 1; i < kPer; ++i) m = mine[i] > m ? mine[i] : m;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t other = __shfl_xor_sync(0xffffffffu, m, o);
+      m = other > m ? other : m;
+    }
+    if (lane == 0) {
+      if (out_key != nullptr) {
+        out_key[rk] = m;
+      } else {
+        const int32_t id = m == pad ? -1 : key_id(m);
+        out_s[rk] = id < 0 ? -INFINITY : key_score(m);
+        out_id[rk] = id;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kPer; ++i)
+      if (mine[i] == m) mine[i] = pad;
+  }
+}
+
+// splits > 1: the candidates of question b are split over `splits` blocks (blockIdx.x =
+// b * splits + s, candidates [C s / splits, C (s + 1) / splits)), so a batch of few questions
+// or long candidate lists still fills the GPU with short per-warp chains; each block leaves its
+// top k in part_keys, and the last block of the question to finish (arrivals[b], self-resetting)
+// merges the splits' lists.
 template <int kWarps, int kSlots, int CPL, bool kTiled>
 __global__ void __launch_bounds__(kWarps * 32) rerank_lists_kernel(
     const __nv_bfloat16* __restrict__ arena, int64_t nrows, int dim, const void* __restrict__ q,
     int q_is_f32, const int32_t* __restrict__ cand, int C, int k, const int32_t* __restrict__ offs,
-    float* __restrict__ out_s, int32_t* __restrict__ out_id) {
+    float* __restrict__ out_s, int32_t* __restrict__ out_id, int splits,
+    uint64_t* __restrict__ part_keys, int32_t* __restrict__ arrivals) {
   extern __shared__ __align__(16) uint8_t sm[];
   const int row_bytes = dim * 2;
   uint8_t* ring = sm;                                                   // [kWarps][kSlots][row]
   uint64_t* lists = reinterpret_cast<uint64_t*>(sm + static_cast<size_t>(kWarps) * kSlots * row_bytes);
-  const int b = blockIdx.x;
+  const int b = blockIdx.x / splits, split = blockIdx.x - b * splits;
+  const int c_beg = static_cast<int>(static_cast<int64_t>(C) * split / splits);
+  const int c_end = static_cast<int>(static_cast<int64_t>(C) * (split + 1) / splits);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int chunks = dim >> 3;
   float2 qr[CPL][4];
@@ -629,8 +671,10 @@ __global__ void __launch_bounds__(kWarps * 32) rerank_lists_kernel(
     }
   }
   const int64_t base = offs != nullptr ? __ldg(offs + b) : 0;  // per-question segment start
-  const int nrow = warp < C ? (C - warp + kWarps - 1) / kWarps : 0;  // <= 32
-  const int32_t my_id = lane < nrow ? __ldg(cand + static_cast<int64_t>(b) * C + warp + kWarps * lane) : -1;
+  const int cw = c_end - c_beg;  // this block's candidates
+  const int nrow = warp < cw ? (cw - warp + kWarps - 1) / kWarps : 0;  // <= 32
+  const int32_t my_id =
+      lane < nrow ? __ldg(cand + static_cast<int64_t>(b) * C + c_beg + warp + kWarps * lane) : -1;
   const bool my_ok = my_id >= 0 && base + my_id < nrows;
   const uint32_t okmask = __ballot_sync(0xffffffffu, my_ok);
   const int64_t r = my_ok ? base + my_id : 0;
@@ -701,25 +745,33 @@ __global__ void __launch_bounds__(kWarps * 32) rerank_lists_kernel(
     const int e = lane + 32 * i;
     mine[i] = e < kWarps * k ? lists[e] : pad_key();
   }
-  const uint64_t pad = pad_key();
-  for (int rk = 0; rk < k; ++rk) {
-    uint64_t m = mine[0];
-#pragma unroll
-    for (int i = 1; i < kPer; ++i) m = mine[i] > m ? mine[i] : m;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const uint64_t other = __shfl_xor_sync(0xffffffffu, m, o);
-      m = other > m ? other : m;
-    }
-    if (lane == 0) {
-      const int32_t id = m == pad ? -1 : key_id(m);
-      out_s[static_cast<int64_t>(b) * k + rk] = id < 0 ? -INFINITY : key_score(m);
-      out_id[static_cast<int64_t>(b) * k + rk] = id;
-    }
-#pragma unroll
-    for (int i = 0; i < kPer; ++i)
-      if (mine[i] == m) mine[i] = pad;  // every copy of this id (duplicate candidates)
+  if (splits == 1) {
+    warp_topk_rounds<kPer>(mine, k, nullptr, out_s + static_cast<int64_t>(b) * k,
+                           out_id + static_cast<int64_t>(b) * k);
+    return;
   }
+  warp_topk_rounds<kPer>(mine, k, part_keys + static_cast<int64_t>(blockIdx.x) * k, nullptr,
+                         nullptr);
+  // the last of the question's blocks merges the splits' lists (threadfence reduction)
+  __shared__ int last;
+  if (lane == 0) {
+    __threadfence();
+    last = atomicAdd(arrivals + b, 1) == splits - 1;
+  }
+  __syncwarp();
+  if (!last) return;
+  __threadfence();
+  uint64_t all[8];  // splits * k <= 256 keys
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int e = lane + 32 * i;
+    all[i] = e < splits * k ? __ldcg(reinterpret_cast<const unsigned long long*>(
+                                  part_keys + static_cast<int64_t>(b) * splits * k + e))
+                            : pad_key();
+  }
+  warp_topk_rounds<8>(all, k, nullptr, out_s + static_cast<int64_t>(b) * k,
+                      out_id + static_cast<int64_t>(b) * k);
+  if (lane == 0) arrivals[b] = 0;  // ready for the next launch on this workspace
 }
 
 // One warp per row: optional L2 normalisation (fp32 math) and cast to bf16.
@@ -1115,10 +1167,17 @@ int launch_rerank_ring_v(const void* arena, int64_t nrows, int dim, const void* 
   return static_cast<int>(cudaGetLastError());
 }
 
+struct RerankSplit {  // split mode scratch (see rerank_lists_kernel)
+  int splits = 1;
+  uint64_t* part_keys = nullptr;  // [B * splits * k]
+  int32_t* arrivals = nullptr;    // [B], zero between launches
+};
+
 template <int kWarps, int kSlots, int CPL, bool kTiled>
 int launch_rerank_lists_v(const void* arena, int64_t nrows, int dim, const void* q, int q_is_f32,
                           int B, const int32_t* cand, int C, int k, const int32_t* offs,
-                          float* out_s, int32_t* out_id, cudaStream_t stream) {
+                          float* out_s, int32_t* out_id, cudaStream_t stream,
+                          const RerankSplit& sp) {
   const size_t smem = static_cast<size_t>(kWarps) * kSlots * dim * 2 +
                       static_cast<size_t>(kWarps) * 32 * sizeof(uint64_t);
   if (smem > 220 * 1024) return static_cast<int>(cudaErrorInvalidValue);
@@ -1128,34 +1187,31 @@ int launch_rerank_lists_v(const void* arena, int64_t nrows, int dim, const void*
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     if (e != cudaSuccess) return static_cast<int>(e);
   }
-  kern<<<B, kWarps * 32, smem, stream>>>(reinterpret_cast<const __nv_bfloat16*>(arena), nrows, dim,
-                                         q, q_is_f32, cand, C, k, offs, out_s, out_id);
+  kern<<<B * sp.splits, kWarps * 32, smem, stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(arena), nrows, dim, q, q_is_f32, cand, C, k, offs,
+      out_s, out_id, sp.splits, sp.part_keys, sp.arrivals);
   return static_cast<int>(cudaGetLastError());
 }
 
 template <int CPL, bool kTiled>
 int launch_rerank_ring_s(int slots, const void* arena, int64_t nrows, int dim, const void* q,
                          int q_is_f32, int B, const int32_t* cand, int C, int k,
-                         const int32_t* offs, float* out_s, int32_t* out_id, cudaStream_t stream) {
-  // (A/B knob: TSV_RERANK_WARPS=8/32 warps per block for the lists kernel, dim 512-1024)
-  if constexpr ((CPL == 3 || CPL == 4) && !kTiled) {
-    const char* w = getenv("TSV_RERANK_WARPS");
-    const int nw = w ? atoi(w) : 16;
-    if (nw == 8 && C <= 8 * 32 && k <= 32)
-      return slots == 2 ? launch_rerank_lists_v<8, 2, CPL, kTiled>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream)
-                        : launch_rerank_lists_v<8, 4, CPL, kTiled>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream);
-    if (nw == 32 && C <= 32 * 32 && k <= 32)
-      return slots == 2 ? launch_rerank_lists_v<32, 2, CPL, kTiled>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream)
-                        : launch_rerank_lists_v<32, 4, CPL, kTiled>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream);
+                         const int32_t* offs, float* out_s, int32_t* out_id, cudaStream_t stream,
+                         const RerankSplit& sp) {
+  // per-warp lists (no block-wide sort) for k <= 32 with at most 32 candidates per warp:
+  // 8 warps per block by default (TSV_RERANK_WARPS=16 / 32 for A/B)
+  const int per_block = (C + sp.splits - 1) / sp.splits;
+  int nw = 8;
+  if (const char* w = getenv("TSV_RERANK_WARPS")) nw = atoi(w);
+  if (per_block > nw * 32) nw = per_block <= 16 * 32 ? 16 : 32;
+  if (k <= 32 && per_block <= nw * 32 && !getenv("TSV_RERANK_SORT")) {
+#define TSV_LISTS(W, S) launch_rerank_lists_v<W, S, CPL, kTiled>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream, sp)
+    if (nw == 8) return slots == 2 ? TSV_LISTS(8, 2) : (slots == 3 ? TSV_LISTS(8, 3) : TSV_LISTS(8, 4));
+    if (nw == 16) return slots == 2 ? TSV_LISTS(16, 2) : (slots == 3 ? TSV_LISTS(16, 3) : TSV_LISTS(16, 4));
+    if (nw == 32 && 32 * 2 * dim * 2 <= 200 * 1024) return TSV_LISTS(32, 2);
+#undef TSV_LISTS
   }
-  // C <= 512 candidates and k <= 32: per-warp lists (no block-wide sort)
-  if (C <= 16 * 32 && k <= 32 && !getenv("TSV_RERANK_SORT")) {
-    switch (slots) {
-      case 2: return launch_rerank_lists_v<16, 2, CPL, kTiled>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream);
-      case 3: return launch_rerank_lists_v<16, 3, CPL, kTiled>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream);
-      default: return launch_rerank_lists_v<16, 4, CPL, kTiled>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream);
-    }
-  }
+  if (sp.splits != 1) return static_cast<int>(cudaErrorInvalidValue);
   switch (slots) {
     case 2: return launch_rerank_ring_v<16, 2, CPL, kTiled>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream);
     case 3: return launch_rerank_ring_v<16, 3, CPL, kTiled>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream);
@@ -1166,30 +1222,45 @@ int launch_rerank_ring_s(int slots, const void* arena, int64_t nrows, int dim, c
 template <bool kTiled>
 int launch_rerank_ring_t(int slots, const void* arena, int64_t nrows, int dim, const void* q,
                          int q_is_f32, int B, const int32_t* cand, int C, int k,
-                         const int32_t* offs, float* out_s, int32_t* out_id, cudaStream_t stream) {
+                         const int32_t* offs, float* out_s, int32_t* out_id, cudaStream_t stream,
+                         const RerankSplit& sp) {
   const int cpl = (dim / 8 + 31) / 32;  // 16-byte chunks per lane
-  if (cpl <= 1) return launch_rerank_ring_s<1, kTiled>(slots, arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream);
-  if (cpl <= 2) return launch_rerank_ring_s<2, kTiled>(slots, arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream);
-  if (cpl <= 3) return launch_rerank_ring_s<3, kTiled>(slots, arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream);
-  if (cpl <= 4) return launch_rerank_ring_s<4, kTiled>(slots, arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream);
-  if (cpl <= 8) return launch_rerank_ring_s<8, kTiled>(slots, arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream);
+#define TSV_RING(N) launch_rerank_ring_s<N, kTiled>(slots, arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream, sp)
+  if (cpl <= 1) return TSV_RING(1);
+  if (cpl <= 2) return TSV_RING(2);
+  if (cpl <= 3) return TSV_RING(3);
+  if (cpl <= 4) return TSV_RING(4);
+  if (cpl <= 8) return TSV_RING(8);
+#undef TSV_RING
   return static_cast<int>(cudaErrorInvalidValue);
 }
 
-// Pipelined gather (bf16 arenas, dim <= 2048). Ring depth per warp: as many rows as keep ~96 KB
-// of a block's rows in flight (2 to 4), so two 16-warp blocks share an SM up to dim 1024.
+int rerank_lists_splits(int B, int C, int k, int dim, int num_sms) {
+  if (k > 32 || dim > 2048 || getenv("TSV_RERANK_SORT")) return 1;
+  int splits = (6 * num_sms + B - 1) / B;  // ~6 blocks of 8 warps per SM
+  splits = std::min(splits, std::max(1, C / 16));  // >= 16 candidates per block
+  splits = std::max(1, std::min(splits, std::min(8, 256 / k)));
+  if (const char* e = getenv("TSV_RERANK_SPLITS")) splits = std::max(1, std::min(8, atoi(e)));
+  while (splits < 8 && (C + splits - 1) / splits > 32 * 32) ++splits;
+  return splits;
+}
+
+// Pipelined gather (bf16 arenas, dim <= 2048): cp.async rings of `slots` rows per warp (2 by
+// default: measured best at C3 with per-warp lists), split over blocks per rerank_lists_splits.
 int launch_rerank_ring(const void* arena, int64_t nrows, int dim, const void* q, int q_is_f32,
                        int B, const int32_t* cand, int C, int k, const int32_t* offs,
-                       float* out_s, int32_t* out_id, cudaStream_t stream, int tiled) {
+                       float* out_s, int32_t* out_id, cudaStream_t stream, int tiled,
+                       int splits, uint64_t* part_keys, int32_t* arrivals) {
   if (B <= 0) return 0;
   const int row_bytes = dim * 2;
-  int slots = (96 * 1024) / (16 * row_bytes);
+  int slots = 2;
   if (const char* e = getenv("TSV_RERANK_SLOTS")) slots = atoi(e);
   slots = slots < 2 ? 2 : (slots > 4 ? 4 : slots);
   while (slots > 2 && 16 * slots * row_bytes > 200 * 1024) --slots;
   if (dim > 2048) return static_cast<int>(cudaErrorInvalidValue);
-  return tiled ? launch_rerank_ring_t<true>(slots, arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream)
-               : launch_rerank_ring_t<false>(slots, arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream);
+  RerankSplit sp{splits, part_keys, arrivals};
+  return tiled ? launch_rerank_ring_t<true>(slots, arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream, sp)
+               : launch_rerank_ring_t<false>(slots, arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream, sp);
 }
 
 int launch_normalize(const void* src, int src_is_f32, int64_t n, int dim, int do_normalize,

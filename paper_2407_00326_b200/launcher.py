@@ -30,6 +30,7 @@ import time
 import torch
 
 from .engines import EngineSet
+from ._native import PrivateStream
 from .errors import ConfigParse
 from .graph import CONTROL_KINDS
 from .runtime import BatchRecord, RuntimeOptions, Simulator
@@ -215,7 +216,10 @@ class CapturedSearch:
         self.k = k
         self.row_range = row_range
         self.id_offset = id_offset
-        stream = torch.cuda.Stream(dev)
+        # a library-created stream kept for the graph's lifetime (never shared through torch's
+        # stream pool): its per-stream scratch in the index is this graph's alone
+        self._stream = PrivateStream(dev.index)
+        stream = self._stream.stream
         with torch.cuda.stream(stream):
             for _ in range(warmup):  # grows the per-stream workspace before capture
                 self._run(stream)
@@ -261,7 +265,10 @@ class CapturedRetrieval:
         self.s_i = torch.empty((questions * expansions, k_search), dtype=torch.int32, device=dev)
         self.r_s = torch.empty((questions, k_rerank), dtype=torch.float32, device=dev)
         self.r_i = torch.empty((questions, k_rerank), dtype=torch.int32, device=dev)
-        stream = torch.cuda.Stream(dev)
+        # a library-created stream kept for the graph's lifetime (never shared through torch's
+        # stream pool): its per-stream scratch in the index is this graph's alone
+        self._stream = PrivateStream(dev.index)
+        stream = self._stream.stream
         with torch.cuda.stream(stream):
             for _ in range(warmup):  # grows the per-stream workspace before capture
                 self._run(stream)
@@ -306,7 +313,10 @@ class CapturedContextual:
         self.s_i = torch.empty((b, k_search), dtype=torch.int32, device=dev)
         self.r_s = torch.empty((b, k_rerank), dtype=torch.float32, device=dev)
         self.r_i = torch.empty((b, k_rerank), dtype=torch.int32, device=dev)
-        stream = torch.cuda.Stream(dev)
+        # a library-created stream kept for the graph's lifetime (never shared through torch's
+        # stream pool): its per-stream scratch in the index is this graph's alone
+        self._stream = PrivateStream(dev.index)
+        stream = self._stream.stream
         with torch.cuda.stream(stream):
             for _ in range(warmup):  # grows the per-stream workspace before capture
                 self._run(stream)

@@ -14,13 +14,13 @@ import torch
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2407_00326_b200.index import DeviceIndex, normalize_rows  # noqa: E402
 
-VARIANTS = [("ldg", {"TSV_RERANK_LDG": "1"}), ("ring", {}), ("ring2", {"TSV_RERANK_SLOTS": "2"}),
-            ("ring3", {"TSV_RERANK_SLOTS": "3"}),
-            ("w8s2", {"TSV_RERANK_WARPS": "8", "TSV_RERANK_SLOTS": "2"}),
-            ("w8s4", {"TSV_RERANK_WARPS": "8", "TSV_RERANK_SLOTS": "4"}),
-            ("w32s2", {"TSV_RERANK_WARPS": "32", "TSV_RERANK_SLOTS": "2"}),
-            ("w32s4", {"TSV_RERANK_WARPS": "32", "TSV_RERANK_SLOTS": "4"})]
-KNOBS = ("TSV_RERANK_LDG", "TSV_RERANK_SLOTS", "TSV_RERANK_WARPS")
+VARIANTS = [("ldg", {"TSV_RERANK_LDG": "1"}), ("default", {}),
+            ("split1_w16", {"TSV_RERANK_SPLITS": "1", "TSV_RERANK_WARPS": "16"}),
+            ("split1_w8", {"TSV_RERANK_SPLITS": "1"}), ("split2", {"TSV_RERANK_SPLITS": "2"}),
+            ("split4", {"TSV_RERANK_SPLITS": "4"}), ("split8", {"TSV_RERANK_SPLITS": "8"}),
+            ("split4_slots4", {"TSV_RERANK_SPLITS": "4", "TSV_RERANK_SLOTS": "4"}),
+            ("split4_w16", {"TSV_RERANK_SPLITS": "4", "TSV_RERANK_WARPS": "16"})]
+KNOBS = ("TSV_RERANK_LDG", "TSV_RERANK_SLOTS", "TSV_RERANK_WARPS", "TSV_RERANK_SPLITS")
 
 
 def graph_time(calls, reps=20):
