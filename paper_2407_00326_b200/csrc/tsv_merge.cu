@@ -777,6 +777,7 @@ __global__ void __launch_bounds__(kWarps * 32) rerank_lists_kernel(
 // One warp per row: optional L2 normalisation (fp32 math) and cast to bf16.
 __global__ void normalize_kernel(const void* __restrict__ src, int src_is_f32, int64_t n, int dim,
                                  int do_normalize, __nv_bfloat16* __restrict__ dst) {
+  pdl_allow_dependents();  // the scan after it sets up while the queries are normalised
   const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= n) return;
@@ -1237,6 +1238,9 @@ int launch_rerank_ring_t(int slots, const void* arena, int64_t nrows, int dim, c
 
 int rerank_lists_splits(int B, int C, int k, int dim, int num_sms) {
   if (k > 32 || dim > 2048 || getenv("TSV_RERANK_SORT")) return 1;
+  // Measured (C3, C5): spreading one question over several blocks is slower (more per-block
+  // setup for a kernel that is bound by instruction issue), so splitting is opt-in.
+  if (!getenv("TSV_RERANK_SPLITS")) return 1;
   int splits = (6 * num_sms + B - 1) / B;  // ~6 blocks of 8 warps per SM
   splits = std::min(splits, std::max(1, C / 16));  // >= 16 candidates per block
   splits = std::max(1, std::min(splits, std::min(8, 256 / k)));

@@ -19,6 +19,8 @@
 #include "tsv_ptx.cuh"
 
 #include <cfloat>
+#include <cstdlib>
+#include <utility>
 
 namespace tsv {
 namespace {
@@ -345,7 +347,6 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32, NB>::kThreads, 1)
   constexpr bool kAppend = KCAP == kAppendCap;
   constexpr int kRegK = (kSmemList || kAppend) ? 1 : KCAP;
   if (threadIdx.x == 0) pdl_allow_dependents();
-  if (p.gate != nullptr && *p.gate == 0) return;
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -385,8 +386,13 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32, NB>::kThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Launched with programmatic stream serialisation: the setup above (barriers, TMEM, descriptor
+  // prefetch) overlaps the tail of the kernel before (the query staging, a merge); from here on
+  // its outputs (queries, floors, the gate) are visible.
+  pdl_wait();
+  const bool gated_off = p.gate != nullptr && *p.gate == 0;  // device-side skip (no host trip)
 
-  const int num_items = (p.flags & kFlagDiagSetupOnly) ? 0 : p.num_items;
+  const int num_items = ((p.flags & kFlagDiagSetupOnly) || gated_off) ? 0 : p.num_items;
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -692,7 +698,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
   constexpr bool kAppend = KCAP == kAppendCap;
   constexpr int kRegK = (kSmemList || kAppend) ? 1 : KCAP;
   if (threadIdx.x == 0) pdl_allow_dependents();
-  if (p.gate != nullptr && *p.gate == 0) return;  // both CTAs of the pair see the same gate
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -740,7 +745,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
   ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int num_items = p.num_items;
+  pdl_wait();  // (see scan_topk_kernel) the previous kernel's outputs are visible from here
+  const bool gated_off = p.gate != nullptr && *p.gate == 0;
+  const int num_items = gated_off ? 0 : p.num_items;
 
   if (warp == 3) {
     // ---- query producer (both CTAs): own half of A per k-block, completion on the leader
@@ -989,6 +996,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair::kThreads, 1)
   }
 }
 
+// Scan launches use programmatic stream serialisation (PDL): the kernel may start while the
+// previous kernel of the stream (query staging, a merge, the seed floor) is finishing and waits
+// for its results in griddepcontrol.wait after its own setup. TSV_NO_PDL=1 launches normally.
+template <typename... KArgs, typename... Args>
+int launch_scan_pdl(void (*kern)(KArgs...), int grid, int threads, int smem, cudaStream_t stream,
+                    Args&&... args) {
+  static const bool no_pdl = getenv("TSV_NO_PDL") != nullptr && getenv("TSV_NO_PDL")[0] == '1';
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = no_pdl ? 0 : 1;
+  return static_cast<int>(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
+
 template <int KCAP>
 int launch_pair_impl(const CUtensorMap& tq, const CUtensorMap& tc, const ScanParams& p, int grid,
                      cudaStream_t stream) {
@@ -999,8 +1026,7 @@ int launch_pair_impl(const CUtensorMap& tq, const CUtensorMap& tc, const ScanPar
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (err != cudaSuccess) return static_cast<int>(err);
   }
-  kern<<<grid, Pair::kThreads, smem, stream>>>(tq, tc, p);
-  return static_cast<int>(cudaGetLastError());
+  return launch_scan_pdl(kern, grid, Pair::kThreads, smem, stream, tq, tc, p);
 }
 
 template <int MB, int KCAP, bool TF32 = false, int NB = 1>
@@ -1015,9 +1041,8 @@ int launch_impl(const CUtensorMap& tq, const CUtensorMap& tc, const ScanParams& 
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
     if (err != cudaSuccess) return static_cast<int>(err);
   }
-  kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, stream>>>(tq, tc, tq_lo ? *tq_lo : tq,
-                                                          tc_lo ? *tc_lo : tc, p);
-  return static_cast<int>(cudaGetLastError());
+  return launch_scan_pdl(kern, grid, Cfg::kThreads, Cfg::kSmemBytes, stream, tq, tc,
+                         tq_lo ? *tq_lo : tq, tc_lo ? *tc_lo : tc, p);
 }
 
 template <int MB>

@@ -15,12 +15,9 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2407_00326_b200.index import DeviceIndex, normalize_rows  # noqa: E402
 
 VARIANTS = [("ldg", {"TSV_RERANK_LDG": "1"}), ("default", {}),
-            ("split1_w16", {"TSV_RERANK_SPLITS": "1", "TSV_RERANK_WARPS": "16"}),
-            ("split1_w8", {"TSV_RERANK_SPLITS": "1"}), ("split2", {"TSV_RERANK_SPLITS": "2"}),
-            ("split4", {"TSV_RERANK_SPLITS": "4"}), ("split8", {"TSV_RERANK_SPLITS": "8"}),
-            ("split4_slots4", {"TSV_RERANK_SPLITS": "4", "TSV_RERANK_SLOTS": "4"}),
-            ("split4_w16", {"TSV_RERANK_SPLITS": "4", "TSV_RERANK_WARPS": "16"})]
-KNOBS = ("TSV_RERANK_LDG", "TSV_RERANK_SLOTS", "TSV_RERANK_WARPS", "TSV_RERANK_SPLITS")
+            ("lists_w16", {"TSV_RERANK_WARPS": "16"}), ("sort", {"TSV_RERANK_SORT": "1"})]
+KNOBS = ("TSV_RERANK_LDG", "TSV_RERANK_SLOTS", "TSV_RERANK_WARPS", "TSV_RERANK_SPLITS",
+         "TSV_RERANK_SORT")
 
 
 def graph_time(calls, reps=20):
@@ -62,6 +59,11 @@ def main():
                 for _ in range(32)]
         hbm = [lambda st, j=j: idx.rerank(q, cands[j % 8], k, stream=st, out=outs[j]) for j in range(32)]
         l2 = [lambda st, j=j: idx.rerank(q, cands[0], k, stream=st, out=outs[j]) for j in range(32)]
+        # sequential candidates (question b gathers rows [b C, b C + C) of a rotating block):
+        # the same bytes as the random gather with DRAM-friendly addresses
+        seqs = [(torch.arange(bq * c, device=dev, dtype=torch.int32).view(bq, c)
+                 + (r * bq * c) % max(1, n - bq * c)) for r in range(8)]
+        seq = [lambda st, j=j: idx.rerank(q, seqs[j % 8], k, stream=st, out=outs[j]) for j in range(32)]
         alg = bq * c * d * 2
         for name, env in VARIANTS:
             for key in KNOBS:
@@ -70,11 +72,13 @@ def main():
             try:
                 th = graph_time(hbm)
                 tl = graph_time(l2)
+                ts = graph_time(seq)
             except Exception as exc:  # noqa: BLE001 - a variant that does not fit this shape
                 print(f"{name} {bq}x{c}x{d}: n/a ({exc})", flush=True)
                 continue
             print(f"{name} {bq}x{c}x{d}: hbm {th:6.2f} us ({alg / th / 1e3:6.0f} GB/s)  "
-                  f"l2 {tl:6.2f} us", flush=True)
+                  f"l2 {tl:6.2f} us  sequential-rows {ts:6.2f} us ({alg / ts / 1e3:6.0f} GB/s)",
+                  flush=True)
         del idx
         torch.cuda.empty_cache()
 
