@@ -30,6 +30,14 @@ def main():
     idx.search_segmented(q, [0, 10, 25, 40], [(0, 48), (48, 3000), (3000, 40_000)], 8)
     cand = torch.randint(0, 40_000, (4, 200), generator=g, device=dev, dtype=torch.int32)
     idx.rerank(q[:4], cand, 10)
+    # K3 variants: per-warp lists (default), ring + block sort, split over blocks, row offsets
+    cand2 = torch.randint(0, 3000, (40, 200), generator=g, device=dev, dtype=torch.int32)
+    offs = torch.arange(0, 40 * 100, 100, device=dev, dtype=torch.int32)
+    idx.rerank(q, cand2, 10, row_offsets=offs)
+    for knob, val in (("TSV_RERANK_SORT", "1"), ("TSV_RERANK_SPLITS", "3")):
+        os.environ[knob] = val
+        idx.rerank(q, cand2, 10)
+        del os.environ[knob]
     s = torch.sort(torch.randn((8, 37, 16), generator=g, device=dev), dim=2, descending=True)[0]
     i = torch.arange(8 * 37 * 16, device=dev, dtype=torch.int32).reshape(8, 37, 16)
     merge_topk(s, i, 10)

@@ -108,7 +108,8 @@ def test_sharded_corpus_behind_the_executor(cuda):
     dim, n, k, nq = 256, 60_000, 10, 16
     c = orc.make_corpus(n, dim, seed=21)
     sh = ShardedIndex(_shards(c, cuda, 2, metric="cosine"), max_batch=1024, max_k=128)
-    backend = RetrievalBackend(dim=dim, arena_rows=1 << 12, global_index=sh)
+    backend = RetrievalBackend(dim=dim, arena_rows=1 << 12, global_index=sh,
+                               release_segments=False)  # keep ctx.data for the check
     es = E.EngineSet.from_dict(prof)
     graphs = [(_global_search_graph(f"q{j}", nq, k), 5.0 * j, 0.0) for j in range(4)]
     sim, trace = R.run_queries(es, graphs, R.RuntimeOptions(), backend=backend)
