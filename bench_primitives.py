@@ -214,12 +214,18 @@ def c5(args, dev, peaks, threads):
     ms_both = dev_time(lambda: (search(), rerank()), args.reps)
     from paper_2407_00326_b200.launcher import CapturedContextual
 
-    chain = CapturedContextual(idx, offs, ranges, k, k_r)
+    chain = CapturedContextual(idx, offs, ranges, k, k_r, fused=False)
     ms_graph = dev_time(lambda: chain.run(q), args.reps)
+    rows = torch.tensor(ranges, dtype=torch.int64, device=dev)
+    ms_fused = dev_time(lambda: idx.search_rerank_segmented(q, rows, seg, k, k_r,
+                                                            local_ids=False), args.reps)
+    fused = CapturedContextual(idx, offs, ranges, k, k_r)
+    ms_fused_graph = dev_time(lambda: fused.run(q), args.reps)
     return {"config": "C5 primitive: 16 queries, each top-32 over its own 48-row segment "
                       "(one segmented launch), rerank 32 -> 3",
             "search_ms": ms_s, "rerank_ms": ms_r, "chain_ms": ms_both,
-            "chain_ms_cuda_graph": ms_graph,
+            "chain_ms_cuda_graph": ms_graph, "fused_chain_ms": ms_fused,
+            "fused_chain_ms_cuda_graph": ms_fused_graph,
             "note": "launch / latency bound (98 KB per segment)",
             "simulated_reference_ms": {"search": simulated("vdb-search0", nq),
                                        "rerank": simulated("rerank0", 32)}}

@@ -131,6 +131,24 @@ TSV_API int tsv_rerank_segmented(tsv_index* idx, const void* q_dev, int q_dtype,
                                  const int32_t* cand_ids_dev, int C, const int32_t* row_offsets_dev,
                                  int k, float* scores_dev, int32_t* ids_dev, void* stream);
 
+/* ---- K3s: contextual retrieval's Searching -> Reranking chain in ONE launch (BASELINE C5;
+ * reference workloads.py:247-257 builds a per-query index, searches it, reranks the hits; the
+ * stage pair is optimizer.py:178-218). Query b searches ITS OWN index segment, arena rows
+ * [q_rows_dev[2b], q_rows_dev[2b+1]) (device int64 [B][2]; at most max_rows <= 1024 rows each,
+ * longer segments are cut at max_rows), keeps the top k_search (written to search_*, [B, k_search],
+ * ids segment-local when local_ids, else arena rows), and reranks those rows against
+ * q_rerank_dev[b] (NULL: the query itself), keeping the top k_rerank <= k_search (rerank_*).
+ * Cosine indexes normalise both vectors in the kernel. bf16 / tiled arenas, dim <= 2048.
+ * Equivalent to tsv_search_segmented + tsv_rerank(_segmented): the rerank scores are
+ * bit-identical to tsv_rerank's for the same rows; the search scores differ from the tensor-core
+ * scan's by summation order only. No workspace, no host round trip: capture-safe. ---- */
+TSV_API int tsv_search_rerank_segmented(tsv_index* idx, const void* q_search_dev,
+                                        const void* q_rerank_dev, int q_dtype, int B,
+                                        const int64_t* q_rows_dev, int max_rows, int k_search,
+                                        int k_rerank, int local_ids, float* search_scores_dev,
+                                        int32_t* search_ids_dev, float* rerank_scores_dev,
+                                        int32_t* rerank_ids_dev, void* stream);
+
 /* ---- K4: merge `lists` sorted lists per query. Input layout [lists][B][kin]; output [B][kout].
  * This is the Aggregate join of split Searching stages (optimizer.py:620-661,
  * runtime.py:544-549) and the cross-shard merge after the all-gather. dedup != 0 keeps one
@@ -150,6 +168,11 @@ TSV_API int tsv_peer_create(int device, int world, int rank, int max_b, int max_
                             tsv_peer_group** out);
 TSV_API int tsv_peer_handle(tsv_peer_group* g, void* handle_out /* 64 bytes */, int* handle_bytes);
 TSV_API int tsv_peer_open(tsv_peer_group* g, int peer, const void* handle);
+/* In-process peer: map rank `peer`'s buffer from its group `other` (created in this process,
+ * same world / max_b / max_k) without IPC — ranks driven by one process on one device or on
+ * peer-accessible devices (enables peer access). Lets one process measure and test the
+ * exchange with every rank's kernel in flight at once. */
+TSV_API int tsv_peer_attach(tsv_peer_group* g, int peer, tsv_peer_group* other);
 TSV_API int tsv_peer_allgather_merge(tsv_peer_group* g, const float* local_scores,
                                      const int32_t* local_ids, int B, int k, float* out_scores,
                                      int32_t* out_ids, void* stream);

@@ -57,11 +57,14 @@ SIGNATURES = {
     "tsv_rerank": (c_int, [c_vp, c_vp, c_int, c_int, c_vp, c_int, c_int, c_vp, c_vp, c_vp]),
     "tsv_rerank_segmented": (c_int, [c_vp, c_vp, c_int, c_int, c_vp, c_int, c_vp, c_int, c_vp,
                                      c_vp, c_vp]),
+    "tsv_search_rerank_segmented": (c_int, [c_vp, c_vp, c_vp, c_int, c_int, c_vp, c_int, c_int,
+                                            c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "tsv_merge_topk": (c_int, [c_vp, c_vp, c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp]),
     "tsv_normalize_rows": (c_int, [c_vp, c_int, c_i64, c_int, c_int, c_vp, c_vp]),
     "tsv_peer_create": (c_int, [c_int, c_int, c_int, c_int, c_int, ctypes.POINTER(c_vp)]),
     "tsv_peer_handle": (c_int, [c_vp, c_vp, ctypes.POINTER(c_int)]),
     "tsv_peer_open": (c_int, [c_vp, c_int, c_vp]),
+    "tsv_peer_attach": (c_int, [c_vp, c_int, c_vp]),
     "tsv_peer_allgather_merge": (c_int, [c_vp, c_vp, c_vp, c_int, c_int, c_vp, c_vp, c_vp]),
     "tsv_peer_set_timeout_ms": (c_int, [c_vp, c_i64]),
     "tsv_peer_status": (c_int, [c_vp, ctypes.POINTER(c_int)]),

@@ -1160,6 +1160,38 @@ static int rerank_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B,
   return TSV_OK;
 }
 
+int tsv_search_rerank_segmented(tsv_index* idx, const void* q_search_dev,
+                                const void* q_rerank_dev, int q_dtype, int B,
+                                const int64_t* q_rows_dev, int max_rows, int k_search,
+                                int k_rerank, int local_ids, float* search_scores_dev,
+                                int32_t* search_ids_dev, float* rerank_scores_dev,
+                                int32_t* rerank_ids_dev, void* stream) {
+  if (idx == nullptr) return fail(TSV_ERR_ARGUMENT, "index is null");
+  int rc = check_dtype(q_dtype);
+  if (rc) return rc;
+  if (B <= 0) return fail(TSV_ERR_CAPACITY, "empty batch");
+  if (k_search <= 0 || k_rerank <= 0) return fail(TSV_ERR_CONFIG, "k must be >= 1");
+  if (k_rerank > k_search)
+    return fail(TSV_ERR_CONFIG, "k_rerank=%d exceeds k_search=%d", k_rerank, k_search);
+  if (max_rows <= 0 || max_rows > tsv::kFusedSegMaxRows)
+    return fail(TSV_ERR_CAPACITY, "max_rows=%d outside [1, %d] (use tsv_search_segmented + "
+                "tsv_rerank for larger segments)", max_rows, tsv::kFusedSegMaxRows);
+  if (idx->storage == TSV_F32 || idx->dim > 2048)
+    return fail(TSV_ERR_CONFIG, "fused search+rerank needs a bf16 arena with dim <= 2048");
+  if (q_search_dev == nullptr || q_rows_dev == nullptr || search_scores_dev == nullptr ||
+      search_ids_dev == nullptr || rerank_scores_dev == nullptr || rerank_ids_dev == nullptr)
+    return fail(TSV_ERR_ARGUMENT, "null buffer");
+  DeviceGuard g(idx->device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  int e = tsv::launch_search_rerank_seg(
+      idx->arena, idx->rows, idx->dim, idx->storage == TSV_BF16_TILED, q_search_dev, q_rerank_dev,
+      q_dtype == TSV_F32, idx->metric == TSV_METRIC_COSINE, q_rows_dev, B, max_rows, k_search,
+      k_rerank, local_ids, search_scores_dev, search_ids_dev, rerank_scores_dev, rerank_ids_dev, st);
+  if (e) return cuda_fail(static_cast<cudaError_t>(e), "search+rerank launch");
+  g_launches++;
+  return TSV_OK;
+}
+
 int tsv_rerank(tsv_index* idx, const void* q_dev, int q_dtype, int B, const int32_t* cand_ids_dev,
                int C, int k, float* scores_dev, int32_t* ids_dev, void* stream) {
   return rerank_impl(idx, q_dev, q_dtype, B, cand_ids_dev, C, nullptr, k, scores_dev, ids_dev,
@@ -1267,6 +1299,29 @@ int tsv_peer_open(tsv_peer_group* pg, int peer, const void* handle) {
   TSV_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
   pg->peers[peer] = ptr;
   pg->opened[peer] = true;
+  pg->dirty = true;
+  return TSV_OK;
+}
+
+int tsv_peer_attach(tsv_peer_group* pg, int peer, tsv_peer_group* other) {
+  if (pg == nullptr || other == nullptr) return fail(TSV_ERR_ARGUMENT, "null argument");
+  if (peer < 0 || peer >= pg->world || other->world != pg->world || other->rank != peer)
+    return fail(TSV_ERR_CONFIG, "group of rank %d (world %d) cannot be peer %d of world %d",
+                other->rank, other->world, peer, pg->world);
+  if (other->max_b != pg->max_b || other->max_k != pg->max_k)
+    return fail(TSV_ERR_CONFIG, "peer groups differ in max_b / max_k");
+  if (peer == pg->rank) return TSV_OK;
+  if (other->device != pg->device) {
+    DeviceGuard g(pg->device);
+    int can = 0;
+    TSV_CUDA(cudaDeviceCanAccessPeer(&can, pg->device, other->device), "cudaDeviceCanAccessPeer");
+    if (!can) return fail(TSV_ERR_DEVICE, "device %d cannot access device %d", pg->device, other->device);
+    cudaError_t e = cudaDeviceEnablePeerAccess(other->device, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+    else if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+  }
+  pg->peers[peer] = other->buf;
+  pg->opened[peer] = false;  // not an IPC mapping: nothing to close
   pg->dirty = true;
   return TSV_OK;
 }

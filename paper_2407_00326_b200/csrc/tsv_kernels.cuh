@@ -175,6 +175,18 @@ int launch_rerank_ring(const void* arena, int64_t nrows, int dim, const void* q,
                        int splits, uint64_t* part_keys, int32_t* arrivals);
 int rerank_lists_splits(int B, int C, int k, int dim, int num_sms);
 
+// Contextual chain in one launch: per query, search its own arena segment (q_rows [B][2],
+// <= max_rows <= 1024 rows; bf16 / tiled arenas, dim % 8 == 0, dim <= 2048), top k_s, rerank
+// those against qr (null: the query itself), top k_r. Questions are normalised in-kernel when
+// do_normalize.
+size_t search_rerank_seg_smem(int dim, int max_rows, int k_s);
+int launch_search_rerank_seg(const void* arena, int64_t nrows, int dim, int tiled, const void* qs,
+                             const void* qr, int q_is_f32, int do_normalize,
+                             const int64_t* q_rows, int B, int max_rows, int k_s, int k_r,
+                             int local_ids, float* os_s, int32_t* os_i, float* or_s,
+                             int32_t* or_i, cudaStream_t stream);
+constexpr int kFusedSegMaxRows = 1024;
+
 int launch_normalize(const void* src, int src_is_f32, int64_t n, int dim, int do_normalize,
                      void* dst_bf16, cudaStream_t stream);
 

@@ -774,6 +774,183 @@ __global__ void __launch_bounds__(kWarps * 32) rerank_lists_kernel(
   if (lane == 0) arrivals[b] = 0;  // ready for the next launch on this workspace
 }
 
+// Contextual retrieval's chain in one launch (reference workloads.py:247-257:
+// each query searches its own small index, then its hits are reranked): query b searches rows
+// [q_rows[2b], q_rows[2b + 1]) of the arena (its own index segment, <= max_rows rows), keeps the
+// top k_s (Searching), then scores those k_s rows against its rerank question and keeps the top
+// k_r (Reranking). Unfused this is normalise + scan + merge + rerank: 4 launches, ~35 us as one
+// CUDA graph, dominated by the scan's fixed costs on a 48-row segment. One block per query:
+//  * warps 0 / 1 L2-normalise the search query / rerank question with the math of
+//    normalize_kernel (so the bf16 vectors equal the unfused chain's staged ones) into shared
+//    memory; every lane then keeps its 16-byte chunks of both as fp32 pairs in registers;
+//  * each warp walks its rows (c = warp + kSegWarps j) through a cp.async ring, as
+//    rerank_lists_kernel does, and scores every row against BOTH vectors from the one copy in
+//    shared memory, with the lists kernel's exact arithmetic (packed FFMA2 over the chunks in
+//    order, butterfly sum): a row's rerank score is bit-identical to K3's;
+//  * selection by rank (count of larger keys; keys are unique: distinct ids): the k_s best
+//    search keys land at their rank, then the k_r best of those by rerank score.
+// The contraction is 2 x 48 rows x D per query: CUDA-core work, latency-bound either way.
+constexpr int kSegWarps = 8;
+constexpr int kSegSlots = 3;
+
+template <int CPL, bool kTiled>
+__global__ void __launch_bounds__(kSegWarps * 32) search_rerank_seg_kernel(
+    const __nv_bfloat16* __restrict__ arena, int64_t nrows, int dim, const void* __restrict__ qs,
+    const void* __restrict__ qr, int q_is_f32, int do_normalize, const int64_t* __restrict__ q_rows,
+    int max_rows, int k_s, int k_r, int local_ids, float* __restrict__ os_s,
+    int32_t* __restrict__ os_i, float* __restrict__ or_s, int32_t* __restrict__ or_i) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int row_bytes = dim * 2;
+  uint8_t* ring = sm;                                                   // [warps][slots][row]
+  __nv_bfloat16* qv = reinterpret_cast<__nv_bfloat16*>(
+      ring + static_cast<size_t>(kSegWarps) * kSegSlots * row_bytes);  // [2][dim]
+  uint64_t* keys_s = reinterpret_cast<uint64_t*>(qv + 2 * dim);
+  const int msel = min(k_s, max_rows);
+  uint64_t* keys_r = keys_s + max_rows;
+  float* score_r = reinterpret_cast<float*>(keys_r + msel);
+  int32_t* sel = reinterpret_cast<int32_t*>(score_r + max_rows);
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  pdl_wait();
+  const int64_t rb = q_rows[2 * b];
+  int64_t re = min(q_rows[2 * b + 1], nrows);
+  if (re < rb) re = rb;
+  const int n = static_cast<int>(min(re - rb, static_cast<int64_t>(max_rows)));
+  auto id_of = [&](int c) { return static_cast<int32_t>(local_ids ? c : rb + c); };
+  const int chunks = dim >> 3;
+  const int64_t kb_per_row = (dim + 63) >> 6;
+  const int nrow = warp < n ? (n - warp + kSegWarps - 1) / kSegWarps : 0;
+  uint8_t* my_ring = ring + static_cast<size_t>(warp) * kSegSlots * row_bytes;
+  auto issue = [&](int j, int slot) {  // whole warp; always commits one group
+    if (j < nrow) {
+      const int64_t r = rb + warp + static_cast<int64_t>(kSegWarps) * j;
+      const uint4* src = kTiled ? reinterpret_cast<const uint4*>(
+                                      arena + ((r >> 7) * kb_per_row * 128 + (r & 127)) * 64)
+                                : reinterpret_cast<const uint4*>(arena + r * dim);
+      uint4* dst = reinterpret_cast<uint4*>(my_ring + static_cast<size_t>(slot) * row_bytes);
+#pragma unroll
+      for (int jj = 0; jj < CPL; ++jj) {
+        const int ch = lane + 32 * jj;
+        if (ch < chunks)
+          cp_async16(dst + ch, src + (kTiled ? static_cast<int64_t>(ch >> 3) * 1024 + (ch & 7) : ch));
+      }
+    }
+    cp_async_commit();
+  };
+  // the rows' round trips start before the questions are normalised
+#pragma unroll
+  for (int s_ = 0; s_ < kSegSlots; ++s_) issue(s_, s_);
+  if (warp < 2) {  // warp 0: search query, warp 1: rerank question (= the query when qr is null)
+    const void* src = (warp == 1 && qr != nullptr) ? qr : qs;
+    const float* sf = reinterpret_cast<const float*>(src) + static_cast<int64_t>(b) * dim;
+    const __nv_bfloat16* sb = reinterpret_cast<const __nv_bfloat16*>(src) + static_cast<int64_t>(b) * dim;
+    float ss = 0.f;
+    if (do_normalize) {
+      for (int d = lane; d < dim; d += 32) {
+        const float x = q_is_f32 ? sf[d] : __bfloat162float(sb[d]);
+        ss = fmaf(x, x, ss);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    }
+    const float scale = (do_normalize && ss > 0.f) ? rsqrtf(ss) : 1.f;
+    __nv_bfloat16* out = qv + warp * dim;
+    for (int d = lane; d < dim; d += 32) {
+      const float x = q_is_f32 ? sf[d] : __bfloat162float(sb[d]);
+      out[d] = __float2bfloat16_rn(x * scale);
+    }
+  }
+  __syncthreads();
+  float2 qa[CPL][4], qb[CPL][4];  // search query / rerank question, this lane's chunks
+#pragma unroll
+  for (int j = 0; j < CPL; ++j) {
+    const int ch = lane + 32 * j;
+    const uint4 wa = ch < chunks ? reinterpret_cast<const uint4*>(qv)[ch] : make_uint4(0, 0, 0, 0);
+    const uint4 wb = ch < chunks ? reinterpret_cast<const uint4*>(qv + dim)[ch] : make_uint4(0, 0, 0, 0);
+    qa[j][0] = bf16x2_to_float2(wa.x);
+    qa[j][1] = bf16x2_to_float2(wa.y);
+    qa[j][2] = bf16x2_to_float2(wa.z);
+    qa[j][3] = bf16x2_to_float2(wa.w);
+    qb[j][0] = bf16x2_to_float2(wb.x);
+    qb[j][1] = bf16x2_to_float2(wb.y);
+    qb[j][2] = bf16x2_to_float2(wb.z);
+    qb[j][3] = bf16x2_to_float2(wb.w);
+  }
+  int slot = 0;
+  for (int j = 0; j < nrow; ++j) {
+    cp_async_wait<kSegSlots - 1>();
+    __syncwarp();
+    const uint4* row = reinterpret_cast<const uint4*>(my_ring + static_cast<size_t>(slot) * row_bytes);
+    float2 a2 = make_float2(0.f, 0.f), b2 = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int jj = 0; jj < CPL; ++jj) {
+      const int ch = lane + 32 * jj;
+      if (ch < chunks) {
+        const uint4 raw = row[ch];
+        const float2 x0 = bf16x2_to_float2(raw.x), x1 = bf16x2_to_float2(raw.y);
+        const float2 x2 = bf16x2_to_float2(raw.z), x3 = bf16x2_to_float2(raw.w);
+        a2 = __ffma2_rn(x0, qa[jj][0], a2);
+        a2 = __ffma2_rn(x1, qa[jj][1], a2);
+        a2 = __ffma2_rn(x2, qa[jj][2], a2);
+        a2 = __ffma2_rn(x3, qa[jj][3], a2);
+        b2 = __ffma2_rn(x0, qb[jj][0], b2);
+        b2 = __ffma2_rn(x1, qb[jj][1], b2);
+        b2 = __ffma2_rn(x2, qb[jj][2], b2);
+        b2 = __ffma2_rn(x3, qb[jj][3], b2);
+      }
+    }
+    float sa = a2.x + a2.y, sb2 = b2.x + b2.y;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sa += __shfl_xor_sync(0xffffffffu, sa, o);
+      sb2 += __shfl_xor_sync(0xffffffffu, sb2, o);
+    }
+    if (lane == 0) {
+      const int c = warp + kSegWarps * j;
+      keys_s[c] = make_key(sa, id_of(c));
+      score_r[c] = sb2;
+    }
+    __syncwarp();  // every lane done reading the slot before it is refilled
+    issue(j + kSegSlots, slot);
+    if (++slot == kSegSlots) slot = 0;
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  // Searching: the k_s best rows by search score, at their rank
+  for (int c = tid; c < n; c += kSegWarps * 32) {
+    const uint64_t key = keys_s[c];
+    int rank = 0;
+    for (int j = 0; j < n; ++j) rank += keys_s[j] > key ? 1 : 0;
+    if (rank < k_s) {
+      os_s[static_cast<int64_t>(b) * k_s + rank] = key_score(key);
+      os_i[static_cast<int64_t>(b) * k_s + rank] = key_id(key);
+      sel[rank] = c;
+    }
+  }
+  for (int r = n + tid; r < k_s; r += kSegWarps * 32) {
+    os_s[static_cast<int64_t>(b) * k_s + r] = -INFINITY;
+    os_i[static_cast<int64_t>(b) * k_s + r] = -1;
+  }
+  const int m = min(k_s, n);
+  __syncthreads();
+  // Reranking of those rows against the question
+  for (int r = tid; r < m; r += kSegWarps * 32) keys_r[r] = make_key(score_r[sel[r]], id_of(sel[r]));
+  __syncthreads();
+  for (int r = tid; r < m; r += kSegWarps * 32) {
+    const uint64_t key = keys_r[r];
+    int rank = 0;
+    for (int j = 0; j < m; ++j) rank += keys_r[j] > key ? 1 : 0;
+    if (rank < k_r) {
+      or_s[static_cast<int64_t>(b) * k_r + rank] = key_score(key);
+      or_i[static_cast<int64_t>(b) * k_r + rank] = key_id(key);
+    }
+  }
+  for (int r = m + tid; r < k_r; r += kSegWarps * 32) {
+    or_s[static_cast<int64_t>(b) * k_r + r] = -INFINITY;
+    or_i[static_cast<int64_t>(b) * k_r + r] = -1;
+  }
+}
+
 // One warp per row: optional L2 normalisation (fp32 math) and cast to bf16.
 __global__ void normalize_kernel(const void* __restrict__ src, int src_is_f32, int64_t n, int dim,
                                  int do_normalize, __nv_bfloat16* __restrict__ dst) {
@@ -874,12 +1051,19 @@ __global__ void seed_floor_kernel(const float* __restrict__ s, const int32_t* __
 //   stamps   [world][max_b] u32: stamps[src][b] = epoch of the last call in which rank src
 //            delivered query b's list into this buffer
 //   recv_s / recv_i [2 parities][world][max_b][max_k]
-// A call (epoch e, parity e & 1):
-//   phase 1  each CTA pushes its queries' local top-k into slot [parity][rank][b] of every
-//            peer's buffer (stores through mapped peer memory), fences at system scope and
-//            writes stamp e into the peer's stamps[rank][b] (release);
-//   phase 2  each CTA waits until stamps[src][b] >= e for every src (acquire), then merges the
-//            world lists of query b and writes the global top-k.
+// A call (epoch e, parity e & 1); CTA c owns a contiguous range of queries [b0, b1):
+//   phase 1  push the range's local top-k lists into slot [parity][rank][b] of every peer's
+//            buffer (stores through mapped peer memory, all threads), then ONE system-scope
+//            fence by thread 0 and relaxed stores of stamp e into every peer's
+//            stamps[rank][b], b in the range (fence + relaxed store = release). The first
+//            version fenced per query and released every stamp separately: ~9 system fences
+//            per query at G = 8, 0.2-0.5 ms per exchange (scripts/k6_probe.py);
+//   phase 2  one thread per (source, query) of the range polls stamps[src][b] >= e (acquire),
+//            then the range's queries are merged one by one by RANK: the world lists of a query
+//            are each sorted (score desc, id asc), so the output position of entry j of list
+//            r is j + (entries of every other list that order before it), a binary search per
+//            list (ties broken by list index, so positions are unique), stopped as soon as the
+//            position reaches k. Two block barriers per query instead of a bitonic sort.
 // Stamps are per (source, query slot), so calls with different batch sizes interleave freely:
 // a slot left untouched by a smaller batch is simply older, and the next call that covers it
 // waits for that call's own stamp. A rank can be at most one call ahead of another (its next
@@ -911,6 +1095,9 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void st_relaxed_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ uint64_t global_timer_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -921,9 +1108,11 @@ __host__ __device__ __forceinline__ size_t peer_stamp_bytes(int world, int max_b
   return ((static_cast<size_t>(world) * max_b * 4 + 255) / 256) * 256;
 }
 
-__global__ void peer_exchange_merge_kernel(const PeerArgs a) {
-  extern __shared__ uint64_t keys[];
-  __shared__ int aborted;
+constexpr int kPeerThreads = 256;
+
+__global__ void __launch_bounds__(kPeerThreads) peer_exchange_merge_kernel(const PeerArgs a) {
+  extern __shared__ uint64_t keys[];  // [world * k] keys of the query being merged
+  __shared__ int nvalid;
   const size_t data_off = kPeerHeaderBytes + peer_stamp_bytes(a.world, a.max_b);
   const size_t plane = static_cast<size_t>(a.world) * a.max_b * a.max_k;  // entries per parity
   auto stamps = [&](void* base) {
@@ -935,76 +1124,104 @@ __global__ void peer_exchange_merge_kernel(const PeerArgs a) {
   auto recv_i = [&](void* base) {
     return reinterpret_cast<int32_t*>(static_cast<uint8_t*>(base) + data_off + 2 * plane * 4);
   };
-  // phase 1: push
-  for (int b = blockIdx.x; b < a.B; b += gridDim.x) {
-    for (int p = 0; p < a.world; ++p) {
-      void* base = a.peers[p];
-      const size_t slot = ((static_cast<size_t>(a.parity) * a.world + a.rank) * a.max_b + b) * a.max_k;
-      for (int j = threadIdx.x; j < a.k; j += blockDim.x) {
-        recv_s(base)[slot + j] = a.local_s[static_cast<int64_t>(b) * a.k + j];
-        recv_i(base)[slot + j] = a.local_i[static_cast<int64_t>(b) * a.k + j];
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence_system();
-      for (int p = 0; p < a.world; ++p)
-        st_release_sys(stamps(a.peers[p]) + static_cast<size_t>(a.rank) * a.max_b + b, a.epoch);
+  const int per = (a.B + gridDim.x - 1) / gridDim.x;
+  const int b0 = blockIdx.x * per, b1 = min(a.B, b0 + per);
+  if (b0 >= b1) return;
+  const int nb = b1 - b0, tid = threadIdx.x;
+  // phase 1: push this range's lists to every rank (own buffer included), one fence, stamps
+  for (int p = 0; p < a.world; ++p) {
+    void* base = a.peers[p];
+    float* ds = recv_s(base);
+    int32_t* di = recv_i(base);
+    const size_t slot0 = ((static_cast<size_t>(a.parity) * a.world + a.rank) * a.max_b) * a.max_k;
+    for (int e = tid; e < nb * a.k; e += blockDim.x) {
+      const int bb = b0 + e / a.k, j = e - (e / a.k) * a.k;
+      ds[slot0 + static_cast<size_t>(bb) * a.max_k + j] = a.local_s[static_cast<int64_t>(bb) * a.k + j];
+      di[slot0 + static_cast<size_t>(bb) * a.max_k + j] = a.local_i[static_cast<int64_t>(bb) * a.k + j];
     }
   }
-  // phase 2: wait for every rank's contribution, merge
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence_system();
+    for (int p = 0; p < a.world; ++p)
+      for (int bb = b0; bb < b1; ++bb)
+        st_relaxed_sys(stamps(a.peers[p]) + static_cast<size_t>(a.rank) * a.max_b + bb, a.epoch);
+  }
+  // phase 2: wait for every (source, query) of the range
   void* own = a.peers[a.rank];
   uint32_t* abort_word = static_cast<uint32_t*>(own);
   const uint32_t* st = stamps(own);
-  const int n = a.world * a.k;
-  const int np = pow2_ceil(n);
   const uint64_t t0 = global_timer_ns();
-  for (int b = blockIdx.x; b < a.B; b += gridDim.x) {
-    if (threadIdx.x == 0) aborted = 0;
+  int bad = 0;
+  for (int w = tid; w < a.world * nb; w += blockDim.x) {
+    const int src = w % a.world, bb = b0 + w / a.world;
+    const uint32_t* sp = st + static_cast<size_t>(src) * a.max_b + bb;
+    // (signed distance: stamps are a wrapping u32 epoch counter)
+    while (static_cast<int32_t>(ld_acquire_sys(sp) - a.epoch) < 0) {
+      if (ld_acquire_sys(abort_word) != 0 || global_timer_ns() - t0 > a.timeout_ns) {
+        bad = 1;
+        break;
+      }
+      __nanosleep(128);
+    }
+    if (bad) break;
+  }
+  if (__syncthreads_or(bad)) {
+    if (tid == 0) {
+      for (int p = 0; p < a.world; ++p) st_release_sys(static_cast<uint32_t*>(a.peers[p]), 1u);
+      *reinterpret_cast<volatile uint32_t*>(a.err) = 1u;
+      __threadfence_system();
+    }
+    for (int e = tid; e < nb * a.k; e += blockDim.x) {
+      a.out_s[static_cast<int64_t>(b0) * a.k + e] = -INFINITY;
+      a.out_i[static_cast<int64_t>(b0) * a.k + e] = -1;
+    }
+    return;
+  }
+  const volatile float* rs = recv_s(own);
+  const volatile int32_t* ri = recv_i(own);
+  const int n = a.world * a.k;
+  const uint64_t pad = pad_key();
+  for (int bb = b0; bb < b1; ++bb) {
+    if (tid == 0) nvalid = 0;
+    for (int i = tid; i < n; i += blockDim.x) {
+      const int r = i / a.k, j = i - (i / a.k) * a.k;
+      const size_t o = ((static_cast<size_t>(a.parity) * a.world + r) * a.max_b + bb) * a.max_k + j;
+      const int32_t id = ri[o];
+      keys[i] = id >= 0 ? make_key(rs[o], id) : pad;
+    }
     __syncthreads();
-    if (threadIdx.x < a.world) {  // one waiting thread per source rank
-      const uint32_t* w = st + static_cast<size_t>(threadIdx.x) * a.max_b + b;
-      // (signed distance: stamps are a wrapping u32 epoch counter)
-      while (static_cast<int32_t>(ld_acquire_sys(w) - a.epoch) < 0) {
-        if (ld_acquire_sys(abort_word) != 0 || global_timer_ns() - t0 > a.timeout_ns) {
-          aborted = 1;
-          break;
+    int mine = 0;
+    for (int i = tid; i < n; i += blockDim.x) {
+      const uint64_t key = keys[i];
+      if (key == pad) continue;
+      ++mine;
+      const int r = i / a.k;
+      int pos = i - r * a.k;
+      for (int r2 = 0; r2 < a.world && pos < a.k; ++r2) {
+        if (r2 == r) continue;
+        const uint64_t* L = keys + r2 * a.k;
+        int lo = 0, hi = a.k;  // entries of list r2 ordered before `key`
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          const uint64_t x = L[mid];
+          if (x > key || (r2 < r && x == key)) lo = mid + 1;
+          else hi = mid;
         }
-        __nanosleep(256);
+        pos += lo;
+      }
+      if (pos < a.k) {
+        a.out_s[static_cast<int64_t>(bb) * a.k + pos] = key_score(key);
+        a.out_i[static_cast<int64_t>(bb) * a.k + pos] = key_id(key);
       }
     }
+    if (mine) atomicAdd(&nvalid, mine);
     __syncthreads();
-    if (aborted) {
-      if (threadIdx.x == 0) {
-        for (int p = 0; p < a.world; ++p) st_release_sys(static_cast<uint32_t*>(a.peers[p]), 1u);
-        *reinterpret_cast<volatile uint32_t*>(a.err) = 1u;
-        __threadfence_system();
-      }
-      for (int j = threadIdx.x; j < a.k; j += blockDim.x) {
-        a.out_s[static_cast<int64_t>(b) * a.k + j] = -INFINITY;
-        a.out_i[static_cast<int64_t>(b) * a.k + j] = -1;
-      }
-      __syncthreads();
-      continue;
+    for (int pos = nvalid + tid; pos < a.k; pos += blockDim.x) {
+      a.out_s[static_cast<int64_t>(bb) * a.k + pos] = -INFINITY;
+      a.out_i[static_cast<int64_t>(bb) * a.k + pos] = -1;
     }
-    for (int i = threadIdx.x; i < np; i += blockDim.x) {
-      uint64_t key = pad_key();
-      if (i < n) {
-        const int r = i / a.k, j = i - (i / a.k) * a.k;
-        const size_t o = ((static_cast<size_t>(a.parity) * a.world + r) * a.max_b + b) * a.max_k + j;
-        const int32_t id = reinterpret_cast<volatile int32_t*>(recv_i(own))[o];
-        if (id >= 0) key = make_key(reinterpret_cast<volatile float*>(recv_s(own))[o], id);
-      }
-      keys[i] = key;
-    }
-    bitonic_sort_desc_fast(keys, np);
-    for (int j = threadIdx.x; j < a.k; j += blockDim.x) {
-      const uint64_t key = keys[j];
-      const int32_t id = key_id(key);
-      a.out_s[static_cast<int64_t>(b) * a.k + j] = id < 0 ? -INFINITY : key_score(key);
-      a.out_i[static_cast<int64_t>(b) * a.k + j] = id;
-    }
-    __syncthreads();
+    __syncthreads();  // keys / nvalid reused by the next query
   }
 }
 
@@ -1039,10 +1256,17 @@ int launch_peer_exchange_merge(void* const* peers_dev, int rank, int world, int 
                                cudaStream_t stream) {
   PeerArgs a{peers_dev, rank, world, B, k, max_b, max_k, static_cast<int>(epoch & 1u), epoch,
              timeout_ns, local_s, local_i, out_s, out_i, err_word};
-  int np = 1;
-  while (np < world * k) np <<= 1;
   const int grid = B < num_sms ? B : num_sms;
-  peer_exchange_merge_kernel<<<grid, 128, np * sizeof(uint64_t), stream>>>(a);
+  const size_t smem = static_cast<size_t>(world) * k * sizeof(uint64_t);
+  if (smem > 48 * 1024) {
+    static std::atomic<uint64_t> configured{0};
+    if (first_on_device(configured)) {
+      cudaError_t e = cudaFuncSetAttribute(peer_exchange_merge_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      if (e != cudaSuccess) return static_cast<int>(e);
+    }
+  }
+  peer_exchange_merge_kernel<<<grid, kPeerThreads, smem, stream>>>(a);
   return static_cast<int>(cudaGetLastError());
 }
 
@@ -1247,6 +1471,48 @@ int rerank_lists_splits(int B, int C, int k, int dim, int num_sms) {
   if (const char* e = getenv("TSV_RERANK_SPLITS")) splits = std::max(1, std::min(8, atoi(e)));
   while (splits < 8 && (C + splits - 1) / splits > 32 * 32) ++splits;
   return splits;
+}
+
+size_t search_rerank_seg_smem(int dim, int max_rows, int k_s) {
+  const int msel = std::min(k_s, max_rows);
+  return static_cast<size_t>(kSegWarps) * kSegSlots * dim * 2 + static_cast<size_t>(dim) * 4 +
+         static_cast<size_t>(max_rows) * 12 + static_cast<size_t>(msel) * 12;
+}
+
+template <int CPL, bool kTiled>
+int launch_search_rerank_seg_v(size_t smem, const void* arena, int64_t nrows, int dim,
+                               const void* qs, const void* qr, int q_is_f32, int do_normalize,
+                               const int64_t* q_rows, int B, int max_rows, int k_s, int k_r,
+                               int local_ids, float* os_s, int32_t* os_i, float* or_s,
+                               int32_t* or_i, cudaStream_t stream) {
+  auto kern = search_rerank_seg_kernel<CPL, kTiled>;
+  static std::atomic<uint64_t> configured{0};
+  if (first_on_device(configured)) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    if (e != cudaSuccess) return static_cast<int>(e);
+  }
+  return launch_pdl(kern, dim3(B), dim3(kSegWarps * 32), smem, stream,
+                    reinterpret_cast<const __nv_bfloat16*>(arena), nrows, dim, qs, qr, q_is_f32,
+                    do_normalize, q_rows, max_rows, k_s, k_r, local_ids, os_s, os_i, or_s, or_i);
+}
+
+int launch_search_rerank_seg(const void* arena, int64_t nrows, int dim, int tiled, const void* qs,
+                             const void* qr, int q_is_f32, int do_normalize,
+                             const int64_t* q_rows, int B, int max_rows, int k_s, int k_r,
+                             int local_ids, float* os_s, int32_t* os_i, float* or_s,
+                             int32_t* or_i, cudaStream_t stream) {
+  if (B <= 0) return 0;
+  const size_t smem = search_rerank_seg_smem(dim, max_rows, k_s);
+  if (smem > 220 * 1024 || dim % 8 != 0 || dim > 2048) return static_cast<int>(cudaErrorInvalidValue);
+  const int cpl = (dim / 8 + 31) / 32;
+#define TSV_SEG(C, T) launch_search_rerank_seg_v<C, T>(smem, arena, nrows, dim, qs, qr, q_is_f32, do_normalize, q_rows, B, max_rows, k_s, k_r, local_ids, os_s, os_i, or_s, or_i, stream)
+#define TSV_SEG_T(C) (tiled ? TSV_SEG(C, true) : TSV_SEG(C, false))
+  if (cpl <= 1) return TSV_SEG_T(1);
+  if (cpl <= 2) return TSV_SEG_T(2);
+  if (cpl <= 4) return TSV_SEG_T(4);
+  return TSV_SEG_T(8);
+#undef TSV_SEG_T
+#undef TSV_SEG
 }
 
 // Pipelined gather (bf16 arenas, dim <= 2048): cp.async rings of `slots` rows per warp (2 by

@@ -235,6 +235,43 @@ class DeviceIndex:
             _stream_handle(stream, self.device)))
         return scores, ids
 
+    def search_rerank_segmented(self, q: torch.Tensor, q_rows: torch.Tensor, max_rows: int,
+                                k_search: int, k_rerank: int,
+                                q_rerank: torch.Tensor | None = None, local_ids: bool = True,
+                                stream: torch.cuda.Stream | None = None, out_search=None,
+                                out_rerank=None):
+        """Contextual retrieval's Searching -> Reranking chain in one launch: query b searches
+        arena rows [q_rows[b, 0], q_rows[b, 1]) (its own index segment; int64 [B, 2] on the
+        device, every segment <= max_rows <= 1024 rows), keeps the top k_search, and reranks
+        them against q_rerank[b] (default: the query itself), keeping the top k_rerank.
+        Returns ((search scores, ids), (rerank scores, ids))."""
+        self._check_queries(q)
+        B = q.shape[0]
+        if q_rerank is not None:
+            self._check_queries(q_rerank)
+            if q_rerank.shape != q.shape or q_rerank.dtype != q.dtype:
+                raise ConfigParse("q_rerank must match q in shape and dtype")
+            q_rerank = q_rerank.contiguous()
+        _require_cuda(q_rows, "q_rows")
+        if (q_rows.dtype != torch.int64 or tuple(q_rows.shape) != (B, 2)
+                or q_rows.device != self.device or not q_rows.is_contiguous()):
+            raise ConfigParse(f"q_rows must be contiguous int64 [{B}, 2] on {self.device}")
+        bufs = []
+        for o, kk in ((out_search, k_search), (out_rerank, k_rerank)):
+            if o is None:
+                o = (torch.empty((B, kk), dtype=torch.float32, device=self.device),
+                     torch.empty((B, kk), dtype=torch.int32, device=self.device))
+            else:
+                _check_out(o, B, int(kk), self.device)
+            bufs.append(o)
+        (ss, si), (rs, ri) = bufs
+        nat.check(nat.load().tsv_search_rerank_segmented(
+            self._h, q.contiguous().data_ptr(), None if q_rerank is None else q_rerank.data_ptr(),
+            _dtype_code(q), B, q_rows.data_ptr(), int(max_rows), int(k_search), int(k_rerank),
+            int(bool(local_ids)), ss.data_ptr(), si.data_ptr(), rs.data_ptr(), ri.data_ptr(),
+            _stream_handle(stream, self.device)))
+        return (ss, si), (rs, ri)
+
     def rerank(self, q: torch.Tensor, cand_ids: torch.Tensor, k: int,
                stream: torch.cuda.Stream | None = None,
                out: tuple[torch.Tensor, torch.Tensor] | None = None,

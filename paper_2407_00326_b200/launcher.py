@@ -295,24 +295,40 @@ class CapturedContextual:
     """The contextual-retrieval chain captured in one CUDA graph: each query
     searches its own per-query index segment (segmented Searching, top-k_search; the
     per-query indexes of workloads.py:95-97 built by each query's Ingestion) and its hits are
-    reranked against it (Reranking, dedup, top-k_rerank). Segment layout is fixed at capture
-    (the item list the graph uploads lives in a pinned buffer owned by the index).
+    reranked against it (Reranking, dedup, top-k_rerank). Segment layout is fixed at capture.
+
+    fused=None (default) runs the chain as ONE kernel (tsv_search_rerank_segmented: the
+    segment's rows are gathered once and scored against the query and the rerank question in
+    the same pass) whenever every segment has <= 1024 rows on a bf16 arena; fused=False keeps the primitive-by-primitive chain (normalise + scan + merge
+    + rerank: its item list lives in a pinned buffer owned by the index).
 
     run(q) copies the queries into the captured buffer and replays; returns the reranked
     (scores, ids) buffers, ids being arena rows (valid until the next call)."""
 
     def __init__(self, index, q_offsets, row_ranges, k_search: int, k_rerank: int,
-                 dtype=torch.bfloat16, warmup: int = 2):
+                 dtype=torch.bfloat16, warmup: int = 2, fused: bool | None = None):
         self.index = index
         dev = index.device
         b = int(q_offsets[-1])
         self.q_offsets, self.row_ranges = list(q_offsets), list(row_ranges)
         self.k_search, self.k_rerank = k_search, k_rerank
+        max_rows = max((e - a for a, e in self.row_ranges), default=0)
+        can_fuse = (index.storage in ("bf16", "bf16_tiled") and index.dim <= 2048
+                    and 0 < max_rows <= 1024 and k_rerank <= k_search)
+        if fused and not can_fuse:
+            raise ConfigParse("fused contextual chain needs a bf16 arena (dim <= 2048) and "
+                              "segments of 1..1024 rows")
+        self.fused = can_fuse if fused is None else bool(fused)
+        self.max_rows = max_rows
         self.q = torch.zeros((b, index.dim), dtype=dtype, device=dev)
         self.s_s = torch.empty((b, k_search), dtype=torch.float32, device=dev)
         self.s_i = torch.empty((b, k_search), dtype=torch.int32, device=dev)
         self.r_s = torch.empty((b, k_rerank), dtype=torch.float32, device=dev)
         self.r_i = torch.empty((b, k_rerank), dtype=torch.int32, device=dev)
+        rows = []
+        for sidx, (a, e) in enumerate(self.row_ranges):
+            rows += [(a, e)] * (self.q_offsets[sidx + 1] - self.q_offsets[sidx])
+        self.q_rows = torch.tensor(rows, dtype=torch.int64).reshape(b, 2).to(dev)
         # a library-created stream kept for the graph's lifetime (never shared through torch's
         # stream pool): its per-stream scratch in the index is this graph's alone
         self._stream = PrivateStream(dev.index)
@@ -326,6 +342,12 @@ class CapturedContextual:
             self._run(torch.cuda.current_stream(dev))
 
     def _run(self, stream):
+        if self.fused:
+            self.index.search_rerank_segmented(self.q, self.q_rows, self.max_rows, self.k_search,
+                                               self.k_rerank, local_ids=False, stream=stream,
+                                               out_search=(self.s_s, self.s_i),
+                                               out_rerank=(self.r_s, self.r_i))
+            return
         self.index.search_segmented(self.q, self.q_offsets, self.row_ranges, self.k_search,
                                     local_ids=False, stream=stream, out=(self.s_s, self.s_i))
         self.index.rerank(self.q, self.s_i, self.k_rerank, stream=stream,
@@ -336,4 +358,3 @@ class CapturedContextual:
         self.q.copy_(q)
         self.graph.replay()
         return self.r_s, self.r_i
-

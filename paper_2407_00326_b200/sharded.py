@@ -113,6 +113,65 @@ class PeerExchange:
             self._h = ctypes.c_void_p()
 
 
+class LocalPeerGroup:
+    """The G ranks of a peer exchange driven from ONE process (tsv_peer_attach, no IPC): every
+    rank's group lives here and maps the others' buffers directly. Used to measure and test
+    K6 with all G kernels in flight at once (ranks on one device, or on peer-accessible
+    devices of one node); a multi-process job uses PeerExchange."""
+
+    def __init__(self, devices: list[int], max_b: int, max_k: int):
+        from . import _native as nat
+
+        self.lib = nat.load()
+        self.check = nat.check
+        self.world = len(devices)
+        self.devices = [torch.device("cuda", d) for d in devices]
+        self.max_b, self.max_k = max_b, max_k
+        self._h = []
+        try:
+            for r, d in enumerate(devices):
+                h = ctypes.c_void_p()
+                self.check(self.lib.tsv_peer_create(int(d), self.world, r, max_b, max_k,
+                                                    ctypes.byref(h)))
+                self._h.append(h)
+            for r in range(self.world):
+                for p in range(self.world):
+                    self.check(self.lib.tsv_peer_attach(self._h[r], p, self._h[p]))
+        except Exception:
+            self.close()
+            raise
+
+    def set_timeout_ms(self, ms: int) -> None:
+        for h in self._h:
+            self.check(self.lib.tsv_peer_set_timeout_ms(h, int(ms)))
+
+    def allgather_merge(self, rank: int, s_loc: torch.Tensor, i_loc: torch.Tensor, k: int,
+                        stream: torch.cuda.Stream | None = None, out=None):
+        """Rank `rank`'s call: push its [B, k] lists, wait for every rank's, merge. Every rank
+        must make the same sequence of calls (each on a stream that can run concurrently)."""
+        B = s_loc.shape[0]
+        dev = self.devices[rank]
+        if out is None:
+            out = (torch.empty((B, k), dtype=torch.float32, device=dev),
+                   torch.empty((B, k), dtype=torch.int32, device=dev))
+        st = (stream or torch.cuda.current_stream(dev)).cuda_stream
+        self.check(self.lib.tsv_peer_allgather_merge(self._h[rank], s_loc.data_ptr(),
+                                                     i_loc.data_ptr(), B, k, out[0].data_ptr(),
+                                                     out[1].data_ptr(), st))
+        return out
+
+    def status(self) -> None:
+        flag = ctypes.c_int()
+        for h in self._h:
+            self.check(self.lib.tsv_peer_status(h, ctypes.byref(flag)))
+
+    def close(self) -> None:
+        for h in self._h:
+            if h.value:
+                self.lib.tsv_peer_destroy(h)
+        self._h = []
+
+
 class ShardedSearch:
     def __init__(self, index, n_rows: int, rank: int | None = None, world: int | None = None,
                  group=None, search_fn: Callable | None = None, merge_fn: Callable | None = None,

@@ -3,8 +3,8 @@
 Each variant replays a CUDA graph of 32 rerank calls whose candidate sets rotate over 8
 random draws (8 x 79 MB > L2: rows come from HBM; `l2` repeats one draw), so the number is the
 kernel's device time per call without the host's per-call issue cost (~15 us from Python).
-Variants: ldg = register gather (TSV_RERANK_LDG=1), ring = cp.async rings (default; slots via
-TSV_RERANK_SLOTS). PROBE_SPAN limits candidates to the first rows of the corpus."""
+Variants: ldg = register gather (TSV_RERANK_LDG=1); default = per-warp lists over cp.async rings
+(ring depth / warps / splits knobs); sort = ring + block sort. PROBE_SPAN limits candidates to the first rows of the corpus."""
 import os
 import sys
 from pathlib import Path
@@ -14,8 +14,11 @@ import torch
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2407_00326_b200.index import DeviceIndex, normalize_rows  # noqa: E402
 
-VARIANTS = [("ldg", {"TSV_RERANK_LDG": "1"}), ("default", {}),
-            ("lists_w16", {"TSV_RERANK_WARPS": "16"}), ("sort", {"TSV_RERANK_SORT": "1"})]
+VARIANTS = [("ldg", {"TSV_RERANK_LDG": "1"}), ("default(lists)", {}),
+            ("lists_s3", {"TSV_RERANK_SLOTS": "3"}), ("lists_s4", {"TSV_RERANK_SLOTS": "4"}),
+            ("lists_w16", {"TSV_RERANK_WARPS": "16"}),
+            ("lists_w16_s4", {"TSV_RERANK_WARPS": "16", "TSV_RERANK_SLOTS": "4"}),
+            ("sort", {"TSV_RERANK_SORT": "1"}), ("split2", {"TSV_RERANK_SPLITS": "2"})]
 KNOBS = ("TSV_RERANK_LDG", "TSV_RERANK_SLOTS", "TSV_RERANK_WARPS", "TSV_RERANK_SPLITS",
          "TSV_RERANK_SORT")
 

@@ -140,7 +140,7 @@ def test_captured_contextual_chain_replays_exactly(cuda):
     idx.append(to_dev_bf16(c, cuda))
     offs = list(range(nq + 1))
     ranges = [(i * seg, (i + 1) * seg) for i in range(nq)]
-    cap = CapturedContextual(idx, offs, ranges, k, k_r)
+    cap = CapturedContextual(idx, offs, ranges, k, k_r, fused=False)
     for seed in (1, 2, 3):
         q, _ = orc.make_queries(c, nq, seed=seed)
         qd = to_dev_bf16(q, cuda)
@@ -167,3 +167,46 @@ def test_captured_replay_rejects_other_shapes(cuda):
     cap = CapturedSearch(idx, batch=16, k=5)
     with pytest.raises(ConfigParse):
         cap.search(to_dev_bf16(c[:1], cuda))  # would broadcast into the 16-row buffer
+
+
+def test_captured_contextual_fused_matches_oracle(cuda):
+    """The default CapturedContextual (C5 at D=1024: 16 queries x own 48-row segment, top-32 ->
+    rerank 3) runs ONE fused kernel per replay; results match the CPU oracle's search + rerank
+    and the unfused chain within the bf16 tolerance, over several replays."""
+    import torch
+    from paper_2407_00326_b200.index import DeviceIndex
+    from paper_2407_00326_b200.launcher import CapturedContextual
+
+    nq, seg, dim, k, k_r = 16, 48, 1024, 32, 3
+    c = orc.make_corpus(nq * seg, dim, seed=0)
+    idx = DeviceIndex(dim, nq * seg, device=cuda.index)
+    idx.append(to_dev_bf16(c, cuda))
+    offs = list(range(nq + 1))
+    ranges = [(i * seg, (i + 1) * seg) for i in range(nq)]
+    cap = CapturedContextual(idx, offs, ranges, k, k_r)
+    assert cap.fused
+    ref = CapturedContextual(idx, offs, ranges, k, k_r, fused=False)
+    n0 = _native_launches()
+    for seed in (1, 2, 3):
+        q, _ = orc.make_queries(c, nq, seed=seed)
+        qd = to_dev_bf16(q, cuda)
+        rs, ri = cap.run(qd)
+        us, ui = ref.run(qd)
+        torch.cuda.synchronize()
+        gs, gi = from_dev(rs), from_dev(ri)
+        np.testing.assert_allclose(gs, from_dev(us), rtol=1e-3, atol=1e-6)
+        for r in range(nq):
+            a, e = ranges[r]
+            probs = orc.check_topk(from_dev(cap.s_s)[r:r + 1], from_dev(cap.s_i)[r:r + 1],
+                                   q[r:r + 1], c[a:e], k, 1e-3, id_offset=a)
+            assert not probs, probs[:3]
+            es, ei = orc.rerank(q[r:r + 1], c, from_dev(cap.s_i)[r:r + 1], k_r)
+            np.testing.assert_allclose(gs[r:r + 1], es, rtol=1e-3, atol=1e-6)
+            assert ((gi[r] >= a) & (gi[r] < e)).all()
+    assert _native_launches() == n0  # replays launch no library calls from the host
+
+
+def _native_launches():
+    from paper_2407_00326_b200 import _native
+
+    return _native.launch_count()

@@ -136,3 +136,39 @@ def test_p2p_missing_peer_times_out(cuda):
     assert out["padded"]
     assert out["status"].startswith("DeviceError")
     assert out["next"] == "DeviceError"
+
+
+@pytest.mark.parametrize("world,k", [(2, 10), (4, 100), (8, 10), (8, 100)])
+def test_in_process_peer_group_equals_merge(cuda, world, k):
+    """tsv_peer_attach: G ranks in one process on one device, every rank's K6 on its own
+    stream; each rank's result equals K4 over all ranks' lists, over varying batch sizes, with
+    lists ordered as K1 / K4 emit them (score desc, id asc) and, every other call, scores on a
+    coarse grid (many exact cross-list ties)."""
+    import torch
+
+    from paper_2407_00326_b200.index import merge_topk
+    from paper_2407_00326_b200.sharded import LocalPeerGroup
+
+    grp = LocalPeerGroup([cuda.index] * world, 64, k)
+    grp.set_timeout_ms(20_000)
+    streams = [torch.cuda.Stream(cuda) for _ in range(world)]
+    g = torch.Generator(device=cuda).manual_seed(world * k)
+    for call, (_, b) in enumerate(CALLS * 2):
+        s = torch.rand((world, b, k), generator=g, device=cuda)
+        if call % 2:
+            s = torch.floor(s * 64) / 64
+        i = torch.randperm(world * b * k, generator=g, device=cuda).to(torch.int32).reshape(world, b, k)
+        o = torch.argsort(i, dim=2)
+        s, i = torch.gather(s, 2, o), torch.gather(i, 2, o)
+        o = torch.sort(s, dim=2, descending=True, stable=True)[1]
+        s, i = torch.gather(s, 2, o).contiguous(), torch.gather(i, 2, o).contiguous()
+        for st in streams:  # the rank streams read lists made on the current stream
+            st.wait_stream(torch.cuda.current_stream(cuda))
+        outs = [grp.allgather_merge(r, s[r], i[r], k, stream=streams[r]) for r in range(world)]
+        torch.cuda.synchronize()
+        grp.status()
+        ref_s, ref_i = merge_topk(s, i, k)
+        for r in range(world):
+            assert torch.equal(outs[r][1], ref_i), (world, k, call, r)
+            assert torch.equal(outs[r][0], ref_s), (world, k, call, r)
+    grp.close()

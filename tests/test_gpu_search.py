@@ -252,6 +252,30 @@ def test_rerank_ring_equals_register_gather(cuda, dim, c, k, slots):
     np.testing.assert_allclose(g1, exp_s, rtol=TOL, atol=1e-6)
 
 
+@pytest.mark.parametrize("dim,c,k", [(768, 200, 10), (1024, 64, 32), (256, 1000, 5)])
+def test_rerank_f32_questions(cuda, dim, c, k):
+    """K3 with fp32 questions on an inner-product bf16 index (the ring kernels keep the fp32
+    question in registers): scores match the oracle's fp64 products of the unrounded fp32
+    question with the bf16 rows."""
+    import torch
+
+    rng = np.random.default_rng(dim * 7 + c)
+    n, b = 6000, 33
+    arena = orc.make_corpus(n, dim, seed=11)
+    qs = rng.standard_normal((b, dim)).astype(np.float32)
+    cand = rng.integers(0, n, size=(b, c)).astype(np.int32)
+    cand[:, 3] = cand[:, 0]
+    cand[::2, 1] = -1
+    idx = _index_from(arena, cuda)
+    s, i = idx.rerank(torch.from_numpy(qs).to(cuda), torch.from_numpy(cand).to(cuda), k)
+    exp_s, exp_i = orc.rerank(qs.astype(np.float64), arena, cand, k)
+    gs, gi = from_dev(s), from_dev(i)
+    np.testing.assert_allclose(gs, exp_s, rtol=2e-5, atol=2e-5)
+    gap_ok = np.abs(np.diff(exp_s, axis=1, prepend=np.inf)) > 1e-4
+    gap_ok &= np.abs(np.diff(exp_s, axis=1, append=-np.inf)) > 1e-4
+    assert (gi[gap_ok] == exp_i[gap_ok]).all()
+
+
 @pytest.mark.parametrize("storage", ["bf16", "bf16_tiled", "f32"])
 def test_rerank_segmented_offsets(cuda, storage):
     """Reranking a batch of questions from different queries in one launch: question b's
@@ -802,3 +826,60 @@ def test_wide_tiles_on_tiled_arena(cuda, n, lo):
     s2, i2 = _search_env(rm, qd, k, row_range=(lo, n), TSV_WIDE=0)
     np.testing.assert_array_equal(i1, i2)
     np.testing.assert_array_equal(s1, s2)
+
+
+@pytest.mark.parametrize("storage", ["bf16", "bf16_tiled"])
+@pytest.mark.parametrize("metric,dim,k_s,k_r,sep_q", [
+    ("cosine", 1024, 32, 3, False), ("ip", 256, 10, 10, True), ("cosine", 768, 50, 5, True),
+    ("ip", 64, 1, 1, False)])
+def test_search_rerank_segmented_fused(cuda, storage, metric, dim, k_s, k_r, sep_q):
+    """tsv_search_rerank_segmented (C5's Searching -> Reranking chain in one kernel): per query,
+    the search over its own segment equals the oracle's (tie bands), and the rerank of the
+    kernel's own search hits against the (separate or same) question equals the oracle's
+    rerank; segments of 0, 1, 7, 33, 48, 300 and 1024 rows, segment-local and arena ids,
+    fp32 and bf16 queries."""
+    import torch
+
+    from paper_2407_00326_b200.index import DeviceIndex
+
+    rng = np.random.default_rng(dim + k_s)
+    sizes = [48, 7, 1024, 33, 0, 300, 1, 48]
+    starts = np.cumsum([0] + sizes)[:-1]
+    n = int(sum(sizes))
+    c = orc.make_corpus(n, dim, seed=3)
+    idx = DeviceIndex(dim, n, metric=metric, device=cuda.index, storage=storage)
+    idx.append(to_dev_bf16(c, cuda))
+    B = len(sizes)
+    q = orc.make_corpus(B, dim, seed=4)
+    qr = orc.make_corpus(B, dim, seed=5) if sep_q else None
+    rows = torch.tensor([[a, a + z] for a, z in zip(starts, sizes)], dtype=torch.int64,
+                        device=cuda)
+    for local in (True, False):
+        for f32 in (False, True):
+            qd = torch.from_numpy(q).to(cuda) if f32 else to_dev_bf16(q, cuda)
+            qrd = None if qr is None else (torch.from_numpy(qr).to(cuda) if f32
+                                           else to_dev_bf16(qr, cuda))
+            (ss, si), (rs, ri) = idx.search_rerank_segmented(qd, rows, max(sizes), k_s, k_r,
+                                                             q_rerank=qrd, local_ids=local)
+            if not local:  # the rerank half is K3's arithmetic: bit-identical scores
+                us, ui = idx.rerank(qd if qrd is None else qrd, si, k_r)
+            torch.cuda.synchronize()
+            gs, gi, hs, hi = from_dev(ss), from_dev(si), from_dev(rs), from_dev(ri)
+            if not local:
+                np.testing.assert_array_equal(hs, from_dev(us))
+                np.testing.assert_array_equal(hi, from_dev(ui))
+            for b, (a, z) in enumerate(zip(starts, sizes)):
+                off = 0 if local else a
+                qb = orc.bf16_round(q[b:b + 1]) if metric == "ip" and not f32 else q[b:b + 1]
+                probs = orc.check_topk(gs[b:b + 1], gi[b:b + 1], qb, c[a:a + z], k_s, TOL,
+                                       id_offset=off)
+                assert not probs, (b, probs[:3])
+                qq = q if qr is None else qr
+                qrb = orc.bf16_round(qq[b:b + 1]) if metric == "ip" and not f32 else qq[b:b + 1]
+                cand = gi[b:b + 1] - off
+                cand[gi[b:b + 1] < 0] = -1
+                es, ei = orc.rerank(qrb, c[a:a + z], cand, k_r)
+                np.testing.assert_allclose(hs[b:b + 1], es, rtol=TOL, atol=1e-6)
+                real = hi[b] >= 0
+                assert real.sum() == min(z, k_r)
+                assert set((hi[b][real] - off).tolist()) <= set(cand[0][cand[0] >= 0].tolist())
