@@ -159,6 +159,8 @@ struct Workspace {
   DevBuf<tsv::ScanItem> items;
   DevBuf<uint64_t> rr_keys;     // K3 split mode: per-block top-k keys
   DevBuf<int32_t> rr_arrive;    // K3 split mode: per-question arrival counters (kept zero)
+  DevBuf<uint64_t> sm_keys;     // K2s: per-row-block top-k keys
+  DevBuf<int32_t> sm_arrive;    // K2s: per-query-group arrival counters (kept zero)
   std::vector<tsv::ScanItem> host_items;
   // Pinned staging for the item table so its upload is a true async copy. A ring of slots,
   // each with an event marking when its upload drained: the host only waits when it laps a
@@ -185,6 +187,8 @@ struct Workspace {
     items.ws = &state;
     rr_keys.ws = &state;
     rr_arrive.ws = &state;
+    sm_keys.ws = &state;
+    sm_arrive.ws = &state;
   }
   void release() {
     for (auto& s : pinned) {
@@ -842,9 +846,151 @@ static int search_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B, in
   return TSV_OK;
 }
 
+// Development: TSV_SMALL_TRACE=1 makes the one-launch searches (K2s / K2t) stamp per-block phase
+// times; each launch then synchronises and prints min / median / max per phase to stderr.
+static unsigned long long* small_trace_buffer() {
+  static unsigned long long* trace = nullptr;
+  if (!env_flag("TSV_SMALL_TRACE")) return nullptr;
+  if (trace == nullptr && cudaMalloc(&trace, sizeof(unsigned long long) * 8 * 4096) != cudaSuccess)
+    return nullptr;
+  cudaMemset(trace, 0, sizeof(unsigned long long) * 8 * 4096);
+  return trace;
+}
+
+static void small_trace_print(unsigned long long* trace, int nb_total, cudaStream_t st) {
+  if (trace == nullptr || nb_total > 4096) return;
+  std::vector<unsigned long long> h(8 * static_cast<size_t>(nb_total));
+  cudaMemcpyAsync(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  unsigned long long t0 = ~0ull;
+  for (int b = 0; b < nb_total; ++b) t0 = std::min(t0, h[b * 8]);
+  fprintf(stderr, "one-launch search trace (%d blocks, ns from first entry): phase min/med/max\n",
+          nb_total);
+  for (int ph = 0; ph < 8; ++ph) {
+    std::vector<long long> v;
+    for (int b = 0; b < nb_total; ++b)
+      if (h[b * 8 + ph]) v.push_back(static_cast<long long>(h[b * 8 + ph] - t0));
+    if (v.empty()) continue;
+    std::sort(v.begin(), v.end());
+    fprintf(stderr, "  phase %d: n=%zu min %lld med %lld max %lld\n", ph, v.size(), v.front(),
+            v[v.size() / 2], v.back());
+  }
+}
+
+// ~128 rows per block (16 per warp: about three ring refills), at most one block per SM over
+// all query groups: few partial lists, so the last block merges them in one L2 round trip.
+static int small_scan_blocks(const tsv_index* idx, int groups, int64_t n) {
+  return std::max(1, static_cast<int>(std::min<int64_t>((n + 127) / 128,
+                                                        std::max(1, idx->num_sms / groups))));
+}
+
+// K2s routing: few queries over a short row range (the scan's fixed costs dominate; at most a
+// few L2-resident passes over the rows, one per query group) -> one small-scan launch.
+static bool small_scan_fits(const tsv_index* idx, int B, int k, int64_t n) {
+  if (idx->storage == TSV_F32 || idx->dim % 8 != 0 || idx->dim > 1024 || k > 16 || B > 64 ||
+      n <= 0 || n > 65536 || env_flag("TSV_NO_SMALL"))
+    return false;
+  const int qg = tsv::small_scan_qg(idx->dim);
+  const int groups = (B + qg - 1) / qg;
+  if (n * idx->dim * 2 * groups > (int64_t(48) << 20)) return false;
+  const int64_t per = (n + small_scan_blocks(idx, groups, n) - 1) / small_scan_blocks(idx, groups, n);
+  return per <= 1024;  // the block's scores stay in shared memory ([QG][per] fp32)
+}
+
+static int small_scan(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k,
+                      int64_t row_beg, int64_t row_end, int32_t id_offset, float* scores_dev,
+                      int32_t* ids_dev, cudaStream_t st) {
+  if (row_beg < 0 || row_end > idx->rows || row_beg > row_end)
+    return fail(TSV_ERR_CAPACITY, "row range [%lld, %lld) outside arena of %lld rows",
+                (long long)row_beg, (long long)row_end, (long long)idx->rows);
+  Workspace& w = ws_for(idx, st);
+  const int qg = tsv::small_scan_qg(idx->dim);
+  const int groups = (B + qg - 1) / qg;
+  const int64_t n = row_end - row_beg;
+  const int nblk = small_scan_blocks(idx, groups, n);
+  int rc = w.sm_keys.ensure(static_cast<size_t>(groups) * nblk * qg * k);
+  if (rc) return rc;
+  const size_t had = w.sm_arrive.cap;
+  rc = w.sm_arrive.ensure(static_cast<size_t>(groups));
+  if (rc) return rc;
+  if (w.sm_arrive.cap != had)
+    TSV_CUDA(cudaMemsetAsync(w.sm_arrive.ptr, 0, w.sm_arrive.cap * sizeof(int32_t), st),
+             "arrivals reset");
+  const int nb_total = nblk * groups;
+  unsigned long long* trace = small_trace_buffer();
+  int e = tsv::launch_small_scan(idx->arena, idx->dim, idx->storage == TSV_BF16_TILED, q_dev,
+                                 q_dtype == TSV_F32, idx->metric == TSV_METRIC_COSINE, B, row_beg,
+                                 row_end, id_offset, k, nblk, w.sm_keys.ptr, w.sm_arrive.ptr,
+                                 scores_dev, ids_dev, st, trace);
+  if (e) return cuda_fail(static_cast<cudaError_t>(e), "small scan launch");
+  g_launches++;
+  small_trace_print(trace, nb_total, st);
+  return TSV_OK;
+}
+
+// K2t routing: the tensor-core one-launch search (bf16 arena, B <= 64, k <= 16, at
+// most two 128-row tiles per SM so the last CTA's merge stays short, queries <= 64 KB of smem).
+static bool tiny_scan_fits(const tsv_index* idx, int B, int k, int64_t n) {
+  if ((idx->storage != TSV_BF16 && idx->storage != TSV_BF16_TILED) || idx->dim % 8 != 0 ||
+      k > 16 || B > 64 || n <= 0 ||
+      env_flag("TSV_NO_TINY") || env_flag("TSV_NO_SMALL"))
+    return false;
+  const int nq = B <= 16 ? 16 : (B <= 32 ? 32 : 64);
+  const int num_kb = (idx->dim + 63) / 64;
+  const int stages = std::min(num_kb, 6);
+  const int64_t tiles = tsv::tiny_scan_blocks(n);
+  // the queries (raw fp32 at most) and the tiles' lists (merged in the ring) must fit on chip
+  return tiles <= 2 * idx->num_sms && num_kb * nq * 128 <= 64 * 1024 &&
+         int64_t(B) * idx->dim * 4 <= 64 * 1024 && tiles * k <= 512 &&
+         int64_t(B) * tiles * k * 8 <= stages * 16384;  // the last CTA stages every list in the ring
+}
+
+static int tiny_scan(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k,
+                     int64_t row_beg, int64_t row_end, int32_t id_offset, float* scores_dev,
+                     int32_t* ids_dev, cudaStream_t st) {
+  if (row_beg < 0 || row_end > idx->rows || row_beg > row_end)
+    return fail(TSV_ERR_CAPACITY, "row range [%lld, %lld) outside arena of %lld rows",
+                (long long)row_beg, (long long)row_end, (long long)idx->rows);
+  Workspace& w = ws_for(idx, st);
+  const int nblk = tsv::tiny_scan_blocks(row_end - row_beg);
+  int rc = w.sm_keys.ensure(static_cast<size_t>(B) * nblk * k);
+  if (rc) return rc;
+  const size_t had = w.sm_arrive.cap;
+  rc = w.sm_arrive.ensure(1);
+  if (rc) return rc;
+  if (w.sm_arrive.cap != had)
+    TSV_CUDA(cudaMemsetAsync(w.sm_arrive.ptr, 0, w.sm_arrive.cap * sizeof(int32_t), st),
+             "arrivals reset");
+  unsigned long long* trace = small_trace_buffer();
+  int e = tsv::launch_tiny_scan(idx->tmap_c, q_dev, q_dtype == TSV_F32,
+                                idx->metric == TSV_METRIC_COSINE, B, idx->dim, row_beg, row_end,
+                                id_offset, k, w.sm_keys.ptr, w.sm_arrive.ptr, scores_dev, ids_dev,
+                                st, trace, idx->storage == TSV_BF16_TILED);
+  if (e) return cuda_fail(static_cast<cudaError_t>(e), "tiny scan launch");
+  g_launches++;
+  small_trace_print(trace, nblk, st);
+  return TSV_OK;
+}
+
 int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int64_t row_beg,
                int64_t row_end, int32_t id_offset, float* scores_dev, int32_t* ids_dev,
                void* stream) {
+  if (idx != nullptr && B > 0 && k > 0 && q_dev != nullptr && scores_dev != nullptr &&
+      ids_dev != nullptr && check_dtype(q_dtype) == TSV_OK &&
+      tiny_scan_fits(idx, B, k, row_end - row_beg) && aligned16(q_dev) &&
+      (idx->storage != TSV_BF16_TILED || row_beg % 128 == 0)) {
+    DeviceGuard g(idx->device);
+    return tiny_scan(idx, q_dev, q_dtype, B, k, row_beg, row_end, id_offset, scores_dev, ids_dev,
+                     reinterpret_cast<cudaStream_t>(stream));
+  }
+  if (idx != nullptr && B > 0 && k > 0 && q_dev != nullptr && scores_dev != nullptr &&
+      ids_dev != nullptr && check_dtype(q_dtype) == TSV_OK &&
+      small_scan_fits(idx, B, k, row_end - row_beg) &&
+      (idx->storage != TSV_BF16_TILED || row_beg % 128 == 0)) {
+    DeviceGuard g(idx->device);
+    return small_scan(idx, q_dev, q_dtype, B, k, row_beg, row_end, id_offset, scores_dev, ids_dev,
+                      reinterpret_cast<cudaStream_t>(stream));
+  }
   // k > 32: a top-k over a 1/32 (k > 100: 1/16) sample of the rows bounds every query's final k-th score from
   // below; the main scan then only has to keep rows above that floor (candidate mode), which
   // keeps the result exact. Ranges of at most kCandCap rows skip the sample: every row is a

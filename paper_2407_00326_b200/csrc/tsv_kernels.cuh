@@ -187,6 +187,25 @@ int launch_search_rerank_seg(const void* arena, int64_t nrows, int dim, int tile
                              int32_t* or_i, cudaStream_t stream);
 constexpr int kFusedSegMaxRows = 1024;
 
+// K2s: one-launch search for latency-bound shapes (few queries, short row ranges; bf16 / tiled
+// arenas, dim % 8 == 0, dim <= 1024, k <= 16). Grid (nblk row blocks) x (query groups of
+// small_scan_qg(dim)); part_keys [groups * nblk * QG * 16] and arrive [groups] (zeroed once; the
+// kernel leaves them zero) are scratch. Queries are normalised in-kernel when do_normalize.
+int small_scan_qg(int dim);
+int launch_small_scan(const void* arena, int dim, int tiled, const void* q, int q_is_f32,
+                      int do_normalize, int B, int64_t row_beg, int64_t row_end, int32_t id_offset,
+                      int k, int nblk, uint64_t* part_keys, int32_t* arrive, float* out_s,
+                      int32_t* out_i, cudaStream_t stream, unsigned long long* trace = nullptr);
+
+// K2t: one-launch tensor-core search for few queries (B <= 64) over a short row range of a
+// bf16 arena (row-major, or tiled with row_beg % 128 == 0): one CTA per 128-row tile (rows on UMMA M, queries on N), per-tile top k
+// to part_keys [B * tiles * k], the last CTA merges; arrive (one int, zeroed once) is left zero.
+int tiny_scan_blocks(int64_t n);
+int launch_tiny_scan(const CUtensorMap& tmap_c, const void* q, int q_is_f32, int do_normalize,
+                     int B, int dim, int64_t row_beg, int64_t row_end, int32_t id_offset, int k,
+                     uint64_t* part_keys, int32_t* arrive, float* out_s, int32_t* out_i,
+                     cudaStream_t stream, unsigned long long* trace = nullptr, int tiled = 0);
+
 int launch_normalize(const void* src, int src_is_f32, int64_t n, int dim, int do_normalize,
                      void* dst_bf16, cudaStream_t stream);
 

@@ -450,6 +450,12 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// (a, b) -> bf16x2 word (a in the low half), round to nearest even
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
 // bf16x2 word -> (element 2t, element 2t+1) as fp32: a bf16 is the high half of an fp32
 __device__ __forceinline__ float2 bf16x2_to_float2(uint32_t w) {
   return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
@@ -949,6 +955,374 @@ __global__ void __launch_bounds__(kSegWarps * 32) search_rerank_seg_kernel(
     or_s[static_cast<int64_t>(b) * k_r + r] = -INFINITY;
     or_i[static_cast<int64_t>(b) * k_r + r] = -1;
   }
+}
+
+// K2s: latency-bound searches in ONE launch (BASELINE C1: 16 queries over a 10k x 384 corpus;
+// reference: the naive-RAG Searching primitive, optimizer.py:178-198). The tensor-core scan
+// costs ~27 us there as normalise + scan + merge (three launches; the scan's first-tile
+// insertion chain and setup dominate a 40-tile corpus). Here a grid of (row blocks x query
+// groups of QG) CTAs, 8 warps each:
+//  * warps < QG L2-normalise one query each (normalize_kernel's math: the same bf16 query the
+//    tensor-core path scans) into shared memory; every lane then holds its 16-byte chunks of
+//    all QG queries as fp32 pairs in registers;
+//  * each warp streams its rows (c = warp + 8 j) through a 6-slot cp.async ring; per row a lane
+//    does CPL x QG x 4 packed FFMA2, and one "transposed" butterfly (QG-1 + 5 - log2 QG
+//    shuffles instead of 5 QG) leaves lane l holding the full score of query l >> (5 - log2 QG);
+//  * the owner lane of each query stores the row's score in shared memory ([QG][rows of the
+//    block]); no per-row selection in the streaming loop (a per-row register-list insertion
+//    was half of its instructions: with ~16 rows per warp most rows enter a k-list);
+//  * then one warp per query selects the block's top k from those scores (lane-local sorted
+//    key lists, k rounds of a warp max; keys (score, id) are unique, ties go to the smaller
+//    id), writes them as keys to scratch, and the last block of the query group (arrival
+//    counter, self-resetting) merges the row blocks' lists and writes the result.
+constexpr int kSmallWarps = 8;
+__device__ __forceinline__ unsigned long long global_ns_small() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+constexpr int kSmallSlots = 6;
+
+// v[0..N) per lane -> full warp sum of v[q] in every lane whose (lane >> (5 - log2 N)) == q.
+template <int N>
+__device__ __forceinline__ float transpose_reduce(float (&v)[N], int lane) {
+  int off = 16;
+#pragma unroll
+  for (int m = N; m > 1; m >>= 1) {
+    const bool hi = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < m / 2; ++i) {
+      const float send = hi ? v[i] : v[i + m / 2];
+      const float keep = hi ? v[i + m / 2] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+    off >>= 1;
+  }
+  float r = v[0];
+  for (; off > 0; off >>= 1) r += __shfl_xor_sync(0xffffffffu, r, off);
+  return r;
+}
+
+// Insert key into a descending register list of K keys (precondition: key > l[K-1]).
+template <int K>
+__device__ __forceinline__ void key_list_insert(uint64_t (&l)[K], uint64_t key) {
+#pragma unroll
+  for (int i = K - 1; i > 0; --i) {
+    const bool keep = l[i] > key;
+    const bool prev_keep = l[i - 1] > key;
+    l[i] = keep ? l[i] : (prev_keep ? key : l[i - 1]);
+  }
+  if (!(l[0] > key)) l[0] = key;
+}
+
+// Scores of one row against the QG queries, accumulated as packed fp32 pairs.
+template <int QG, int CPL>
+__device__ __forceinline__ void small_row_dot(const uint4* __restrict__ row, int lane, int chunks,
+                                              const float2 (&qf)[QG][CPL][4], float2 (&acc)[QG]) {
+#pragma unroll
+  for (int qi = 0; qi < QG; ++qi) acc[qi] = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int jj = 0; jj < CPL; ++jj) {
+    const int ch = lane + 32 * jj;
+    if (ch < chunks) {
+      const uint4 raw = row[ch];
+      const float2 x0 = bf16x2_to_float2(raw.x), x1 = bf16x2_to_float2(raw.y);
+      const float2 x2 = bf16x2_to_float2(raw.z), x3 = bf16x2_to_float2(raw.w);
+#pragma unroll
+      for (int qi = 0; qi < QG; ++qi) {
+        acc[qi] = __ffma2_rn(x0, qf[qi][jj][0], acc[qi]);
+        acc[qi] = __ffma2_rn(x1, qf[qi][jj][1], acc[qi]);
+        acc[qi] = __ffma2_rn(x2, qf[qi][jj][2], acc[qi]);
+        acc[qi] = __ffma2_rn(x3, qf[qi][jj][3], acc[qi]);
+      }
+    }
+  }
+}
+
+// k rounds of a warp-wide max over up to 32 * N keys held N per lane (pad-filled; keys unique):
+// round r's key goes to out[r] (lane 0).
+template <int N>
+__device__ __forceinline__ void warp_select_rounds(uint64_t (&v)[N], int k, uint64_t* out, int lane) {
+  const uint64_t pad = pad_key();
+  for (int r = 0; r < k; ++r) {
+    uint64_t m = v[0];
+#pragma unroll
+    for (int i = 1; i < N; ++i) m = v[i] > m ? v[i] : m;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t x = __shfl_xor_sync(0xffffffffu, m, o);
+      m = x > m ? x : m;
+    }
+    if (lane == 0) out[r] = m;
+    if (m == pad) {
+      for (int rr = r + 1; rr < k && lane == 0; ++rr) out[rr] = pad;
+      break;
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = v[i] == m ? pad : v[i];
+  }
+}
+
+template <int QG, int CPL, int KC, bool kTiled>
+__global__ void __launch_bounds__(kSmallWarps * 32, 1) small_scan_kernel(
+    const __nv_bfloat16* __restrict__ arena, int dim, const void* __restrict__ q, int q_is_f32,
+    int do_normalize, int B, int64_t row_beg, int64_t row_end, int32_t id_offset, int k,
+    int resident, uint64_t* __restrict__ part_keys, int32_t* __restrict__ arrive,
+    float* __restrict__ out_s, int32_t* __restrict__ out_i, unsigned long long* __restrict__ trace) {
+  // (trace: development timestamps per block and phase, TSV_SMALL_TRACE; null in production)
+  auto stamp = [&](int ph) {
+    if (trace != nullptr && threadIdx.x == 0)
+      trace[(blockIdx.y * gridDim.x + blockIdx.x) * 8 + ph] = global_ns_small();
+  };
+  stamp(0);
+  constexpr int kLog = QG == 16 ? 4 : (QG == 8 ? 3 : (QG == 4 ? 2 : (QG == 2 ? 1 : 0)));
+  static_assert((1 << kLog) == QG, "QG must be a power of two <= 16");
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int row_bytes = dim * 2;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = blockIdx.y, q0 = g * QG, nq = min(QG, B - q0);
+  const int nblk = gridDim.x;
+  const int64_t n = row_end - row_beg;
+  const int64_t per = (n + nblk - 1) / nblk;
+  const int64_t r0 = row_beg + blockIdx.x * per, r1 = min(row_end, r0 + per);
+  const int nr = r1 > r0 ? static_cast<int>(r1 - r0) : 0;
+  const int nrow = warp < nr ? (nr - warp + kSmallWarps - 1) / kSmallWarps : 0;
+  // resident: every row of the warp has its own buffer (all loads issued at once, one round
+  // trip); otherwise a kSmallSlots-deep ring
+  const int slots = resident ? static_cast<int>((per + kSmallWarps - 1) / kSmallWarps) : kSmallSlots;
+  uint8_t* ring = sm;                                                   // [warps][slots][row]
+  __nv_bfloat16* qv = reinterpret_cast<__nv_bfloat16*>(
+      ring + static_cast<size_t>(kSmallWarps) * slots * row_bytes);   // [QG][dim]
+  float* sc = reinterpret_cast<float*>(qv + QG * dim);                  // [QG][per] scores
+  __shared__ int last;
+  __shared__ uint64_t sel_s[kSmallWarps][16];  // final selection, one row per warp
+  const int chunks = dim >> 3;
+  const int64_t kb_per_row = (dim + 63) >> 6;
+  uint8_t* my_ring = ring + static_cast<size_t>(warp) * slots * row_bytes;
+  pdl_wait();
+  stamp(1);
+  auto issue = [&](int j, int slot) {
+    if (j < nrow) {
+      const int64_t r = r0 + warp + static_cast<int64_t>(kSmallWarps) * j;
+      const uint4* src = kTiled ? reinterpret_cast<const uint4*>(
+                                      arena + ((r >> 7) * kb_per_row * 128 + (r & 127)) * 64)
+                                : reinterpret_cast<const uint4*>(arena + r * dim);
+      uint4* dst = reinterpret_cast<uint4*>(my_ring + static_cast<size_t>(slot) * row_bytes);
+#pragma unroll
+      for (int jj = 0; jj < CPL; ++jj) {
+        const int ch = lane + 32 * jj;
+        if (ch < chunks)
+          cp_async16(dst + ch, src + (kTiled ? static_cast<int64_t>(ch >> 3) * 1024 + (ch & 7) : ch));
+      }
+    }
+  };
+  if (resident) {
+    for (int j = 0; j < nrow; ++j) issue(j, j);
+    cp_async_commit();
+  } else {
+#pragma unroll
+    for (int s_ = 0; s_ < kSmallSlots; ++s_) {
+      issue(s_, s_);
+      cp_async_commit();
+    }
+  }
+  // queries of this group -> shared memory, L2-normalised in fp32 and rounded to bf16 (K5's
+  // arithmetic; each lane sums its 16-byte chunks, so the sum order is the chunk order): one
+  // global round trip per query
+  for (int qi = warp; qi < QG; qi += kSmallWarps) {
+    uint4* out = reinterpret_cast<uint4*>(qv + qi * dim);
+    float x[CPL][8];
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) {
+      const int ch = lane + 32 * j;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) x[j][t] = 0.f;
+      if (qi < nq && ch < chunks) {
+        const int64_t o = static_cast<int64_t>(q0 + qi) * dim + ch * 8;
+        if (q_is_f32) {
+          const float4 a = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(q) + o));
+          const float4 b = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(q) + o + 4));
+          x[j][0] = a.x; x[j][1] = a.y; x[j][2] = a.z; x[j][3] = a.w;
+          x[j][4] = b.x; x[j][5] = b.y; x[j][6] = b.z; x[j][7] = b.w;
+        } else {
+          const uint4 w = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(q) + o));
+          const float2 p0 = bf16x2_to_float2(w.x), p1 = bf16x2_to_float2(w.y);
+          const float2 p2 = bf16x2_to_float2(w.z), p3 = bf16x2_to_float2(w.w);
+          x[j][0] = p0.x; x[j][1] = p0.y; x[j][2] = p1.x; x[j][3] = p1.y;
+          x[j][4] = p2.x; x[j][5] = p2.y; x[j][6] = p3.x; x[j][7] = p3.y;
+        }
+      }
+    }
+    float ss = 0.f;
+    if (do_normalize) {
+#pragma unroll
+      for (int j = 0; j < CPL; ++j)
+#pragma unroll
+        for (int t = 0; t < 8; ++t) ss = fmaf(x[j][t], x[j][t], ss);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    }
+    const float scale = (do_normalize && ss > 0.f) ? rsqrtf(ss) : 1.f;
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) {
+      const int ch = lane + 32 * j;
+      if (ch < chunks) {
+        uint4 w;
+        w.x = pack_bf16x2(x[j][0] * scale, x[j][1] * scale);
+        w.y = pack_bf16x2(x[j][2] * scale, x[j][3] * scale);
+        w.z = pack_bf16x2(x[j][4] * scale, x[j][5] * scale);
+        w.w = pack_bf16x2(x[j][6] * scale, x[j][7] * scale);
+        out[ch] = w;
+      }
+    }
+  }
+  __syncthreads();
+  stamp(2);
+  float2 qf[QG][CPL][4];
+#pragma unroll
+  for (int qi = 0; qi < QG; ++qi)
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) {
+      const int ch = lane + 32 * j;
+      const uint4 w = ch < chunks ? reinterpret_cast<const uint4*>(qv + qi * dim)[ch]
+                                  : make_uint4(0, 0, 0, 0);
+      qf[qi][j][0] = bf16x2_to_float2(w.x);
+      qf[qi][j][1] = bf16x2_to_float2(w.y);
+      qf[qi][j][2] = bf16x2_to_float2(w.z);
+      qf[qi][j][3] = bf16x2_to_float2(w.w);
+    }
+  const int my_q = lane >> (5 - kLog);
+  const bool owner = (lane & ((1 << (5 - kLog)) - 1)) == 0;
+  if (resident) {
+    cp_async_wait<0>();
+    __syncwarp();
+    // two rows per step: their dot products and butterflies are independent (ILP)
+    int j = 0;
+    for (; j + 1 < nrow; j += 2) {
+      float2 a0[QG], a1[QG];
+      small_row_dot<QG, CPL>(reinterpret_cast<const uint4*>(my_ring + static_cast<size_t>(j) * row_bytes),
+                             lane, chunks, qf, a0);
+      small_row_dot<QG, CPL>(reinterpret_cast<const uint4*>(my_ring + static_cast<size_t>(j + 1) * row_bytes),
+                             lane, chunks, qf, a1);
+      float v0[QG], v1[QG];
+#pragma unroll
+      for (int qi = 0; qi < QG; ++qi) {
+        v0[qi] = a0[qi].x + a0[qi].y;
+        v1[qi] = a1[qi].x + a1[qi].y;
+      }
+      const float s0 = transpose_reduce<QG>(v0, lane);
+      const float s1 = transpose_reduce<QG>(v1, lane);
+      if (owner) {
+        sc[my_q * per + warp + kSmallWarps * j] = s0;
+        sc[my_q * per + warp + kSmallWarps * (j + 1)] = s1;
+      }
+    }
+    if (j < nrow) {
+      float2 a0[QG];
+      small_row_dot<QG, CPL>(reinterpret_cast<const uint4*>(my_ring + static_cast<size_t>(j) * row_bytes),
+                             lane, chunks, qf, a0);
+      float v0[QG];
+#pragma unroll
+      for (int qi = 0; qi < QG; ++qi) v0[qi] = a0[qi].x + a0[qi].y;
+      const float s0 = transpose_reduce<QG>(v0, lane);
+      if (owner) sc[my_q * per + warp + kSmallWarps * j] = s0;
+    }
+  } else {
+    int slot = 0;
+    for (int j = 0; j < nrow; ++j) {
+      cp_async_wait<kSmallSlots - 1>();
+      __syncwarp();
+      float2 acc[QG];
+      small_row_dot<QG, CPL>(reinterpret_cast<const uint4*>(my_ring + static_cast<size_t>(slot) * row_bytes),
+                             lane, chunks, qf, acc);
+      __syncwarp();  // every lane done reading the slot before it is refilled
+      issue(j + kSmallSlots, slot);
+      cp_async_commit();
+      if (++slot == kSmallSlots) slot = 0;
+      float v[QG];
+#pragma unroll
+      for (int qi = 0; qi < QG; ++qi) v[qi] = acc[qi].x + acc[qi].y;
+      const float score = transpose_reduce<QG>(v, lane);
+      if (owner) sc[my_q * per + warp + kSmallWarps * j] = score;
+    }
+    cp_async_wait<0>();
+  }
+  __syncthreads();
+  stamp(3);
+  // block top-k per query (one warp per query: lane-local lists over the block's scores, then
+  // k rounds of a warp max; (score, id) keys are unique, ties go to the smaller id) ->
+  // scratch [groups][QG][nblk][k] (a query's lists contiguous for the final merge)
+  const uint64_t pad = pad_key();
+  for (int qi = warp; qi < nq; qi += kSmallWarps) {
+    uint64_t l[KC];
+#pragma unroll
+    for (int i = 0; i < KC; ++i) l[i] = pad;
+    for (int c = lane; c < nr; c += 32) {
+      const uint64_t key = make_key(sc[qi * per + c], static_cast<int32_t>(r0 + c) + id_offset);
+      if (key > l[KC - 1]) key_list_insert<KC>(l, key);
+    }
+    uint64_t* part = part_keys + ((static_cast<int64_t>(g) * QG + qi) * nblk + blockIdx.x) * k;
+    for (int r = 0; r < k; ++r) {
+      uint64_t m = l[0];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t x = __shfl_xor_sync(0xffffffffu, m, o);
+        m = x > m ? x : m;
+      }
+      if (lane == 0) part[r] = m;
+      if (l[0] == m && m != pad) {  // exactly one lane pops its head
+#pragma unroll
+        for (int i = 0; i < KC - 1; ++i) l[i] = l[i + 1];
+        l[KC - 1] = pad;
+      }
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  stamp(4);
+  if (tid == 0) last = atomicAdd(arrive + g, 1) == nblk - 1;
+  __syncthreads();
+  stamp(5);
+  if (!last) return;
+  __threadfence();
+  // last block of the group: one warp per query takes the top k of the row blocks' nblk * k
+  // keys (contiguous: coalesced loads, all issued before any compare)
+  for (int qi = warp; qi < nq; qi += kSmallWarps) {
+    const uint64_t* src = part_keys + (static_cast<int64_t>(g) * QG + qi) * nblk * k;
+    const int total = nblk * k;
+    uint64_t* sel = sel_s[warp];
+    if (total <= 32 * 16) {
+      uint64_t v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int e = lane + 32 * u;
+        v[u] = e < total ? static_cast<uint64_t>(__ldcg(reinterpret_cast<const unsigned long long*>(src + e)))
+                         : pad;
+      }
+      warp_select_rounds<16>(v, k, sel, lane);
+    } else {  // (many row blocks) lane-local lists first
+      uint64_t l[KC];
+#pragma unroll
+      for (int i = 0; i < KC; ++i) l[i] = pad;
+      for (int e = lane; e < total; e += 32) {
+        const uint64_t key = static_cast<uint64_t>(__ldcg(reinterpret_cast<const unsigned long long*>(src + e)));
+        if (key > l[KC - 1]) key_list_insert<KC>(l, key);
+      }
+      warp_select_rounds<KC>(l, k, sel, lane);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      for (int r = 0; r < k; ++r) {
+        const uint64_t m = sel[r];
+        const int32_t id = m == pad ? -1 : key_id(m);
+        out_s[static_cast<int64_t>(q0 + qi) * k + r] = id < 0 ? -INFINITY : key_score(m);
+        out_i[static_cast<int64_t>(q0 + qi) * k + r] = id;
+      }
+    }
+  }
+  if (tid == 0) arrive[g] = 0;  // ready for the next launch on this scratch
+  __syncthreads();
+  stamp(6);
 }
 
 // One warp per row: optional L2 normalisation (fp32 math) and cast to bf16.
@@ -1513,6 +1887,50 @@ int launch_search_rerank_seg(const void* arena, int64_t nrows, int dim, int tile
   return TSV_SEG_T(8);
 #undef TSV_SEG_T
 #undef TSV_SEG
+}
+
+int small_scan_qg(int dim) { return dim <= 256 ? 16 : (dim <= 512 ? 8 : 4); }
+
+template <int QG, int CPL, int KC, bool kTiled>
+int launch_small_scan_v(const void* arena, int dim, const void* q, int q_is_f32, int do_normalize,
+                        int B, int64_t row_beg, int64_t row_end, int32_t id_offset, int k,
+                        int nblk, uint64_t* part_keys, int32_t* arrive, float* out_s,
+                        int32_t* out_i, cudaStream_t stream, unsigned long long* trace) {
+  const int64_t n = row_end - row_beg;
+  const int64_t per = (n + nblk - 1) / nblk;
+  const size_t fixed = static_cast<size_t>(QG) * dim * 2 + static_cast<size_t>(QG) * per * 4;
+  const int64_t rows_per_warp = (per + kSmallWarps - 1) / kSmallWarps;
+  // every row of the block resident in shared memory when it fits (one load round trip)
+  const size_t res_bytes = static_cast<size_t>(kSmallWarps) * rows_per_warp * dim * 2 + fixed;
+  const int resident = res_bytes <= 200 * 1024 && !getenv("TSV_SMALL_RING") ? 1 : 0;
+  const size_t smem = resident ? res_bytes
+                               : static_cast<size_t>(kSmallWarps) * kSmallSlots * dim * 2 + fixed;
+  if (smem > 200 * 1024) return static_cast<int>(cudaErrorInvalidValue);
+  auto kern = small_scan_kernel<QG, CPL, KC, kTiled>;
+  static std::atomic<uint64_t> configured{0};
+  if (first_on_device(configured)) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return static_cast<int>(e);
+  }
+  const int groups = (B + QG - 1) / QG;
+  return launch_pdl(kern, dim3(nblk, groups), dim3(kSmallWarps * 32), smem, stream,
+                    reinterpret_cast<const __nv_bfloat16*>(arena), dim, q, q_is_f32, do_normalize,
+                    B, row_beg, row_end, id_offset, k, resident, part_keys, arrive, out_s, out_i,
+                    trace);
+}
+
+int launch_small_scan(const void* arena, int dim, int tiled, const void* q, int q_is_f32,
+                      int do_normalize, int B, int64_t row_beg, int64_t row_end, int32_t id_offset,
+                      int k, int nblk, uint64_t* part_keys, int32_t* arrive, float* out_s,
+                      int32_t* out_i, cudaStream_t stream, unsigned long long* trace) {
+  if (dim % 8 != 0 || dim > 1024 || k > 16) return static_cast<int>(cudaErrorInvalidValue);
+#define TSV_SMALL(QG, CPL, KC, T) launch_small_scan_v<QG, CPL, KC, T>(arena, dim, q, q_is_f32, do_normalize, B, row_beg, row_end, id_offset, k, nblk, part_keys, arrive, out_s, out_i, stream, trace)
+#define TSV_SMALL_K(QG, CPL, T) (k <= 8 ? TSV_SMALL(QG, CPL, 8, T) : TSV_SMALL(QG, CPL, 16, T))
+#define TSV_SMALL_D(T) (dim <= 256 ? TSV_SMALL_K(16, 1, T) : (dim <= 512 ? TSV_SMALL_K(8, 2, T) : TSV_SMALL_K(4, 4, T)))
+  return tiled ? TSV_SMALL_D(true) : TSV_SMALL_D(false);
+#undef TSV_SMALL_D
+#undef TSV_SMALL_K
+#undef TSV_SMALL
 }
 
 // Pipelined gather (bf16 arenas, dim <= 2048): cp.async rings of `slots` rows per warp (2 by

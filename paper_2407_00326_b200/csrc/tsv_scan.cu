@@ -18,6 +18,7 @@
 #include "tsv_kernels.cuh"
 #include "tsv_ptx.cuh"
 
+#include <cuda_bf16.h>
 #include <cfloat>
 #include <cstdlib>
 #include <utility>
@@ -1098,6 +1099,384 @@ int dispatch_pair(int kcap, const CUtensorMap& tq, const CUtensorMap& tc, const 
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// K2t: a latency-bound search (few queries, a short row range) in ONE launch on the tensor
+// cores (BASELINE C1: 16 queries over a 10k x 384 corpus; reference: the naive-RAG Searching
+// primitive, optimizer.py:178-198). The general scan puts queries on the UMMA M side and pays
+// normalise + scan + merge launches and a per-item pipeline start for a 40-tile corpus (27 us).
+// Here each CTA owns one 128-row tile with the rows on M and every query on N:
+//  * TMA streams the tile's k-blocks (128 rows x 64 elements, SWIZZLE_128B: the arena's own
+//    tensor map) into a ring while the four warps L2-normalise the queries (K5's arithmetic,
+//    chunk-order sums) straight into the B operand in the canonical K-major SWIZZLE_128B
+//    layout (16-byte chunk c of query r at chunk c ^ (r & 7) of its 128-byte row);
+//  * one elected thread issues D[128 x NQ] += A[128 x 16] * B[NQ x 16]^T per k-step
+//    (tcgen05.mma kind::f16, fp32 accumulators in TMEM, NQ columns);
+//  * each thread tcgen05.ld's its row's NQ query scores, parks them in shared memory as
+//    [query][row], and one warp per query takes the tile's top k (lane-local key lists, k
+//    rounds of a warp max; (score, id) keys are unique, ties go to the smaller id);
+//  * the last CTA to finish (arrival counter, self-resetting) merges the tiles' lists.
+constexpr int kTinyRows = 128;
+constexpr int kTinyThreads = 256;  // warps 0-3: TMEM lanes 0-127 (epilogue); all 8 stage / select
+
+__device__ __forceinline__ uint64_t tk_key(float s, int32_t id) {
+  uint32_t u = __float_as_uint(s);
+  u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+  return (static_cast<uint64_t>(u) << 32) | static_cast<uint32_t>(~static_cast<uint32_t>(id));
+}
+__device__ __forceinline__ float tk_score(uint64_t k) {
+  uint32_t u = static_cast<uint32_t>(k >> 32);
+  u = (u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u;
+  return __uint_as_float(u);
+}
+__device__ __forceinline__ int32_t tk_id(uint64_t k) {
+  return static_cast<int32_t>(~static_cast<uint32_t>(k & 0xFFFFFFFFu));
+}
+__device__ __forceinline__ uint64_t tk_pad() { return tk_key(-INFINITY, -1); }
+// Two independent top-k selections interleaved (v[0, N): first set, v[N, 2N): second set):
+// k rounds of (lane-local max below the previous round's key, warp max via shuffles).
+template <int N>
+__device__ __forceinline__ void tk_select2(const uint64_t (&v)[2 * N], int k, uint64_t* out0,
+                                           uint64_t* out1, int lane) {
+  const uint64_t pad = tk_pad();
+  uint64_t p0 = ~0ull, p1 = ~0ull;
+  for (int r = 0; r < k; ++r) {
+    uint64_t b0 = pad, b1 = pad;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      b0 = (v[i] < p0 && v[i] > b0) ? v[i] : b0;
+      b1 = (v[N + i] < p1 && v[N + i] > b1) ? v[N + i] : b1;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t y0 = __shfl_xor_sync(0xffffffffu, b0, o);
+      const uint64_t y1 = __shfl_xor_sync(0xffffffffu, b1, o);
+      b0 = y0 > b0 ? y0 : b0;
+      b1 = y1 > b1 ? y1 : b1;
+    }
+    if (lane == 0) out0[r] = b0;
+    if (lane == 1 && out1 != nullptr) out1[r] = b1;
+    p0 = b0;
+    p1 = b1;
+  }
+}
+__device__ __forceinline__ uint32_t tk_pack(float a, float b) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+// 8 consecutive elements (index o) of the raw query matrix staged in shared memory, as fp32
+__device__ __forceinline__ void tk_load8s(const uint8_t* qraw, int q_is_f32, int64_t o, float (&x)[8]) {
+  if (q_is_f32) {
+    const float4 a = *reinterpret_cast<const float4*>(qraw + o * 4);
+    const float4 b = *reinterpret_cast<const float4*>(qraw + o * 4 + 16);
+    x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+    x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+  } else {
+    const uint4 w = *reinterpret_cast<const uint4*>(qraw + o * 2);
+    const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      x[2 * t] = __uint_as_float(ww[t] << 16);
+      x[2 * t + 1] = __uint_as_float(ww[t] & 0xFFFF0000u);
+    }
+  }
+}
+
+template <int NQ>
+__global__ void __launch_bounds__(kTinyThreads, 1) tiny_scan_kernel(
+    const __grid_constant__ CUtensorMap tmap_c, const void* __restrict__ q, int q_is_f32,
+    int do_normalize, int B, int dim, int64_t row_beg, int64_t row_end, int32_t id_offset, int k,
+    int stages, int tiled, uint64_t* __restrict__ part_keys, int32_t* __restrict__ arrive,
+    float* __restrict__ out_s, int32_t* __restrict__ out_i, unsigned long long* __restrict__ trace) {
+  // (trace: development timestamps per CTA and phase, TSV_SMALL_TRACE; null in production)
+  auto stamp = [&](int ph) {
+    if (trace != nullptr && threadIdx.x == 0) trace[blockIdx.x * 8 + ph] = global_ns();
+  };
+  stamp(0);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  const int num_kb = (dim + kBlockK - 1) / kBlockK;
+  constexpr int kABytes = kTinyRows * 128;           // one k-block of the row tile
+  constexpr int kBkb = NQ * 128;                     // one k-block of the queries
+  uint8_t* ring = smem;                              // [stages][16 KB]
+  uint8_t* qtile = ring + static_cast<size_t>(stages) * kABytes;  // [num_kb][NQ x 128 B]
+  float* sc = reinterpret_cast<float*>(qtile + static_cast<size_t>(num_kb) * kBkb);  // [NQ][128]
+  uint8_t* qraw = reinterpret_cast<uint8_t*>(sc + NQ * kTinyRows);  // [B][dim] as given
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(
+      qraw + ((static_cast<size_t>(B) * dim * (q_is_f32 ? 4 : 2) + 15) & ~static_cast<size_t>(15)));
+  uint64_t* empty_bar = full_bar + stages;
+  uint64_t* acc_bar = empty_bar + stages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_bar + 1);
+  __shared__ int last_s;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t row0 = row_beg + static_cast<int64_t>(blockIdx.x) * kTinyRows;
+  const int nvalid = static_cast<int>(min(static_cast<int64_t>(kTinyRows), row_end - row0));
+  constexpr uint32_t kTmemCols = NQ < 32 ? 32 : NQ;
+  if (tid == 0) {
+    ptx::tma_prefetch_desc(&tmap_c);
+    for (int s_ = 0; s_ < stages; ++s_) {
+      ptx::mbar_init(&full_bar[s_], 1);
+      ptx::mbar_init(&empty_bar[s_], 1);
+    }
+    ptx::mbar_init(acc_bar, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) {
+    ptx::tmem_alloc(tmem_slot, kTmemCols);
+    ptx::tmem_relinquish();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // the queries (and rows) may be the previous kernel's output
+  stamp(1);
+  const uint64_t pol = ptx::policy_evict_normal();
+  // k-block kb of the tile: a 2-D box of the row-major arena, or (tiled arena, row0 a multiple
+  // of 128) the contiguous [128 x 64] block ((row0 / 128) * num_kb + kb): the same operand bytes,
+  // so both layouts give bit-identical scores
+  auto load_kb = [&](int kb, int slot) {  // whole warp; one elected lane issues
+    ptx::mbar_arrive_expect_tx_warp(&full_bar[slot], kABytes);
+    if (tiled)
+      ptx::tma_load_3d_warp(ring + slot * kABytes, &tmap_c, &full_bar[slot], 0, 0,
+                            static_cast<int32_t>((row0 >> 7) * num_kb + kb), pol);
+    else
+      ptx::tma_load_2d_warp(ring + slot * kABytes, &tmap_c, &full_bar[slot], kb * kBlockK,
+                            static_cast<int32_t>(row0), pol);
+  };
+  if (warp == 0)  // first ring-full of k-blocks in flight before the queries are staged
+    for (int kb = 0; kb < min(stages, num_kb); ++kb) load_kb(kb, kb);
+  // raw queries -> shared memory in one round trip (cp.async, all threads), then normalised
+  // (K5's arithmetic, chunk-order sums) into the B operand: query r, 16-byte chunk ch
+  // (elements 8 ch ..) goes to k-block ch / 8, chunk position (ch % 8) ^ (r % 8) of row r;
+  // 8-row atoms 1024 B apart; padding queries are zero
+  const int chunks = dim >> 3;
+  const int esz = q_is_f32 ? 4 : 2;
+  const int raw_chunks = B * dim * esz / 16;  // 16-byte chunks of the raw query matrix
+  for (int c = tid; c < raw_chunks; c += kTinyThreads) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(qraw + c * 16));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d),
+                 "l"(reinterpret_cast<const uint8_t*>(q) + static_cast<int64_t>(c) * 16)
+                 : "memory");
+  }
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  for (int r = warp; r < NQ; r += kTinyThreads / 32) {
+    float ss = 0.f;
+    if (r < B && do_normalize) {
+      for (int ch = lane; ch < chunks; ch += 32) {
+        float x[8];
+        tk_load8s(qraw, q_is_f32, static_cast<int64_t>(r) * dim + ch * 8, x);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) ss = fmaf(x[t], x[t], ss);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    }
+    const float scale = (do_normalize && ss > 0.f) ? rsqrtf(ss) : 1.f;
+    for (int ch = lane; ch < num_kb * 8; ch += 32) {
+      uint4 w = make_uint4(0, 0, 0, 0);
+      if (r < B && ch < chunks) {
+        float x[8];
+        tk_load8s(qraw, q_is_f32, static_cast<int64_t>(r) * dim + ch * 8, x);
+        w.x = tk_pack(x[0] * scale, x[1] * scale);
+        w.y = tk_pack(x[2] * scale, x[3] * scale);
+        w.z = tk_pack(x[4] * scale, x[5] * scale);
+        w.w = tk_pack(x[6] * scale, x[7] * scale);
+      }
+      const int kb = ch >> 3, c = ch & 7;
+      *reinterpret_cast<uint4*>(qtile + kb * kBkb + (r >> 3) * 1024 + (r & 7) * 128 +
+                                ((c ^ (r & 7)) << 4)) = w;
+    }
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> UMMA reads
+  __syncthreads();
+  stamp(2);
+  if (warp == 0) {
+    // producer: the rest of the k-blocks through the ring
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int kb = 0; kb < num_kb; ++kb) {
+      if (kb >= stages) {
+        ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+        load_kb(kb, stage);
+      }
+      if (++stage == stages) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+  } else if (warp == 1) {
+    // MMA issuer (warp-uniform loop, one elected lane issues)
+    constexpr uint32_t idesc = ptx::idesc_bf16_f32(kTinyRows, NQ);
+    const uint64_t adesc0 = ptx::umma_desc_sw128(ptx::smem_u32(ring));
+    const uint64_t bdesc0 = ptx::umma_desc_sw128(ptx::smem_u32(qtile));
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int kb = 0; kb < num_kb; ++kb) {
+      ptx::mbar_wait(&full_bar[stage], phase);
+      ptx::tc_fence_after();
+      const uint64_t ad = adesc0 + static_cast<uint64_t>((stage * kABytes) >> 4);
+      const uint64_t bd = bdesc0 + static_cast<uint64_t>((kb * kBkb) >> 4);
+#pragma unroll
+      for (int kk = 0; kk < kBlockK / 16; ++kk)
+        ptx::mma_f16_ss_warp(tmem_base, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0 ? 1u : 0u);
+      ptx::mma_commit_warp(&empty_bar[stage]);
+      if (++stage == stages) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+    ptx::mma_commit_warp(acc_bar);
+  }
+  // epilogue: thread = row (TMEM lane), NQ query scores -> shared memory [query][row]
+  if (warp < 4) {
+    ptx::mbar_wait(acc_bar, 0);
+    ptx::tc_fence_after();
+    const uint32_t taddr = tmem_base + (static_cast<uint32_t>(warp * 32) << 16);
+    const int row = warp * 32 + lane;
+#pragma unroll
+    for (int c = 0; c < NQ; c += 32) {
+      uint32_t v[32];
+      ptx::tmem_ld_32x32b_x32(taddr + c, v);
+      ptx::tmem_ld_wait();
+      ptx::tmem_regs_ready(v);
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (c + j < NQ) sc[(c + j) * kTinyRows + row] = __uint_as_float(v[j]);
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  stamp(3);
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem_base, kTmemCols);
+  }
+  // the tile's top k per query -> scratch [query][tile][k]
+  const uint64_t pad = tk_pad();
+  const int nblk = gridDim.x;
+  for (int qa = warp; qa < B; qa += 2 * (kTinyThreads / 32)) {
+    const int qb = qa + kTinyThreads / 32;
+    uint64_t v[2 * (kTinyRows / 32)];  // two queries' rows, one chain each in tk_select2
+#pragma unroll
+    for (int u = 0; u < kTinyRows / 32; ++u) {
+      const int r = lane + 32 * u;
+      const int32_t id = static_cast<int32_t>(row0 + r) + id_offset;
+      v[u] = r < nvalid ? tk_key(sc[qa * kTinyRows + r], id) : pad;
+      v[kTinyRows / 32 + u] = (r < nvalid && qb < B) ? tk_key(sc[qb * kTinyRows + r], id) : pad;
+    }
+    tk_select2<kTinyRows / 32>(v, k, part_keys + (static_cast<int64_t>(qa) * nblk + blockIdx.x) * k,
+                               qb < B ? part_keys + (static_cast<int64_t>(qb) * nblk + blockIdx.x) * k
+                                      : nullptr,
+                               lane);
+  }
+  stamp(4);
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last_s = atomicAdd(arrive, 1) == nblk - 1;
+  __syncthreads();
+  stamp(5);
+  if (!last_s) return;
+  __threadfence();
+  // last CTA: one warp per query. Every tile's list is sorted, and tile t alone holds k keys
+  // >= its k-th key, so the global k-th key is >= tau = max_t (k-th key of tile t): only keys
+  // >= tau can be in the result. One warp max finds tau, a ballot compacts the survivors
+  // (usually a few more than k) into shared memory, and each survivor's output position is
+  // the number of survivors above it. (More than 64 survivors: k rounds of a warp max.)
+  // every tile's lists of every query -> shared memory with 16-byte async copies (one L2 round
+  // trip; the ring is free now), then everything below reads shared memory
+  const int total = nblk * k;   // <= 512 keys per query (checked on the host)
+  const int all_n = B * total;  // <= 64 x 512 keys: fits the ring (checked on the host)
+  uint64_t* allk = reinterpret_cast<uint64_t*>(ring);
+#pragma unroll 1
+  for (int e = 2 * tid; e < all_n; e += 2 * kTinyThreads) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(allk + e));
+    if (e + 1 < all_n)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(part_keys + e) : "memory");
+    else
+      allk[e] = static_cast<uint64_t>(__ldcg(reinterpret_cast<const unsigned long long*>(part_keys + e)));
+  }
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  stamp(6);
+  // one warp per two queries (interleaved: two independent dependency chains): k rounds of
+  // (lane-local max below the previous round's key, warp max) over the keys in shared memory
+  constexpr int kW = kTinyThreads / 32;
+#pragma unroll 1
+  for (int q0 = warp; q0 < B; q0 += 2 * kW) {
+    const int q1 = q0 + kW < B ? q0 + kW : q0;  // (odd count: the second chain repeats q0)
+    const uint64_t* s0 = allk + static_cast<int64_t>(q0) * total;
+    const uint64_t* s1 = allk + static_cast<int64_t>(q1) * total;
+    uint64_t p0 = ~0ull, p1 = ~0ull;
+#pragma unroll 1
+    for (int r = 0; r < k; ++r) {
+      uint64_t b0 = pad, b1 = pad;
+#pragma unroll 4
+      for (int e = lane; e < total; e += 32) {
+        const uint64_t x0 = s0[e], x1 = s1[e];
+        b0 = (x0 < p0 && x0 > b0) ? x0 : b0;
+        b1 = (x1 < p1 && x1 > b1) ? x1 : b1;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t y0 = __shfl_xor_sync(0xffffffffu, b0, o);
+        const uint64_t y1 = __shfl_xor_sync(0xffffffffu, b1, o);
+        b0 = y0 > b0 ? y0 : b0;
+        b1 = y1 > b1 ? y1 : b1;
+      }
+      if (lane == 0) {
+        out_s[static_cast<int64_t>(q0) * k + r] = b0 == pad ? -INFINITY : tk_score(b0);
+        out_i[static_cast<int64_t>(q0) * k + r] = b0 == pad ? -1 : tk_id(b0);
+      } else if (lane == 1) {
+        out_s[static_cast<int64_t>(q1) * k + r] = b1 == pad ? -INFINITY : tk_score(b1);
+        out_i[static_cast<int64_t>(q1) * k + r] = b1 == pad ? -1 : tk_id(b1);
+      }
+      p0 = b0;
+      p1 = b1;
+    }
+  }
+  if (tid == 0) *arrive = 0;  // ready for the next launch on this scratch
+  __syncthreads();
+  stamp(7);
+}
+
+template <int NQ>
+int launch_tiny_v(const CUtensorMap& tmap_c, const void* q, int q_is_f32, int do_normalize,
+                  int B, int dim, int64_t row_beg, int64_t row_end, int32_t id_offset, int k,
+                  uint64_t* part_keys, int32_t* arrive, float* out_s, int32_t* out_i,
+                  cudaStream_t stream, unsigned long long* trace, int tiled) {
+  const int num_kb = (dim + kBlockK - 1) / kBlockK;
+  const int stages = num_kb < 6 ? num_kb : 6;
+  const size_t qraw = (static_cast<size_t>(B) * dim * (q_is_f32 ? 4 : 2) + 15) & ~size_t(15);
+  const size_t smem = 1024 + static_cast<size_t>(stages) * kTinyRows * 128 +
+                      static_cast<size_t>(num_kb) * NQ * 128 + NQ * kTinyRows * 4 + qraw +
+                      (2 * stages + 2) * 8 + 16;
+  const int64_t tiles = (row_end - row_beg + kTinyRows - 1) / kTinyRows;
+  if (smem > 200 * 1024 || tiles * k > 512) return static_cast<int>(cudaErrorInvalidValue);
+  auto kern = tiny_scan_kernel<NQ>;
+  static std::atomic<uint64_t> configured{0};
+  if (first_on_device(configured)) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         200 * 1024);
+    if (e != cudaSuccess) return static_cast<int>(e);
+  }
+  const int nblk = static_cast<int>((row_end - row_beg + kTinyRows - 1) / kTinyRows);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nblk);
+  cfg.blockDim = dim3(kTinyThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return static_cast<int>(cudaLaunchKernelEx(&cfg, kern, tmap_c, q, q_is_f32, do_normalize, B,
+                                             dim, row_beg, row_end, id_offset, k, stages, tiled,
+                                             part_keys, arrive, out_s, out_i, trace));
+}
+
 }  // namespace
 
 int dispatch_tf32(int kcap, const CUtensorMap& tq, const CUtensorMap& tc, const CUtensorMap& tq_lo,
@@ -1126,6 +1505,21 @@ int launch_scan_topk_tf32(int kcap, const CUtensorMap& tmap_q, const CUtensorMap
                           const ScanParams& p, int grid, cudaStream_t stream) {
   if (grid <= 0) return 0;
   return dispatch_tf32(kcap, tmap_q, tmap_c, tmap_q_lo, tmap_c_lo, p, grid, stream);
+}
+
+int tiny_scan_blocks(int64_t n) { return static_cast<int>((n + kTinyRows - 1) / kTinyRows); }
+
+int launch_tiny_scan(const CUtensorMap& tmap_c, const void* q, int q_is_f32, int do_normalize,
+                     int B, int dim, int64_t row_beg, int64_t row_end, int32_t id_offset, int k,
+                     uint64_t* part_keys, int32_t* arrive, float* out_s, int32_t* out_i,
+                     cudaStream_t stream, unsigned long long* trace, int tiled) {
+  if (B <= 0 || B > 64 || k > 16 || dim % 8 != 0 || (tiled && row_beg % kTinyRows != 0))
+    return static_cast<int>(cudaErrorInvalidValue);
+#define TSV_TINY(NQ) launch_tiny_v<NQ>(tmap_c, q, q_is_f32, do_normalize, B, dim, row_beg, row_end, id_offset, k, part_keys, arrive, out_s, out_i, stream, trace, tiled)
+  if (B <= 16) return TSV_TINY(16);
+  if (B <= 32) return TSV_TINY(32);
+  return TSV_TINY(64);
+#undef TSV_TINY
 }
 
 int launch_scan_topk(int mb, int kcap, const CUtensorMap& tmap_q, const CUtensorMap& tmap_c,

@@ -51,6 +51,15 @@ def main():
     for B, k in ((1024, 100), (1024, 10), (2048, 10), (200, 64)):
         big.search(normalize_rows(torch.randn((B, 128), generator=g, device=dev)), k)
     idx.search_segmented(q, [0, 10, 25, 40], [(0, 48), (48, 3000), (3000, 9000)], 64)
+    # one-launch searches: K2t (tcgen05, row-major) and K2s (CUDA cores, tiled); fused C5 chain
+    c1 = DeviceIndex(384, 10_000, metric="cosine", device=0)
+    c1.append(torch.randn((10_000, 384), generator=g, device=dev))
+    c1.search(torch.randn((16, 384), generator=g, device=dev), 5)
+    c1t = DeviceIndex(256, 3000, metric="ip", device=0, storage="bf16_tiled")
+    c1t.append(torch.randn((3000, 256), generator=g, device=dev))
+    c1t.search(torch.randn((40, 256), generator=g, device=dev), 12)
+    rows = torch.tensor([[0, 48], [48, 96], [96, 103], [200, 1224]], dtype=torch.int64, device=dev)
+    c1.search_rerank_segmented(torch.randn((4, 384), generator=g, device=dev), rows, 1024, 32, 3)
     f32 = DeviceIndex(64, 5000, metric="ip", device=0, storage="f32")
     f32.append(torch.randn((5000, 64), generator=g, device=dev))
     f32.search(torch.randn((20, 64), generator=g, device=dev), 10)

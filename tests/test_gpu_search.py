@@ -883,3 +883,52 @@ def test_search_rerank_segmented_fused(cuda, storage, metric, dim, k_s, k_r, sep
                 real = hi[b] >= 0
                 assert real.sum() == min(z, k_r)
                 assert set((hi[b][real] - off).tolist()) <= set(cand[0][cand[0] >= 0].tolist())
+
+
+@pytest.mark.parametrize("n,dim,b,k,metric,storage,f32q", [
+    (10000, 384, 16, 5, "cosine", "bf16", False),    # C1
+    (10000, 384, 16, 5, "cosine", "bf16", True),
+    (4097, 256, 40, 16, "ip", "bf16", False), (65536, 128, 3, 10, "cosine", "bf16", False),
+    (7, 64, 5, 10, "ip", "bf16", False), (1, 1024, 64, 1, "cosine", "bf16", False),
+    (3000, 1024, 17, 8, "ip", "bf16_tiled", False), (2500, 520, 9, 12, "cosine", "bf16", True),
+    (8000, 768, 12, 16, "ip", "bf16", False)])
+def test_small_scan_matches_oracle_and_tensor_path(cuda, n, dim, b, k, metric, storage, f32q,
+                                                  monkeypatch):
+    """One-launch searches for few queries over short row ranges (routed automatically: K2t on
+    the tensor cores for row-major arenas, K2s on the CUDA cores for tiled ones or with
+    TSV_NO_TINY) vs the CPU oracle and vs the general scan (TSV_NO_SMALL=1) on the same
+    inputs: query groups of 16 / 8 / 4 by dim, k <= 16, fp32 and bf16 queries, cosine and
+    inner product, row-major and tiled arenas, a row sub-range with an id offset, fewer rows
+    than k."""
+    import torch
+
+    from paper_2407_00326_b200 import _native
+    from paper_2407_00326_b200.index import DeviceIndex
+
+    c = orc.make_corpus(n, dim, seed=n % 97)
+    q, _ = orc.make_queries(c, b, seed=2)
+    idx = DeviceIndex(dim, n, metric=metric, device=cuda.index, storage=storage)
+    idx.append(to_dev_bf16(c, cuda))
+    qd = torch.from_numpy(q).to(cuda) if f32q else to_dev_bf16(q, cuda)
+    qo = orc.normalize_rows(q) if metric == "cosine" else (q if f32q else orc.bf16_round(q))
+    n0 = _native.launch_count()
+    s, i = idx.search(qd, k)
+    torch.cuda.synchronize()
+    assert _native.launch_count() - n0 == 1  # one launch: no staging, no merge
+    assert_topk(s, i, qo, c, k, TOL)
+    monkeypatch.setenv("TSV_NO_TINY", "1")  # the CUDA-core K2s instead of the tcgen05 K2t
+    s1, i1 = idx.search(qd, k)
+    torch.cuda.synchronize()
+    assert_topk(s1, i1, qo, c, k, TOL)
+    np.testing.assert_allclose(from_dev(s), from_dev(s1), rtol=1e-5, atol=1e-6)
+    monkeypatch.delenv("TSV_NO_TINY")
+    monkeypatch.setenv("TSV_NO_SMALL", "1")
+    s2, i2 = idx.search(qd, k)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(from_dev(s), from_dev(s2), rtol=1e-5, atol=1e-6)
+    # a sub-range of rows with an id offset (row-major arenas; tiled ranges start at 128 k)
+    monkeypatch.delenv("TSV_NO_SMALL")
+    lo = 128 if n > 256 else 0
+    s3, i3 = idx.search(qd, k, row_range=(lo, n), id_offset=1000)
+    torch.cuda.synchronize()
+    assert_topk(s3, i3, qo, c[lo:], k, TOL, id_offset=1000 + lo)  # ids = arena row + offset

@@ -49,8 +49,14 @@ def test_sharded_index_equals_single_index(cuda, n, dim, b, k, parts):
     s1, i1 = sh.search(qd, k)
     s2, i2 = whole.search(qd, k)
     torch.cuda.synchronize()
-    np.testing.assert_array_equal(from_dev(i1), from_dev(i2))
-    np.testing.assert_array_equal(from_dev(s1), from_dev(s2))
+    # a shard may take another kernel than the whole corpus (the one-launch searches serve
+    # short ranges), whose fp32 sums differ in the last bits: scores equal to 1e-5, ids equal
+    # wherever neighbouring scores are further apart
+    g1, g2 = from_dev(s1), from_dev(s2)
+    np.testing.assert_allclose(g1, g2, rtol=1e-5, atol=1e-6)
+    sep = np.abs(np.diff(g2, axis=1, prepend=np.inf)) > 1e-4
+    sep &= np.abs(np.diff(g2, axis=1, append=-np.inf)) > 1e-4
+    assert (from_dev(i1)[sep] == from_dev(i2)[sep]).all()
     sub = np.r_[0:min(b, 8), max(0, b - 8):b]
     assert_topk(from_dev(s1)[sub], from_dev(i1)[sub], q[sub], c, k, TOL)
     sh.close()
