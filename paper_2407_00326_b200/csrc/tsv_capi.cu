@@ -110,10 +110,34 @@ struct WsState {
   bool captured = false;
 };
 
+// The library's own stream-ordered memory pool on the current device, with an unlimited release
+// threshold: memory freed by workspace growth stays mapped and is reused instead of being
+// returned to the OS at every synchronisation point (the default pool's threshold is 0).
+static cudaMemPool_t workspace_pool() {
+  static std::mutex mu;
+  static std::map<int, cudaMemPool_t> pools;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = pools.find(dev);
+  if (it != pools.end()) return it->second;
+  cudaMemPoolProps props = {};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = dev;
+  cudaMemPool_t pool = nullptr;
+  if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) return nullptr;
+  uint64_t keep = ~0ull;
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  pools.emplace(dev, pool);
+  return pool;
+}
+
 // Workspace buffer that grows on demand. Growth is stream-ordered (cudaFreeAsync /
-// cudaMallocAsync on the workspace's stream): no device-wide synchronisation inside a search
-// call, and the old buffer is released only after the work queued before it. Once a graph was
-// captured on the stream, growth is refused instead (the graph would keep the old address).
+// cudaMallocFromPoolAsync on the workspace's stream): no device-wide synchronisation inside a
+// search call, and the old buffer is released only after the work queued before it. Once a
+// graph was captured on the stream, growth is refused instead (the graph would keep the old
+// address).
 template <typename T>
 struct DevBuf {
   T* ptr = nullptr;
@@ -131,8 +155,11 @@ struct DevBuf {
     if (ptr) cudaFreeAsync(ptr, st);
     ptr = nullptr;
     cap = 0;
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ptr),
-                                    std::max<size_t>(n, 1) * sizeof(T), st);
+    cudaMemPool_t pool = workspace_pool();
+    cudaError_t e = pool == nullptr ? cudaErrorMemoryAllocation
+                                    : cudaMallocFromPoolAsync(reinterpret_cast<void**>(&ptr),
+                                                              std::max<size_t>(n, 1) * sizeof(T),
+                                                              pool, st);
     if (e != cudaSuccess) return cuda_fail(e, "workspace cudaMallocAsync");
     cap = n;
     return TSV_OK;
@@ -160,6 +187,8 @@ struct Workspace {
   DevBuf<uint64_t> rr_keys;     // K3 split mode: per-block top-k keys
   DevBuf<int32_t> rr_arrive;    // K3 split mode: per-question arrival counters (kept zero)
   DevBuf<uint64_t> sm_keys;     // K2s: per-row-block top-k keys
+  DevBuf<int64_t> qrows;        // segment kernel: per-query (row_begin, row_end)
+  std::vector<int64_t> host_rows;
   DevBuf<int32_t> sm_arrive;    // K2s: per-query-group arrival counters (kept zero)
   std::vector<tsv::ScanItem> host_items;
   // Pinned staging for the item table so its upload is a true async copy. A ring of slots,
@@ -188,6 +217,7 @@ struct Workspace {
     rr_keys.ws = &state;
     rr_arrive.ws = &state;
     sm_keys.ws = &state;
+    qrows.ws = &state;
     sm_arrive.ws = &state;
   }
   void release() {
@@ -1070,6 +1100,48 @@ int tsv_search(tsv_index* idx, const void* q_dev, int q_dtype, int B, int k, int
                      stream);
 }
 
+// Host table -> device buffer, asynchronously: through a ring of pinned slots (the host waits
+// only when it laps a slot whose copy is still queued), or, under CUDA-graph capture, from a
+// never-reused region of the per-stream capture pool (the captured memcpy node reads its host
+// source at every replay).
+static int upload_table(Workspace& w, const void* host, size_t bytes, void* dev, cudaStream_t st) {
+  cudaStreamCaptureStatus capturing = cudaStreamCaptureStatusNone;
+  TSV_CUDA(cudaStreamIsCapturing(st, &capturing), "cudaStreamIsCapturing");
+  if (capturing != cudaStreamCaptureStatusNone) {
+    const size_t need = (bytes + 255) & ~size_t(255);
+    if (w.capture_pool == nullptr || w.capture_used + need > Workspace::kCapturePoolBytes)
+      return fail(TSV_ERR_CAPACITY,
+                  "segmented search under graph capture: run it once on this stream outside "
+                  "the capture first (pinned pool %s)",
+                  w.capture_pool == nullptr ? "not allocated" : "exhausted");
+    uint8_t* hp = w.capture_pool + w.capture_used;
+    w.capture_used += need;
+    std::memcpy(hp, host, bytes);
+    TSV_CUDA(cudaMemcpyAsync(dev, hp, bytes, cudaMemcpyHostToDevice, st),
+             "table upload (graph capture)");
+    return TSV_OK;
+  }
+  if (w.capture_pool == nullptr)
+    TSV_CUDA(cudaMallocHost(&w.capture_pool, Workspace::kCapturePoolBytes), "cudaMallocHost");
+  Workspace::Pinned& slot = w.pinned[w.pinned_next];
+  w.pinned_next = (w.pinned_next + 1) % Workspace::kPinnedSlots;
+  if (slot.done == nullptr)
+    TSV_CUDA(cudaEventCreateWithFlags(&slot.done, cudaEventDisableTiming), "cudaEventCreate");
+  else
+    TSV_CUDA(cudaEventSynchronize(slot.done), "cudaEventSynchronize");
+  const size_t items = (bytes + sizeof(tsv::ScanItem) - 1) / sizeof(tsv::ScanItem);
+  if (items > slot.cap) {
+    if (slot.ptr) cudaFreeHost(slot.ptr);
+    slot.ptr = nullptr;
+    TSV_CUDA(cudaMallocHost(&slot.ptr, items * 2 * sizeof(tsv::ScanItem)), "cudaMallocHost");
+    slot.cap = items * 2;
+  }
+  std::memcpy(slot.ptr, host, bytes);
+  TSV_CUDA(cudaMemcpyAsync(dev, slot.ptr, bytes, cudaMemcpyHostToDevice, st), "table upload");
+  TSV_CUDA(cudaEventRecord(slot.done, st), "cudaEventRecord");
+  return TSV_OK;
+}
+
 int tsv_search_segmented(tsv_index* idx, const void* q_dev, int q_dtype, int nseg,
                          const int32_t* seg_q_beg, const int64_t* seg_row_beg,
                          const int64_t* seg_row_end, int k, int local_ids, float* scores_dev,
@@ -1096,9 +1168,39 @@ int tsv_search_segmented(tsv_index* idx, const void* q_dev, int q_dtype, int nse
   }
   DeviceGuard g(idx->device);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  // one segment: a plain range search (ids shifted to the segment when local), which routes
+  // short ranges to the one-launch kernels
+  if (nseg == 1 && seg_row_beg[0] <= INT32_MAX)
+    return tsv_search(idx, q_dev, q_dtype, B, k, seg_row_beg[0], seg_row_end[0],
+                      local_ids ? static_cast<int32_t>(-seg_row_beg[0]) : 0, scores_dev, ids_dev,
+                      stream);
   Workspace& w = ws_for(idx, st);
   const bool f32 = idx->storage == TSV_F32;
   const bool tiled = idx->storage == TSV_BF16_TILED;
+  // short segments (<= 1024 rows each, the per-query indexes of a topology-aware batch): one
+  // launch of the segment kernel in search-only mode, a block per query over its own segment
+  if (!f32 && idx->dim <= 2048 && idx->dim % 8 == 0 && max_rows <= tsv::kFusedSegMaxRows &&
+      !env_flag("TSV_NO_SEG_FUSED")) {
+    std::vector<int64_t>& qr = w.host_rows;
+    qr.resize(2 * static_cast<size_t>(B));
+    for (int s_ = 0; s_ < nseg; ++s_)
+      for (int qi = seg_q_beg[s_]; qi < seg_q_beg[s_ + 1]; ++qi) {
+        qr[2 * qi] = seg_row_beg[s_];
+        qr[2 * qi + 1] = seg_row_end[s_];
+      }
+    rc = w.qrows.ensure(qr.size());
+    if (rc) return rc;
+    rc = upload_table(w, qr.data(), qr.size() * sizeof(int64_t), w.qrows.ptr, st);
+    if (rc) return rc;
+    const int mr = static_cast<int>(std::max<int64_t>(max_rows, 1));
+    int e = tsv::launch_search_rerank_seg(idx->arena, idx->rows, idx->dim, tiled, q_dev, nullptr,
+                                          q_dtype == TSV_F32, idx->metric == TSV_METRIC_COSINE,
+                                          w.qrows.ptr, B, mr, k, 0, local_ids, scores_dev, ids_dev,
+                                          nullptr, nullptr, st);
+    if (e) return cuda_fail(static_cast<cudaError_t>(e), "segment search launch");
+    g_launches++;
+    return TSV_OK;
+  }
   for (int s_ = 0; tiled && s_ < nseg; ++s_)
     if (seg_row_beg[s_] % 128 != 0)
       return fail(TSV_ERR_CONFIG, "tiled index: segment %d must start at a multiple of 128", s_);
@@ -1144,44 +1246,8 @@ int tsv_search_segmented(tsv_index* idx, const void* q_dev, int q_dtype, int nse
   }
   rc = w.items.ensure(hi.size());
   if (rc) return rc;
-  cudaStreamCaptureStatus capturing = cudaStreamCaptureStatusNone;
-  TSV_CUDA(cudaStreamIsCapturing(st, &capturing), "cudaStreamIsCapturing");
-  if (capturing != cudaStreamCaptureStatusNone) {
-    // Inside a CUDA-graph capture the upload becomes a memcpy node that reads its host source
-    // at every replay: give it a region of the capture pool that is never reused.
-    const size_t bytes = (hi.size() * sizeof(tsv::ScanItem) + 255) & ~size_t(255);
-    if (w.capture_pool == nullptr || w.capture_used + bytes > Workspace::kCapturePoolBytes)
-      return fail(TSV_ERR_CAPACITY,
-                  "segmented search under graph capture: run it once on this stream outside "
-                  "the capture first (pinned pool %s)",
-                  w.capture_pool == nullptr ? "not allocated" : "exhausted");
-    uint8_t* hp = w.capture_pool + w.capture_used;
-    w.capture_used += bytes;
-    std::memcpy(hp, hi.data(), hi.size() * sizeof(tsv::ScanItem));
-    TSV_CUDA(cudaMemcpyAsync(w.items.ptr, hp, hi.size() * sizeof(tsv::ScanItem),
-                             cudaMemcpyHostToDevice, st),
-             "items upload (graph capture)");
-  } else {
-  if (w.capture_pool == nullptr)
-    TSV_CUDA(cudaMallocHost(&w.capture_pool, Workspace::kCapturePoolBytes), "cudaMallocHost");
-  Workspace::Pinned& slot = w.pinned[w.pinned_next];
-  w.pinned_next = (w.pinned_next + 1) % Workspace::kPinnedSlots;
-  if (slot.done == nullptr)
-    TSV_CUDA(cudaEventCreateWithFlags(&slot.done, cudaEventDisableTiming), "cudaEventCreate");
-  else
-    TSV_CUDA(cudaEventSynchronize(slot.done), "cudaEventSynchronize");
-  if (hi.size() > slot.cap) {
-    if (slot.ptr) cudaFreeHost(slot.ptr);
-    slot.ptr = nullptr;
-    TSV_CUDA(cudaMallocHost(&slot.ptr, hi.size() * 2 * sizeof(tsv::ScanItem)), "cudaMallocHost");
-    slot.cap = hi.size() * 2;
-  }
-  std::memcpy(slot.ptr, hi.data(), hi.size() * sizeof(tsv::ScanItem));
-  TSV_CUDA(cudaMemcpyAsync(w.items.ptr, slot.ptr, hi.size() * sizeof(tsv::ScanItem),
-                           cudaMemcpyHostToDevice, st),
-           "items upload");
-  TSV_CUDA(cudaEventRecord(slot.done, st), "cudaEventRecord");
-  }
+  rc = upload_table(w, hi.data(), hi.size() * sizeof(tsv::ScanItem), w.items.ptr, st);
+  if (rc) return rc;
   tsv::ScanParams p{};
   p.items = w.items.ptr;
   p.num_items = static_cast<int>(hi.size());

@@ -938,6 +938,7 @@ __global__ void __launch_bounds__(kSegWarps * 32) search_rerank_seg_kernel(
     os_i[static_cast<int64_t>(b) * k_s + r] = -1;
   }
   const int m = min(k_s, n);
+  if (k_r <= 0) return;  // search-only mode (a batch of segmented Searching requests)
   __syncthreads();
   // Reranking of those rows against the question
   for (int r = tid; r < m; r += kSegWarps * 32) keys_r[r] = make_key(score_r[sel[r]], id_of(sel[r]));

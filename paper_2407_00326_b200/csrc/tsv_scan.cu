@@ -583,10 +583,14 @@ __global__ void __launch_bounds__(ScanCfg<MB, KCAP, TF32, NB>::kThreads, 1)
             ptx::tmem_ld_32x32b_x32(taddr + kBlockN + c, vb);
             ptx::tmem_ld_32x32b_x32(taddr + 2 * kBlockN + c, vc);
             ptx::tmem_ld_wait();
-            const float odd = p.num_kb > 1 ? 1.f : 0.f;  // odd-k accumulator unused if 1 k-block
+            // With one k-block the odd-k accumulator is never written: its TMEM columns hold
+            // whatever an earlier kernel left there (possibly NaN), so it is skipped by a select,
+            // not multiplied by 0 (0 * NaN = NaN: the first fp32-mode search of a 16..32-dim index
+            // after other tensor-core kernels admitted nothing).
+            const bool has_odd = p.num_kb > 1;
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-              va[j] = __float_as_uint(__uint_as_float(va[j]) + odd * __uint_as_float(vb[j]) +
+              va[j] = __float_as_uint(__uint_as_float(va[j]) + (has_odd ? __uint_as_float(vb[j]) : 0.f) +
                                       __uint_as_float(vc[j]));
             if constexpr (kSmemList)
               scan_chunk_coop<KCAP>(va, list_s, list_i, quad * 32, lane, tau, id0 + c, valid - c,

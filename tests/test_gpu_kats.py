@@ -200,3 +200,28 @@ def test_shard_kat_across_ranks(cuda, exchange):
     for r in range(world):
         np.testing.assert_array_equal(out[r][1], ei)
         np.testing.assert_array_equal(out[r][0], es)
+
+
+def test_fp32_single_kblock_ignores_stale_tmem(cuda):
+    """fp32 mode with one k-block (dim <= 32) never writes its odd-k accumulator; that TMEM
+    holds whatever the previous kernel left. Leave NaN there (a search over a corpus with NaN
+    rows) and the planted KAT must still come out exact (the epilogue selects, not 0 * x)."""
+    import torch
+
+    from paper_2407_00326_b200.index import DeviceIndex
+
+    rng = np.random.default_rng(0)
+    junk = rng.standard_normal((4096, 64)).astype(np.float32)
+    junk[::3] = np.nan
+    bad = DeviceIndex(64, 4096, metric="ip", device=cuda.index)
+    bad.append(torch.from_numpy(junk).to(cuda))
+    for b in (300, 100):  # pair and single-CTA tcgen05 kernels fill TMEM with NaN scores
+        bad.search(torch.from_numpy(junk[:b].copy()).to(cuda), 10)
+    torch.cuda.synchronize()
+    kat = KATS["planted"]
+    c, q = _arrays(kat)
+    idx = _index(c, cuda, "f32")
+    for dtype in (torch.bfloat16, torch.float32):
+        s, i = idx.search(_q(q, cuda, dtype), kat["k"])
+        torch.cuda.synchronize()
+        _assert_exact(s, i, kat)
