@@ -56,9 +56,13 @@ class StreamRuntime(Simulator):
 
     def __init__(self, engines: EngineSet, backend, options: RuntimeOptions | None = None,
                  speed: float = 1.0, poll_us: float = 20.0, timeout_s: float = 60.0,
-                 stream_order: bool = True):
+                 stream_order: bool = True, busy_poll: bool = True):
+        """busy_poll: while device batches are in flight, poll their events without sleeping
+        (an OS sleep of 20 us lasts ~60-80 us, which would add to every device -> host hop);
+        the loop sleeps only when nothing is in flight and the next event is in the future."""
         super().__init__(engines, options, backend=backend)
         self.speed = speed
+        self.busy_poll = busy_poll
         self.poll_s = poll_us * 1e-6
         self.timeout_s = timeout_s
         self.stream_order = stream_order
@@ -174,7 +178,7 @@ class StreamRuntime(Simulator):
             for eid in sorted(self._dirty):
                 self._try_form(eid, t)
             self._dirty.clear()
-            if not progressed:
+            if not progressed and not (self.busy_poll and (self._inflight or self._parked)):
                 nxt = self._events[0][0] if self._events else math.inf
                 wait_s = min(self.poll_s, max(0.0, (nxt - t) / 1000.0 / self.speed))
                 if wait_s > 0:

@@ -30,17 +30,22 @@ def main():
         backend = RetrievalBackend(dim=1024, arena_rows=1 << 16, release_segments=False)
         backend.warmup()
         # time every launch() call on the host (input assembly + library calls)
-        host = []
+        host, launches = [], []
         orig = backend.launch
+        holder = {}
 
         def timed(profile, plan, instance, _orig=orig):
             t0 = time.perf_counter()
+            t_wall = holder["rt"]._wall()
             out = _orig(profile, plan, instance)
             host.append((time.perf_counter() - t0) * 1000)
+            launches.append((t_wall, profile.engine_id, {t.ctx.query_id for t, _ in plan.entries},
+                             {t.node_id for t, _ in plan.entries}, out))
             return out
 
         backend.launch = timed
         rt = StreamRuntime(es, backend, speed=1.0, timeout_s=120)
+        holder["rt"] = rt
         for g, arrival, _ in case["graphs"]:
             rt.submit_query(parse_graph(g), arrival, arrival_ms=arrival)
         rt.run()
@@ -49,29 +54,22 @@ def main():
         done = {}
         for t, q, n in rt.device_done:
             done.setdefault(q, []).append(t)
+        # per query: the retrieval tail after its last Searching input arrived: last search
+        # batch launched -> last rerank batch done on the device, against the device time of
+        # the batches in that window (search stages launched before it are excluded)
         spans, dev = [], []
-        for q in {b_.node_ids[0].split("/")[0] for b_ in gpu} | set(done):
-            pass
-        by_q = {}
-        for b_ in gpu:
-            for nid in b_.node_ids:
-                by_q.setdefault(nid.split("::")[0], []).append(b_)
-        # batches carry node ids; map them to queries through the runtime's contexts
-        q_of = {}
         for ctx in rt.contexts.values():
-            for nid in ctx.graph.nodes:
-                q_of[(ctx.query_id, nid)] = ctx.query_id
-        per_q = {}
-        for b_ in gpu:
-            qs = {ctx.query_id for ctx in rt.contexts.values()
-                  for nid in b_.node_ids if nid in ctx.graph.nodes}
-            for q in qs:
-                per_q.setdefault(q, []).append(b_)
-        for q, bs in per_q.items():
-            first = min(b_.start_ms for b_ in bs)
-            last = max(done.get(q, [max(b_.end_ms for b_ in bs)]))
-            spans.append(last - first)
-            dev.append(sum(b_.device_ms for b_ in bs))
+            q = ctx.query_id
+            srch = [x for x in launches if x[1] == "vdb-search0" and q in x[2]]
+            rr = [x for x in launches if x[1] == "rerank0" and q in x[2]]
+            if not srch or not rr:
+                continue
+            t_launch = max(x[0] for x in srch)
+            rr_nodes = set().union(*(x[3] for x in rr))
+            t_done = max(t for t, qq, nid in rt.device_done if qq == q and nid in rr_nodes)
+            window = [x for x in srch + rr if x[0] >= t_launch]
+            spans.append(t_done - t_launch)
+            dev.append(sum(x[4][0].elapsed_time(x[4][1]) for x in window))
         ratio = [s / d for s, d in zip(spans, dev) if d > 0]
         print(json.dumps({
             "app": name, "queries": len(rt.contexts), "gpu_batches": len(gpu),
