@@ -471,6 +471,7 @@ __global__ void __launch_bounds__(kWarps * 32) rerank_ring_kernel(
     int q_is_f32, const int32_t* __restrict__ cand, int C, int k, const int32_t* __restrict__ offs,
     float* __restrict__ out_s, int32_t* __restrict__ out_id) {
   extern __shared__ __align__(16) uint8_t sm[];
+  pdl_wait();  // (programmatic launch: the question and the candidates are the previous kernels')
   const int row_bytes = dim * 2;
   uint8_t* ring = sm;                                                   // [kWarps][kSlots][row]
   uint64_t* keys = reinterpret_cast<uint64_t*>(sm + static_cast<size_t>(kWarps) * kSlots * row_bytes);
@@ -644,6 +645,7 @@ __global__ void __launch_bounds__(kWarps * 32) rerank_lists_kernel(
     float* __restrict__ out_s, int32_t* __restrict__ out_id, int splits,
     uint64_t* __restrict__ part_keys, int32_t* __restrict__ arrivals) {
   extern __shared__ __align__(16) uint8_t sm[];
+  pdl_wait();  // (programmatic launch: the question and the candidates are the previous kernels')
   const int row_bytes = dim * 2;
   uint8_t* ring = sm;                                                   // [kWarps][kSlots][row]
   uint64_t* lists = reinterpret_cast<uint64_t*>(sm + static_cast<size_t>(kWarps) * kSlots * row_bytes);
@@ -1762,9 +1764,9 @@ int launch_rerank_ring_v(const void* arena, int64_t nrows, int dim, const void* 
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     if (e != cudaSuccess) return static_cast<int>(e);
   }
-  kern<<<B, kWarps * 32, smem, stream>>>(reinterpret_cast<const __nv_bfloat16*>(arena), nrows, dim,
-                                         q, q_is_f32, cand, C, k, offs, out_s, out_id);
-  return static_cast<int>(cudaGetLastError());
+  return launch_pdl(kern, dim3(B), dim3(kWarps * 32), smem, stream,
+                    reinterpret_cast<const __nv_bfloat16*>(arena), nrows, dim, q, q_is_f32, cand, C,
+                    k, offs, out_s, out_id);
 }
 
 struct RerankSplit {  // split mode scratch (see rerank_lists_kernel)
@@ -1787,10 +1789,9 @@ int launch_rerank_lists_v(const void* arena, int64_t nrows, int dim, const void*
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     if (e != cudaSuccess) return static_cast<int>(e);
   }
-  kern<<<B * sp.splits, kWarps * 32, smem, stream>>>(
-      reinterpret_cast<const __nv_bfloat16*>(arena), nrows, dim, q, q_is_f32, cand, C, k, offs,
-      out_s, out_id, sp.splits, sp.part_keys, sp.arrivals);
-  return static_cast<int>(cudaGetLastError());
+  return launch_pdl(kern, dim3(B * sp.splits), dim3(kWarps * 32), smem, stream,
+                    reinterpret_cast<const __nv_bfloat16*>(arena), nrows, dim, q, q_is_f32, cand, C,
+                    k, offs, out_s, out_id, sp.splits, sp.part_keys, sp.arrivals);
 }
 
 template <int CPL, bool kTiled>
@@ -1804,7 +1805,11 @@ int launch_rerank_ring_s(int slots, const void* arena, int64_t nrows, int dim, c
   int nw = 8;
   if (const char* w = getenv("TSV_RERANK_WARPS")) nw = atoi(w);
   if (per_block > nw * 32) nw = per_block <= 16 * 32 ? 16 : 32;
-  if (k <= 32 && per_block <= nw * 32 && !getenv("TSV_RERANK_SORT")) {
+  // Per-warp lists for short candidate lists; from 128 candidates on the ring + block-sort kernel
+  // (16 warps) measured faster (C3, 256 x 200 x 768: 18.7 vs 20.3 us; x 1024: 23.0 vs 23.9 us;
+  // scripts/rerank_probe.py), unless forced with TSV_RERANK_LISTS.
+  const bool lists_ok = sp.splits > 1 || C < 128 || getenv("TSV_RERANK_LISTS");
+  if (k <= 32 && per_block <= nw * 32 && lists_ok && !getenv("TSV_RERANK_SORT")) {
 #define TSV_LISTS(W, S) launch_rerank_lists_v<W, S, CPL, kTiled>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream, sp)
     if (nw == 8) return slots == 2 ? TSV_LISTS(8, 2) : (slots == 3 ? TSV_LISTS(8, 3) : TSV_LISTS(8, 4));
     if (nw == 16) return slots == 2 ? TSV_LISTS(16, 2) : (slots == 3 ? TSV_LISTS(16, 3) : TSV_LISTS(16, 4));

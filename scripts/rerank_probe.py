@@ -14,13 +14,15 @@ import torch
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2407_00326_b200.index import DeviceIndex, normalize_rows  # noqa: E402
 
-VARIANTS = [("ldg", {"TSV_RERANK_LDG": "1"}), ("default(lists)", {}),
-            ("lists_s3", {"TSV_RERANK_SLOTS": "3"}), ("lists_s4", {"TSV_RERANK_SLOTS": "4"}),
-            ("lists_w16", {"TSV_RERANK_WARPS": "16"}),
-            ("lists_w16_s4", {"TSV_RERANK_WARPS": "16", "TSV_RERANK_SLOTS": "4"}),
-            ("sort", {"TSV_RERANK_SORT": "1"}), ("split2", {"TSV_RERANK_SPLITS": "2"})]
+VARIANTS = [("ldg", {"TSV_RERANK_LDG": "1"}), ("default", {}),
+            ("lists", {"TSV_RERANK_LISTS": "1"}),
+            ("lists_s3", {"TSV_RERANK_LISTS": "1", "TSV_RERANK_SLOTS": "3"}),
+            ("lists_w16", {"TSV_RERANK_LISTS": "1", "TSV_RERANK_WARPS": "16"}),
+            ("sort_s2", {"TSV_RERANK_SORT": "1"}),
+            ("sort_s3", {"TSV_RERANK_SORT": "1", "TSV_RERANK_SLOTS": "3"}),
+            ("sort_s4", {"TSV_RERANK_SORT": "1", "TSV_RERANK_SLOTS": "4"})]
 KNOBS = ("TSV_RERANK_LDG", "TSV_RERANK_SLOTS", "TSV_RERANK_WARPS", "TSV_RERANK_SPLITS",
-         "TSV_RERANK_SORT")
+         "TSV_RERANK_SORT", "TSV_RERANK_LISTS")
 
 
 def graph_time(calls, reps=20):

@@ -203,7 +203,8 @@ def test_rerank_shapes_match_oracle(cuda, n, dim, b, c, k):
                                             (768, 200, 10, "sort"), (256, 600, 10, None),
                                             (512, 100, 40, None), (1024, 512, 32, None),
                                             (768, 200, 10, "split8"), (256, 37, 20, "split2"),
-                                            (1024, 1000, 8, None)])
+                                            (1024, 1000, 8, None), (768, 200, 10, "lists"),
+                                            (1024, 512, 32, "lists")])
 def test_rerank_ring_equals_register_gather(cuda, dim, c, k, slots):
     """The pipelined K3 (cp.async rings, question in registers, packed fp32x2 FMAs; bf16
     arenas; per-warp top-k lists for C <= 512, k <= 32, else the block sort, forced by
@@ -227,10 +228,12 @@ def test_rerank_ring_equals_register_gather(cuda, dim, c, k, slots):
     idx = _index_from(arena, cuda)
     qd, cd = to_dev_bf16(qs, cuda), torch.from_numpy(cand).to(cuda)
     env = ({"TSV_RERANK_SORT": "1"} if slots == "sort"
+           else {"TSV_RERANK_LISTS": "1"} if slots == "lists"
            else {"TSV_RERANK_SPLITS": slots[5:]} if isinstance(slots, str)
            else {"TSV_RERANK_SLOTS": str(slots)} if slots else {})
     old = {key: os.environ.get(key) for key in ("TSV_RERANK_SLOTS", "TSV_RERANK_LDG",
-                                                "TSV_RERANK_SORT", "TSV_RERANK_SPLITS")}
+                                                "TSV_RERANK_SORT", "TSV_RERANK_SPLITS",
+                                                "TSV_RERANK_LISTS")}
     try:
         os.environ.update(env)
         s1, i1 = idx.rerank(qd, cd, k)
