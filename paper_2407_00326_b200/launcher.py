@@ -56,13 +56,14 @@ class StreamRuntime(Simulator):
 
     def __init__(self, engines: EngineSet, backend, options: RuntimeOptions | None = None,
                  speed: float = 1.0, poll_us: float = 20.0, timeout_s: float = 60.0,
-                 stream_order: bool = True, busy_poll: bool = True):
+                 stream_order: bool = True, busy_poll: bool = True, affinity: bool = True):
         """busy_poll: while device batches are in flight, poll their events without sleeping
         (an OS sleep of 20 us lasts ~60-80 us, which would add to every device -> host hop);
         the loop sleeps only when nothing is in flight and the next event is in the future."""
         super().__init__(engines, options, backend=backend)
         self.speed = speed
         self.busy_poll = busy_poll
+        self.affinity = affinity
         self.poll_s = poll_us * 1e-6
         self.timeout_s = timeout_s
         self.stream_order = stream_order
@@ -114,7 +115,9 @@ class StreamRuntime(Simulator):
             return super()._dispatch(state, plan, t)
         from .engines import select_instance
 
-        instance = select_instance(state.instances, profile.category, t)
+        instance = self._affine_instance(state, plan, t) if self.affinity else None
+        if instance is None:
+            instance = select_instance(state.instances, profile.category, t)
         assert instance is not None
         start, end = self.backend.launch(profile, plan, instance)
         instance.busy_until = math.inf  # busy until the end event fires
@@ -130,6 +133,32 @@ class StreamRuntime(Simulator):
                 self._push(t, self._REQ_DONE, (task, n))
         state.queue = [task for task in state.queue if task.pending() > 0]
         self._inflight.append((end, start, state, instance, plan, t))
+
+    def _affine_instance(self, state, plan, t):
+        """Index-location affinity (the reference picks the least-loaded replica,
+        engines.py:156-164, blind to data placement): an idle replica on the GPU that holds the
+        per-query indexes of most of the batch's entries, so no segment is pulled over NVLink.
+        Ties and batches without per-query indexes keep select_instance's choice."""
+        home = getattr(self.backend, "home", None)
+        if home is None or len(state.instances) < 2:
+            return None
+        idle = [i for i in state.instances if i.idle(t)]
+        if len(idle) < 2:
+            return None
+        votes: dict[int, int] = {}
+        for task, n in plan.entries:
+            if any(e.dst == task.node_id and e.key == "index" for e in task.ctx.graph.edges) or \
+                    task.node.kind.value == "Reranking":
+                r = home(task.ctx.query_id)
+                votes[r] = votes.get(r, 0) + n
+        if not votes:
+            return None
+        n_rep = len(self.backend.replicas)
+        best = max(votes.items(), key=lambda kv: (kv[1], -kv[0]))[0]
+        on_home = [i for i in idle if i.instance_id % n_rep == best]
+        if not on_home:
+            return None
+        return min(on_home, key=lambda i: (i.executed_requests, i.instance_id))
 
     def _poll(self, t: float) -> bool:
         progressed = False

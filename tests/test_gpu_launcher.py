@@ -210,3 +210,34 @@ def _native_launches():
     from paper_2407_00326_b200 import _native
 
     return _native.launch_count()
+
+
+def test_stream_runtime_index_affinity(cuda):
+    """Two replicas: with index-location affinity the per-query indexes stay on their home
+    replica (segments pulled to the other replica only when the home one is busy), and the
+    results are the same real results; without it, the least-loaded choice copies more."""
+    from paper_2407_00326_b200 import engines as E
+    from paper_2407_00326_b200.backend import RetrievalBackend
+    from paper_2407_00326_b200.graph import parse_graph
+    from paper_2407_00326_b200.launcher import StreamRuntime
+
+    traces = json.loads((GOLD / "ref_traces.json").read_text())
+    prof = json.loads((GOLD / "ref_profiles.json").read_text())["default"]["profiles"]
+    for p_ in prof["engines"]:
+        if p_["engine_id"] in ("vdb-search0", "rerank0"):
+            p_["instances"] = 2
+    copies = {}
+    for affinity in (True, False):
+        es = E.EngineSet.from_dict(prof)
+        backend = RetrievalBackend(dim=1024, devices=[0, 0], arena_rows=1 << 16,
+                                   release_segments=False)
+        rt = StreamRuntime(es, backend, speed=20.0, affinity=affinity)
+        for name in ("advanced_c3", "contextual"):
+            case = next(c for c in traces if c["case"] == name and c["scheduler"] == "topo")
+            for g, a, _ in case["graphs"]:
+                rt.submit_query(parse_graph(g), a, arrival_ms=a)
+        rt.run()
+        assert all(ctx.finish_ms is not None for ctx in rt.contexts.values())
+        assert _check_outputs(rt, backend) > 0
+        copies[affinity] = sum(1 for (q, _, r) in backend.segments if r != backend.home(q))
+    assert copies[True] <= copies[False]
