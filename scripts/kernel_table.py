@@ -30,7 +30,13 @@ CASES = [
     ("K2 segmented", "16 queries x own 48-row segment, k=32 (C5)"),
     ("K3 rerank", "256 questions x 200 candidates x 768 -> 10 (C3)"),
     ("K1f fp32 mode", "1M x 1024 fp32 (3xTF32), B=1024, k=10"),
+    ("K2t one-launch search", "10k x 384, B=16, k=5 (C1; tcgen05, rows on M)"),
+    ("K2s one-launch search", "10k x 384, B=16, k=5 (C1; CUDA-core path, TSV_NO_TINY)"),
+    ("K3s fused contextual chain", "16 queries x own 48-row segment, top-32 -> rerank 3 (C5)"),
 ]
+# (K6, the peer exchange, is not in this table: ncu serialises kernels, so rank 0's exchange waits
+# for a rank whose kernel cannot start until it finishes, and ends at its timeout. Its latency
+# with every rank in flight comes from scripts/k6_probe.py.)
 
 
 def run():
@@ -57,6 +63,12 @@ def run():
     f32 = DeviceIndex(D, 1 << 20, metric="cosine", device=0, storage="f32")
     f32.append(torch.randn((1 << 20, D), device=dev))
     qf = torch.randn((1024, D), device=dev)
+    c1 = DeviceIndex(384, 10_000, metric="cosine", device=0)
+    c1.append(torch.randn((10_000, 384), device=dev))
+    qc1 = torch.randn((16, 384), device=dev)
+    seg_rows = torch.tensor([[48 * s, 48 * s + 48] for s in range(16)], dtype=torch.int64,
+                            device=dev)
+    import os
 
     def one_pass():
         normalize_rows(raw)
@@ -67,6 +79,11 @@ def run():
                                  32)
         c3.rerank(q3, cand, 10)
         f32.search(qf, 10)
+        c1.search(qc1, 5)
+        os.environ["TSV_NO_TINY"] = "1"
+        c1.search(qc1, 5)
+        del os.environ["TSV_NO_TINY"]
+        seg_idx.search_rerank_segmented(seg_q, seg_rows, 48, 32, 3, local_ids=False)
         torch.cuda.synchronize()
 
     one_pass()
