@@ -428,6 +428,64 @@ class RetrievalBackend:
         self.records.append(rec)
         return start, end
 
+    def launch_chain(self, profile: EngineProfile, plan, instance, reranks):
+        """One launch for a batch of Searching requests AND the Reranking node each feeds
+        (StreamRuntime's fused chain dispatch): every entry searches its own per-query index
+        segment (<= 1024 rows) with its query vector, keeps the node's top-k, and reranks those
+        hits against the query's question, keeping the rerank node's top_k — the segment
+        kernel (tsv_search_rerank_segmented). Both nodes' results go to their accumulators.
+        Returns (start, end) events, or None when the batch does not fit the kernel (the
+        caller then launches the search alone)."""
+        rep = self.replica_for(instance)
+        if rep.arena.storage not in ("bf16", "bf16_tiled") or self.dim > 2048:
+            return None
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        with self._on(rep):
+            qs, qr, rows, meta = [], [], [], []
+            k_s = k_r = 1
+            for (task, n), rr in zip(plan.entries, reranks):
+                node = task.node
+                key_out = next(iter(node.meta.outputs))
+                k = node.meta.outputs[key_out].items
+                top_k = rr.meta.outputs[next(iter(rr.meta.outputs))].items
+                idx = self._inputs(task.ctx, node, "index")
+                seg = self._local_segment(task.ctx.query_id, idx[0][1][1], self.replicas.index(rep))
+                if seg.row_end - seg.row_beg > 1024 or top_k > k:
+                    return None
+                qs.append(self._query_rows(rep, task, 0, 1))
+                qr.append(self._question(rep, task.ctx).reshape(1, -1))
+                rows += [seg.row_beg, seg.row_end]
+                meta.append((task, rr, k, top_k))
+                k_s, k_r = max(k_s, k), max(k_r, top_k)
+            q = torch.cat(qs) if len(qs) > 1 else qs[0]
+            qq = torch.cat(qr) if len(qr) > 1 else qr[0]
+            if qq.dtype != q.dtype:
+                qq = qq.to(q.dtype)
+            q_rows = torch.tensor(rows, dtype=torch.int64).reshape(-1, 2).to(rep.device,
+                                                                               non_blocking=True)
+            max_rows = max(b - a for a, b in zip(rows[::2], rows[1::2]))
+            start.record(rep.stream)
+            (ss, si), (rs, ri) = rep.arena.search_rerank_segmented(
+                q, q_rows, max(1, max_rows), k_s, k_r, q_rerank=qq, local_ids=True,
+                stream=rep.stream)
+            ready = self._record(rep)
+            end.record(rep.stream)
+        r = self.replicas.index(rep)
+        for j, (task, rr, k, top_k) in enumerate(meta):
+            self.acc.setdefault((task.ctx.query_id, task.node_id), []).append(
+                (0, ss[j:j + 1, :k], si[j:j + 1, :k], ready, r))
+            self.acc.setdefault((task.ctx.query_id, rr.node_id), []).append(
+                (0, rs[j:j + 1, :top_k], ri[j:j + 1, :top_k], ready, r))
+        self.launches += 1
+        rows_n = sum(b - a for a, b in zip(rows[::2], rows[1::2]))
+        rec = LaunchRecord(profile.engine_id, r, "search+rerank", len(meta), rows_n, k_s, self.dim,
+                           bytes=rows_n * self.dim * 2 + len(meta) * self.dim * 4 +
+                           len(meta) * (k_s + k_r) * 8,
+                           flops=4 * rows_n * self.dim, start=start, end=end)
+        self.records.append(rec)
+        return start, end
+
     def execute(self, profile: EngineProfile, plan, t: float, instance) -> tuple[float, float | None]:
         """Simulator hook: run the batch; duration = profile latency ("profile") or the device
         time of the launches ("measured", synchronises on the batch's end event)."""

@@ -56,7 +56,8 @@ class StreamRuntime(Simulator):
 
     def __init__(self, engines: EngineSet, backend, options: RuntimeOptions | None = None,
                  speed: float = 1.0, poll_us: float = 20.0, timeout_s: float = 60.0,
-                 stream_order: bool = True, busy_poll: bool = True, affinity: bool = True):
+                 stream_order: bool = True, busy_poll: bool = True, affinity: bool = True,
+                 fuse_chains: bool = True):
         """busy_poll: while device batches are in flight, poll their events without sleeping
         (an OS sleep of 20 us lasts ~60-80 us, which would add to every device -> host hop);
         the loop sleeps only when nothing is in flight and the next event is in the future."""
@@ -64,6 +65,9 @@ class StreamRuntime(Simulator):
         self.speed = speed
         self.busy_poll = busy_poll
         self.affinity = affinity
+        self.fuse_chains = fuse_chains and stream_order
+        self._chained: dict[tuple[str, str], object] = {}  # (query, rerank node) -> end event
+        self._chain_nodes: dict[int, list] = {}  # id(end event) -> fused rerank nodes
         self.poll_s = poll_us * 1e-6
         self.timeout_s = timeout_s
         self.stream_order = stream_order
@@ -99,6 +103,20 @@ class StreamRuntime(Simulator):
         return out
 
     def _node_ready(self, ctx, nid: str, t: float) -> None:
+        end = self._chained.pop((ctx.query_id, nid), None)
+        if end is not None:
+            # a Reranking node whose result the fused chain launch already computes: it
+            # completes in stream order, without a batch of its own (its consumers on modelled
+            # engines wait for the launch's end event)
+            node = ctx.graph.nodes[nid]
+            self._node_events.setdefault((ctx.query_id, nid), []).append(end)
+            if ctx.stats[nid].ready_ms is None:
+                ctx.stats[nid].ready_ms = t
+            self._emit(t, ctx, node, "enqueue")
+            ctx.stats[nid].first_start_ms = t
+            self._emit(t, ctx, node, "start")
+            self.on_primitive_complete(ctx, nid, t)
+            return
         node = ctx.graph.nodes[nid]
         if self.stream_order and node.kind not in CONTROL_KINDS and not self._gpu(node):
             pending = [ev for ev in self._upstream_events(ctx, nid) if not ev.query()]
@@ -119,7 +137,18 @@ class StreamRuntime(Simulator):
         if instance is None:
             instance = select_instance(state.instances, profile.category, t)
         assert instance is not None
-        start, end = self.backend.launch(profile, plan, instance)
+        chain = self._chain_reranks(plan) if (self.fuse_chains and profile.category == "search") else None
+        launched = None
+        if chain is not None and hasattr(self.backend, "launch_chain"):
+            launched = self.backend.launch_chain(profile, plan, instance, chain)
+        if launched is not None:
+            start, end = launched
+            for (task, _), rr in zip(plan.entries, chain):
+                self._chained[(task.ctx.query_id, rr.node_id)] = end
+            self._chain_nodes[id(end)] = [(task.ctx.query_id, rr.node_id)
+                                          for (task, _), rr in zip(plan.entries, chain)]
+        else:
+            start, end = self.backend.launch(profile, plan, instance)
         instance.busy_until = math.inf  # busy until the end event fires
         instance.executed_requests += sum(n for _, n in plan.entries)
         for task, n in plan.entries:
@@ -133,6 +162,31 @@ class StreamRuntime(Simulator):
                 self._push(t, self._REQ_DONE, (task, n))
         state.queue = [task for task in state.queue if task.pending() > 0]
         self._inflight.append((end, start, state, instance, plan, t))
+
+    def _chain_reranks(self, plan):
+        """Fused dispatch of a search -> rerank chain (the contextual workflow's stage pair):
+        for every entry, the whole Searching node (one query vector, a per-query index) whose
+        only consumer is a Reranking node on a backend engine, fed by nothing else — the
+        rerank's result can be computed by the same launch (tsv_search_rerank_segmented).
+        Returns the rerank nodes in entry order, or None when any entry does not qualify."""
+        out = []
+        for task, n in plan.entries:
+            node, g = task.node, task.ctx.graph
+            if task.next_request != 0 or n != len(task.loads) or node.meta.batch_items != 1:
+                return None
+            if not any(e.dst == node.node_id and e.key == "index" for e in g.edges):
+                return None
+            consumers = [e.dst for e in g.edges if e.src == node.node_id]
+            if len(consumers) != 1:
+                return None
+            rr = g.nodes[consumers[0]]
+            if rr.kind.value != "Reranking" or not self._gpu(rr):
+                return None
+            feeds = [e for e in g.edges if e.dst == rr.node_id and e.key is not None]
+            if any(e.src != node.node_id for e in feeds):
+                return None
+            out.append(rr)
+        return out
 
     def _affine_instance(self, state, plan, t):
         """Index-location affinity (the reference picks the least-loaded replica,
@@ -185,6 +239,8 @@ class StreamRuntime(Simulator):
                 if not self.stream_order:
                     self._push(t, self._REQ_DONE, (task, n))
                 self.device_done.append((t, task.ctx.query_id, task.node_id))
+            for qid, rr_id in self._chain_nodes.pop(id(end), []):
+                self.device_done.append((t, qid, rr_id))
             self._push(t, self._BATCH_DONE, (state.profile.engine_id, instance.instance_id, 0.0))
             self.trace.batches.append(BatchRecord(state.profile.engine_id, instance.instance_id,
                                                   t0, t, plan.load, self._cap(state), plan.phase,
