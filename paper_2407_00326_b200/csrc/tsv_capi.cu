@@ -992,12 +992,21 @@ static int tiny_scan(tsv_index* idx, const void* q_dev, int q_dtype, int B, int 
     TSV_CUDA(cudaMemsetAsync(w.sm_arrive.ptr, 0, w.sm_arrive.cap * sizeof(int32_t), st),
              "arrivals reset");
   unsigned long long* trace = small_trace_buffer();
+  // The cross-tile merge as a second grid launched behind the scan (PDL): the queries' merges
+  // run in parallel on B SMs instead of one after another in the scan's last CTA (C1 in a CUDA
+  // graph: 16.0 vs 20.0 us). Issued call by call the extra launch costs more host time than
+  // it saves on the device (back-to-back calls: 25.1 vs 20.2 us), so the split is used where
+  // launches are free: under graph capture. TSV_TINY_SPLIT=0/1 forces either.
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cap);
+  int split = cap != cudaStreamCaptureStatusNone ? 1 : 0;
+  if (const char* v = getenv("TSV_TINY_SPLIT")) split = atoi(v) != 0;
   int e = tsv::launch_tiny_scan(idx->tmap_c, q_dev, q_dtype == TSV_F32,
                                 idx->metric == TSV_METRIC_COSINE, B, idx->dim, row_beg, row_end,
                                 id_offset, k, w.sm_keys.ptr, w.sm_arrive.ptr, scores_dev, ids_dev,
-                                st, trace, idx->storage == TSV_BF16_TILED);
+                                st, trace, idx->storage == TSV_BF16_TILED, split);
   if (e) return cuda_fail(static_cast<cudaError_t>(e), "tiny scan launch");
-  g_launches++;
+  g_launches += split ? 2 : 1;  // scan (+ merge grid, PDL-overlapped)
   small_trace_print(trace, nblk, st);
   return TSV_OK;
 }

@@ -204,7 +204,8 @@ int tiny_scan_blocks(int64_t n);
 int launch_tiny_scan(const CUtensorMap& tmap_c, const void* q, int q_is_f32, int do_normalize,
                      int B, int dim, int64_t row_beg, int64_t row_end, int32_t id_offset, int k,
                      uint64_t* part_keys, int32_t* arrive, float* out_s, int32_t* out_i,
-                     cudaStream_t stream, unsigned long long* trace = nullptr, int tiled = 0);
+                     cudaStream_t stream, unsigned long long* trace = nullptr, int tiled = 0,
+                     int split = 0);  // split: cross-tile merge as a second (PDL) grid
 
 int launch_normalize(const void* src, int src_is_f32, int64_t n, int dim, int do_normalize,
                      void* dst_bf16, cudaStream_t stream);

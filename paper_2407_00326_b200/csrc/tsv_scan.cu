@@ -1189,13 +1189,17 @@ template <int NQ>
 __global__ void __launch_bounds__(kTinyThreads, 1) tiny_scan_kernel(
     const __grid_constant__ CUtensorMap tmap_c, const void* __restrict__ q, int q_is_f32,
     int do_normalize, int B, int dim, int64_t row_beg, int64_t row_end, int32_t id_offset, int k,
-    int stages, int tiled, uint64_t* __restrict__ part_keys, int32_t* __restrict__ arrive,
+    int stages, int tiled, int split_merge, uint64_t* __restrict__ part_keys,
+    int32_t* __restrict__ arrive,
     float* __restrict__ out_s, int32_t* __restrict__ out_i, unsigned long long* __restrict__ trace) {
   // (trace: development timestamps per CTA and phase, TSV_SMALL_TRACE; null in production)
   auto stamp = [&](int ph) {
     if (trace != nullptr && threadIdx.x == 0) trace[blockIdx.x * 8 + ph] = global_ns();
   };
   stamp(0);
+  // split_merge: the merge runs in tiny_merge_kernel, launched behind this one with
+  // programmatic serialisation; let it launch now (it waits in griddepcontrol.wait)
+  if (split_merge && threadIdx.x == 0) pdl_allow_dependents();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -1376,6 +1380,7 @@ __global__ void __launch_bounds__(kTinyThreads, 1) tiny_scan_kernel(
                                lane);
   }
   stamp(4);
+  if (split_merge) return;  // (the merge kernel reads the lists after this grid completes)
   __threadfence();
   __syncthreads();
   if (tid == 0) last_s = atomicAdd(arrive, 1) == nblk - 1;
@@ -1445,11 +1450,68 @@ __global__ void __launch_bounds__(kTinyThreads, 1) tiny_scan_kernel(
   stamp(7);
 }
 
+// The cross-tile merge of K2t as its own grid (one CTA per query, launched with programmatic
+// serialisation behind the scan, which allows it at its start): the 16 queries' merges run on 16
+// SMs at once instead of one after another in the scan's last CTA, and the scan needs no
+// arrival counter or fence. Each CTA loads its query's nblk * k keys (<= 512: two per thread,
+// one round trip), every warp selects the top k of its 64 keys (k rounds of a warp max below
+// the previous round's key), then warp 0 the top k of those.
+__global__ void __launch_bounds__(256) tiny_merge_kernel(const uint64_t* __restrict__ part_keys,
+                                                         int nblk, int k,
+                                                         float* __restrict__ out_s,
+                                                         int32_t* __restrict__ out_i) {
+  __shared__ uint64_t wsel[8][16];
+  __shared__ uint64_t fin[16];
+  pdl_wait();
+  const int q = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int total = nblk * k;
+  const uint64_t* src = part_keys + static_cast<int64_t>(q) * total;
+  const uint64_t pad = tk_pad();
+  uint64_t v[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int e = tid + 256 * u;
+    v[u] = e < total ? static_cast<uint64_t>(__ldcg(reinterpret_cast<const unsigned long long*>(src + e)))
+                     : pad;
+  }
+  auto rounds = [&](const uint64_t* vals, int n, uint64_t* out) {
+    uint64_t prev = ~0ull;
+    for (int r = 0; r < k; ++r) {
+      uint64_t best = pad;
+      for (int i = 0; i < n; ++i) best = (vals[i] < prev && vals[i] > best) ? vals[i] : best;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t y = __shfl_xor_sync(0xffffffffu, best, o);
+        best = y > best ? y : best;
+      }
+      if (lane == 0) out[r] = best;
+      prev = best;
+    }
+  };
+  rounds(v, 2, wsel[warp]);
+  __syncthreads();
+  if (warp != 0) return;
+  uint64_t w[4];  // 8 warps x k <= 16 keys
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int e = lane + 32 * u, ww = e >> 4, r = e & 15;
+    w[u] = r < k ? wsel[ww][r] : pad;
+  }
+  rounds(w, 4, fin);
+  __syncwarp();
+  for (int r = lane; r < k; r += 32) {
+    const uint64_t m = fin[r];
+    const int32_t id = m == pad ? -1 : tk_id(m);
+    out_s[static_cast<int64_t>(q) * k + r] = id < 0 ? -INFINITY : tk_score(m);
+    out_i[static_cast<int64_t>(q) * k + r] = id;
+  }
+}
+
 template <int NQ>
 int launch_tiny_v(const CUtensorMap& tmap_c, const void* q, int q_is_f32, int do_normalize,
                   int B, int dim, int64_t row_beg, int64_t row_end, int32_t id_offset, int k,
                   uint64_t* part_keys, int32_t* arrive, float* out_s, int32_t* out_i,
-                  cudaStream_t stream, unsigned long long* trace, int tiled) {
+                  cudaStream_t stream, unsigned long long* trace, int tiled, int split) {
   const int num_kb = (dim + kBlockK - 1) / kBlockK;
   const int stages = num_kb < 6 ? num_kb : 6;
   const size_t qraw = (static_cast<size_t>(B) * dim * (q_is_f32 ? 4 : 2) + 15) & ~size_t(15);
@@ -1476,9 +1538,17 @@ int launch_tiny_v(const CUtensorMap& tmap_c, const void* q, int q_is_f32, int do
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return static_cast<int>(cudaLaunchKernelEx(&cfg, kern, tmap_c, q, q_is_f32, do_normalize, B,
-                                             dim, row_beg, row_end, id_offset, k, stages, tiled,
-                                             part_keys, arrive, out_s, out_i, trace));
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tmap_c, q, q_is_f32, do_normalize, B, dim,
+                                     row_beg, row_end, id_offset, k, stages, tiled, split,
+                                     part_keys, arrive, out_s, out_i, trace);
+  if (e != cudaSuccess || !split) return static_cast<int>(e);
+  cudaLaunchConfig_t mc = cfg;
+  mc.gridDim = dim3(B);
+  mc.blockDim = dim3(256);
+  mc.dynamicSmemBytes = 0;
+  return static_cast<int>(cudaLaunchKernelEx(&mc, tiny_merge_kernel,
+                                             static_cast<const uint64_t*>(part_keys), nblk, k,
+                                             out_s, out_i));
 }
 
 }  // namespace
@@ -1516,10 +1586,10 @@ int tiny_scan_blocks(int64_t n) { return static_cast<int>((n + kTinyRows - 1) / 
 int launch_tiny_scan(const CUtensorMap& tmap_c, const void* q, int q_is_f32, int do_normalize,
                      int B, int dim, int64_t row_beg, int64_t row_end, int32_t id_offset, int k,
                      uint64_t* part_keys, int32_t* arrive, float* out_s, int32_t* out_i,
-                     cudaStream_t stream, unsigned long long* trace, int tiled) {
+                     cudaStream_t stream, unsigned long long* trace, int tiled, int split) {
   if (B <= 0 || B > 64 || k > 16 || dim % 8 != 0 || (tiled && row_beg % kTinyRows != 0))
     return static_cast<int>(cudaErrorInvalidValue);
-#define TSV_TINY(NQ) launch_tiny_v<NQ>(tmap_c, q, q_is_f32, do_normalize, B, dim, row_beg, row_end, id_offset, k, part_keys, arrive, out_s, out_i, stream, trace, tiled)
+#define TSV_TINY(NQ) launch_tiny_v<NQ>(tmap_c, q, q_is_f32, do_normalize, B, dim, row_beg, row_end, id_offset, k, part_keys, arrive, out_s, out_i, stream, trace, tiled, split)
   if (B <= 16) return TSV_TINY(16);
   if (B <= 32) return TSV_TINY(32);
   return TSV_TINY(64);
