@@ -57,7 +57,7 @@ class StreamRuntime(Simulator):
     def __init__(self, engines: EngineSet, backend, options: RuntimeOptions | None = None,
                  speed: float = 1.0, poll_us: float = 20.0, timeout_s: float = 60.0,
                  stream_order: bool = True, busy_poll: bool = True, affinity: bool = True,
-                 fuse_chains: bool = True):
+                 fuse_chains: bool = True, queue_on_stream: bool = False):
         """busy_poll: while device batches are in flight, poll their events without sleeping
         (an OS sleep of 20 us lasts ~60-80 us, which would add to every device -> host hop);
         the loop sleeps only when nothing is in flight and the next event is in the future."""
@@ -66,6 +66,12 @@ class StreamRuntime(Simulator):
         self.busy_poll = busy_poll
         self.affinity = affinity
         self.fuse_chains = fuse_chains and stream_order
+        # queue_on_stream: a GPU replica takes its next batch as soon as the previous one is
+        # launched (the replica's stream still runs them one at a time). Off by default: with
+        # 30 concurrent C3 queries it made batches smaller and the retrieval tail longer (4.0 vs
+        # 3.0 ms, scripts/stream_probe.py) — each batch costs ~0.14 ms of host time, so batching
+        # behind the previous launch's completion pays
+        self.queue_on_stream = queue_on_stream and stream_order
         self._chained: dict[tuple[str, str], object] = {}  # (query, rerank node) -> end event
         self._chain_nodes: dict[int, list] = {}  # id(end event) -> fused rerank nodes
         self.poll_s = poll_us * 1e-6
@@ -149,7 +155,8 @@ class StreamRuntime(Simulator):
                                           for (task, _), rr in zip(plan.entries, chain)]
         else:
             start, end = self.backend.launch(profile, plan, instance)
-        instance.busy_until = math.inf  # busy until the end event fires
+        # busy until the end event fires (or, queued on the stream, free for the next batch)
+        instance.busy_until = t if self.queue_on_stream else math.inf
         instance.executed_requests += sum(n for _, n in plan.entries)
         for task, n in plan.entries:
             task.next_request += n
@@ -233,7 +240,8 @@ class StreamRuntime(Simulator):
             return progressed
         self._inflight = still
         for end, start, state, instance, plan, t0 in done:
-            instance.busy_until = t
+            if not self.queue_on_stream:
+                instance.busy_until = t
             device_ms = start.elapsed_time(end)
             for task, n in plan.entries:
                 if not self.stream_order:

@@ -54,3 +54,4 @@ print("launches", backend.launches)
 st = pstats.Stats(pr)
 st.sort_stats("tottime").print_stats(30)
 st.sort_stats("cumtime").print_stats("backend|index|_native", 25)
+st.print_callees("launch_chain|_search_batch|_rerank_batch|search_segmented|rerank\\b")
