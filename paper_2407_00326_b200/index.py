@@ -49,9 +49,18 @@ def _check_out(out, B: int, k: int, device: torch.device) -> None:
             raise ConfigParse(f"{name} must be contiguous")
 
 
+_RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def _stream_handle(stream: torch.cuda.Stream | None, device: torch.device) -> int:
-    s = stream if stream is not None else torch.cuda.current_stream(device)
-    return s.cuda_stream
+    """cudaStream_t of `stream`, or of the device's current torch stream. The current stream is
+    read through torch's raw-handle accessor when it exists: building a Stream object costs
+    ~6 us per call, about half of a search call's host time."""
+    if stream is not None:
+        return stream.cuda_stream
+    if _RAW_STREAM is not None:
+        return _RAW_STREAM(device.index if device.index is not None else torch.cuda.current_device())
+    return torch.cuda.current_stream(device).cuda_stream
 
 
 class _ArenaView:
