@@ -699,20 +699,46 @@ class RetrievalBackend:
             rep.stream.synchronize()
 
 
+_GET_STREAM = getattr(torch._C, "_cuda_getCurrentStream", None)
+_SET_STREAM = getattr(torch._C, "_cuda_setStream", None)
+
+
 class _StreamCtx:
+    """Make the replica's device and stream current for torch ops issued inside (and restore
+    both on exit). Uses torch's raw stream accessors when present: torch.cuda.device +
+    torch.cuda.stream build Stream objects on every entry (~10-20 us per use, several uses per
+    retrieval batch on the runtime's critical path)."""
+
     def __init__(self, rep: Replica):
         self.rep = rep
-        self._dev = torch.cuda.device(rep.device)
-        self._st = torch.cuda.stream(rep.stream)
 
     def __enter__(self):
-        self._dev.__enter__()
-        self._st.__enter__()
-        return self.rep
+        rep = self.rep
+        idx = rep.device.index
+        if _GET_STREAM is None or _SET_STREAM is None:
+            self._slow = (torch.cuda.device(rep.device), torch.cuda.stream(rep.stream))
+            for c in self._slow:
+                c.__enter__()
+            return rep
+        self._slow = None
+        self._prev_dev = torch.cuda.current_device()
+        if self._prev_dev != idx:
+            torch.cuda.set_device(idx)
+        self._prev = _GET_STREAM(idx)  # (stream id, device index, device type)
+        st = rep.stream
+        _SET_STREAM(stream_id=st.stream_id, device_index=st.device_index,
+                    device_type=st.device_type)
+        return rep
 
     def __exit__(self, *exc):
-        self._st.__exit__(*exc)
-        self._dev.__exit__(*exc)
+        if self._slow is not None:
+            for c in reversed(self._slow):
+                c.__exit__(*exc)
+            return False
+        sid, didx, dtype = self._prev
+        _SET_STREAM(stream_id=sid, device_index=didx, device_type=dtype)
+        if self._prev_dev != self.rep.device.index:
+            torch.cuda.set_device(self._prev_dev)
         return False
 
 
