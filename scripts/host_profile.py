@@ -52,6 +52,6 @@ pr.disable()
 print("launches profiled", backend.launches - n0)
 print("launches", backend.launches)
 st = pstats.Stats(pr)
-st.sort_stats("tottime").print_stats(30)
+st.sort_stats("tottime").print_stats(40)
 st.sort_stats("cumtime").print_stats("backend|index|_native", 25)
-st.print_callees("launch_chain|_search_batch|_rerank_batch|search_segmented|rerank\\b")
+

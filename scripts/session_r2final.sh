@@ -10,5 +10,5 @@ timeout 900 ncu --profile-from-start off --clock-control none --csv --log-file g
 python scripts/kernel_table.py --summarize gpurun_out/ktable_r2.csv > gpurun_out/ktable_r2.txt 2>&1; cat gpurun_out/ktable_r2.txt
 timeout 600 python bench_primitives.py > gpurun_out/prims_final.jsonl 2> gpurun_out/prims_final.err; echo "prims rc=$?"
 timeout 600 python scripts/k6_probe.py > gpurun_out/k6_final.txt 2>&1; echo "k6 rc=$?"
-timeout 900 python bench_workflows.py > gpurun_out/workflows_final.jsonl 2>&1; echo "wf rc=$?"
+timeout 1500 python bench_workflows.py > gpurun_out/workflows_final.jsonl 2>&1; echo "wf rc=$?"
 timeout 600 python scripts/stream_probe.py > gpurun_out/stream_final.jsonl 2>&1; echo "stream rc=$?"
