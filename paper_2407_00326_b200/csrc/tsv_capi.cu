@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <set>
 #include <numeric>
 #include <mutex>
 #include <string>
@@ -459,6 +460,24 @@ static int create_common(int device, int dim, int metric, tsv_index** out) {
   return TSV_OK;
 }
 
+}  // extern "C"
+
+// Live indexes, so that destroying a library stream can drop the per-stream workspaces it left
+// in them: the driver reuses stream handles, and a later stream with the same handle must not
+// inherit a workspace (possibly marked as captured by a CUDA graph) of a destroyed one.
+static std::mutex g_index_mu;
+static std::set<tsv_index*> g_indexes;
+static void register_index(tsv_index* idx) {
+  std::lock_guard<std::mutex> lock(g_index_mu);
+  g_indexes.insert(idx);
+}
+static void unregister_index(tsv_index* idx) {
+  std::lock_guard<std::mutex> lock(g_index_mu);
+  g_indexes.erase(idx);
+}
+
+extern "C" {
+
 int tsv_index_create2(int device, int dim, int metric, int storage, int64_t cap_rows,
                       tsv_index** out) {
   int rc = create_common(device, dim, metric, out);
@@ -497,6 +516,7 @@ int tsv_index_create2(int device, int dim, int metric, int storage, int64_t cap_
     delete idx;
     return rc;
   }
+  register_index(idx);
   *out = idx;
   return TSV_OK;
 }
@@ -528,12 +548,14 @@ int tsv_index_create_view(int device, int dim, int metric, const void* rows_dev,
     delete idx;
     return rc;
   }
+  register_index(idx);
   *out = idx;
   return TSV_OK;
 }
 
 int tsv_index_destroy(tsv_index* idx) {
   if (idx == nullptr) return TSV_OK;
+  unregister_index(idx);
   DeviceGuard g(idx->device);
   for (auto& kv : idx->ws) kv.second.release();
   for (auto& t : idx->timed) {
@@ -920,6 +942,10 @@ static bool small_scan_fits(const tsv_index* idx, int B, int k, int64_t n) {
   if (idx->storage == TSV_F32 || idx->dim % 8 != 0 || idx->dim > 1024 || k > 16 || B > 64 ||
       n <= 0 || n > 65536 || env_flag("TSV_NO_SMALL"))
     return false;
+  // where K2s beats the general scan (scripts/small_route_sweep.py, CUDA-graph replays): up to
+  // 4k rows at any k <= 16, up to 16k rows at k <= 8; longer ranges or k = 16 lose to it
+  // (e.g. 10k x 384, B=1, k=16: 37 vs 27 us) — those shapes go to K2t or the general scan
+  if (!(n <= 4096 || (n <= 16384 && k <= 8)) && !env_flag("TSV_FORCE_SMALL")) return false;
   const int qg = tsv::small_scan_qg(idx->dim);
   const int groups = (B + qg - 1) / qg;
   if (n * idx->dim * 2 * groups > (int64_t(48) << 20)) return false;
@@ -1797,8 +1823,19 @@ int tsv_stream_create(int device, void** out) {
 
 int tsv_stream_destroy(void* stream) {
   if (stream == nullptr) return TSV_OK;
-  TSV_CUDA(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)), "cudaStreamSynchronize");
-  TSV_CUDA(cudaStreamDestroy(reinterpret_cast<cudaStream_t>(stream)), "cudaStreamDestroy");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  TSV_CUDA(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+  {  // drop every index's workspace bound to this stream (see register_index)
+    std::lock_guard<std::mutex> lock(g_index_mu);
+    for (tsv_index* idx : g_indexes) {
+      auto it = idx->ws.find(st);
+      if (it == idx->ws.end()) continue;
+      DeviceGuard g(idx->device);
+      it->second.release();
+      idx->ws.erase(it);
+    }
+  }
+  TSV_CUDA(cudaStreamDestroy(st), "cudaStreamDestroy");
   return TSV_OK;
 }
 

@@ -241,3 +241,26 @@ def test_stream_runtime_index_affinity(cuda):
         assert _check_outputs(rt, backend) > 0
         copies[affinity] = sum(1 for (q, _, r) in backend.segments if r != backend.home(q))
     assert copies[True] <= copies[False]
+
+
+def test_captured_objects_recycle_streams(cuda):
+    """Captured searches of growing shapes created and dropped one after another on one index:
+    a destroyed library stream's workspace (marked captured) must not be inherited by a new
+    stream that reuses its handle (the next capture would be refused from growing it)."""
+    import gc
+
+    import torch
+    from paper_2407_00326_b200.index import DeviceIndex
+    from paper_2407_00326_b200.launcher import CapturedSearch
+
+    c = orc.make_corpus(30000, 256, seed=0)
+    idx = DeviceIndex(256, 30000, device=cuda.index)
+    idx.append(to_dev_bf16(c, cuda))
+    for b, k in ((1, 5), (16, 5), (64, 16), (200, 10), (300, 32), (1, 5), (512, 10)):
+        q, _ = orc.make_queries(c, b, seed=b)
+        cap = CapturedSearch(idx, b, k)
+        s, i = cap.search(to_dev_bf16(q, cuda))
+        torch.cuda.synchronize()
+        assert not orc.check_topk(from_dev(s), from_dev(i), q, c, k, 1e-3)
+        del cap
+        gc.collect()

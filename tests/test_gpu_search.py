@@ -908,6 +908,9 @@ def test_small_scan_matches_oracle_and_tensor_path(cuda, n, dim, b, k, metric, s
     from paper_2407_00326_b200 import _native
     from paper_2407_00326_b200.index import DeviceIndex
 
+    # (TSV_FORCE_SMALL: K2s serves every shape it fits here, also those the default routing
+    # leaves to the general scan because it is faster there)
+    monkeypatch.setenv("TSV_FORCE_SMALL", "1")
     c = orc.make_corpus(n, dim, seed=n % 97)
     q, _ = orc.make_queries(c, b, seed=2)
     idx = DeviceIndex(dim, n, metric=metric, device=cuda.index, storage=storage)
