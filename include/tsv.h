@@ -130,6 +130,12 @@ TSV_API int tsv_rerank(tsv_index* idx, const void* q_dev, int q_dtype, int B, co
 TSV_API int tsv_rerank_segmented(tsv_index* idx, const void* q_dev, int q_dtype, int B,
                                  const int32_t* cand_ids_dev, int C, const int32_t* row_offsets_dev,
                                  int k, float* scores_dev, int32_t* ids_dev, void* stream);
+/* The same with the row offsets in host memory (int32 [B]): uploaded on the stream through the
+ * library's pinned slots (no device table for the caller to build per batch). */
+TSV_API int tsv_rerank_segmented_host(tsv_index* idx, const void* q_dev, int q_dtype, int B,
+                                      const int32_t* cand_ids_dev, int C,
+                                      const int32_t* row_offsets_host, int k, float* scores_dev,
+                                      int32_t* ids_dev, void* stream);
 
 /* ---- K3s: contextual retrieval's Searching -> Reranking chain in ONE launch (BASELINE C5;
  * reference workloads.py:247-257 builds a per-query index, searches it, reranks the hits; the
@@ -213,6 +219,28 @@ TSV_API int tsv_stream_destroy(void* stream);
 /* ---- K5: L2-normalise (normalize != 0) and cast rows to bf16. ---- */
 TSV_API int tsv_normalize_rows(const void* src_dev, int src_dtype, int64_t n, int dim, int normalize,
                        void* dst_bf16_dev, void* stream);
+
+/* ---- Host scheduler: the engine queue of the topology-aware batch scheduler in native
+ * memory (replaces the per-call rebuild in form_batch_topo, pkg/src/teola_sim/runtime.py:189-268,
+ * and the dispatch-time queue filter, runtime.py:603-606). Host-only: no CUDA calls, no GPU
+ * needed. A task is pushed once with its static fields (query id, node id, graph depth, phase
+ * code, arrival time) and its request loads; tsv_topo_form forms one batch with the
+ * reference's decisions (per-query buckets in order of earliest arrival, deepest nodes first
+ * in node-id order, passes until the cap is reached) and writes (task handle, request count)
+ * pairs; tsv_topo_commit consumes a dispatched batch's requests and drops drained tasks.
+ * tsv_topo_form returns TSV_ERR_CAPACITY with *n_entries set when cap_entries is too small. */
+typedef struct tsv_topo_queue tsv_topo_queue;
+TSV_API int tsv_topo_create(double eps, tsv_topo_queue** out);
+TSV_API int tsv_topo_destroy(tsv_topo_queue* q);
+TSV_API int64_t tsv_topo_size(const tsv_topo_queue* q);
+TSV_API int tsv_topo_push(tsv_topo_queue* q, int64_t handle, const char* query_id,
+                          const char* node_id, int depth, int phase, double arrival_ms,
+                          const double* loads, int64_t n_loads, int64_t next);
+TSV_API int tsv_topo_form(tsv_topo_queue* q, double max_slots, int64_t cap_entries,
+                          int64_t* handles, int64_t* counts, int64_t* n_entries, double* load,
+                          int* phase);
+TSV_API int tsv_topo_commit(tsv_topo_queue* q, const int64_t* handles, const int64_t* counts,
+                            int64_t n);
 
 #ifdef __cplusplus
 }

@@ -57,6 +57,8 @@ SIGNATURES = {
     "tsv_rerank": (c_int, [c_vp, c_vp, c_int, c_int, c_vp, c_int, c_int, c_vp, c_vp, c_vp]),
     "tsv_rerank_segmented": (c_int, [c_vp, c_vp, c_int, c_int, c_vp, c_int, c_vp, c_int, c_vp,
                                      c_vp, c_vp]),
+    "tsv_rerank_segmented_host": (c_int, [c_vp, c_vp, c_int, c_int, c_vp, c_int, c_vp, c_int, c_vp,
+                                     c_vp, c_vp]),
     "tsv_search_rerank_segmented": (c_int, [c_vp, c_vp, c_vp, c_int, c_int, c_vp, c_int, c_int,
                                             c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "tsv_merge_topk": (c_int, [c_vp, c_vp, c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp]),
@@ -73,6 +75,15 @@ SIGNATURES = {
     "tsv_sharded_search": (c_int, [c_vp, c_vp, c_int, c_int, c_int, c_vp, c_vp, c_vp]),
     "tsv_sharded_destroy": (c_int, [c_vp]),
     "tsv_stream_create": (c_int, [c_int, ctypes.POINTER(c_vp)]),
+    "tsv_topo_create": (c_int, [ctypes.c_double, ctypes.POINTER(c_vp)]),
+    "tsv_topo_destroy": (c_int, [c_vp]),
+    "tsv_topo_size": (c_i64, [c_vp]),
+    "tsv_topo_push": (c_int, [c_vp, c_i64, ctypes.c_char_p, ctypes.c_char_p, c_int, c_int,
+                              ctypes.c_double, c_vp, c_i64, c_i64]),
+    "tsv_topo_form": (c_int, [c_vp, ctypes.c_double, c_i64, c_vp, c_vp,
+                              ctypes.POINTER(c_i64), ctypes.POINTER(ctypes.c_double),
+                              ctypes.POINTER(c_int)]),
+    "tsv_topo_commit": (c_int, [c_vp, c_vp, c_vp, c_i64]),
     "tsv_stream_destroy": (c_int, [c_vp]),
 }
 

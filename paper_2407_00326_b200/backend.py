@@ -139,44 +139,11 @@ class LaunchRecord:
         return self.start.elapsed_time(self.end)
 
 
-class PinnedRing:
-    """Reused pinned host slots for small per-batch uploads (segment offsets): a slot is
-    refilled only after the copy that last read it has run (its event), so uploads stay
-    asynchronous and no pinned memory is allocated per batch."""
-
-    def __init__(self, slots: int = 8, capacity: int = 4096):
-        self.bufs = [torch.empty(capacity, dtype=torch.int32, pin_memory=True)
-                     for _ in range(slots)]
-        self.events: list[torch.cuda.Event | None] = [None] * slots
-        self.capacity = capacity
-        self.next = 0
-
-    def upload(self, values: list[int], device: torch.device,
-               stream: torch.cuda.Stream) -> torch.Tensor:
-        n = len(values)
-        if n > self.capacity:
-            return torch.tensor(values, dtype=torch.int32).to(device, non_blocking=False)
-        j = self.next
-        self.next = (j + 1) % len(self.bufs)
-        if self.events[j] is not None:
-            self.events[j].synchronize()
-        buf = self.bufs[j]
-        buf[:n] = torch.as_tensor(values, dtype=torch.int32)
-        out = torch.empty(n, dtype=torch.int32, device=device)
-        with torch.cuda.stream(stream):
-            out.copy_(buf[:n], non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(stream)
-        self.events[j] = ev
-        return out
-
-
 @dataclass
 class Replica:
     device: torch.device
     stream: torch.cuda.Stream
     arena: DeviceIndex
-    pinned: PinnedRing = field(default_factory=PinnedRing)
     # released index segments: (row_beg, rows, event the reuse must wait for)
     free: list = field(default_factory=list)
 
@@ -417,11 +384,12 @@ class RetrievalBackend:
         with self._on(rep):
             # inputs are assembled first; `start` is recorded right before the library calls,
             # so the measured window is the device work of the batch
+            # `end` is recorded by the batch right after its library calls and doubles as the
+            # results' ready event (one event record fewer per batch)
             if profile.category == "search":
-                rec = self._search_batch(rep, plan, start)
+                rec = self._search_batch(rep, plan, start, end)
             else:
-                rec = self._rerank_batch(rep, plan, start)
-            end.record(rep.stream)
+                rec = self._rerank_batch(rep, plan, start, end)
         self.launches += 1
         rec.engine_id, rec.replica, rec.start, rec.end = (profile.engine_id,
                                                           self.replicas.index(rep), start, end)
@@ -469,8 +437,8 @@ class RetrievalBackend:
             (ss, si), (rs, ri) = rep.arena.search_rerank_segmented(
                 q, q_rows, max(1, max_rows), k_s, k_r, q_rerank=qq, local_ids=True,
                 stream=rep.stream)
-            ready = self._record(rep)
             end.record(rep.stream)
+            ready = end
         r = self.replicas.index(rep)
         for j, (task, rr, k, top_k) in enumerate(meta):
             self.acc.setdefault((task.ctx.query_id, task.node_id), []).append(
@@ -527,7 +495,8 @@ class RetrievalBackend:
             raise CapacityExceeded(f"{node.node_id}: query vectors for [{a}, {b}) not available")
         return torch.cat(parts) if len(parts) > 1 else parts[0]
 
-    def _search_batch(self, rep: Replica, plan, start: torch.cuda.Event) -> None:
+    def _search_batch(self, rep: Replica, plan, start: torch.cuda.Event,
+                      end: torch.cuda.Event) -> LaunchRecord:
         """One topology-aware batch of Searching requests: entries with a per-query index input
         become one segmented launch (each entry searches its own query's segment); entries
         without one search the resident global corpus in one launch. A batch mixing both runs
@@ -571,7 +540,8 @@ class RetrievalBackend:
         if q_glob is not None:
             out = self.global_index.search(q_glob, kmax, stream=rep.stream)
             launches.append((out, glob_meta))
-        ready = self._record(rep)
+        end.record(rep.stream)
+        ready = end
         r = self.replicas.index(rep)
         for (scores, ids), metas in launches:
             a = 0
@@ -598,7 +568,8 @@ class RetrievalBackend:
         rep.stream.wait_event(ready)
         return qv if qv.device == rep.device else qv.to(rep.device)
 
-    def _rerank_batch(self, rep: Replica, plan, start: torch.cuda.Event) -> None:
+    def _rerank_batch(self, rep: Replica, plan, start: torch.cuda.Event,
+                      end: torch.cuda.Event) -> LaunchRecord:
         """One batch of Reranking requests = ONE K3 launch: question j scores its own candidate
         row (ids local to its query's index segment, offset on the device by the segment's
         first arena row), duplicates dropped, the best max(top_k) kept; each entry takes its
@@ -633,12 +604,14 @@ class RetrievalBackend:
                     cand = torch.stack([torch.nn.functional.pad(j[5], (0, n_c - j[5].shape[0]),
                                                                 value=-1) for j in jobs])
                 qs = torch.cat([j[4].reshape(1, -1) for j in jobs])
-        offs = rep.pinned.upload([j[3].row_beg for j in jobs], rep.device, rep.stream)
+        # segment offsets go to the library as a host list (uploaded through its pinned slots)
+        offs = [j[3].row_beg for j in jobs]
         if not cand.is_contiguous():
             cand = cand.contiguous()
         start.record(rep.stream)
         s_all, i_all = rep.arena.rerank(qs, cand, k_out, stream=rep.stream, row_offsets=offs)
-        ready = self._record(rep)
+        end.record(rep.stream)
+        ready = end
         r = self.replicas.index(rep)
         for j, (task, lo, top_k, seg, qv, part) in enumerate(jobs):
             self.acc.setdefault((task.ctx.query_id, task.node_id), []).append(

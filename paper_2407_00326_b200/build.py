@@ -17,7 +17,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "lib"
 LIB = LIB_DIR / "libtsv.so"
-SOURCES = ["tsv_scan.cu", "tsv_merge.cu", "tsv_capi.cu"]
+SOURCES = ["tsv_scan.cu", "tsv_merge.cu", "tsv_capi.cu", "tsv_sched.cpp"]
 GENCODE = "-gencode=arch=compute_100a,code=sm_100a"
 
 
@@ -32,7 +32,7 @@ def _stale() -> bool:
     if not LIB.exists():
         return True
     t = LIB.stat().st_mtime
-    deps = list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "tsv.h"]
+    deps = (list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.cpp"))) + [ROOT / "include" / "tsv.h"]
     return any(p.stat().st_mtime > t for p in deps)
 
 

@@ -189,6 +189,7 @@ struct Workspace {
   DevBuf<int32_t> rr_arrive;    // K3 split mode: per-question arrival counters (kept zero)
   DevBuf<uint64_t> sm_keys;     // K2s: per-row-block top-k keys
   DevBuf<int64_t> qrows;        // segment kernel: per-query (row_begin, row_end)
+  DevBuf<int32_t> roffs;        // K3 over per-query indexes: row offsets uploaded from the host
   std::vector<int64_t> host_rows;
   DevBuf<int32_t> sm_arrive;    // K2s: per-query-group arrival counters (kept zero)
   std::vector<tsv::ScanItem> host_items;
@@ -219,6 +220,7 @@ struct Workspace {
     rr_arrive.ws = &state;
     sm_keys.ws = &state;
     qrows.ws = &state;
+    roffs.ws = &state;
     sm_arrive.ws = &state;
   }
   void release() {
@@ -1451,6 +1453,23 @@ int tsv_rerank_segmented(tsv_index* idx, const void* q_dev, int q_dtype, int B,
   if (row_offsets_dev == nullptr) return fail(TSV_ERR_ARGUMENT, "row_offsets_dev is null");
   return rerank_impl(idx, q_dev, q_dtype, B, cand_ids_dev, C, row_offsets_dev, k, scores_dev,
                      ids_dev, stream);
+}
+
+int tsv_rerank_segmented_host(tsv_index* idx, const void* q_dev, int q_dtype, int B,
+                              const int32_t* cand_ids_dev, int C, const int32_t* row_offsets_host,
+                              int k, float* scores_dev, int32_t* ids_dev, void* stream) {
+  if (idx == nullptr) return fail(TSV_ERR_ARGUMENT, "index is null");
+  if (row_offsets_host == nullptr) return fail(TSV_ERR_ARGUMENT, "row_offsets_host is null");
+  if (B <= 0) return fail(TSV_ERR_CAPACITY, "empty batch");
+  DeviceGuard g(idx->device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  Workspace& w = ws_for(idx, st);
+  int rc = w.roffs.ensure(static_cast<size_t>(B));
+  if (rc) return rc;
+  rc = upload_table(w, row_offsets_host, static_cast<size_t>(B) * sizeof(int32_t), w.roffs.ptr, st);
+  if (rc) return rc;
+  return rerank_impl(idx, q_dev, q_dtype, B, cand_ids_dev, C, w.roffs.ptr, k, scores_dev, ids_dev,
+                     stream);
 }
 
 int tsv_merge_topk(const float* in_scores, const int32_t* in_ids, int lists, int B, int kin,

@@ -52,6 +52,13 @@ def _check_out(out, B: int, k: int, device: torch.device) -> None:
 _RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", None)
 
 
+def _out_pair(B: int, k: int, device) -> tuple[torch.Tensor, torch.Tensor]:
+    """(scores fp32 [B, k], ids int32 [B, k]) carved from ONE allocation: a caching-allocator
+    call costs tens of microseconds when the host path is cold (inside a scheduler loop)."""
+    buf = torch.empty((2, B, k), dtype=torch.int32, device=device)
+    return buf[0].view(torch.float32), buf[1]
+
+
 def _stream_handle(stream: torch.cuda.Stream | None, device: torch.device) -> int:
     """cudaStream_t of `stream`, or of the device's current torch stream. The current stream is
     read through torch's raw-handle accessor when it exists: building a Stream object costs
@@ -206,8 +213,7 @@ class DeviceIndex:
         lo, hi = row_range if row_range is not None else (0, self.rows)
         B = q.shape[0]
         if out is None:
-            scores = torch.empty((B, k), dtype=torch.float32, device=self.device)
-            ids = torch.empty((B, k), dtype=torch.int32, device=self.device)
+            scores, ids = _out_pair(B, k, self.device)
         else:
             _check_out(out, B, int(k), self.device)
             scores, ids = out
@@ -232,8 +238,7 @@ class DeviceIndex:
         re = (ctypes.c_int64 * nseg)(*[int(b) for _, b in row_ranges])
         B = q.shape[0]
         if out is None:
-            scores = torch.empty((B, k), dtype=torch.float32, device=self.device)
-            ids = torch.empty((B, k), dtype=torch.int32, device=self.device)
+            scores, ids = _out_pair(B, k, self.device)
         else:
             _check_out(out, B, int(k), self.device)
             scores, ids = out
@@ -268,8 +273,7 @@ class DeviceIndex:
         bufs = []
         for o, kk in ((out_search, k_search), (out_rerank, k_rerank)):
             if o is None:
-                o = (torch.empty((B, kk), dtype=torch.float32, device=self.device),
-                     torch.empty((B, kk), dtype=torch.int32, device=self.device))
+                o = _out_pair(B, kk, self.device)
             else:
                 _check_out(o, B, int(kk), self.device)
             bufs.append(o)
@@ -286,8 +290,9 @@ class DeviceIndex:
                out: tuple[torch.Tensor, torch.Tensor] | None = None,
                row_offsets: torch.Tensor | None = None):
         """Score cand_ids[b, :] (arena rows) against q[b]; dedup ids; keep the best k.
-        row_offsets (int32 [B] on the device): the candidates of question b are rows of its
-        own index segment starting at arena row row_offsets[b]; ids stay segment-local."""
+        row_offsets (int32 [B] on the device, or a host list of B ints): the candidates of
+        question b are rows of its own index segment starting at arena row row_offsets[b]; ids
+        stay segment-local."""
         self._check_queries(q)
         _require_cuda(cand_ids, "cand_ids")
         if cand_ids.dtype != torch.int32 or cand_ids.dim() != 2 or cand_ids.shape[0] != q.shape[0]:
@@ -296,11 +301,19 @@ class DeviceIndex:
             raise DeviceError(f"cand_ids are on {cand_ids.device}, the index on {self.device}")
         B, C = cand_ids.shape
         if out is None:
-            scores = torch.empty((B, k), dtype=torch.float32, device=self.device)
-            ids = torch.empty((B, k), dtype=torch.int32, device=self.device)
+            scores, ids = _out_pair(B, k, self.device)
         else:
             _check_out(out, B, int(k), self.device)
             scores, ids = out
+        if isinstance(row_offsets, (list, tuple)):
+            if len(row_offsets) != B:
+                raise ConfigParse(f"row_offsets must have {B} entries")
+            offs = (ctypes.c_int32 * B)(*row_offsets)
+            nat.check(nat.load().tsv_rerank_segmented_host(
+                self._h, q.data_ptr(), _dtype_code(q), B, cand_ids.data_ptr(), C,
+                ctypes.cast(offs, ctypes.c_void_p), int(k), scores.data_ptr(), ids.data_ptr(),
+                _stream_handle(stream, self.device)))
+            return scores, ids
         if row_offsets is not None:
             _require_cuda(row_offsets, "row_offsets")
             if (row_offsets.dtype != torch.int32 or row_offsets.numel() != B
@@ -328,8 +341,7 @@ def merge_topk(scores: torch.Tensor, ids: torch.Tensor, k: int,
     if scores.dtype != torch.float32 or ids.dtype != torch.int32:
         raise ConfigParse("scores must be float32 and ids int32")
     L, B, kin = scores.shape
-    out_s = torch.empty((B, k), dtype=torch.float32, device=scores.device)
-    out_i = torch.empty((B, k), dtype=torch.int32, device=scores.device)
+    out_s, out_i = _out_pair(B, k, scores.device)
     nat.check(nat.load().tsv_merge_topk(scores.data_ptr(), ids.data_ptr(), L, B, kin, int(k),
                                         int(bool(dedup)), out_s.data_ptr(), out_i.data_ptr(),
                                         _stream_handle(stream, scores.device)))

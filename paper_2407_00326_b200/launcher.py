@@ -167,7 +167,7 @@ class StreamRuntime(Simulator):
             self._node_events.setdefault((task.ctx.query_id, task.node_id), []).append(end)
             if self.stream_order:  # consumers queue behind this batch in stream order
                 self._push(t, self._REQ_DONE, (task, n))
-        state.queue = [task for task in state.queue if task.pending() > 0]
+        self._drop_drained(state, plan)
         self._inflight.append((end, start, state, instance, plan, t))
 
     def _chain_reranks(self, plan):

@@ -17,6 +17,7 @@ from paper_2407_00326_b200 import engines as E  # noqa: E402
 from paper_2407_00326_b200.backend import RetrievalBackend  # noqa: E402
 from paper_2407_00326_b200.graph import parse_graph  # noqa: E402
 from paper_2407_00326_b200.launcher import StreamRuntime  # noqa: E402
+from paper_2407_00326_b200.runtime import RuntimeOptions  # noqa: E402
 
 GOLD = ROOT / "tests" / "golden"
 REPS = 10
@@ -63,7 +64,8 @@ def main():
         for rep_i, reps in enumerate((1, REPS)):
             host.clear()
             launches.clear()
-            rt = StreamRuntime(es, backend, speed=1.0, timeout_s=300)
+            rt = StreamRuntime(es, backend, speed=1.0, timeout_s=300,
+                               options=RuntimeOptions(native_queue="--python-queue" not in sys.argv))
             holder["rt"] = rt
             for r in range(reps):
                 for j, (g, arrival, _) in enumerate(case["graphs"]):

@@ -308,6 +308,11 @@ def test_rerank_segmented_offsets(cuda, storage):
         es, ei = orc.rerank(qs[b:b + 1], arena[a:a + sz], cand[b:b + 1], k)
         np.testing.assert_allclose(from_dev(s)[b:b + 1], es, rtol=TOL, atol=1e-6)
         assert set(from_dev(i)[b].tolist()) <= set(cand[b].tolist())
+    # the same offsets as a host list (tsv_rerank_segmented_host): identical results
+    s2, i2 = idx.rerank(qd, torch.from_numpy(cand).to(cuda), k,
+                        row_offsets=[int(a) for a in starts])
+    torch.cuda.synchronize()
+    assert torch.equal(s2, s) and torch.equal(i2, i)
 
 
 def test_merge_matches_oracle(cuda):

@@ -14,6 +14,7 @@ import pytest
 from paper_2407_00326_b200 import engines as E
 from paper_2407_00326_b200 import runtime as R
 from paper_2407_00326_b200 import stages as S
+from paper_2407_00326_b200.sched import TopoQueue
 from paper_2407_00326_b200.graph import (EGraph, MetadataProfile, PrimitiveKind, PrimitiveNode,
                                          parse_graph, serialize_graph)
 
@@ -94,11 +95,15 @@ def test_optimized_advanced_graph_isomorphic_to_golden():
 TRACE_CASES = load("ref_traces.json")
 
 
+@pytest.mark.parametrize("native", [True, False], ids=["native-queue", "python-queue"])
 @pytest.mark.parametrize("case", TRACE_CASES, ids=[f"{c['case']}-{c['scheduler']}" for c in TRACE_CASES])
-def test_simulated_trace_matches_reference(case, profiles):
+def test_simulated_trace_matches_reference(case, native, profiles):
+    if not native and case["scheduler"] != "topo":
+        pytest.skip("the native queue serves the topo scheduler only")
     es = E.EngineSet.from_dict(profiles["default"]["profiles"])
     subs = [(parse_graph(g), a, b) for g, a, b in case["graphs"]]
-    sim, trace = R.run_queries(es, subs, R.RuntimeOptions(scheduler=case["scheduler"]))
+    sim, trace = R.run_queries(es, subs, R.RuntimeOptions(scheduler=case["scheduler"],
+                                                          native_queue=native))
     assert [list(e) for e in trace.events] == case["events"]
     got = [[b.engine_id, b.instance_id, b.start_ms, b.end_ms, b.load, b.cap, b.phase,
             list(b.node_ids)] for b in trace.batches]
@@ -134,6 +139,12 @@ def test_batch_formation_matches_reference():
                     "phase": plan.phase}
 
         assert enc(R.form_batch_topo(tasks, c["cap"], c["now"])) == c["topo"]
+        # the native engine queue (csrc/tsv_sched.cpp) forms the same batch
+        nq = TopoQueue(R.EPS)
+        for t in tasks:
+            nq.push(t)
+        assert enc(nq.form(c["cap"])) == c["topo"]
+        nq.close()
         p, w = R.form_batch_blind(tasks, c["cap"], c["timeout"], c["now"], bundle_mode=False)
         assert [enc(p), w] == c["blind_to"]
         p, w = R.form_batch_blind(tasks, c["cap"], c["timeout"], c["now"], bundle_mode=True)
