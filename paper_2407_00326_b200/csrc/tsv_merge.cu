@@ -118,6 +118,53 @@ __device__ void bitonic_sort_desc_fast(uint64_t* keys, int n) {
   __syncthreads();
 }
 
+// The k best of keys[0, n) with duplicates dropped, by ONE warp, written to out_s / out_id
+// (padded with -inf / -1): lane l holds keys l + 32 i in registers; each round takes the warp
+// maximum (five u64 shuffle steps) and every lane clears its copies of it. Duplicate candidate
+// ids carry identical keys (same row, same arithmetic), so clearing equal keys is the dedup.
+// Replaces a block-wide bitonic sort + serial scan (2.3 + 0.8 us at C = 200) for n <= 32 KPL.
+template <int KPL>
+__device__ void warp_select_dedup(const uint64_t* keys, int n, int k, float* out_s,
+                                  int32_t* out_id) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t pad = pad_key();
+  uint64_t r[KPL];
+#pragma unroll
+  for (int i = 0; i < KPL; ++i) {
+    const int c = lane + 32 * i;
+    r[i] = c < n ? keys[c] : pad;
+  }
+  uint64_t lm = pad;
+#pragma unroll
+  for (int i = 0; i < KPL; ++i) lm = r[i] > lm ? r[i] : lm;
+  int w = 0;
+  for (; w < k; ++w) {
+    uint64_t m = lm;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t x = __shfl_xor_sync(0xffffffffu, m, o);
+      m = x > m ? x : m;
+    }
+    if (key_id(m) < 0) break;  // only padding / invalid candidates left
+    if (lane == 0) {
+      out_s[w] = key_score(m);
+      out_id[w] = key_id(m);
+    }
+    if (lm == m) {
+      lm = pad;
+#pragma unroll
+      for (int i = 0; i < KPL; ++i) {
+        r[i] = r[i] == m ? pad : r[i];
+        lm = r[i] > lm ? r[i] : lm;
+      }
+    }
+  }
+  for (int j = w + lane; j < k; j += 32) {
+    out_s[j] = -INFINITY;
+    out_id[j] = -1;
+  }
+}
+
 __device__ __forceinline__ int pow2_ceil(int n) {
   int p = 1;
   while (p < n) p <<= 1;
@@ -469,7 +516,7 @@ template <int kWarps, int kSlots, int CPL, bool kTiled>
 __global__ void __launch_bounds__(kWarps * 32) rerank_ring_kernel(
     const __nv_bfloat16* __restrict__ arena, int64_t nrows, int dim, const void* __restrict__ q,
     int q_is_f32, const int32_t* __restrict__ cand, int C, int k, const int32_t* __restrict__ offs,
-    float* __restrict__ out_s, int32_t* __restrict__ out_id) {
+    float* __restrict__ out_s, int32_t* __restrict__ out_id, int use_sort) {
   extern __shared__ __align__(16) uint8_t sm[];
   pdl_wait();  // (programmatic launch: the question and the candidates are the previous kernels')
   const int row_bytes = dim * 2;
@@ -569,6 +616,20 @@ __global__ void __launch_bounds__(kWarps * 32) rerank_ring_kernel(
     if (++slot == kSlots) slot = 0;
   }
   cp_async_wait<0>();
+  if (C <= 256 && !use_sort) {  // one warp selects: no block-wide sort
+    __syncthreads();
+    if (warp == 0)
+      warp_select_dedup<8>(keys, C, k, out_s + static_cast<int64_t>(b) * k,
+                           out_id + static_cast<int64_t>(b) * k);
+    return;
+  }
+  if (C <= 512 && !use_sort) {
+    __syncthreads();
+    if (warp == 0)
+      warp_select_dedup<16>(keys, C, k, out_s + static_cast<int64_t>(b) * k,
+                            out_id + static_cast<int64_t>(b) * k);
+    return;
+  }
   bitonic_sort_desc_fast(keys, np);
   // Dedup: duplicates of one id carry identical scores, so they are adjacent after the sort.
   if (threadIdx.x == 0) {
@@ -1749,6 +1810,13 @@ int launch_rerank(const void* arena, const float* arena_hi, const float* arena_l
                                     cand, C, k, out_s, out_id, stream, tiled, smem, offs);
 }
 
+// TSV_RERANK_BITONIC=1: the ring kernel's block-wide bitonic sort + serial dedup (the round-2
+// middle version) instead of the one-warp selection, for A/B runs.
+static int rerank_use_sort() {
+  const char* v = getenv("TSV_RERANK_BITONIC");
+  return v != nullptr && v[0] != '\0' && v[0] != '0';
+}
+
 template <int kWarps, int kSlots, int CPL, bool kTiled>
 int launch_rerank_ring_v(const void* arena, int64_t nrows, int dim, const void* q, int q_is_f32,
                          int B, const int32_t* cand, int C, int k, const int32_t* offs,
@@ -1766,7 +1834,7 @@ int launch_rerank_ring_v(const void* arena, int64_t nrows, int dim, const void* 
   }
   return launch_pdl(kern, dim3(B), dim3(kWarps * 32), smem, stream,
                     reinterpret_cast<const __nv_bfloat16*>(arena), nrows, dim, q, q_is_f32, cand, C,
-                    k, offs, out_s, out_id);
+                    k, offs, out_s, out_id, rerank_use_sort());
 }
 
 struct RerankSplit {  // split mode scratch (see rerank_lists_kernel)
@@ -1805,10 +1873,12 @@ int launch_rerank_ring_s(int slots, const void* arena, int64_t nrows, int dim, c
   int nw = 8;
   if (const char* w = getenv("TSV_RERANK_WARPS")) nw = atoi(w);
   if (per_block > nw * 32) nw = per_block <= 16 * 32 ? 16 : 32;
-  // Per-warp lists for short candidate lists; from 128 candidates on the ring + block-sort kernel
-  // (16 warps) measured faster (C3, 256 x 200 x 768: 18.7 vs 20.3 us; x 1024: 23.0 vs 23.9 us;
-  // scripts/rerank_probe.py), unless forced with TSV_RERANK_LISTS.
-  const bool lists_ok = sp.splits > 1 || C < 128 || getenv("TSV_RERANK_LISTS");
+  // The ring kernel (16 warps, one-warp selection) wherever its blocks fit one wave (B <= 2
+  // per SM): C3 256 x 200 x 768 18.6 vs 20.2 us (lists), C5 16 x 32 x 1024 4.4 vs 4.9,
+  // 64 x 100 x 1024 9.9 vs 11.9, 256 x 32 x 768 5.6 vs 6.1. Many questions with short lists
+  // go to the per-warp lists (8-warp blocks, more resident per SM): 1024 x 50 x 768 23.1 vs
+  // 34.1 us (scripts/rerank_probe.py with PROBE_SHAPES). TSV_RERANK_LISTS forces the lists.
+  const bool lists_ok = sp.splits > 1 || (B > 296 && C < 128) || getenv("TSV_RERANK_LISTS");
   if (k <= 32 && per_block <= nw * 32 && lists_ok && !getenv("TSV_RERANK_SORT")) {
 #define TSV_LISTS(W, S) launch_rerank_lists_v<W, S, CPL, kTiled>(arena, nrows, dim, q, q_is_f32, B, cand, C, k, offs, out_s, out_id, stream, sp)
     if (nw == 8) return slots == 2 ? TSV_LISTS(8, 2) : (slots == 3 ? TSV_LISTS(8, 3) : TSV_LISTS(8, 4));

@@ -19,10 +19,11 @@ VARIANTS = [("ldg", {"TSV_RERANK_LDG": "1"}), ("default", {}),
             ("lists_s3", {"TSV_RERANK_LISTS": "1", "TSV_RERANK_SLOTS": "3"}),
             ("lists_w16", {"TSV_RERANK_LISTS": "1", "TSV_RERANK_WARPS": "16"}),
             ("sort_s2", {"TSV_RERANK_SORT": "1"}),
+            ("sort_bitonic", {"TSV_RERANK_SORT": "1", "TSV_RERANK_BITONIC": "1"}),
             ("sort_s3", {"TSV_RERANK_SORT": "1", "TSV_RERANK_SLOTS": "3"}),
             ("sort_s4", {"TSV_RERANK_SORT": "1", "TSV_RERANK_SLOTS": "4"})]
 KNOBS = ("TSV_RERANK_LDG", "TSV_RERANK_SLOTS", "TSV_RERANK_WARPS", "TSV_RERANK_SPLITS",
-         "TSV_RERANK_SORT", "TSV_RERANK_LISTS")
+         "TSV_RERANK_SORT", "TSV_RERANK_LISTS", "TSV_RERANK_BITONIC")
 
 
 def graph_time(calls, reps=20):
@@ -51,8 +52,16 @@ def main():
     dev = torch.device("cuda", 0)
     g = torch.Generator(device=dev).manual_seed(0)
     out = []
-    for n, d, bq, c, k in ((1_000_000, 768, 256, 200, 10), (1_000_000, 1024, 16, 32, 3),
-                           (1_000_000, 1024, 256, 200, 10)):
+    shapes = ((1_000_000, 768, 256, 200, 10), (1_000_000, 1024, 16, 32, 3),
+              (1_000_000, 1024, 256, 200, 10))
+    if os.environ.get("PROBE_SHAPES"):  # "B:C:D:k,..." over a 1M-row corpus
+        shapes = tuple((1_000_000, int(d), int(b), int(c), int(k)) for b, c, d, k in
+                       (x.split(":") for x in os.environ["PROBE_SHAPES"].split(",")))
+    variants = VARIANTS
+    if os.environ.get("PROBE_VARIANTS"):
+        keep = os.environ["PROBE_VARIANTS"].split(",")
+        variants = [v for v in VARIANTS if v[0] in keep]
+    for n, d, bq, c, k in shapes:
         idx = DeviceIndex(d, n, metric="ip", device=0)
         for a in range(0, n, 1 << 18):
             idx.append(normalize_rows(torch.randn((min(1 << 18, n - a), d), generator=g, device=dev)))
@@ -70,7 +79,7 @@ def main():
                  + (r * bq * c) % max(1, n - bq * c)) for r in range(8)]
         seq = [lambda st, j=j: idx.rerank(q, seqs[j % 8], k, stream=st, out=outs[j]) for j in range(32)]
         alg = bq * c * d * 2
-        for name, env in VARIANTS:
+        for name, env in variants:
             for key in KNOBS:
                 os.environ.pop(key, None)
             os.environ.update(env)

@@ -204,11 +204,13 @@ def test_rerank_shapes_match_oracle(cuda, n, dim, b, c, k):
                                             (512, 100, 40, None), (1024, 512, 32, None),
                                             (768, 200, 10, "split8"), (256, 37, 20, "split2"),
                                             (1024, 1000, 8, None), (768, 200, 10, "lists"),
-                                            (1024, 512, 32, "lists")])
+                                            (1024, 512, 32, "lists"), (768, 200, 10, "bitonic"),
+                                            (128, 6, 12, None), (256, 400, 40, None)])
 def test_rerank_ring_equals_register_gather(cuda, dim, c, k, slots):
     """The pipelined K3 (cp.async rings, question in registers, packed fp32x2 FMAs; bf16
-    arenas; per-warp top-k lists for C <= 512, k <= 32, else the block sort, forced by
-    TSV_RERANK_SORT) against the register-gather K3 (TSV_RERANK_LDG=1) and the oracle: scores
+    arenas; 16-warp ring blocks with a one-warp top-k selection (C <= 512; block bitonic sort
+    above, or with TSV_RERANK_BITONIC), per-warp top-k lists for many short lists or forced by
+    TSV_RERANK_LISTS) against the register-gather K3 (TSV_RERANK_LDG=1) and the oracle: scores
     equal up to the summation order (even / odd halves), ids equal wherever neighbouring scores
     differ; ring depths 2-4, candidate counts below / above one ring's worth and the lists
     path's limits, invalid ids, duplicates."""
@@ -228,12 +230,13 @@ def test_rerank_ring_equals_register_gather(cuda, dim, c, k, slots):
     idx = _index_from(arena, cuda)
     qd, cd = to_dev_bf16(qs, cuda), torch.from_numpy(cand).to(cuda)
     env = ({"TSV_RERANK_SORT": "1"} if slots == "sort"
+           else {"TSV_RERANK_SORT": "1", "TSV_RERANK_BITONIC": "1"} if slots == "bitonic"
            else {"TSV_RERANK_LISTS": "1"} if slots == "lists"
            else {"TSV_RERANK_SPLITS": slots[5:]} if isinstance(slots, str)
            else {"TSV_RERANK_SLOTS": str(slots)} if slots else {})
     old = {key: os.environ.get(key) for key in ("TSV_RERANK_SLOTS", "TSV_RERANK_LDG",
                                                 "TSV_RERANK_SORT", "TSV_RERANK_SPLITS",
-                                                "TSV_RERANK_LISTS")}
+                                                "TSV_RERANK_LISTS", "TSV_RERANK_BITONIC")}
     try:
         os.environ.update(env)
         s1, i1 = idx.rerank(qd, cd, k)
