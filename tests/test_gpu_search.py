@@ -318,6 +318,47 @@ def test_rerank_segmented_offsets(cuda, storage):
     assert torch.equal(s2, s) and torch.equal(i2, i)
 
 
+def test_rerank_host_offsets_under_graph_capture(cuda):
+    """tsv_rerank_segmented_host inside a CUDA graph: the offsets' upload becomes a graph node
+    reading the library's capture pool (filled at capture time), so replays reproduce the
+    eager result; a call outside capture on the same stream first allocates that pool."""
+    import torch
+
+    from paper_2407_00326_b200._native import PrivateStream
+
+    rng = np.random.default_rng(21)
+    dim, k, sizes = 512, 4, [40, 64, 50]
+    starts = [int(x) for x in np.cumsum([0] + sizes)[:-1]]
+    arena = orc.make_corpus(int(sum(sizes)), dim, seed=7)
+    qs = orc.make_corpus(len(sizes), dim, seed=8)
+    cand = np.stack([rng.integers(0, sz, size=24) for sz in sizes]).astype(np.int32)
+    idx = _index_from(arena, cuda)
+    qd, cd = to_dev_bf16(qs, cuda), torch.from_numpy(cand).to(cuda)
+    ps = PrivateStream(cuda.index)
+    try:
+        st = ps.stream
+        eager = idx.rerank(qd, cd, k, row_offsets=starts, stream=st)
+        out = (torch.empty((3, k), dtype=torch.float32, device=cuda),
+               torch.empty((3, k), dtype=torch.int32, device=cuda))
+        st.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            idx.rerank(qd, cd, k, row_offsets=starts, stream=st, out=out)
+        for _ in range(3):
+            out[0].fill_(0)
+            out[1].fill_(-7)
+            g.replay()
+            torch.cuda.synchronize()
+            assert torch.equal(out[0], eager[0]) and torch.equal(out[1], eager[1])
+        for b, (a, sz) in enumerate(zip(starts, sizes)):
+            es, _ = orc.rerank(qs[b:b + 1], arena[a:a + sz], cand[b:b + 1], k)
+            np.testing.assert_allclose(from_dev(out[0])[b:b + 1], es, rtol=TOL, atol=1e-6)
+        del g
+    finally:
+        torch.cuda.synchronize()
+        ps.close()
+
+
 def test_merge_matches_oracle(cuda):
     import torch
     from paper_2407_00326_b200.index import merge_topk
