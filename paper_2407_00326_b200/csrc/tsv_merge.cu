@@ -118,9 +118,19 @@ __device__ void bitonic_sort_desc_fast(uint64_t* keys, int n) {
   __syncthreads();
 }
 
+// Warp-wide maximum of a 64-bit key in two redux.sync steps: the largest high word, then the
+// largest low word among the lanes holding it (a lane without it offers 0, the low word of
+// padding, which never beats a real key's). Five u64 shuffle + compare steps before.
+__device__ __forceinline__ uint64_t warp_max_key(uint64_t v) {
+  const uint32_t hi = static_cast<uint32_t>(v >> 32), lo = static_cast<uint32_t>(v);
+  const uint32_t mh = __reduce_max_sync(0xffffffffu, hi);
+  const uint32_t ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+  return (static_cast<uint64_t>(mh) << 32) | ml;
+}
+
 // The k best of keys[0, n) with duplicates dropped, by ONE warp, written to out_s / out_id
 // (padded with -inf / -1): lane l holds keys l + 32 i in registers; each round takes the warp
-// maximum (five u64 shuffle steps) and every lane clears its copies of it. Duplicate candidate
+// maximum (warp_max_key) and every lane clears its copies of it. Duplicate candidate
 // ids carry identical keys (same row, same arithmetic), so clearing equal keys is the dedup.
 // Replaces a block-wide bitonic sort + serial scan (2.3 + 0.8 us at C = 200) for n <= 32 KPL.
 template <int KPL>
@@ -139,12 +149,7 @@ __device__ void warp_select_dedup(const uint64_t* keys, int n, int k, float* out
   for (int i = 0; i < KPL; ++i) lm = r[i] > lm ? r[i] : lm;
   int w = 0;
   for (; w < k; ++w) {
-    uint64_t m = lm;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const uint64_t x = __shfl_xor_sync(0xffffffffu, m, o);
-      m = x > m ? x : m;
-    }
+    const uint64_t m = warp_max_key(lm);
     if (key_id(m) < 0) break;  // only padding / invalid candidates left
     if (lane == 0) {
       out_s[w] = key_score(m);
@@ -518,6 +523,9 @@ __global__ void __launch_bounds__(kWarps * 32) rerank_ring_kernel(
     int q_is_f32, const int32_t* __restrict__ cand, int C, int k, const int32_t* __restrict__ offs,
     float* __restrict__ out_s, int32_t* __restrict__ out_id, int use_sort) {
   extern __shared__ __align__(16) uint8_t sm[];
+  // once every block has passed here the next launch on the stream may be scheduled (its blocks
+  // take free SM slots and wait for this grid's completion in their own griddepcontrol.wait)
+  if (threadIdx.x == 0) pdl_allow_dependents();
   pdl_wait();  // (programmatic launch: the question and the candidates are the previous kernels')
   const int row_bytes = dim * 2;
   uint8_t* ring = sm;                                                   // [kWarps][kSlots][row]
@@ -674,11 +682,7 @@ __device__ __forceinline__ void warp_topk_rounds(uint64_t (&mine)[kPer], int k, 
     uint64_t m = mine[0];
 #pragma unroll
     for (int i = 1; i < kPer; ++i) m = mine[i] > m ? mine[i] : m;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const uint64_t other = __shfl_xor_sync(0xffffffffu, m, o);
-      m = other > m ? other : m;
-    }
+    m = warp_max_key(m);
     if (lane == 0) {
       if (out_key != nullptr) {
         out_key[rk] = m;
@@ -880,6 +884,7 @@ __global__ void __launch_bounds__(kSegWarps * 32) search_rerank_seg_kernel(
   int32_t* sel = reinterpret_cast<int32_t*>(score_r + max_rows);
   const int b = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) pdl_allow_dependents();  // (see rerank_ring_kernel)
   pdl_wait();
   const int64_t rb = q_rows[2 * b];
   int64_t re = min(q_rows[2 * b + 1], nrows);
@@ -1112,11 +1117,7 @@ __device__ __forceinline__ void warp_select_rounds(uint64_t (&v)[N], int k, uint
     uint64_t m = v[0];
 #pragma unroll
     for (int i = 1; i < N; ++i) m = v[i] > m ? v[i] : m;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const uint64_t x = __shfl_xor_sync(0xffffffffu, m, o);
-      m = x > m ? x : m;
-    }
+    m = warp_max_key(m);
     if (lane == 0) out[r] = m;
     if (m == pad) {
       for (int rr = r + 1; rr < k && lane == 0; ++rr) out[rr] = pad;
@@ -1328,11 +1329,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32, 1) small_scan_kernel(
     uint64_t* part = part_keys + ((static_cast<int64_t>(g) * QG + qi) * nblk + blockIdx.x) * k;
     for (int r = 0; r < k; ++r) {
       uint64_t m = l[0];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const uint64_t x = __shfl_xor_sync(0xffffffffu, m, o);
-        m = x > m ? x : m;
-      }
+      m = warp_max_key(m);
       if (lane == 0) part[r] = m;
       if (l[0] == m && m != pad) {  // exactly one lane pops its head
 #pragma unroll
