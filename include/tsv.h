@@ -155,6 +155,18 @@ TSV_API int tsv_search_rerank_segmented(tsv_index* idx, const void* q_search_dev
                                         int32_t* search_ids_dev, float* rerank_scores_dev,
                                         int32_t* rerank_ids_dev, void* stream);
 
+/* The same chain with the per-query row ranges as a HOST array (int64 [B][2]), uploaded
+ * through the library's pinned staging slots on `stream` (stream-ordered, no pageable copy;
+ * under CUDA-graph capture the table is baked into the graph): the executor's per-batch call,
+ * which has the segment table on the host (reference runtime.py:625-656 builds the batch there). */
+TSV_API int tsv_search_rerank_segmented_host(tsv_index* idx, const void* q_search_dev,
+                                             const void* q_rerank_dev, int q_dtype, int B,
+                                             const int64_t* q_rows_host, int max_rows,
+                                             int k_search, int k_rerank, int local_ids,
+                                             float* search_scores_dev, int32_t* search_ids_dev,
+                                             float* rerank_scores_dev, int32_t* rerank_ids_dev,
+                                             void* stream);
+
 /* ---- K4: merge `lists` sorted lists per query. Input layout [lists][B][kin]; output [B][kout].
  * This is the Aggregate join of split Searching stages (optimizer.py:620-661,
  * runtime.py:544-549) and the cross-shard merge after the all-gather. dedup != 0 keeps one

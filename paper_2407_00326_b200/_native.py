@@ -61,6 +61,9 @@ SIGNATURES = {
                                      c_vp, c_vp]),
     "tsv_search_rerank_segmented": (c_int, [c_vp, c_vp, c_vp, c_int, c_int, c_vp, c_int, c_int,
                                             c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "tsv_search_rerank_segmented_host": (c_int, [c_vp, c_vp, c_vp, c_int, c_int, c_vp, c_int,
+                                                 c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp,
+                                                 c_vp]),
     "tsv_merge_topk": (c_int, [c_vp, c_vp, c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp]),
     "tsv_normalize_rows": (c_int, [c_vp, c_int, c_i64, c_int, c_int, c_vp, c_vp]),
     "tsv_peer_create": (c_int, [c_int, c_int, c_int, c_int, c_int, ctypes.POINTER(c_vp)]),

@@ -183,6 +183,7 @@ class RetrievalBackend:
         self.segments: dict[tuple[str, str, int], IndexSegment] = {}  # (query, key, replica)
         # (query id, node id) -> [(first request, scores, ids)] of batches run so far
         self.acc: dict[tuple[str, str], list] = {}
+        self._edge_index: dict[int, tuple] = {}  # id(graph) -> (graph, edge count, in-edges)
         self.launches = 0
         self.device_ms_total = 0.0
         self.records: list[LaunchRecord] = []
@@ -228,6 +229,7 @@ class RetrievalBackend:
             rep.free.append((seg.row_beg, seg.row_end - seg.row_beg, evs))
         for key in [k for k in self.acc if k[0] == ctx.query_id]:
             del self.acc[key]
+        self._edge_index.pop(id(ctx.graph), None)
         ctx.data.clear()
 
     def on_complete(self, ctx, node: PrimitiveNode) -> None:
@@ -430,12 +432,11 @@ class RetrievalBackend:
             qq = torch.cat(qr) if len(qr) > 1 else qr[0]
             if qq.dtype != q.dtype:
                 qq = qq.to(q.dtype)
-            q_rows = torch.tensor(rows, dtype=torch.int64).reshape(-1, 2).to(rep.device,
-                                                                               non_blocking=True)
+            # the segment table goes to the library as a host list (its pinned staging slots)
             max_rows = max(b - a for a, b in zip(rows[::2], rows[1::2]))
             start.record(rep.stream)
             (ss, si), (rs, ri) = rep.arena.search_rerank_segmented(
-                q, q_rows, max(1, max_rows), k_s, k_r, q_rerank=qq, local_ids=True,
+                q, rows, max(1, max_rows), k_s, k_r, q_rerank=qq, local_ids=True,
                 stream=rep.stream)
             end.record(rep.stream)
             ready = end
@@ -465,16 +466,29 @@ class RetrievalBackend:
             return ms, ms
         return latency(profile, plan.load), None
 
+    def _in_edges(self, graph) -> dict:
+        """node id -> [(producer, key)] of its keyed input edges, built once per graph (a batch
+        looks its inputs up several times; scanning every edge each time cost more host time
+        than the lookups)."""
+        got = self._edge_index.get(id(graph))
+        if got is None or got[0] is not graph or got[1] != len(graph.edges):
+            idx: dict = {}
+            for e in graph.edges:
+                if e.key is not None:
+                    idx.setdefault(e.dst, []).append((e.src, e.key))
+            got = (graph, len(graph.edges), idx)
+            self._edge_index[id(graph)] = got
+        return got[2]
+
     def _inputs(self, ctx, node, want: str):
         """Data arriving on the node's input edges whose producer tag is `want`."""
         out = []
-        for e in ctx.graph.edges:
-            if e.dst == node.node_id and e.key is not None:
-                d = ctx.data.get((e.src, e.key))
-                if isinstance(d, tuple) and d[0] == want:
-                    out.append((e.src, d))
-                elif want == "result" and isinstance(d, SearchResult):
-                    out.append((e.src, d))
+        for src, key in self._in_edges(ctx.graph).get(node.node_id, ()):
+            d = ctx.data.get((src, key))
+            if isinstance(d, tuple) and d[0] == want:
+                out.append((src, d))
+            elif want == "result" and isinstance(d, SearchResult):
+                out.append((src, d))
         return out
 
     def _query_rows(self, rep, task, lo: int, hi: int) -> torch.Tensor:

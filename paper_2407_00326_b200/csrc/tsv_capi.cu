@@ -1397,7 +1397,7 @@ static int rerank_impl(tsv_index* idx, const void* q_dev, int q_dtype, int B,
     }
     e = tsv::launch_rerank_ring(idx->arena, idx->rows, idx->dim, q, q_f32, B, cand_ids_dev, C, k,
                                 row_offsets_dev, scores_dev, ids_dev, st, tiled, splits,
-                                part_keys, arrivals);
+                                part_keys, arrivals, idx->num_sms);
   } else {
     e = tsv::launch_rerank(f32 ? nullptr : idx->arena,
                            f32 ? static_cast<const float*>(idx->arena) : nullptr,
@@ -1439,6 +1439,27 @@ int tsv_search_rerank_segmented(tsv_index* idx, const void* q_search_dev,
   if (e) return cuda_fail(static_cast<cudaError_t>(e), "search+rerank launch");
   g_launches++;
   return TSV_OK;
+}
+
+int tsv_search_rerank_segmented_host(tsv_index* idx, const void* q_search_dev,
+                                     const void* q_rerank_dev, int q_dtype, int B,
+                                     const int64_t* q_rows_host, int max_rows, int k_search,
+                                     int k_rerank, int local_ids, float* search_scores_dev,
+                                     int32_t* search_ids_dev, float* rerank_scores_dev,
+                                     int32_t* rerank_ids_dev, void* stream) {
+  if (idx == nullptr) return fail(TSV_ERR_ARGUMENT, "index is null");
+  if (q_rows_host == nullptr) return fail(TSV_ERR_ARGUMENT, "q_rows_host is null");
+  if (B <= 0) return fail(TSV_ERR_CAPACITY, "empty batch");
+  DeviceGuard g(idx->device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  Workspace& w = ws_for(idx, st);
+  int rc = w.qrows.ensure(2 * static_cast<size_t>(B));
+  if (rc) return rc;
+  rc = upload_table(w, q_rows_host, 2 * static_cast<size_t>(B) * sizeof(int64_t), w.qrows.ptr, st);
+  if (rc) return rc;
+  return tsv_search_rerank_segmented(idx, q_search_dev, q_rerank_dev, q_dtype, B, w.qrows.ptr,
+                                     max_rows, k_search, k_rerank, local_ids, search_scores_dev,
+                                     search_ids_dev, rerank_scores_dev, rerank_ids_dev, stream);
 }
 
 int tsv_rerank(tsv_index* idx, const void* q_dev, int q_dtype, int B, const int32_t* cand_ids_dev,

@@ -172,7 +172,7 @@ int launch_rerank(const void* arena, const float* arena_hi, const float* arena_l
 int launch_rerank_ring(const void* arena, int64_t nrows, int dim, const void* q, int q_is_f32,
                        int B, const int32_t* cand, int C, int k, const int32_t* offs,
                        float* out_s, int32_t* out_id, cudaStream_t stream, int tiled,
-                       int splits, uint64_t* part_keys, int32_t* arrivals);
+                       int splits, uint64_t* part_keys, int32_t* arrivals, int num_sms);
 int rerank_lists_splits(int B, int C, int k, int dim, int num_sms);
 
 // Contextual chain in one launch: per query, search its own arena segment (q_rows [B][2],

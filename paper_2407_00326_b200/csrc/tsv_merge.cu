@@ -594,34 +594,52 @@ __global__ void __launch_bounds__(kWarps * 32) rerank_ring_kernel(
   };
 #pragma unroll
   for (int s = 0; s < kSlots; ++s) issue(warp + s * kWarps, s);
+  // R rows per step: with 4 slots a warp scores two landed rows at once (two independent FFMA2 /
+  // butterfly chains interleaved, each row's operation order unchanged, so the scores are
+  // bit-identical) while the other two are in flight.
+  constexpr int R = kSlots == 4 ? 2 : 1;
   int slot = 0;
-  for (int c = warp; c < C; c += kWarps) {
-    cp_async_wait<kSlots - 1>();  // the oldest group (candidate c) has landed
+  for (int c = warp; c < C; c += R * kWarps) {
+    cp_async_wait<kSlots - R>();  // the oldest R groups (candidates c, c + kWarps) have landed
     __syncwarp();
-    if (valid(c)) {
-      const uint4* row = reinterpret_cast<const uint4*>(my_ring + static_cast<size_t>(slot) * row_bytes);
-      float2 a2 = make_float2(0.f, 0.f);
+    float2 a2[R];
 #pragma unroll
-      for (int j = 0; j < CPL; ++j) {
-        const int ch = lane + 32 * j;
-        if (ch < chunks) {
-          const uint4 raw = row[ch];
-          a2 = __ffma2_rn(bf16x2_to_float2(raw.x), qr[j][0], a2);
-          a2 = __ffma2_rn(bf16x2_to_float2(raw.y), qr[j][1], a2);
-          a2 = __ffma2_rn(bf16x2_to_float2(raw.z), qr[j][2], a2);
-          a2 = __ffma2_rn(bf16x2_to_float2(raw.w), qr[j][3], a2);
+    for (int r = 0; r < R; ++r) a2[r] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) {
+      const int ch = lane + 32 * j;
+      if (ch < chunks) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const uint4 raw = reinterpret_cast<const uint4*>(
+              my_ring + static_cast<size_t>(slot + r) * row_bytes)[ch];
+          a2[r] = __ffma2_rn(bf16x2_to_float2(raw.x), qr[j][0], a2[r]);
+          a2[r] = __ffma2_rn(bf16x2_to_float2(raw.y), qr[j][1], a2[r]);
+          a2[r] = __ffma2_rn(bf16x2_to_float2(raw.z), qr[j][2], a2[r]);
+          a2[r] = __ffma2_rn(bf16x2_to_float2(raw.w), qr[j][3], a2[r]);
         }
       }
-      float acc = a2.x + a2.y;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) keys[c] = make_key(acc, ids[c]);
-    } else if (lane == 0) {
-      keys[c] = pad_key();
     }
-    __syncwarp();  // every lane done reading the slot before it is refilled
-    issue(c + kSlots * kWarps, slot);
-    if (++slot == kSlots) slot = 0;
+    float acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = a2[r].x + a2[r].y;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int cr = c + r * kWarps;  // (a slot of an invalid candidate holds stale bytes)
+        if (cr < C) keys[cr] = valid(cr) ? make_key(acc[r], ids[cr]) : pad_key();
+      }
+    }
+    __syncwarp();  // every lane done reading the slots before they are refilled
+#pragma unroll
+    for (int r = 0; r < R; ++r) issue(c + r * kWarps + kSlots * kWarps, slot + r);
+    slot += R;
+    if (slot == kSlots) slot = 0;
   }
   cp_async_wait<0>();
   if (C <= 256 && !use_sort) {  // one warp selects: no block-wide sort
@@ -2006,15 +2024,18 @@ int launch_small_scan(const void* arena, int dim, int tiled, const void* q, int 
 #undef TSV_SMALL
 }
 
-// Pipelined gather (bf16 arenas, dim <= 2048): cp.async rings of `slots` rows per warp (2 by
-// default: measured best at C3 with per-warp lists), split over blocks per rerank_lists_splits.
+// Pipelined gather (bf16 arenas, dim <= 2048): cp.async rings of `slots` rows per warp, split
+// over blocks per rerank_lists_splits. 2 slots where two blocks share an SM (C3, 256 x 200 x
+// 768: 17.7 us vs 19.1 with 4); 4 slots scored two rows at a time where the grid leaves one
+// block per SM and each warp has >= 4 rows (128 x 200 x 1024: 15.4 vs 16.8 us, 64 x 100 x
+// 1024: 9.6 vs 10.2; C5's 16 x 32: 4.3 vs 4.2; profiles/r02/rerank_probe_paired.txt).
 int launch_rerank_ring(const void* arena, int64_t nrows, int dim, const void* q, int q_is_f32,
                        int B, const int32_t* cand, int C, int k, const int32_t* offs,
                        float* out_s, int32_t* out_id, cudaStream_t stream, int tiled,
-                       int splits, uint64_t* part_keys, int32_t* arrivals) {
+                       int splits, uint64_t* part_keys, int32_t* arrivals, int num_sms) {
   if (B <= 0) return 0;
   const int row_bytes = dim * 2;
-  int slots = 2;
+  int slots = (B * splits <= num_sms && C >= 64) ? 4 : 2;
   if (const char* e = getenv("TSV_RERANK_SLOTS")) slots = atoi(e);
   slots = slots < 2 ? 2 : (slots > 4 ? 4 : slots);
   while (slots > 2 && 16 * slots * row_bytes > 200 * 1024) --slots;

@@ -256,9 +256,10 @@ class DeviceIndex:
                                 out_rerank=None):
         """Contextual retrieval's Searching -> Reranking chain in one launch: query b searches
         arena rows [q_rows[b, 0], q_rows[b, 1]) (its own index segment; int64 [B, 2] on the
-        device, every segment <= max_rows <= 1024 rows), keeps the top k_search, and reranks
-        them against q_rerank[b] (default: the query itself), keeping the top k_rerank.
-        Returns ((search scores, ids), (rerank scores, ids))."""
+        device, or a host sequence of 2 B ints [b0, e0, b1, e1, ...] uploaded through the
+        library's pinned slots; every segment <= max_rows <= 1024 rows), keeps the top
+        k_search, and reranks them against q_rerank[b] (default: the query itself), keeping
+        the top k_rerank. Returns ((search scores, ids), (rerank scores, ids))."""
         self._check_queries(q)
         B = q.shape[0]
         if q_rerank is not None:
@@ -266,10 +267,17 @@ class DeviceIndex:
             if q_rerank.shape != q.shape or q_rerank.dtype != q.dtype:
                 raise ConfigParse("q_rerank must match q in shape and dtype")
             q_rerank = q_rerank.contiguous()
-        _require_cuda(q_rows, "q_rows")
-        if (q_rows.dtype != torch.int64 or tuple(q_rows.shape) != (B, 2)
-                or q_rows.device != self.device or not q_rows.is_contiguous()):
-            raise ConfigParse(f"q_rows must be contiguous int64 [{B}, 2] on {self.device}")
+        host_rows = isinstance(q_rows, (list, tuple))
+        if host_rows:
+            if len(q_rows) != 2 * B:
+                raise ConfigParse(f"q_rows must hold {2 * B} ints (begin, end per query)")
+            rows_arg = ctypes.cast((ctypes.c_int64 * (2 * B))(*q_rows), ctypes.c_void_p)
+        else:
+            _require_cuda(q_rows, "q_rows")
+            if (q_rows.dtype != torch.int64 or tuple(q_rows.shape) != (B, 2)
+                    or q_rows.device != self.device or not q_rows.is_contiguous()):
+                raise ConfigParse(f"q_rows must be contiguous int64 [{B}, 2] on {self.device}")
+            rows_arg = q_rows.data_ptr()
         bufs = []
         for o, kk in ((out_search, k_search), (out_rerank, k_rerank)):
             if o is None:
@@ -278,9 +286,11 @@ class DeviceIndex:
                 _check_out(o, B, int(kk), self.device)
             bufs.append(o)
         (ss, si), (rs, ri) = bufs
-        nat.check(nat.load().tsv_search_rerank_segmented(
+        fn = (nat.load().tsv_search_rerank_segmented_host if host_rows
+              else nat.load().tsv_search_rerank_segmented)
+        nat.check(fn(
             self._h, q.contiguous().data_ptr(), None if q_rerank is None else q_rerank.data_ptr(),
-            _dtype_code(q), B, q_rows.data_ptr(), int(max_rows), int(k_search), int(k_rerank),
+            _dtype_code(q), B, rows_arg, int(max_rows), int(k_search), int(k_rerank),
             int(bool(local_ids)), ss.data_ptr(), si.data_ptr(), rs.data_ptr(), ri.data_ptr(),
             _stream_handle(stream, self.device)))
         return (ss, si), (rs, ri)

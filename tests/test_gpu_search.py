@@ -889,7 +889,8 @@ def test_search_rerank_segmented_fused(cuda, storage, metric, dim, k_s, k_r, sep
     the search over its own segment equals the oracle's (tie bands), and the rerank of the
     kernel's own search hits against the (separate or same) question equals the oracle's
     rerank; segments of 0, 1, 7, 33, 48, 300 and 1024 rows, segment-local and arena ids,
-    fp32 and bf16 queries."""
+    fp32 and bf16 queries; the segment table from the device and from a host list give
+    identical results."""
     import torch
 
     from paper_2407_00326_b200.index import DeviceIndex
@@ -915,8 +916,14 @@ def test_search_rerank_segmented_fused(cuda, storage, metric, dim, k_s, k_r, sep
                                                              q_rerank=qrd, local_ids=local)
             if not local:  # the rerank half is K3's arithmetic: bit-identical scores
                 us, ui = idx.rerank(qd if qrd is None else qrd, si, k_r)
+            # the host-table entry point (tsv_search_rerank_segmented_host) is the same launch
+            host_rows = [int(x) for x in rows.cpu().reshape(-1)]
+            (ss2, si2), (rs2, ri2) = idx.search_rerank_segmented(qd, host_rows, max(sizes), k_s,
+                                                                 k_r, q_rerank=qrd, local_ids=local)
             torch.cuda.synchronize()
             gs, gi, hs, hi = from_dev(ss), from_dev(si), from_dev(rs), from_dev(ri)
+            for x, y in ((gs, ss2), (gi, si2), (hs, rs2), (hi, ri2)):
+                np.testing.assert_array_equal(x, from_dev(y))
             if not local:
                 np.testing.assert_array_equal(hs, from_dev(us))
                 np.testing.assert_array_equal(hi, from_dev(ui))
