@@ -38,6 +38,13 @@ def main():
         os.environ[knob] = val
         idx.rerank(q, cand2, 10)
         del os.environ[knob]
+    # ring routing: B <= #SMs with C >= 64 -> 4 slots scored in pairs (above); more questions
+    # than SMs -> 2 slots; C not a multiple of the pair stride, duplicate and invalid ids
+    qb = normalize_rows(torch.randn((200, 256), generator=g, device=dev))
+    cand3 = torch.randint(-1, 40_000, (200, 77), generator=g, device=dev, dtype=torch.int32)
+    cand3[:, 5] = cand3[:, 4]
+    idx.rerank(qb, cand3, 7)
+    idx.rerank(qb[:50], cand3[:50], 7)
     s = torch.sort(torch.randn((8, 37, 16), generator=g, device=dev), dim=2, descending=True)[0]
     i = torch.arange(8 * 37 * 16, device=dev, dtype=torch.int32).reshape(8, 37, 16)
     merge_topk(s, i, 10)
