@@ -129,10 +129,15 @@ __device__ __forceinline__ uint64_t warp_max_key(uint64_t v) {
 }
 
 // The k best of keys[0, n) with duplicates dropped, by ONE warp, written to out_s / out_id
-// (padded with -inf / -1): lane l holds keys l + 32 i in registers; each round takes the warp
-// maximum (warp_max_key) and every lane clears its copies of it. Duplicate candidate
-// ids carry identical keys (same row, same arithmetic), so clearing equal keys is the dedup.
-// Replaces a block-wide bitonic sort + serial scan (2.3 + 0.8 us at C = 200) for n <= 32 KPL.
+// (padded with -inf / -1): lane l holds keys l + 32 i in registers, sorted descending once
+// (odd-even transposition network), so its best key is always r[0]; each round takes the warp
+// maximum of the heads (warp_max_key) and every lane whose head equals it pops it (a shift,
+// no compares on the round's critical path). Duplicate candidate ids carry identical keys
+// (same row, same arithmetic) and sit together at a lane's head, so popping equal heads is
+// the dedup. Replaces a block-wide bitonic sort + serial scan (2.3 + 0.8 us at C = 200) for
+// n <= 32 KPL. A round costs ~0.13 us (k = 10 vs k = 1: +1.2 us at C = 16 or 200); a one-redux
+// fast path for rounds whose best score sits on one lane, and results kept in registers with a
+// predicated pop, measured the same or slower.
 template <int KPL>
 __device__ void warp_select_dedup(const uint64_t* keys, int n, int k, float* out_s,
                                   int32_t* out_id) {
@@ -144,24 +149,27 @@ __device__ void warp_select_dedup(const uint64_t* keys, int n, int k, float* out
     const int c = lane + 32 * i;
     r[i] = c < n ? keys[c] : pad;
   }
-  uint64_t lm = pad;
 #pragma unroll
-  for (int i = 0; i < KPL; ++i) lm = r[i] > lm ? r[i] : lm;
+  for (int p = 0; p < KPL; ++p) {
+#pragma unroll
+    for (int i = p & 1; i + 1 < KPL; i += 2) {
+      const uint64_t a = r[i], b = r[i + 1];
+      r[i] = a > b ? a : b;
+      r[i + 1] = a > b ? b : a;
+    }
+  }
   int w = 0;
   for (; w < k; ++w) {
-    const uint64_t m = warp_max_key(lm);
+    const uint64_t m = warp_max_key(r[0]);
     if (key_id(m) < 0) break;  // only padding / invalid candidates left
     if (lane == 0) {
       out_s[w] = key_score(m);
       out_id[w] = key_id(m);
     }
-    if (lm == m) {
-      lm = pad;
+    while (r[0] == m) {  // this lane's copies of m (at most a few; usually none)
 #pragma unroll
-      for (int i = 0; i < KPL; ++i) {
-        r[i] = r[i] == m ? pad : r[i];
-        lm = r[i] > lm ? r[i] : lm;
-      }
+      for (int i = 0; i + 1 < KPL; ++i) r[i] = r[i + 1];
+      r[KPL - 1] = pad;
     }
   }
   for (int j = w + lane; j < k; j += 32) {

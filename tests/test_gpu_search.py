@@ -197,6 +197,50 @@ def test_rerank_shapes_match_oracle(cuda, n, dim, b, c, k):
         assert len(got) == len(set(got))
 
 
+@pytest.mark.parametrize("dim,c,b,k", [(768, 200, 70, 10), (1024, 64, 148, 8), (256, 77, 5, 7),
+                                      (520, 131, 149, 5), (2048, 90, 33, 12), (64, 65, 1, 3)])
+def test_rerank_paired_ring_bit_identical(cuda, dim, c, b, k):
+    """4-slot rings scoring two rows per step (the default where B <= #SMs and C >= 64) give
+    BIT-identical scores and ids to 2-slot rings (each row's FFMA2 / butterfly order is the
+    same), write nothing outside their [B, k] outputs (sentinel guard rows around them), and
+    match the oracle; odd candidate counts, invalid and duplicate ids, dim 2048 (3 slots)."""
+    import os
+
+    import torch
+
+    rng = np.random.default_rng(dim * 7 + c)
+    n = 3000
+    arena = orc.make_corpus(n, dim, seed=6)
+    qs = orc.make_corpus(b, dim, seed=7)
+    cand = rng.integers(-1, n + 3, size=(b, c)).astype(np.int32)
+    cand[:, 3] = cand[:, 2]
+    idx = _index_from(arena, cuda)
+    qd, cd = to_dev_bf16(qs, cuda), torch.from_numpy(cand).to(cuda)
+    outs = {}
+    old = os.environ.get("TSV_RERANK_SLOTS")
+    try:
+        for slots in ("2", "4"):
+            os.environ["TSV_RERANK_SLOTS"] = slots
+            gs = torch.full((b + 2, k), 12345.0, device=cuda)
+            gi = torch.full((b + 2, k), 777, dtype=torch.int32, device=cuda)
+            idx.rerank(qd, cd, k, out=(gs[1:b + 1], gi[1:b + 1]))
+            torch.cuda.synchronize()
+            gs, gi = from_dev(gs), from_dev(gi)
+            for row in (0, b + 1):
+                assert (gs[row] == 12345.0).all() and (gi[row] == 777).all(), slots
+            outs[slots] = (gs[1:b + 1], gi[1:b + 1])
+    finally:
+        if old is None:
+            os.environ.pop("TSV_RERANK_SLOTS", None)
+        else:
+            os.environ["TSV_RERANK_SLOTS"] = old
+    np.testing.assert_array_equal(outs["2"][0], outs["4"][0])
+    np.testing.assert_array_equal(outs["2"][1], outs["4"][1])
+    valid = np.where((cand >= 0) & (cand < n), cand, -1)
+    exp_s, _ = orc.rerank(qs, arena, valid, k)
+    np.testing.assert_allclose(outs["4"][0], exp_s, rtol=TOL, atol=1e-6)
+
+
 @pytest.mark.parametrize("dim,c,k,slots", [(768, 200, 10, None), (1024, 32, 3, None),
                                             (384, 57, 5, 2), (256, 300, 12, 4), (2048, 40, 4, None),
                                             (64, 3, 3, 3), (520, 77, 6, None),
