@@ -440,6 +440,45 @@ def make_queries(N, D, B, dev, normalize_rows):
     return normalize_rows(q), gid
 
 
+def p2p_self_check(sharded, q, k, dev, backend) -> None:
+    """First sharded step through the fused peer exchange (K6), checked against the NCCL
+    all-gather + K4 merge of the same per-rank lists: the ranks agree (all-reduce) to keep p2p
+    only if every rank's exchange completed and matched bit for bit; otherwise every rank
+    switches to NCCL and the JSON line says why. Peer waits are bounded (10 s here) so a peer
+    mapping that does not deliver surfaces as an error instead of a hang."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2407_00326_b200.errors import TeolaError
+
+    ok, why = 1, ""
+    try:
+        s_p, i_p = sharded.search(q, k)  # creates the peer group (collective) on first use
+        if sharded.exchange == "p2p" and sharded._peer is not None:
+            sharded._peer.set_timeout_ms(10_000)
+            s_p, i_p = sharded.search(q, k)
+            torch.cuda.synchronize(dev)
+            sharded._peer.status()
+            sharded._peer.set_timeout_ms(60_000)
+        s_p, i_p = s_p.clone(), i_p.clone()
+    except (TeolaError, RuntimeError) as exc:
+        ok, why = 0, f"{type(exc).__name__}: {exc}"
+        s_p = i_p = None
+    saved = sharded.exchange
+    sharded.exchange = "nccl"
+    s_n, i_n = sharded.search(q, k)
+    torch.cuda.synchronize(dev)
+    if ok and saved == "p2p" and not (torch.equal(s_p, s_n) and torch.equal(i_p, i_n)):
+        ok, why = 0, "fused exchange result differs from NCCL all-gather + merge"
+    flag = torch.tensor([ok], dtype=torch.int32, device=dev if backend == "nccl" else "cpu")
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    if int(flag.item()) == 1 and saved == "p2p":
+        sharded.exchange = "p2p"
+        sharded.p2p_checked = "first step bit-identical to NCCL all-gather + merge on every rank"
+    elif saved == "p2p":
+        sharded.p2p_error = why or "another rank's p2p self-check failed"
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -487,6 +526,8 @@ def run_ours(args):
     s_host = torch.empty((B, k), dtype=torch.float32, pin_memory=True)
     i_host = torch.empty((B, k), dtype=torch.int32, pin_memory=True)
     sharded = ShardedSearch(idx, N, rank=rank, world=world, exchange=args.exchange)
+    if world > 1 and sharded.exchange == "p2p":
+        p2p_self_check(sharded, q_dev, k, dev, backend)
 
     def step(q):
         return sharded.search(q, k)
@@ -744,6 +785,7 @@ def run_ours(args):
             "exchange_used": (None if world == 1 else sharded.exchange
                               + (f" (p2p unavailable: {sharded.p2p_error})"
                                  if sharded.p2p_error else "")),
+            "exchange_check": getattr(sharded, "p2p_checked", None),
             "e2e": {"value": e2e_value, "unit": "queries/s",
                     "h2d_bytes_per_step": B * D * 2, "d2h_bytes_per_step": B * k * 8,
                     "ms_per_step": e2e_ms / args.steps,

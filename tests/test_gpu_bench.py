@@ -63,6 +63,8 @@ def test_bench_ranks_sharded(cuda, world, exchange):
     assert d["n_gpus"] == world and d["config"]["shard_rows"] == 1_000_000 // world
     assert d["config"]["exchange"] == exchange
     assert d["planted_top1"] == 1.0  # global ids survive the exchange + merge
+    if exchange == "p2p":  # the first fused exchange matched NCCL all-gather + K4 on every rank
+        assert d["exchange_used"] == "p2p" and d["exchange_check"]
 
 
 def test_bench_spawns_its_own_ranks(cuda):
