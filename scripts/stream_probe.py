@@ -4,6 +4,7 @@ batch launched -> last retrieval batch finished on the device) against the devic
 batches, and each batch's host assembly time (launch() call) — what VERDICT r1 item 5 / 7 ask
 for. Prints one JSON line per app."""
 import json
+import os
 import sys
 import time
 from pathlib import Path
@@ -21,11 +22,20 @@ from paper_2407_00326_b200.runtime import RuntimeOptions  # noqa: E402
 
 GOLD = ROOT / "tests" / "golden"
 REPS = 10
+# PROBE_ISOLATED=1: queries arrive 50 ms apart (each chain runs alone), separating the host /
+# launch path's cost from queueing behind other queries' batches
+ISOLATED = os.environ.get("PROBE_ISOLATED") == "1"
 
 
 def main():
     traces = json.loads((GOLD / "ref_traces.json").read_text())
     prof = json.loads((GOLD / "ref_profiles.json").read_text())["default"]["profiles"]
+    if os.environ.get("PROBE_PROFILE") == "b200":
+        # the retrieval engines' measured B200 profiles (profiler.py): batch limits from the
+        # device, not from the reference's CPU vector store (the graphs stay the reference's)
+        meas = {e["engine_id"]: e for e in json.loads(
+            (ROOT / "profiles" / "b200_engines.json").read_text())["engines"]}
+        prof = dict(prof, engines=[meas.get(e["engine_id"], e) for e in prof["engines"]])
     for name in ("advanced_c3", "contextual"):
         case = next(c for c in traces if c["case"] == name and c["scheduler"] == "topo")
         es = E.EngineSet.from_dict(prof)
@@ -73,7 +83,11 @@ def main():
                     eg.query_id = f"{eg.query_id}-{rep_i}-{r}-{j}"
                     for node in eg.nodes.values():
                         node.meta.query_id = eg.query_id
-                    rt.submit_query(eg, arrival + 20.0 * r, arrival_ms=arrival + 20.0 * r)
+                    if ISOLATED:  # one query in flight at a time: no queueing behind others
+                        arrival = 50.0 * (r * len(case["graphs"]) + j)
+                    else:
+                        arrival = arrival + 20.0 * r
+                    rt.submit_query(eg, arrival, arrival_ms=arrival)
             rt.run()
         torch.cuda.synchronize()
         gpu = [b for b in rt.trace.batches if b.engine_id in ("vdb-search0", "rerank0")]
@@ -99,7 +113,7 @@ def main():
             dev.append(sum(x[4][0].elapsed_time(x[4][1]) for x in window))
         ratio = [s / d for s, d in zip(spans, dev) if d > 0]
         print(json.dumps({
-            "app": name, "queries": len(rt.contexts), "gpu_batches": len(gpu),
+            "app": name, "isolated": ISOLATED, "profile": os.environ.get("PROBE_PROFILE", "reference"), "queries": len(rt.contexts), "gpu_batches": len(gpu),
             "chain_span_ms_p50": float(np.median(spans)), "chain_device_ms_p50": float(np.median(dev)),
             "span_over_device_p50": float(np.median(ratio)), "span_over_device_max": float(max(ratio)),
             "batch_device_ms_p50": float(np.median([b_.device_ms for b_ in gpu])),
