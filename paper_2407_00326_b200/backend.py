@@ -184,6 +184,7 @@ class RetrievalBackend:
         # (query id, node id) -> [(first request, scores, ids)] of batches run so far
         self.acc: dict[tuple[str, str], list] = {}
         self._edge_index: dict[int, tuple] = {}  # id(graph) -> (graph, edge count, in-edges)
+        self._waited: dict = {}  # (replica, event) pairs already waited in the current launch
         self.launches = 0
         self.device_ms_total = 0.0
         self.records: list[LaunchRecord] = []
@@ -381,6 +382,7 @@ class RetrievalBackend:
         if not plan.entries:
             raise CapacityExceeded("empty batch")
         rep = self.replica_for(instance)
+        self._waited = {}
         start = torch.cuda.Event(enable_timing=True)
         end = torch.cuda.Event(enable_timing=True)
         with self._on(rep):
@@ -409,6 +411,7 @@ class RetrievalBackend:
         rep = self.replica_for(instance)
         if rep.arena.storage not in ("bf16", "bf16_tiled") or self.dim > 2048:
             return None
+        self._waited = {}
         start = torch.cuda.Event(enable_timing=True)
         end = torch.cuda.Event(enable_timing=True)
         with self._on(rep):
@@ -480,6 +483,15 @@ class RetrievalBackend:
             self._edge_index[id(graph)] = got
         return got[2]
 
+    def _wait(self, rep: Replica, ev) -> None:
+        """rep.stream waits for `ev` once per launch: a batch's entries often share producer
+        events (one query's results, one upstream batch), and every cudaStreamWaitEvent is a
+        few microseconds of host time."""
+        key = (id(rep), id(ev))
+        if key not in self._waited:
+            self._waited[key] = ev  # (holds the event: its id stays unique during the launch)
+            rep.stream.wait_event(ev)
+
     def _inputs(self, ctx, node, want: str):
         """Data arriving on the node's input edges whose producer tag is `want`."""
         out = []
@@ -503,7 +515,7 @@ class RetrievalBackend:
             _, key, s_lo, s_hi, total, vecs, ready = d
             x0, x1 = max(a, s_lo), min(b, s_hi)
             if x0 < x1:
-                rep.stream.wait_event(ready)
+                self._wait(rep, ready)
                 parts.append(vecs[x0 - s_lo:x1 - s_lo].to(rep.device))
         if not parts or sum(p_.shape[0] for p_ in parts) != b - a:
             raise CapacityExceeded(f"{node.node_id}: query vectors for [{a}, {b}) not available")
@@ -579,7 +591,7 @@ class RetrievalBackend:
                 qv = self.data.question(rep.device, ctx.query_id)
             return qv
         qv, ready = got
-        rep.stream.wait_event(ready)
+        self._wait(rep, ready)
         return qv if qv.device == rep.device else qv.to(rep.device)
 
     def _rerank_batch(self, rep: Replica, plan, start: torch.cuda.Event,
@@ -599,7 +611,7 @@ class RetrievalBackend:
                 raise CapacityExceeded(f"{node.node_id}: no candidate input")
             res = cands[0][1]
             if res.ready is not None:
-                rep.stream.wait_event(res.ready)
+                self._wait(rep, res.ready)
             lo = task.next_request
             part = res.ids.reshape(-1)[lo:lo + n]
             idx = self._inputs(ctx, node, "index") or self._index_of_search(ctx, cands[0][0])
@@ -662,8 +674,8 @@ class RetrievalBackend:
         key = next(iter(node.meta.outputs))
         rep = self.replicas[parts[0][4]]
         with self._on(rep):
-            for p_ in parts:
-                rep.stream.wait_event(p_[3])
+            for ev in {id(p_[3]): p_[3] for p_ in parts}.values():
+                rep.stream.wait_event(ev)
             if node.kind is PrimitiveKind.SEARCHING:
                 q_lo, q_hi = _stage_queries(node, key)
                 res = SearchResult(torch.cat([p_[1] for p_ in parts]),
