@@ -178,6 +178,81 @@ __device__ void warp_select_dedup(const uint64_t* keys, int n, int k, float* out
   }
 }
 
+// The same selection without k serial rounds, for 16 <= k <= 32: the KPL columns (key l + 32 i
+// in lane l) are each bitonic-sorted across the warp (descending), then merged pairwise keeping
+// the top 32 (max of a column and its partner reversed is bitonic; five more stages sort it),
+// so lane l ends with the l-th largest key of all n. Duplicates are adjacent there: a lane
+// keeps its key when it differs from lane l-1's, and a ballot gives each kept key its output
+// position. Returns false (nothing written) when the 32 largest hold fewer than k distinct
+// keys while more valid keys exist below them; the caller then runs warp_select_dedup.
+// Below k = 16 the k serial rounds are cheaper (C3's k = 10: 17.6 vs 18.1 us with the network;
+// k = 20: 19.1 vs 18.2, k = 32 at 148 x 200: 16.3 vs 13.8; profiles/r02/rerank_probe_topk_net.txt).
+constexpr int kNetMinK = 16;
+__device__ __forceinline__ uint64_t u64_max(uint64_t a, uint64_t b) { return a > b ? a : b; }
+__device__ __forceinline__ uint64_t u64_min(uint64_t a, uint64_t b) { return a > b ? b : a; }
+
+template <int N>
+__device__ __forceinline__ void warp_bitonic_stages_desc(uint64_t (&v)[N], int lane, int size) {
+  // the merge stages of one bitonic level: blocks of `size` lanes, descending where
+  // (lane & size) == 0 (size = 64: the whole warp descending)
+  const bool desc = (lane & size) == 0;
+#pragma unroll
+  for (int stride = 16; stride > 0; stride >>= 1) {
+    if (stride >= size) continue;
+    const bool keep_max = ((lane & stride) == 0) == desc;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const uint64_t o = __shfl_xor_sync(0xffffffffu, v[i], stride);
+      v[i] = keep_max ? u64_max(v[i], o) : u64_min(v[i], o);
+    }
+  }
+}
+
+template <int KPL>
+__device__ bool warp_topk_net(const uint64_t* keys, int n, int k, float* out_s, int32_t* out_id) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t pad = pad_key();
+  uint64_t r[KPL];
+#pragma unroll
+  for (int i = 0; i < KPL; ++i) {
+    const int c = lane + 32 * i;
+    r[i] = c < n ? keys[c] : pad;
+  }
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) warp_bitonic_stages_desc<KPL>(r, lane, size == 32 ? 64 : size);
+#pragma unroll
+  for (int w = KPL / 2; w >= 1; w >>= 1) {
+#pragma unroll
+    for (int i = 0; i < w; ++i) r[i] = u64_max(r[i], __shfl_sync(0xffffffffu, r[i + w], 31 - lane));
+#pragma unroll
+    for (int stride = 16; stride > 0; stride >>= 1) {
+      const bool keep_max = (lane & stride) == 0;
+#pragma unroll
+      for (int i = 0; i < w; ++i) {
+        const uint64_t o = __shfl_xor_sync(0xffffffffu, r[i], stride);
+        r[i] = keep_max ? u64_max(r[i], o) : u64_min(r[i], o);
+      }
+    }
+  }
+  const uint64_t v = r[0];
+  const uint64_t prev = __shfl_up_sync(0xffffffffu, v, 1);
+  const bool keep = key_id(v) >= 0 && (lane == 0 || v != prev);
+  const uint32_t mask = __ballot_sync(0xffffffffu, keep);
+  const int distinct = __popc(mask);
+  const bool more_below = key_id(__shfl_sync(0xffffffffu, v, 31)) >= 0 && n > 32;
+  if (distinct < k && more_below) return false;
+  const int pos = __popc(mask & ((1u << lane) - 1u));
+  if (keep && pos < k) {
+    out_s[pos] = key_score(v);
+    out_id[pos] = key_id(v);
+  }
+  for (int j = distinct + lane; j < k; j += 32) {
+    out_s[j] = -INFINITY;
+    out_id[j] = -1;
+  }
+  return true;
+}
+
 __device__ __forceinline__ int pow2_ceil(int n) {
   int p = 1;
   while (p < n) p <<= 1;
@@ -650,11 +725,16 @@ __global__ void __launch_bounds__(kWarps * 32) rerank_ring_kernel(
     if (slot == kSlots) slot = 0;
   }
   cp_async_wait<0>();
+  const bool net = !(use_sort & 2) && k >= kNetMinK && k <= 32;
+  use_sort &= 1;
   if (C <= 256 && !use_sort) {  // one warp selects: no block-wide sort
     __syncthreads();
-    if (warp == 0)
-      warp_select_dedup<8>(keys, C, k, out_s + static_cast<int64_t>(b) * k,
-                           out_id + static_cast<int64_t>(b) * k);
+    if (warp == 0) {
+      float* os = out_s + static_cast<int64_t>(b) * k;
+      int32_t* oi = out_id + static_cast<int64_t>(b) * k;
+      if (!(net && warp_topk_net<8>(keys, C, k, os, oi)))
+        warp_select_dedup<8>(keys, C, k, os, oi);
+    }
     return;
   }
   if (C <= 512 && !use_sort) {
@@ -1835,9 +1915,10 @@ int launch_rerank(const void* arena, const float* arena_hi, const float* arena_l
 
 // TSV_RERANK_BITONIC=1: the ring kernel's block-wide bitonic sort + serial dedup (the round-2
 // middle version) instead of the one-warp selection, for A/B runs.
+// TSV_RERANK_NO_NET=1: k serial selection rounds instead of the warp top-k network (bit 1).
 static int rerank_use_sort() {
-  const char* v = getenv("TSV_RERANK_BITONIC");
-  return v != nullptr && v[0] != '\0' && v[0] != '0';
+  auto on = [](const char* v) { return v != nullptr && v[0] != '\0' && v[0] != '0'; };
+  return (on(getenv("TSV_RERANK_BITONIC")) ? 1 : 0) | (on(getenv("TSV_RERANK_NO_NET")) ? 2 : 0);
 }
 
 template <int kWarps, int kSlots, int CPL, bool kTiled>

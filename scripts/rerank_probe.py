@@ -23,9 +23,9 @@ VARIANTS = [("ldg", {"TSV_RERANK_LDG": "1"}), ("default", {}),
             ("sort_s3", {"TSV_RERANK_SORT": "1", "TSV_RERANK_SLOTS": "3"}),
             ("sort_s4", {"TSV_RERANK_SORT": "1", "TSV_RERANK_SLOTS": "4"}),
             ("ring_s2", {"TSV_RERANK_SLOTS": "2"}), ("ring_s3", {"TSV_RERANK_SLOTS": "3"}),
-            ("ring_s4", {"TSV_RERANK_SLOTS": "4"})]
+            ("ring_s4", {"TSV_RERANK_SLOTS": "4"}), ("no_net", {"TSV_RERANK_NO_NET": "1"})]
 KNOBS = ("TSV_RERANK_LDG", "TSV_RERANK_SLOTS", "TSV_RERANK_WARPS", "TSV_RERANK_SPLITS",
-         "TSV_RERANK_SORT", "TSV_RERANK_LISTS", "TSV_RERANK_BITONIC")
+         "TSV_RERANK_SORT", "TSV_RERANK_LISTS", "TSV_RERANK_BITONIC", "TSV_RERANK_NO_NET")
 
 
 def graph_time(calls, reps=20):

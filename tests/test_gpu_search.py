@@ -158,6 +158,45 @@ def test_rerank_dedups_and_matches_oracle(cuda):
     assert (gi[gap_ok] == exp_i[gap_ok]).all()
 
 
+@pytest.mark.parametrize("c,k,dups", [(200, 16, 0), (200, 32, 0), (256, 17, 0), (200, 24, 40),
+                                      (200, 20, 150), (33, 16, 10), (40, 30, 0)])
+def test_rerank_topk_network_equals_rounds(cuda, c, k, dups):
+    """The warp top-k network (16 <= k <= 32, C <= 256) is bit-identical to the k serial
+    selection rounds (TSV_RERANK_NO_NET=1) and to the oracle's scores, including candidate
+    lists whose 32 best keys hold fewer than k distinct ids (heavy duplication: the network
+    hands over to the rounds) and lists with invalid ids."""
+    import os
+
+    import torch
+
+    rng = np.random.default_rng(c * 31 + k + dups)
+    n, b, dim = 3000, 40, 256
+    arena = orc.make_corpus(n, dim, seed=8)
+    qs = orc.make_corpus(b, dim, seed=9)
+    cand = rng.integers(-1, n, size=(b, c)).astype(np.int32)
+    if dups:  # the row each question scores highest, repeated `dups` times
+        best = np.argmax(qs @ arena.T, axis=1).astype(np.int32)
+        cand[:, :dups] = best[:, None]
+    idx = _index_from(arena, cuda)
+    qd, cd = to_dev_bf16(qs, cuda), torch.from_numpy(cand).to(cuda)
+    old = os.environ.get("TSV_RERANK_NO_NET")
+    try:
+        os.environ.pop("TSV_RERANK_NO_NET", None)
+        s1, i1 = idx.rerank(qd, cd, k)
+        os.environ["TSV_RERANK_NO_NET"] = "1"
+        s2, i2 = idx.rerank(qd, cd, k)
+        torch.cuda.synchronize()
+    finally:
+        if old is None:
+            os.environ.pop("TSV_RERANK_NO_NET", None)
+        else:
+            os.environ["TSV_RERANK_NO_NET"] = old
+    np.testing.assert_array_equal(from_dev(s1), from_dev(s2))
+    np.testing.assert_array_equal(from_dev(i1), from_dev(i2))
+    exp_s, _ = orc.rerank(qs, arena, cand, k)
+    np.testing.assert_allclose(from_dev(s1), exp_s, rtol=TOL, atol=1e-6)
+
+
 def test_rerank_fewer_distinct_than_k_pads(cuda):
     import torch
 
